@@ -1,0 +1,233 @@
+"""Seeded synthetic inputs for the SU(N) unfold (shared by the oracle, the tests and bench.py).
+
+This module holds NO arithmetic of the method (no basis, no structure constants,
+no Lindbladian).  It only builds the N x N input operators H0, H1, {L_p} and the
+rates {gamma_p} for the five BASELINE.json configurations, as complex128 CSR
+arrays in host memory.  Both sides of every parity test (the CUDA path through
+the C-ABI and the CPU oracle) consume exactly these arrays.
+
+Recipes (DESIGN.md "Input recipe" restates them):
+
+* c0  N=4, P=1.  rng = numpy.random.default_rng(0).  A = g(N,N) + i g(N,N)
+      (real block drawn first, then imaginary block), H = (A + A^H)/2 (dense,
+      has a trace).  Then L1 = g(N,N) + i g(N,N) (dense, has a trace).
+      gamma_1 = 1.0.  No drive.                      BASELINE.json configs[0]
+* c1  Bose-Hubbard dimer, N=64 states (N-1 bosons), Fock index a = n1,
+      n2 = N-1-a:  H = -J(b1^+ b2 + b2^+ b1) + (U/2N) sum_j n_j(n_j-1), J=1, U=2;
+      L = (b1^+ + b2^+)(b1 - b2), gamma = 0.1.  No drive.  configs[1]
+      (Eq. 12-13, with BASELINE's normalisation.)
+* c2  c1 at N=256 plus H1 = n2 - n1 = diag(N-1-2a); eps(t) = 1 + 1.5 sin t.
+* c3  N=512 random banded.  rng = default_rng(3).  H: for each diagonal offset
+      k = 1..3 (in that order) draw re = g(N-k), im = g(N-k) and set
+      H[a, a+k] = re + i im, H[a+k, a] = conj; then the real diagonal g(N).
+      Then for p = 1..4: for k = -2..2 (in that order) draw re = g(N-|k|),
+      im = g(N-|k|) and set L_p[a, a+k] (a ranging over valid rows ascending).
+      Finally gamma = uniform(0.05, 0.5, size=4).            configs[3]
+* c4  c2's dimer and drive at N=1000 with c1's dissipator.   configs[4]
+
+CSR layout (the C-ABI's sun_zcsr): row_ptr int64[N+1], col int32[nnz] ascending
+within each row, val complex128[nnz] (== interleaved re,im float64[2 nnz]).
+Exact zeros are not stored.
+"""
+from __future__ import annotations
+
+import dataclasses
+from typing import List, Optional
+
+import numpy as np
+
+
+@dataclasses.dataclass
+class ZCSR:
+    """N x N complex operator in CSR form (host numpy arrays)."""
+
+    n: int
+    row_ptr: np.ndarray  # int64 [n+1]
+    col: np.ndarray  # int32 [nnz]
+    val: np.ndarray  # complex128 [nnz]
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col.shape[0])
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros((self.n, self.n), dtype=np.complex128)
+        for r in range(self.n):
+            lo, hi = int(self.row_ptr[r]), int(self.row_ptr[r + 1])
+            out[r, self.col[lo:hi]] = self.val[lo:hi]
+        return out
+
+    @staticmethod
+    def from_dense(a: np.ndarray) -> "ZCSR":
+        a = np.asarray(a, dtype=np.complex128)
+        n = a.shape[0]
+        assert a.shape == (n, n)
+        rows, cols = np.nonzero(a)
+        order = np.lexsort((cols, rows))
+        rows, cols = rows[order], cols[order]
+        row_ptr = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(row_ptr, rows + 1, 1)
+        row_ptr = np.cumsum(row_ptr).astype(np.int64)
+        return ZCSR(n, row_ptr, cols.astype(np.int32), a[rows, cols].copy())
+
+    @staticmethod
+    def from_triplets(n: int, rows, cols, vals) -> "ZCSR":
+        """Build from (row, col, value) triplets; duplicates are not allowed, zeros dropped."""
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        vals = np.asarray(vals, dtype=np.complex128)
+        keep = vals != 0
+        rows, cols, vals = rows[keep], cols[keep], vals[keep]
+        order = np.lexsort((cols, rows))
+        rows, cols, vals = rows[order], cols[order], vals[order]
+        if rows.size > 1:
+            dup = (rows[1:] == rows[:-1]) & (cols[1:] == cols[:-1])
+            assert not dup.any(), "duplicate (row, col) in triplets"
+        row_ptr = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(row_ptr, rows + 1, 1)
+        row_ptr = np.cumsum(row_ptr).astype(np.int64)
+        return ZCSR(n, row_ptr, cols.astype(np.int32), vals)
+
+
+@dataclasses.dataclass
+class Problem:
+    """One unfold problem: H(t) = H0 + eps(t) H1 and dissipators {(L_p, gamma_p)}."""
+
+    name: str
+    n: int
+    H0: ZCSR
+    H1: Optional[ZCSR]
+    Ls: List[ZCSR]
+    gammas: List[float]
+    eps: Optional[dict] = None  # drive eps(t) = eps0 + eps1 sin(omega t) (R10)
+
+    @property
+    def m(self) -> int:
+        return self.n * self.n - 1
+
+
+# ----------------------------------------------------------------------------
+# Bose-Hubbard dimer (Eq. 12; Eq. 13, P:242-245;
+# normalisation and sign per BASELINE.json configs[1], R8/R9/R11)
+# ----------------------------------------------------------------------------
+
+def dimer_hamiltonian(n: int, J: float = 1.0, U: float = 2.0) -> ZCSR:
+    """H = -J(b1^+ b2 + b2^+ b1) + (U/2N) sum_j n_j(n_j - 1) in the Fock basis a = n1."""
+    a = np.arange(n, dtype=np.float64)
+    n1, n2 = a, (n - 1) - a
+    diag = (U / (2.0 * n)) * (n1 * (n1 - 1.0) + n2 * (n2 - 1.0))
+    off = -J * np.sqrt((a[:-1] + 1.0) * (n - 1.0 - a[:-1]))  # H[a+1,a] = H[a,a+1]
+    rows = np.concatenate([np.arange(n), np.arange(n - 1), np.arange(1, n)])
+    cols = np.concatenate([np.arange(n), np.arange(1, n), np.arange(n - 1)])
+    vals = np.concatenate([diag, off, off]).astype(np.complex128)
+    return ZCSR.from_triplets(n, rows, cols, vals)
+
+
+def dimer_drive(n: int) -> ZCSR:
+    """H1 = n2 - n1 = diag(N-1-2a) (the operator multiplying eps(t) in Eq. 12)."""
+    a = np.arange(n)
+    return ZCSR.from_triplets(n, a, a, ((n - 1) - 2 * a).astype(np.complex128))
+
+
+def dimer_dissipator(n: int) -> ZCSR:
+    """L = (b1^+ + b2^+)(b1 - b2) = n1 - n2 - b1^+ b2 + b2^+ b1 (no prefactor, R9)."""
+    a = np.arange(n, dtype=np.float64)
+    diag = 2.0 * a - (n - 1.0)
+    s = np.sqrt((a[:-1] + 1.0) * (n - 1.0 - a[:-1]))
+    rows = np.concatenate([np.arange(n), np.arange(1, n), np.arange(n - 1)])
+    cols = np.concatenate([np.arange(n), np.arange(n - 1), np.arange(1, n)])
+    # L[a+1, a] = -s_a ; L[a, a+1] = +s_a
+    vals = np.concatenate([diag, -s, s]).astype(np.complex128)
+    return ZCSR.from_triplets(n, rows, cols, vals)
+
+
+def dimer_problem(n: int, drive: bool, gamma: float = 0.1, name: str = "") -> Problem:
+    return Problem(
+        name=name or f"dimer_N{n}",
+        n=n,
+        H0=dimer_hamiltonian(n),
+        H1=dimer_drive(n) if drive else None,
+        Ls=[dimer_dissipator(n)],
+        gammas=[gamma],
+        eps={"eps0": 1.0, "eps1": 1.5, "omega": 1.0} if drive else None,
+    )
+
+
+# ----------------------------------------------------------------------------
+# Random inputs
+# ----------------------------------------------------------------------------
+
+def dense_random_problem(n: int = 4, seed: int = 0, gamma: float = 1.0, P: int = 1) -> Problem:
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    H = (A + A.conj().T) / 2.0
+    Ls = []
+    for _ in range(P):
+        Ls.append(ZCSR.from_dense(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))))
+    return Problem(f"dense_N{n}_s{seed}", n, ZCSR.from_dense(H), None, Ls, [gamma] * P)
+
+
+def _band_hermitian(rng, n: int, w: int) -> np.ndarray:
+    H = np.zeros((n, n), dtype=np.complex128)
+    for k in range(1, w + 1):
+        if n - k <= 0:
+            continue
+        re = rng.standard_normal(n - k)
+        im = rng.standard_normal(n - k)
+        idx = np.arange(n - k)
+        H[idx, idx + k] = re + 1j * im
+        H[idx + k, idx] = re - 1j * im
+    H[np.arange(n), np.arange(n)] = rng.standard_normal(n)
+    return H
+
+
+def _band_general(rng, n: int, w: int) -> np.ndarray:
+    L = np.zeros((n, n), dtype=np.complex128)
+    for k in range(-w, w + 1):
+        m = n - abs(k)
+        if m <= 0:
+            continue
+        re = rng.standard_normal(m)
+        im = rng.standard_normal(m)
+        rows = np.arange(m) if k >= 0 else np.arange(-k, n)
+        L[rows, rows + k] = re + 1j * im
+    return L
+
+
+def banded_random_problem(n: int = 512, seed: int = 3, wH: int = 3, wL: int = 2, P: int = 4,
+                          drive_w: Optional[int] = None) -> Problem:
+    rng = np.random.default_rng(seed)
+    H = _band_hermitian(rng, n, wH)
+    Ls = [_band_general(rng, n, wL) for _ in range(P)]
+    gammas = rng.uniform(0.05, 0.5, size=P).tolist()
+    H1 = None
+    if drive_w is not None:
+        H1 = ZCSR.from_dense(_band_hermitian(rng, n, drive_w))
+    return Problem(f"banded_N{n}_s{seed}", n, ZCSR.from_dense(H), H1,
+                   [ZCSR.from_dense(L) for L in Ls], gammas)
+
+
+def config(idx: int) -> Problem:
+    """The five BASELINE.json configurations (index = position in configs[])."""
+    if idx == 0:
+        return dense_random_problem(4, seed=0, gamma=1.0)
+    if idx == 1:
+        return dimer_problem(64, drive=False, name="c1_dimer_N64")
+    if idx == 2:
+        return dimer_problem(256, drive=True, name="c2_dimer_N256_drive")
+    if idx == 3:
+        p = banded_random_problem(512, seed=3)
+        p.name = "c3_banded_N512_P4"
+        return p
+    if idx == 4:
+        return dimer_problem(1000, drive=True, name="c4_dimer_N1000_drive")
+    raise ValueError(idx)
+
+
+CONFIG_NAMES = {
+    0: "c0_dense_N4_P1",
+    1: "c1_dimer_N64",
+    2: "c2_dimer_N256_drive",
+    3: "c3_banded_N512_P4",
+    4: "c4_dimer_N1000_drive",
+}
