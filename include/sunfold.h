@@ -1,0 +1,154 @@
+/*
+ * sunfold.h — C-ABI of the B200 (sm_100a) SU(N) unfold of the GKSL master equation.
+ *
+ * Paper: "Unfolding quantum master equation into a system of real-valued equations:
+ * computationally effective expansion over the basis of SU(N) generators",
+ * arXiv:1812.11626.  Citations P:n are PAPER.md line numbers.
+ *
+ * What the library computes (Eq. 1, Eq. 5, Eq. 6 P:171-174,
+ * Eq. 9, Eqs. 10-11; Table I Step 2 P:287):
+ *
+ *   Given H(t) = H0 + eps(t) H1 and dissipators {L_p, gamma_p}, p = 1..P, the GKSL generator
+ *     L(t) rho = -i[H(t), rho] + sum_p gamma_p (L_p rho L_p^+ - 1/2 {L_p^+ L_p, rho})
+ *   is unfolded over the SU(N) generators F_1..F_M (M = N^2 - 1; basis P:135-144, DESIGN.md
+ *   readings R4/R5) into the real system
+ *     dv/dt = (Q0 + eps(t) Q1) v + K,      rho = I/N + sum_j v_j F_j,
+ *   with  Q0_sm = Tr(F_s L0(F_m)),  Q1_sm = Tr(F_s (-i[H1, F_m])),  K_s = Tr(F_s L0(I/N)),
+ *   where L0 is L with H = H0.  Q0 contains both the paper's Q (Eq. 6, from H0) and R
+ *   (Eq. 10); K is Eq. 11 (with gamma_p, R2).  A trace of L_p is allowed (R3).
+ *
+ * Generator order (part of the ABI, R5), 0-based, a < b, l = 1..N-1:
+ *   idx(S_ab) = p(a,b), idx(J_ab) = N(N-1)/2 + p(a,b), idx(D^l) = N(N-1) + l - 1,
+ *   p(a,b) = a(2N-a-1)/2 + (b-a-1).
+ *
+ * Stored pattern (R6): an entry q is stored iff |q| > tau, with
+ *   tau(Q0) = 1e-14 (||H0||_F + sum_p gamma_p ||L_p||_F^2),  tau(Q1) = 1e-14 ||H1||_F.
+ * Columns ascend within each row.  Results are bitwise deterministic.
+ *
+ * Memory ownership: every array argument is a DEVICE pointer owned by the caller (the
+ * Python binding allocates with torch); the library never allocates device memory.
+ * `stream` is a cudaStream_t passed as void*.  A plan is bound to one stream and is not
+ * thread-safe.  Nothing throws across the ABI: every call returns a sun_status.
+ *
+ * Call sequence (the paper's two-step CRS fill: "the number of nonzero elements
+ * in each row is computed. Next, the elements are calculated and indexes are written"):
+ *   sun_workspace_bytes(n, P) -> caller allocates the device workspace
+ *   sun_plan_create  -> validate + analyse the operator patterns (one small readback)
+ *   sun_count        -> expand (a1), count pass (a3), prefix scan (a4)          [async]
+ *   sun_plan_nnz     -> synchronises; nnz of Q0 / Q1 (16-byte readback)
+ *   caller allocates Q0 / Q1 CSR (row_ptr int64[M+1], col int32[nnz], val double[nnz]), K
+ *   sun_unfold       -> fill pass with fused K (a5), Q1 (a6)                     [async]
+ *   sun_apply        -> dv/dt = Q0 v + eps Q1 v + K (a7)                         [async]
+ */
+#ifndef SUNFOLD_H_
+#define SUNFOLD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SUN_OK = 0,
+  SUN_ERR_ARG = 1,           /* null / inconsistent pointers or sizes, malformed CSR        */
+  SUN_ERR_DIM = 2,           /* N < 2, N > 46340 (M must fit int32), operators of other N   */
+  SUN_ERR_NOT_HERMITIAN = 3, /* max|H - H^+| > 1e-12 ||H||_F for H0 or H1    */
+  SUN_ERR_RATE = 4,          /* gamma_p < 0 or non-finite                   */
+  SUN_ERR_CAPACITY = 5,      /* an output CSR capacity is below the required nnz            */
+  SUN_ERR_CUDA = 6,          /* CUDA runtime error; sun_status_string() reports it          */
+  SUN_ERR_BANDWIDTH = 7,     /* half-bandwidth beyond the banded kernels' limit  */
+  SUN_ERR_STATE = 8          /* call out of sequence (e.g. sun_unfold before sun_count)     */
+} sun_status;
+
+/* N x N complex operator, CSR, device memory.  row_ptr int64[n+1]; col int32[nnz], strictly
+ * ascending within a row, in [0, n); val = interleaved (re, im) float64[2*nnz]. */
+typedef struct {
+  int32_t n;
+  int64_t nnz;
+  const int64_t* row_ptr;
+  const int32_t* col;
+  const double* val;
+} sun_zcsr;
+
+/* M x M real output, CSR, device memory.  `nnz` is the CAPACITY of col/val on input.
+ * row_ptr int64[m+1]; col int32[capacity]; val float64[capacity]. */
+typedef struct {
+  int64_t m;
+  int64_t nnz;
+  int64_t* row_ptr;
+  int32_t* col;
+  double* val;
+} sun_dcsr;
+
+typedef struct sun_plan_s* sun_plan;
+
+/* Plan diagnostics (host struct filled by sun_plan_info). */
+typedef struct {
+  int32_t n, P;
+  int32_t w_h0, w_h1, w_l, w_k; /* half-bandwidths: H0, H1, max_p L_p, K = H0 + i/2 sum gamma L^+L */
+  double tau_q0, tau_q1;        /* drop thresholds (R6) */
+  int32_t mode_q0, mode_q1;     /* 0: thread-per-pair with shared-memory staging; 1: warp-per-pair */
+  int32_t pairs_per_tile_q0, pairs_per_tile_q1;
+  int64_t tiles_q0, tiles_q1;   /* number of row tiles (count/fill CTAs) */
+  int32_t has_h1;
+  int32_t npos_far_q0, npos_far_q1; /* candidate positions per far pair */
+} sun_plan_info_t;
+
+/* Bytes of device workspace a plan for dimension n with P dissipators needs (0 if n or P is
+ * out of range).  The workspace holds the band-expanded operators, the per-row counts
+ * (2 x 4 bytes per output row) and the tile offsets; it must be 256-byte aligned. */
+size_t sun_workspace_bytes(int32_t n, int32_t P);
+
+/* Validate the inputs and analyse their patterns (half-bandwidths, Frobenius norms) on the
+ * device, then build the plan.
+ *   H0: required.  H1: NULL if there is no periodic drive (then Q1 is not produced).
+ *   L: array of P pointers to operators (may be NULL if P == 0); gamma: HOST array of P rates.
+ *   workspace: device, >= sun_workspace_bytes(H0->n, P); owned by the caller, bound to the
+ *   plan until sun_plan_destroy.
+ * Runs one kernel on `stream` and synchronises on a small readback.  The input operators
+ * must stay valid until sun_count has completed on the stream (their values are read there;
+ * their patterns, i.e. bandwidths, are fixed by the plan).  Errors: SUN_ERR_DIM, _ARG (also
+ * malformed CSR: unsorted/out-of-range columns), _RATE, _BANDWIDTH, _CUDA; *out is NULL then. */
+int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const sun_zcsr* const* L,
+                    const double* gamma, int32_t P, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Expand H0/H1/L_p into band storage, form K = H0 + (i/2) sum_p gamma_p L_p^+ L_p, run the
+ * count pass and the prefix scan for Q0 (and Q1).  Asynchronous on `stream`. */
+int sun_count(sun_plan plan, void* stream);
+
+/* Synchronise the sun_count stream and return nnz(Q0) and nnz(Q1) (0 if no drive); reports
+ * SUN_ERR_NOT_HERMITIAN / SUN_ERR_ARG found by the device-side validation. */
+int sun_plan_nnz(sun_plan plan, int64_t* nnz_q0, int64_t* nnz_q1);
+
+/* Fill pass: write Q0 (CSR), K (float64[M]) and, if the plan has H1, Q1.  Q1 may be NULL
+ * only if the plan has no H1.  Capacities (nnz fields) must be >= sun_plan_nnz's values.
+ * Asynchronous on `stream`. */
+int sun_unfold(sun_plan plan, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream);
+
+/* dv/dt = Q0 v + eps Q1 v + K  (Eq. 9).  Q1 may be NULL; K may be NULL (= 0).
+ * v, dvdt: float64[M], must not alias.  Asynchronous on `stream`. */
+int sun_apply(const sun_dcsr* Q0, const sun_dcsr* Q1, double eps, const double* K, const double* v,
+              double* dvdt, void* stream);
+
+/* Fill a diagnostics struct for the plan. */
+int sun_plan_info(sun_plan plan, sun_plan_info_t* info);
+
+/* Free the host-side plan (it owns no device memory). */
+void sun_plan_destroy(sun_plan plan);
+
+/* Human-readable status (includes the last CUDA error text for SUN_ERR_CUDA). */
+const char* sun_status_string(int status);
+
+/* Canonical generator index (host helper, R5): kind 0 = S_ab, 1 = J_ab (a < b),
+ * 2 = D^l (a = l in [1, n-1], b ignored).  Returns -1 for invalid arguments. */
+int64_t sun_gen_index(int32_t n, int32_t kind, int32_t a, int32_t b);
+
+/* Library version string. */
+const char* sun_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SUNFOLD_H_ */

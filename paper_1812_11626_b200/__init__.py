@@ -1,0 +1,214 @@
+"""B200-native SU(N) unfold of the GKSL master equation (arXiv:1812.11626).
+
+Thin Python binding of the C-ABI in include/sunfold.h (argument marshalling only; every
+step of the path runs in the sm_100a kernels of libsunfold.so).  PyTorch provides device
+memory and streams.  There is no CPU fallback: if the CUDA library cannot be loaded the
+import of the ops raises.
+
+    plan = Plan(H0, H1, Ls, gammas)      # sun_plan_create (validation + pattern analysis)
+    Q0, Q1, K = plan.run()               # sun_count -> sun_plan_nnz -> sun_unfold
+    dvdt = apply(Q0, Q1, eps, K, v)      # sun_apply
+
+Operators are `DeviceZCSR` (torch CUDA tensors) or any object with `n, row_ptr, col, val`
+host arrays (e.g. workloads.ZCSR), which are copied to the device.
+Outputs are `CSR(row_ptr int64[M+1], col int32[nnz], val float64[nnz])` CUDA tensors and
+K float64[M].  Generator order and the stored-pattern rule are those of include/sunfold.h.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import NamedTuple, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+
+__all__ = ["CSR", "DeviceZCSR", "Plan", "unfold", "apply", "gen_index", "lib", "SunError"]
+
+
+class SunError(RuntimeError):
+    pass
+
+
+class CSR(NamedTuple):
+    row_ptr: torch.Tensor  # int64 [m+1]
+    col: torch.Tensor  # int32 [nnz]
+    val: torch.Tensor  # float64 [nnz]
+
+    @property
+    def m(self) -> int:
+        return int(self.row_ptr.shape[0] - 1)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.col.shape[0])
+
+
+class DeviceZCSR(NamedTuple):
+    n: int
+    row_ptr: torch.Tensor  # int64 [n+1] cuda
+    col: torch.Tensor  # int32 [nnz] cuda
+    val: torch.Tensor  # complex128 [nnz] cuda
+
+    @staticmethod
+    def from_host(A, device="cuda", non_blocking: bool = False) -> "DeviceZCSR":
+        def t(x, dt):
+            x = torch.as_tensor(np.ascontiguousarray(x))
+            if x.dtype != dt:
+                x = x.to(dt)
+            return x.to(device, non_blocking=non_blocking)
+
+        return DeviceZCSR(int(A.n), t(A.row_ptr, torch.int64), t(A.col, torch.int32), t(A.val, torch.complex128))
+
+
+def lib():
+    return _lib.load()
+
+
+def _check(status: int, what: str):
+    if status != 0:
+        raise SunError(f"{what}: {lib().sun_status_string(status).decode()} (status {status})")
+
+
+def _stream_handle(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _to_device(A) -> DeviceZCSR:
+    if isinstance(A, DeviceZCSR):
+        return A
+    return DeviceZCSR.from_host(A)
+
+
+def _zcsr_struct(A: DeviceZCSR) -> _lib.SunZCSR:
+    assert A.row_ptr.is_cuda and A.col.is_cuda and A.val.is_cuda
+    assert A.row_ptr.dtype == torch.int64 and A.col.dtype == torch.int32 and A.val.dtype == torch.complex128
+    return _lib.SunZCSR(int(A.n), int(A.col.shape[0]), A.row_ptr.data_ptr(), A.col.data_ptr(), A.val.data_ptr())
+
+
+def _dcsr_struct(Q: CSR) -> _lib.SunDCSR:
+    return _lib.SunDCSR(Q.m, Q.nnz, Q.row_ptr.data_ptr(), Q.col.data_ptr(), Q.val.data_ptr())
+
+
+def gen_index(n: int, kind: str, a: int, b: int = -1) -> int:
+    """Canonical generator index (R5): kind 'S', 'J' (a < b) or 'D' (a = l)."""
+    return int(lib().sun_gen_index(n, {"S": 0, "J": 1, "D": 2}[kind], a, b))
+
+
+class Plan:
+    """A validated, analysed unfold problem bound to a device workspace (sun_plan_create)."""
+
+    def __init__(self, H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), stream=None):
+        L = lib()
+        self.stream = stream
+        self.H0 = _to_device(H0)
+        self.H1 = _to_device(H1) if H1 is not None else None
+        self.Ls = [_to_device(x) for x in Ls]
+        self.gammas = np.ascontiguousarray(np.asarray(list(gammas), dtype=np.float64))
+        if len(self.Ls) != len(self.gammas):
+            raise ValueError("len(Ls) != len(gammas)")
+        self.n = self.H0.n
+        self.m = self.n * self.n - 1
+        self.P = len(self.Ls)
+        nbytes = int(L.sun_workspace_bytes(self.n, self.P))
+        if nbytes == 0:
+            _check(2, "sun_workspace_bytes")
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        self._s_h0 = _zcsr_struct(self.H0)
+        self._s_h1 = _zcsr_struct(self.H1) if self.H1 is not None else None
+        self._s_ls = [_zcsr_struct(x) for x in self.Ls]
+        arr = (ctypes.c_void_p * max(self.P, 1))()
+        for i, s in enumerate(self._s_ls):
+            arr[i] = ctypes.addressof(s)
+        self._arr = arr
+        plan = ctypes.c_void_p()
+        st = L.sun_plan_create(
+            ctypes.addressof(plan), ctypes.addressof(self._s_h0),
+            ctypes.addressof(self._s_h1) if self._s_h1 is not None else None,
+            ctypes.addressof(arr) if self.P else None,
+            self.gammas.ctypes.data_as(ctypes.c_void_p) if self.P else None,
+            self.P, ctypes.c_void_p(self.workspace.data_ptr()), ctypes.c_size_t(nbytes),
+            ctypes.c_void_p(_stream_handle(stream)))
+        _check(st, "sun_plan_create")
+        self._plan = plan
+
+    # -- the three phases ----------------------------------------------------------------
+    def count(self):
+        _check(lib().sun_count(self._plan, ctypes.c_void_p(_stream_handle(self.stream))), "sun_count")
+
+    def nnz(self):
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().sun_plan_nnz(self._plan, ctypes.addressof(a), ctypes.addressof(b)), "sun_plan_nnz")
+        return int(a.value), int(b.value)
+
+    def fill(self, nnz0: int, nnz1: int, out=None):
+        dev = self.workspace.device
+        if out is None:
+            Q0 = CSR(torch.empty(self.m + 1, dtype=torch.int64, device=dev),
+                     torch.empty(nnz0, dtype=torch.int32, device=dev),
+                     torch.empty(nnz0, dtype=torch.float64, device=dev))
+            Q1 = None
+            if self.H1 is not None:
+                Q1 = CSR(torch.empty(self.m + 1, dtype=torch.int64, device=dev),
+                         torch.empty(nnz1, dtype=torch.int32, device=dev),
+                         torch.empty(nnz1, dtype=torch.float64, device=dev))
+            K = torch.empty(self.m, dtype=torch.float64, device=dev)
+        else:
+            Q0, Q1, K = out
+        s0 = _dcsr_struct(Q0)
+        s1 = _dcsr_struct(Q1) if Q1 is not None else None
+        _check(lib().sun_unfold(self._plan, ctypes.addressof(s0), ctypes.addressof(s1) if s1 is not None else None,
+                                ctypes.c_void_p(K.data_ptr()), ctypes.c_void_p(_stream_handle(self.stream))),
+               "sun_unfold")
+        if out is not None:  # trim views to the produced nnz
+            Q0 = CSR(Q0.row_ptr, Q0.col[:nnz0], Q0.val[:nnz0])
+            if Q1 is not None:
+                Q1 = CSR(Q1.row_ptr, Q1.col[:nnz1], Q1.val[:nnz1])
+        return Q0, Q1, K
+
+    def run(self, out=None):
+        """count -> nnz readback -> allocate -> fill.  Returns (Q0, Q1 or None, K)."""
+        self.count()
+        nnz0, nnz1 = self.nnz()
+        return self.fill(nnz0, nnz1, out)
+
+    def info(self) -> dict:
+        inf = _lib.SunPlanInfo()
+        _check(lib().sun_plan_info(self._plan, ctypes.addressof(inf)), "sun_plan_info")
+        return {f: getattr(inf, f) for f, _ in _lib.SunPlanInfo._fields_}
+
+    def close(self):
+        if getattr(self, "_plan", None):
+            lib().sun_plan_destroy(self._plan)
+            self._plan = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def unfold(H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), stream=None):
+    """expand(H, {L_p, gamma_p}) -> (Q0 CSR, Q1 CSR or None, K), all on the GPU."""
+    plan = Plan(H0, H1, Ls, gammas, stream)
+    try:
+        return plan.run()
+    finally:
+        plan.close()
+
+
+def apply(Q0: CSR, Q1: Optional[CSR], eps: float, K: Optional[torch.Tensor], v: torch.Tensor,
+          out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """dv/dt = Q0 v + eps Q1 v + K (Eq. 9) via sun_apply."""
+    assert v.is_cuda and v.dtype == torch.float64 and v.shape[0] == Q0.m
+    y = out if out is not None else torch.empty_like(v)
+    s0 = _dcsr_struct(Q0)
+    s1 = _dcsr_struct(Q1) if Q1 is not None else None
+    _check(lib().sun_apply(ctypes.addressof(s0), ctypes.addressof(s1) if s1 is not None else None, ctypes.c_double(eps),
+                           ctypes.c_void_p(K.data_ptr()) if K is not None else None,
+                           ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(y.data_ptr()),
+                           ctypes.c_void_p(_stream_handle(stream))), "sun_apply")
+    return y

@@ -1,0 +1,197 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle O2.
+
+Bar (BASELINE.json north_star; R6/R7):
+  * CSR pattern (row_ptr, col) bit-exact;
+  * values: max |q_gpu - q_oracle| <= 1e-12 max |q_oracle| per matrix (normwise, R7),
+    and per-entry relative error <= 1e-12 on >= 99% of the entries;
+  * K: max |K_gpu - K_oracle| <= 1e-12 max(1, max |K_oracle|);
+  * bitwise determinism across runs; Q1 of a diagonal drive exactly skew-symmetric.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import basis, sparse
+from workloads import (ZCSR, banded_random_problem, config, dense_random_problem, dimer_problem)
+
+pytestmark = pytest.mark.gpu
+
+
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1812_11626_b200 as sun
+
+    return sun
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _compare_csr(gpu_csr, ref, name):
+    rp, col, val = _np(gpu_csr.row_ptr), _np(gpu_csr.col), _np(gpu_csr.val)
+    assert np.array_equal(rp, ref["row_ptr"]), f"{name}: row_ptr differs"
+    assert np.array_equal(col, ref["col"]), f"{name}: col differs"
+    if val.size == 0:
+        return 0.0
+    scale = np.abs(ref["val"]).max()
+    err = np.abs(val - ref["val"])
+    assert err.max() <= 1e-12 * scale, f"{name}: max err {err.max()} vs scale {scale}"
+    rel = err / np.abs(ref["val"])
+    assert np.mean(rel <= 1e-12) >= 0.99, f"{name}: per-entry rel err too large: {np.quantile(rel, 0.99)}"
+    return float(err.max() / scale)
+
+
+def _run(sun, prob):
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    Q0, Q1, K = plan.run()
+    torch.cuda.synchronize()
+    info = plan.info()
+    return plan, Q0, Q1, K, info
+
+
+def _check_problem(sun, prob, determinism=True):
+    ref = sparse.unfold_problem(prob)
+    tau0 = sparse.tau_q0(prob)
+    sparse.assert_gap(ref["Q0"], tau0, factor=100)
+    plan, Q0, Q1, K, info = _run(sun, prob)
+    assert abs(info["tau_q0"] - tau0) <= 1e-12 * tau0
+    _compare_csr(Q0, ref["Q0"], prob.name + ":Q0")
+    kref = ref["Q0"]["K"]
+    assert np.abs(_np(K) - kref).max() <= 1e-12 * max(1.0, np.abs(kref).max())
+    if prob.H1 is not None:
+        _compare_csr(Q1, ref["Q1"], prob.name + ":Q1")
+    else:
+        assert Q1 is None
+    if determinism:
+        Q0b, Q1b, Kb = plan.run()
+        torch.cuda.synchronize()
+        assert torch.equal(Q0.row_ptr, Q0b.row_ptr) and torch.equal(Q0.col, Q0b.col)
+        assert torch.equal(Q0.val, Q0b.val) and torch.equal(K, Kb)
+        if Q1 is not None:
+            assert torch.equal(Q1.val, Q1b.val)
+    plan.close()
+    return Q0, Q1, K, info
+
+
+SMALL = [
+    dense_random_problem(2, seed=1),
+    dense_random_problem(3, seed=2, P=2),
+    dense_random_problem(4, seed=0),
+    dense_random_problem(6, seed=3),
+    dense_random_problem(8, seed=5, P=3),
+    dimer_problem(2, True), dimer_problem(3, True), dimer_problem(5, True), dimer_problem(16, True),
+    dimer_problem(33, True), dimer_problem(130, True),
+    banded_random_problem(9, seed=4, wH=2, wL=1, P=2, drive_w=1),
+    banded_random_problem(20, seed=5),
+    banded_random_problem(64, seed=6),
+    banded_random_problem(97, seed=7, wH=1, wL=3, P=2),
+    banded_random_problem(150, seed=8, wH=5, wL=0, P=1, drive_w=2),
+    banded_random_problem(70, seed=9, wH=15, wL=7, P=1),
+]
+
+
+@pytest.mark.parametrize("prob", SMALL, ids=lambda p: p.name)
+def test_parity_small(prob):
+    sun = _gpu()
+    _check_problem(sun, prob)
+
+
+@pytest.mark.parametrize("idx", [0, 1, 2, 3, 4])
+def test_parity_baseline_configs(idx):
+    """Full element-by-element parity at every BASELINE.json config (c4 = N=1000, the bench case)."""
+    sun = _gpu()
+    prob = config(idx)
+    Q0, Q1, K, info = _check_problem(sun, prob, determinism=(idx == 4))
+    if Q1 is not None and idx in (2, 4):
+        # diagonal drive: Q1 exactly skew-symmetric, one entry per S/J row
+        rp, col, val = _np(Q1.row_ptr), _np(Q1.col), _np(Q1.val)
+        rows = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+        d = {(int(r), int(c)): v for r, c, v in zip(rows, col, val)}
+        for (r, c), v in d.items():
+            assert d[(c, r)] == -v
+
+
+def test_apply_matches_lindbladian_c4():
+    """Q(t) v + K from the GPU (sun_apply) equals proj L(t)(rho) for a random density matrix."""
+    sun = _gpu()
+    prob = config(4)
+    Q0, Q1, K = sun.unfold(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    rng = np.random.default_rng(4)
+    n = prob.n
+    B = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    rho = B @ B.conj().T
+    rho /= np.trace(rho)
+    v = basis.project(rho).real
+    eps = 1.0 + 1.5 * np.sin(0.3)
+    y = sun.apply(Q0, Q1, eps, K, torch.tensor(v, device="cuda"))
+    H = prob.H0.to_dense() + eps * prob.H1.to_dense()
+    L = prob.Ls[0].to_dense()
+    g = prob.gammas[0]
+    LdL = L.conj().T @ L
+    Lr = -1j * (H @ rho - rho @ H) + g * (L @ rho @ L.conj().T - 0.5 * (LdL @ rho + rho @ LdL))
+    ref = basis.project(Lr).real
+    assert np.abs(_np(y) - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_apply_against_oracle_spmv_c3():
+    sun = _gpu()
+    prob = config(3)
+    ref = sparse.unfold_problem(prob)["Q0"]
+    Q0, Q1, K = sun.unfold(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    v = np.random.default_rng(3).standard_normal(prob.m)
+    y = _np(sun.apply(Q0, None, 0.0, K, torch.tensor(v, device="cuda")))
+    rows = np.repeat(np.arange(prob.m), np.diff(ref["row_ptr"]))
+    yr = np.zeros(prob.m)
+    np.add.at(yr, rows, ref["val"] * v[ref["col"]])
+    yr += ref["K"]
+    assert np.abs(y - yr).max() <= 1e-12 * np.abs(yr).max()
+
+
+def test_edge_cases():
+    sun = _gpu()
+    n = 6
+    # H only (P = 0), no drive
+    p = dimer_problem(n, False)
+    p.Ls, p.gammas = [], []
+    _check_problem(sun, p)
+    # gamma = 0 -> same as H only
+    q = dimer_problem(n, False)
+    q.gammas = [0.0]
+    Q0a, _, Ka, _ = _check_problem(sun, q)
+    assert torch.count_nonzero(Ka) == 0
+    # zero Hamiltonian and no dissipator: empty Q0
+    z = ZCSR.from_dense(np.zeros((n, n), complex))
+    Q0, Q1, K = sun.unfold(z, None, [], [])
+    assert Q0.nnz == 0 and int(Q0.row_ptr[-1]) == 0 and torch.count_nonzero(K) == 0
+    # pure dissipation (H = 0) with a traceful L
+    rng = np.random.default_rng(1)
+    L = rng.standard_normal((5, 5)) + 1j * rng.standard_normal((5, 5))
+    from workloads import Problem
+    pd = Problem("pure_diss", 5, ZCSR.from_dense(np.zeros((5, 5), complex)), None, [ZCSR.from_dense(L)], [0.4])
+    _check_problem(sun, pd)
+
+
+def test_error_codes():
+    sun = _gpu()
+    rng = np.random.default_rng(0)
+    A = rng.standard_normal((5, 5)) + 1j * rng.standard_normal((5, 5))
+    with pytest.raises(sun.SunError, match="Hermitian"):
+        sun.unfold(ZCSR.from_dense(A), None, [], [])  # not Hermitian
+    H = ZCSR.from_dense(A + A.conj().T)
+    with pytest.raises(sun.SunError, match="rate"):
+        sun.Plan(H, None, [ZCSR.from_dense(A)], [-0.1])
+    big = banded_random_problem(60, seed=1, wH=16, wL=0, P=0)
+    with pytest.raises(sun.SunError, match="bandwidth"):
+        sun.Plan(big.H0, None, [], [])
+    p = dimer_problem(8, True)
+    plan = sun.Plan(p.H0, p.H1, p.Ls, p.gammas)
+    plan.count()
+    nnz0, nnz1 = plan.nnz()
+    with pytest.raises(sun.SunError, match="capacity"):
+        plan.fill(nnz0 - 1, nnz1)
+    other = dimer_problem(9, False)
+    with pytest.raises(sun.SunError, match="dimension"):
+        sun.Plan(p.H0, None, other.Ls, other.gammas)
+    plan.close()
