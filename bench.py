@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark of the SU(N) unfold hot path (BASELINE.json metric) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+A step is one full unfold of the BASELINE workload (default configs[4]: the driven
+Bose-Hubbard dimer at N = 1000, M = 999 999): the public call expand(H0, H1, {L_p, gamma_p})
+-> (Q0 CSR, Q1 CSR, K) = sun_plan_create (pattern analysis) + sun_count (expand, count
+pass, prefix scan) + sun_plan_nnz (16-byte readback) + output allocation + sun_unfold
+(fill pass with K, and Q1).  Inputs are resident in HBM when a timed step starts; L2 is
+flushed (a 512 MiB write) between timed steps, outside the per-step CUDA events.
+
+value = (nnz(Q0) + nnz(Q1)) x ranks / max-over-ranks(mean step time)   [nnz/s]
+Multi-GPU: replicas only: every rank unfolds its own copy; there is
+no data-path collective.  `--impl reference` times the CPU oracle (oracle/sparse_o2.c) on the
+host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Q nonzeros assembled/sec (fp64) and unfold wall time at N=1000; % HBM roofline"
+UNIT = "nnz/s"
+LAUNCHES_PER_STEP = {"plan": 1, "count": 5, "count_q1": 2, "fill": 1, "fill_q1": 1}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------------------
+# distributed plumbing (replicas only)
+# ---------------------------------------------------------------------------------------
+def dist_init(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._thr = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._thr = threading.Thread(target=self._run, daemon=True)
+        self._thr.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thr:
+            self._thr.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for nm, v in zip(names, r[4:8]):
+                if v.strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------------------
+# CPU baseline: the oracle (O2) as it stands
+# ---------------------------------------------------------------------------------------
+def cpu_oracle_run(prob, reps: int = 1):
+    from oracle import sparse
+
+    times = []
+    nnz = 0
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        r = sparse.unfold_problem(prob)
+        times.append(time.perf_counter() - t0)
+        nnz = len(r["Q0"]["col"]) + (len(r["Q1"]["col"]) if "Q1" in r else 0)
+    return nnz, times, sparse.max_threads()
+
+
+def cpu_baseline(prob, reps: int = 2):
+    nnz, times, cores = cpu_oracle_run(prob, reps)
+    t = statistics.mean(times)
+    return {"value": nnz / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{reps} full unfolds (Q0+K+Q1) of {prob.name} by oracle O2 (oracle/sparse_o2.c, "
+                      f"OpenMP, column-wise trace definition); mean {t:.3f} s each",
+            "seconds_per_unfold": t}
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host cores, same metric/config (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from workloads import CONFIG_NAMES, config
+
+    prob = config(args.config)
+    for _ in range(args.warmup):
+        cpu_oracle_run(prob, 1)
+    nnz, times, cores = cpu_oracle_run(prob, args.steps)
+    t = statistics.mean(times)
+    v = nnz / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_NAMES[args.config], "N": prob.n, "M": prob.m, "nnz_total": nnz},
+        "cpu_baseline": {"value": v, "unit": UNIT, "kind": "oracle", "cores": cores,
+                         "sample": f"{args.steps} full unfolds of {prob.name} by oracle O2 (sparse_o2.c)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+    import torch
+
+    rank, world, local = dist_init(args)
+    torch.cuda.set_device(local)
+    import paper_1812_11626_b200 as sun
+    from workloads import CONFIG_NAMES, config
+
+    prob = config(args.config)
+    stream = torch.cuda.current_stream()
+    H0 = sun.DeviceZCSR.from_host(prob.H0)
+    H1 = sun.DeviceZCSR.from_host(prob.H1) if prob.H1 is not None else None
+    Ls = [sun.DeviceZCSR.from_host(x) for x in prob.Ls]
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def one_step(timing):
+        e0, e1, e2, e3 = ev(), ev(), ev(), ev()
+        e0.record(stream)
+        plan = sun.Plan(H0, H1, Ls, prob.gammas)           # pattern analysis (1 readback)
+        plan.count()                                        # expand + count + scan
+        e1.record(stream)
+        nnz0, nnz1 = plan.nnz()                             # 16-byte readback
+        e2.record(stream)
+        Q0, Q1, K = plan.fill(nnz0, nnz1)                   # allocate + fill pass (+K, Q1)
+        e3.record(stream)
+        timing.append((e0, e1, e2, e3))
+        plan.close()
+        return nnz0 + nnz1, (Q0, Q1, K)
+
+    for _ in range(args.warmup):
+        nnz_total, _ = one_step([])
+    torch.cuda.synchronize()
+
+    timings = []
+    keep = []
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        t_wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.fill_(1.0)  # L2 flush (512 MiB > 126 MB L2), outside the step events
+            nnz_total, out = one_step(timings)
+            keep.append(out)
+            if len(keep) > 2:
+                keep.pop(0)
+        torch.cuda.synchronize()
+        t_wall = time.perf_counter() - t_wall0
+    barrier(world)
+    torch.cuda.synchronize()
+    step_ms = [e0.elapsed_time(e3) for e0, e1, e2, e3 in timings]
+    count_ms = [e0.elapsed_time(e1) for e0, e1, e2, e3 in timings]
+    fill_ms = [e2.elapsed_time(e3) for e0, e1, e2, e3 in timings]
+    ms_local = statistics.mean(step_ms)
+    ms = max_over_ranks(ms_local, world)
+    fill_mean = max_over_ranks(statistics.mean(fill_ms), world)
+    value = nnz_total * world / (ms * 1e-3)
+
+    # roofline of the dominant kernel: the fill pass (k_fill for Q0 and Q1 in sun_unfold)
+    Q0, Q1, K = keep[-1]
+    m = prob.m
+    fill_bytes = (8 * (m + 1) + 12 * Q0.nnz + 8 * m) + ((8 * (m + 1) + 12 * Q1.nnz) if Q1 is not None else 0)
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    # isolated fill-pass timing (steady state, inputs counted): repeat the fill on one plan
+    plan = sun.Plan(H0, H1, Ls, prob.gammas)
+    plan.count()
+    n0, n1 = plan.nnz()
+    outs = plan.fill(n0, n1)
+    iso = []
+    for _ in range(max(5, args.steps)):
+        flush.fill_(1.0)
+        a, b = ev(), ev()
+        a.record(stream)
+        plan.fill(n0, n1, out=outs)
+        b.record(stream)
+        iso.append((a, b))
+    torch.cuda.synchronize()
+    iso_ms = statistics.mean([a.elapsed_time(b) for a, b in iso])
+    # count phase alone (expand + count + scan), device time
+    cnt_ev = []
+    for _ in range(max(5, args.steps)):
+        flush.fill_(1.0)
+        a, b = ev(), ev()
+        a.record(stream)
+        plan.count()
+        b.record(stream)
+        cnt_ev.append((a, b))
+    torch.cuda.synchronize()
+    count_dev_ms = statistics.mean([a.elapsed_time(b) for a, b in cnt_ev])
+    info = plan.info()
+    plan.close()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "fill_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    achieved = fill_bytes / (iso_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "peak_source": peak_src, "kernel": "k_fill (sun_unfold: Q0 + K + Q1)",
+                "algorithmic_bytes_per_launch": fill_bytes, "launch_ms": iso_ms,
+                "fill_ms_in_step": fill_mean}
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        import numpy as np
+
+        def pin(x, dt):
+            return torch.as_tensor(np.ascontiguousarray(x)).to(dt).pin_memory()
+
+        hostH0 = (pin(prob.H0.row_ptr, torch.int64), pin(prob.H0.col, torch.int32), pin(prob.H0.val, torch.complex128))
+        hostH1 = (pin(prob.H1.row_ptr, torch.int64), pin(prob.H1.col, torch.int32),
+                  pin(prob.H1.val, torch.complex128)) if prob.H1 is not None else None
+        hostLs = [(pin(x.row_ptr, torch.int64), pin(x.col, torch.int32), pin(x.val, torch.complex128)) for x in prob.Ls]
+        h2d = sum(t.numel() * t.element_size() for grp in [hostH0] + ([hostH1] if hostH1 else []) + hostLs
+                  for t in grp)
+        host_out = None
+
+        def e2e_step():
+            nonlocal host_out
+            dev = lambda g, n: sun.DeviceZCSR(n, *(t.to("cuda", non_blocking=True) for t in g))  # noqa: E731
+            q0, q1, k = sun.unfold(dev(hostH0, prob.n), dev(hostH1, prob.n) if hostH1 else None,
+                                   [dev(x, prob.n) for x in hostLs], prob.gammas)
+            outs_ = [q0.row_ptr, q0.col, q0.val, k] + ([q1.row_ptr, q1.col, q1.val] if q1 is not None else [])
+            if host_out is None or [h.numel() for h in host_out] != [t.numel() for t in outs_]:
+                host_out = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs_]
+            for h, t in zip(host_out, outs_):
+                h.copy_(t, non_blocking=True)
+            torch.cuda.synchronize()
+            return sum(t.numel() * t.element_size() for t in outs_), q0.nnz + (q1.nnz if q1 is not None else 0)
+
+        for _ in range(3):
+            e2e_step()
+        ts = []
+        for _ in range(max(3, min(args.steps, 10))):
+            t0 = time.perf_counter()
+            d2h, nz = e2e_step()
+            ts.append(time.perf_counter() - t0)
+        t_e2e = max_over_ranks(statistics.mean(ts), world)
+        e2e = {"value": nz * world / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": t_e2e * 1e3,
+               "note": "sun.unfold() on host (pinned) CSR inputs; full Q0/Q1/K copied back to pinned host memory"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(prob)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CONFIG_NAMES[args.config], "N": prob.n, "M": prob.m, "P": len(prob.Ls),
+                   "nnz_q0": int(Q0.nnz), "nnz_q1": int(Q1.nnz) if Q1 is not None else 0,
+                   "l2": "flushed between timed steps (512 MiB write, outside step events)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                   "step": "sun_plan_create + sun_count + sun_plan_nnz + alloc + sun_unfold"},
+        "unfold_wall_ms": ms,
+        "phases_ms": {"plan+count (host-visible)": max_over_ranks(statistics.mean(count_ms), world),
+                      "count device (expand+count+scan)": count_dev_ms, "fill in step": fill_mean,
+                      "fill isolated": iso_ms},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": args.steps * (LAUNCHES_PER_STEP["plan"] + LAUNCHES_PER_STEP["count"] + LAUNCHES_PER_STEP["fill"]
+                                      + ((LAUNCHES_PER_STEP["count_q1"] + LAUNCHES_PER_STEP["fill_q1"]) if prob.H1 else 0)),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "plan": {k: info[k] for k in ("w_h0", "w_l", "w_k", "mode_q0", "npos_far_q0", "tiles_q0")},
+        "wall_s_timed_region": t_wall,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
