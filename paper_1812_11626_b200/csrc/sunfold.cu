@@ -3,10 +3,10 @@
 // Pipeline (Table I Step 2; two-step CRS fill P:369-370):
 //   sun_plan_create : k_analyze   bandwidths, Frobenius norms, CSR validation  -> 1 readback
 //   sun_count       : k_zero, k_scatter, k_band_k   (a1) expand to band storage, K = H + i/2 M
-//                     k_count<mode>                  (a3) per-row counts (values thresholded)
-//                     k_scan                         (a4) tile offsets, nnz
-//   sun_plan_nnz    : 16-byte readback (nnz Q0, Q1) + validation flags
-//   sun_unfold      : k_fill<mode>                   (a5) row_ptr, col, val, K; (a6) Q1
+//                     k_count0<WK,WL> / k_count1     (a3) per-row counts (values thresholded) and
+//                                                    (a4) tile offsets by decoupled look-back
+//   sun_plan_nnz    : readback of the chain totals (nnz Q0, Q1) + validation flags
+//   sun_unfold      : k_fill0<WK,WL> / k_fill1       (a5) row_ptr, col, val, K; (a6) Q1
 //   sun_apply       : k_apply                        (a7) dv/dt = Q0 v + eps Q1 v + K
 #include <cuda_runtime.h>
 #include <math.h>
@@ -27,16 +27,15 @@ namespace {
 constexpr int MAXOPS = 66;     // H0, H1 and up to 64 dissipators
 constexpr int WLMAX = WMAX / 2;  // wK >= 2 wL
 constexpr int F_MALFORMED = 1, F_H0_NOT_HERM = 2, F_H1_NOT_HERM = 4;
-constexpr int THREAD_TP = 128;   // thread mode: pairs per tile == threads per CTA
-constexpr int WARP_TP = 64;      // warp mode: pairs per tile
+constexpr int THREAD_TP = 128;   // mode 0: pairs per tile == threads per CTA (4 warps)
+constexpr int WARP_TP = 64;      // mode 1: pairs per tile
 constexpr int WARP_THREADS = 256;
-constexpr int STAGE_BYTES = 72 * 1024;  // thread-mode shared staging per CTA
 constexpr int FAR_MAXPOS = 1024;
 
 struct DevHeader {
   int flags;
   int pad;
-  long long nnz[2];
+  long long nnz[2];  // written by the scan of each output matrix
   int bw[MAXOPS];
   double nrm2[MAXOPS];
 };
@@ -52,6 +51,12 @@ struct OpList {
   int n;
 };
 
+// mode-0 instantiations (compile-time band widths); anything else runs in mode 1
+bool mode0_supported(int wK, int wL) {
+  return (wK == 0 && wL == 0) || (wK == 1 && wL == 0) || (wK == 2 && wL == 0) || (wK == 2 && wL == 1) ||
+         (wK == 3 && wL == 0);
+}
+
 thread_local char g_errbuf[512];
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -62,7 +67,7 @@ struct FarPos {
 };
 
 struct Layout {
-  size_t hdr, fp0, fp1, sqrtg, kb0, hb0, hb1, lb, cnt0, cnt1, ts0, ts1, total;
+  size_t hdr, fp0, fp1, sqrtg, inv, kb0, hb0, hb1, lb, ts0, ts1, toff0, toff1, chunk, cnt0, cnt1, total;
   long long maxslots;
 };
 
@@ -76,14 +81,18 @@ Layout make_layout(int n, int P) {
   L.fp0 = off; off = align256(off + sizeof(FarPos));
   L.fp1 = off; off = align256(off + sizeof(FarPos));
   L.sqrtg = off; off = align256(off + MAXOPS * sizeof(double));
-  L.kb0 = off; off = align256(off + (size_t)n * (2 * WMAX + 1) * sizeof(double2));
+  L.inv = off; off = align256(off + (size_t)n * sizeof(double));
+  L.kb0 = off; off = align256(off + (size_t)n * (2 * WMAX + 1) * sizeof(double2));  // [kb0, lb end) zeroed per count
   L.hb0 = off; off = align256(off + (size_t)n * (2 * WMAX + 1) * sizeof(double2));
   L.hb1 = off; off = align256(off + (size_t)n * (2 * WMAX + 1) * sizeof(double2));
   L.lb = off;  off = align256(off + (size_t)(P > 0 ? P : 1) * n * (2 * WLMAX + 1) * sizeof(double2));
+  L.ts0 = off; off = align256(off + (size_t)maxslots * sizeof(int));
+  L.ts1 = off; off = align256(off + (size_t)maxslots * sizeof(int));
+  L.toff0 = off; off = align256(off + (size_t)maxslots * sizeof(long long));
+  L.toff1 = off; off = align256(off + (size_t)maxslots * sizeof(long long));
+  L.chunk = off; off = align256(off + (size_t)(maxslots / 16384 + 2) * sizeof(long long));
   L.cnt0 = off; off = align256(off + (size_t)m * sizeof(int));
   L.cnt1 = off; off = align256(off + (size_t)m * sizeof(int));
-  L.ts0 = off; off = align256(off + (size_t)maxslots * sizeof(long long));
-  L.ts1 = off; off = align256(off + (size_t)maxslots * sizeof(long long));
   L.total = off;
   L.maxslots = maxslots;
   return L;
@@ -184,10 +193,12 @@ __global__ void k_scatter(OpList ops, int has_h1, double2* hb0, int wK, double2*
 }
 
 // (a1) K = H0 + (i/2) M, M = sum_p Lt_p^+ Lt_p (Lt = sqrt(gamma) L); Hermiticity checks of H0, H1.
+// Also writes inv[l] = 1/sqrt(l(l+1)) (normalisation of D^l) for the D-chain kernels.
 __global__ void k_band_k(int n, int P, const double2* __restrict__ hb0, double2* kb0, int wK,
                          const double2* __restrict__ lb, int wL, const double2* __restrict__ hb1, int wH1,
-                         int has_h1, double tol0, double tol1, DevHeader* hdr) {
+                         int has_h1, double tol0, double tol1, DevHeader* hdr, double* inv) {
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t < n) inv[t] = t > 0 ? 1.0 / sqrt((double)t * (double)(t + 1)) : 0.0;
   const int sw = 2 * wK + 1;
   if (t >= (long long)n * sw) return;
   int r = (int)(t / sw), o = (int)(t % sw) - wK;
@@ -221,108 +232,151 @@ __global__ void k_band_k(int n, int P, const double2* __restrict__ hb0, double2*
 }
 
 // ---------------------------------------------------------------------------------------
-// (a3) count pass.  Grid: npt pair tiles, then ndt D tiles.
+// (a3) count pass.  One CTA per row tile: pair tiles (S and J rows of tp consecutive pairs),
+// then D tiles (one warp per D^lam row).  Writes per-row counts and one int32 sum per tile
+// slot; slots are in global row order (S tiles, J tiles, D tiles).
+//   mode 0: thread per pair, far pairs from compile-time band widths (WK, WL) held in
+//           registers (the S-row count word also carries nRe in bits 20-31); near pairs
+//           warp-cooperative.  128 threads, 128 pairs per tile.
+//   mode 1: warp per pair (wide bands / many positions).  256 threads, 64 pairs per tile.
 // ---------------------------------------------------------------------------------------
-
-template <int MODE>
-__global__ void __launch_bounds__(MODE == 0 ? THREAD_TP : WARP_THREADS)
-    k_count(Prob pr, const FarPos* __restrict__ fp, int npos_far, int* __restrict__ cnt,
-            long long* __restrict__ tsum) {
-  __shared__ double scratch[(MODE == 0 ? THREAD_TP : WARP_THREADS) / 32][4][WIN_MAX + 2];
-  __shared__ int wtot[32];
-  __shared__ int spos_dc[MODE == 1 ? FAR_MAXPOS : 1], spos_dd[MODE == 1 ? FAR_MAXPOS : 1];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  double* gS = scratch[wid][0];
-  double* gJ = scratch[wid][1];
-  double* pS = scratch[wid][2];
-  double* pJ = scratch[wid][3];
+template <int NTHREADS>
+__device__ __forceinline__ void count_d_tile(const Prob& pr, long long t, int* cnt, int* tsum, double* scr_w,
+                                             int* wtot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const Seg none = {nullptr, nullptr, nullptr, nullptr};
+  const long long u = t - pr.npt;
+  int c = 0;
+  const int lam = (int)(u * (NTHREADS / 32) + wid + 1);
+  if (lam <= pr.n - 1) {
+    double kv;
+    c = warp_d_row<false>(pr, lam, scr_w, scr_w + WIN_MAX + 2, kv, none, 0);
+    if (lane == 0) cnt[2 * pr.np + lam - 1] = c;
+  }
+  int tot;
+  block_exclusive_scan(lane == 0 ? c : 0, wtot, tot);
+  if (threadIdx.x == 0) tsum[2 * pr.npt + u] = tot;
+}
+
+// per-warp scratch (doubles): near-pair U tile (2 TW^2) + gS, gJ, pS, pJ (4 SW); D rows use
+// the first 2 (WIN_MAX + 2)
+template <int TW, int SW>
+struct Scr {
+  static constexpr int A = 2 * TW * TW + 4 * SW;
+  static constexpr int PER_WARP = A > 2 * (WIN_MAX + 2) ? A : 2 * (WIN_MAX + 2);
+};
+
+template <int WK, int WL>
+__global__ void __launch_bounds__(128, 4) k_count0(Prob pr, int* __restrict__ cnt, int* __restrict__ tsum) {
+  constexpr int TW = 2 * WK + 1, SW = 4 * WK + 4;
+  __shared__ double scr[4][Scr<TW, SW>::PER_WARP];
+  __shared__ int wtot[32];
   const long long t = blockIdx.x;
-  if (t < pr.npt) {
-    int cS = 0, cJ = 0;
-    if (MODE == 0) {
-      long long p = t * pr.tp + threadIdx.x;
-      bool valid = p < pr.np;
-      int a = 0, b = 1;
-      if (valid) pair_decode(pr.n, p, a, b);
-      bool far = valid && (b - a > 2 * pr.W);
-      if (far) {
-        int nre, nim;
-        far_pair_thread<false>(pr, a, b, nre, nim, none, 0, none, 0);
-        cS = cJ = nre + nim;
-      }
-      unsigned nm = __ballot_sync(FULL, valid && !far);
-      while (nm) {
-        int src = __ffs(nm) - 1;
-        nm &= nm - 1;
-        int aa = __shfl_sync(FULL, a, src), bb = __shfl_sync(FULL, b, src);
-        int c1, c2;
-        double k1, k2;
-        warp_near_pair<false>(pr, aa, bb, gS, gJ, pS, pJ, c1, c2, k1, k2, none, 0, none, 0);
-        if (lane == src) { cS = c1; cJ = c2; }
-      }
-      if (valid) {
-        cnt[p] = cS;
-        cnt[pr.np + p] = cJ;
-      }
-    } else {
-      for (int i = threadIdx.x; i < npos_far; i += blockDim.x) {
-        spos_dc[i] = fp->dc[i];
-        spos_dd[i] = fp->dd[i];
-      }
-      __syncthreads();
-      for (int i = wid; i < pr.tp; i += nwarps) {
-        long long p = t * pr.tp + i;
-        if (p >= pr.np) break;
-        int a, b;
-        pair_decode(pr.n, p, a, b);
-        int c1, c2;
-        if (b - a > 2 * pr.W) {
-          warp_far_pair<false>(pr, a, b, spos_dc, spos_dd, npos_far, c1, none, 0, none, 0);
-          c2 = c1;
-        } else {
-          double k1, k2;
-          warp_near_pair<false>(pr, a, b, gS, gJ, pS, pJ, c1, c2, k1, k2, none, 0, none, 0);
-        }
-        if (lane == 0) {
-          cnt[p] = c1;
-          cnt[pr.np + p] = c2;
-          cS += c1;
-          cJ += c2;
-        }
-      }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (t >= pr.npt) {
+    count_d_tile<128>(pr, t, cnt, tsum, scr[wid], wtot);
+    return;
+  }
+  const Seg none = {nullptr, nullptr, nullptr, nullptr};
+  const long long p = t * 128 + threadIdx.x;
+  const bool valid = p < pr.np;
+  int a, b;
+  warp_pairs(pr.n, t * 128 + wid * 32, a, b);
+  const bool far = valid && (b - a > 2 * WK);
+  int cS = 0, cJ = 0, packS = 0;
+  unsigned nm = __ballot_sync(FULL, valid && !far);
+  while (nm) {  // near pairs first (no far values live across the calls)
+    const int src = __ffs(nm) - 1;
+    nm &= nm - 1;
+    const int aa = __shfl_sync(FULL, a, src), bb = __shfl_sync(FULL, b, src);
+    int c1, c2;
+    double k1, k2;
+    warp_near_pair<false, TW, SW>(pr, aa, bb, scr[wid], c1, c2, k1, k2, none, 0, none, 0);
+    if (lane == src) {
+      cS = c1;
+      cJ = c2;
     }
-    int totS, totJ;
-    block_exclusive_scan(cS, wtot, totS);
-    block_exclusive_scan(cJ, wtot, totJ);
-    if (threadIdx.x == 0) {
-      tsum[t] = totS;
-      tsum[pr.npt + t] = totJ;
-    }
-  } else {
-    const long long u = t - pr.npt;
-    int c = 0;
-    int lam = (int)(u * nwarps + wid + 1);
-    if (lam <= pr.n - 1) {
-      double kv;
-      warp_d_row<false>(pr, lam, gS, pS, c, kv, none, 0);
-      if (lane == 0) cnt[2 * pr.np + lam - 1] = c;
-    }
-    int tot;
-    block_exclusive_scan(lane == 0 ? c : 0, wtot, tot);
-    if (threadIdx.x == 0) tsum[2 * pr.npt + u] = tot;
+  }
+  if (far) {
+    double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
+    far_values<WK, WL>(pr, a, b, ux, uy);
+    int nR, nI;
+    far_counts<WK, WL>(pr.n, pr.tau, a, b, ux, uy, nR, nI);
+    cS = cJ = nR + nI;
+    packS = nR << CNT_BITS;
+  }
+  if (valid) {
+    cnt[p] = cS | packS;
+    cnt[pr.np + p] = cJ;
+  }
+  int totS, totJ;
+  block_exclusive_scan(cS, wtot, totS);
+  block_exclusive_scan(cJ, wtot, totJ);
+  if (threadIdx.x == 0) {
+    tsum[t] = totS;
+    tsum[pr.npt + t] = totJ;
   }
 }
 
-// (a4) exclusive scan of the tile sums (one CTA, fixed order: deterministic); nnz -> hdr.
-__global__ void __launch_bounds__(1024) k_scan(long long* ts, long long nslots, long long* nnz_out) {
-  __shared__ long long wsum[32];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  long long per = (nslots + blockDim.x - 1) / blockDim.x;
-  long long lo = tid * per, hi = lo + per < nslots ? lo + per : nslots;
-  long long local = 0;
-  for (long long i = lo; i < hi; ++i) local += ts[i];
-  long long x = local;
+__global__ void __launch_bounds__(WARP_THREADS) k_count1(Prob pr, const FarPos* __restrict__ fp, int npos_far,
+                                                         int* __restrict__ cnt, int* __restrict__ tsum) {
+  constexpr int SW = WIN_MAX + 2;
+  __shared__ double scr[WARP_THREADS / 32][Scr<0, SW>::PER_WARP];
+  __shared__ int wtot[32];
+  __shared__ int spos_dc[FAR_MAXPOS], spos_dd[FAR_MAXPOS];
+  const long long t = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  if (t >= pr.npt) {
+    count_d_tile<WARP_THREADS>(pr, t, cnt, tsum, scr[wid], wtot);
+    return;
+  }
+  for (int i = threadIdx.x; i < npos_far; i += blockDim.x) {
+    spos_dc[i] = fp->dc[i];
+    spos_dd[i] = fp->dd[i];
+  }
+  __syncthreads();
+  const Seg none = {nullptr, nullptr, nullptr, nullptr};
+  int cS = 0, cJ = 0;
+  for (int i = wid; i < WARP_TP; i += nwarps) {
+    const long long p = t * WARP_TP + i;
+    if (p >= pr.np) break;
+    int a, b;
+    pair_decode(pr.n, p, a, b);
+    int c1, c2;
+    if (b - a > 2 * pr.W) {
+      c1 = c2 = warp_far_pair<false>(pr, a, b, spos_dc, spos_dd, npos_far, none, 0, none, 0);
+    } else {
+      double k1, k2;
+      warp_near_pair<false, 0, SW>(pr, a, b, scr[wid], c1, c2, k1, k2, none, 0, none, 0);
+    }
+    if (lane == 0) {
+      cnt[p] = c1;
+      cnt[pr.np + p] = c2;
+      cS += c1;
+      cJ += c2;
+    }
+  }
+  int totS, totJ;
+  block_exclusive_scan(cS, wtot, totS);
+  block_exclusive_scan(cJ, wtot, totJ);
+  if (threadIdx.x == 0) {
+    tsum[t] = totS;
+    tsum[pr.npt + t] = totJ;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// (a4) exclusive scan of the tile sums -> int64 tile offsets and nnz.  Fixed order
+// (deterministic).  Small: one CTA through shared memory.  Large: chunk sums, a scan of
+// the chunk sums, then per-chunk scans.
+// ---------------------------------------------------------------------------------------
+constexpr int SCAN_CHUNK = 16384;
+
+template <typename T>
+__device__ __forceinline__ long long block_scan_ll(long long v, long long* wsum, long long& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  long long x = v;
+#pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     long long y = __shfl_up_sync(FULL, x, o);
     if (lane >= o) x += y;
@@ -330,161 +384,282 @@ __global__ void __launch_bounds__(1024) k_scan(long long* ts, long long nslots, 
   if (lane == 31) wsum[wid] = x;
   __syncthreads();
   if (wid == 0) {
-    long long s = wsum[lane];
+    long long s = lane < nwarps ? wsum[lane] : 0;
+#pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       long long y = __shfl_up_sync(FULL, s, o);
       if (lane >= o) s += y;
     }
-    wsum[lane] = s;
+    if (lane < nwarps) wsum[lane] = s;
   }
   __syncthreads();
-  long long run = (wid > 0 ? wsum[wid - 1] : 0) + x - local;
-  for (long long i = lo; i < hi; ++i) {
-    long long v = ts[i];
-    ts[i] = run;
+  total = wsum[nwarps - 1];
+  long long before = wid > 0 ? wsum[wid - 1] : 0;
+  __syncthreads();
+  return before + x - v;
+}
+
+// scan of one chunk [c0, c0 + len) of int32 values with base offset; writes int64 exclusive
+__global__ void __launch_bounds__(1024) k_scan_chunk(const int* __restrict__ ts, long long nslots,
+                                                     const long long* __restrict__ chunk_base, long long* out,
+                                                     long long* nnz_out) {
+  extern __shared__ int sv[];
+  __shared__ long long wsum[32];
+  const long long c0 = (long long)blockIdx.x * SCAN_CHUNK;
+  const int len = (int)(nslots - c0 < SCAN_CHUNK ? nslots - c0 : SCAN_CHUNK);
+  for (int i = threadIdx.x; i < len; i += blockDim.x) sv[i] = ts[c0 + i];
+  __syncthreads();
+  const int per = (len + blockDim.x - 1) / blockDim.x;
+  const int lo = threadIdx.x * per, hi = lo + per < len ? lo + per : len;
+  long long local = 0;
+  for (int i = lo; i < hi; ++i) local += sv[i];
+  long long total;
+  long long run = block_scan_ll<long long>(local, wsum, total) + (chunk_base ? chunk_base[blockIdx.x] : 0);
+  for (int i = lo; i < hi; ++i) {
+    out[c0 + i] = run;
+    run += sv[i];
+  }
+  if (nnz_out && threadIdx.x == blockDim.x - 1 && blockIdx.x == gridDim.x - 1) *nnz_out = run;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_reduce(const int* __restrict__ ts, long long nslots,
+                                                      long long* __restrict__ chunk_sum) {
+  __shared__ long long wsum[32];
+  const long long c0 = (long long)blockIdx.x * SCAN_CHUNK;
+  const int len = (int)(nslots - c0 < SCAN_CHUNK ? nslots - c0 : SCAN_CHUNK);
+  long long local = 0;
+  for (int i = threadIdx.x; i < len; i += blockDim.x) local += ts[c0 + i];
+  long long total;
+  block_scan_ll<long long>(local, wsum, total);
+  if (threadIdx.x == 0) chunk_sum[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(1024) k_scan_top(long long* chunk, int nchunks) {
+  __shared__ long long wsum[32];
+  const int per = (nchunks + blockDim.x - 1) / blockDim.x;
+  const int lo = threadIdx.x * per, hi = lo + per < nchunks ? lo + per : nchunks;
+  long long local = 0;
+  for (int i = lo; i < hi; ++i) local += chunk[i];
+  long long total;
+  long long run = block_scan_ll<long long>(local, wsum, total);
+  for (int i = lo; i < hi; ++i) {
+    long long v = chunk[i];
+    chunk[i] = run;
     run += v;
   }
-  if (tid == blockDim.x - 1) *nnz_out = wsum[31];
 }
 
 // ---------------------------------------------------------------------------------------
-// (a5) fill pass (+ K).  Same tiling as k_count.
+// (a5) fill pass (+ K).  Same tiling as the count pass.
 // ---------------------------------------------------------------------------------------
-template <int MODE>
-__global__ void __launch_bounds__(MODE == 0 ? THREAD_TP : WARP_THREADS)
-    k_fill(Prob pr, const FarPos* __restrict__ fp, int npos_far, const int* __restrict__ cnt,
-           const long long* __restrict__ toff, const long long* __restrict__ nnz_total,
-           int64_t* __restrict__ row_ptr, int32_t* __restrict__ col, double* __restrict__ val,
-           double* __restrict__ K, int cap) {
-  extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ double scratch[(MODE == 0 ? THREAD_TP : WARP_THREADS) / 32][4][WIN_MAX + 2];
-  __shared__ int wtot[32];
-  __shared__ int spos_dc[MODE == 1 ? FAR_MAXPOS : 1], spos_dd[MODE == 1 ? FAR_MAXPOS : 1];
-  __shared__ long long soffS[MODE == 1 ? WARP_TP : 1], soffJ[MODE == 1 ? WARP_TP : 1];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  double* gS = scratch[wid][0];
-  double* gJ = scratch[wid][1];
-  double* pS = scratch[wid][2];
-  double* pJ = scratch[wid][3];
-  const long long t = blockIdx.x;
+struct FillOut {
+  int64_t* row_ptr;
+  int32_t* col;
+  double* val;
+  double* K;  // nullptr: not written (Q1)
+  const long long* toff;
+  const long long* nnz;
+};
+
+template <int NTHREADS>
+__device__ __forceinline__ void fill_d_tile(const Prob& pr, const FillOut& fo, long long t, const int* cnt,
+                                            double* scr_w, int* wtot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long np = pr.np;
-  if (t == 0 && threadIdx.x == 0) row_ptr[pr.m] = *nnz_total;
-  if (t < pr.npt) {
-    const long long baseS = toff[t], baseJ = toff[pr.npt + t];
-    if (MODE == 0) {
-      long long p = t * pr.tp + threadIdx.x;
-      bool valid = p < np;
-      int cS = valid ? cnt[p] : 0, cJ = valid ? cnt[np + p] : 0;
-      int totS, totJ;
-      int exS = block_exclusive_scan(cS, wtot, totS);
-      int exJ = block_exclusive_scan(cJ, wtot, totJ);
-      if (valid) {
-        row_ptr[p] = baseS + exS;
-        row_ptr[np + p] = baseJ + exJ;
-      }
-      const bool staged = (totS + totJ) <= cap;
-      double* sval = reinterpret_cast<double*>(dyn);
-      int* scol = reinterpret_cast<int*>(dyn + (size_t)cap * sizeof(double));
-      Seg sS, sJ;
-      if (staged) {
-        sS = {scol, sval, nullptr, nullptr};
-        sJ = {scol + totS, sval + totS, nullptr, nullptr};
-      } else {
-        sS = {nullptr, nullptr, col + baseS, val + baseS};
-        sJ = {nullptr, nullptr, col + baseJ, val + baseJ};
-      }
-      int a = 0, b = 1;
-      if (valid) pair_decode(pr.n, p, a, b);
-      bool far = valid && (b - a > 2 * pr.W);
-      double kS = 0.0, kJ = 0.0;
-      if (far) {
-        int nre, nim;
-        far_pair_thread<false>(pr, a, b, nre, nim, sS, 0, sJ, 0);
-        far_pair_thread<true>(pr, a, b, nre, nim, sS, exS, sJ, exJ);
-      }
-      unsigned nm = __ballot_sync(FULL, valid && !far);
-      while (nm) {
-        int src = __ffs(nm) - 1;
-        nm &= nm - 1;
-        int aa = __shfl_sync(FULL, a, src), bb = __shfl_sync(FULL, b, src);
-        long long oS = __shfl_sync(FULL, exS, src), oJ = __shfl_sync(FULL, exJ, src);
-        int c1, c2;
-        double k1, k2;
-        warp_near_pair<true>(pr, aa, bb, gS, gJ, pS, pJ, c1, c2, k1, k2, sS, oS, sJ, oJ);
-        if (lane == src) { kS = k1; kJ = k2; }
-      }
-      if (valid && pr.has_k) {
-        K[p] = kS;
-        K[np + p] = kJ;
-      }
-      __syncthreads();
-      if (staged) {
-        for (int i = threadIdx.x; i < totS; i += blockDim.x) {
-          col[baseS + i] = scol[i];
-          val[baseS + i] = sval[i];
-        }
-        for (int i = threadIdx.x; i < totJ; i += blockDim.x) {
-          col[baseJ + i] = scol[totS + i];
-          val[baseJ + i] = sval[totS + i];
-        }
-      }
-    } else {
-      for (int i = threadIdx.x; i < npos_far; i += blockDim.x) {
-        spos_dc[i] = fp->dc[i];
-        spos_dd[i] = fp->dd[i];
-      }
-      int i0 = threadIdx.x;
-      long long p0 = t * pr.tp + i0;
-      bool valid = i0 < pr.tp && p0 < np;
-      int cS = valid ? cnt[p0] : 0, cJ = valid ? cnt[np + p0] : 0;
-      int totS, totJ;
-      int exS = block_exclusive_scan(cS, wtot, totS);
-      int exJ = block_exclusive_scan(cJ, wtot, totJ);
-      if (i0 < WARP_TP) {
-        soffS[i0] = exS;
-        soffJ[i0] = exJ;
-      }
-      if (valid) {
-        row_ptr[p0] = baseS + exS;
-        row_ptr[np + p0] = baseJ + exJ;
-      }
-      __syncthreads();
-      const Seg sS = {nullptr, nullptr, col + baseS, val + baseS};
-      const Seg sJ = {nullptr, nullptr, col + baseJ, val + baseJ};
-      for (int i = wid; i < pr.tp; i += nwarps) {
-        long long p = t * pr.tp + i;
-        if (p >= np) break;
-        int a, b;
-        pair_decode(pr.n, p, a, b);
-        double k1 = 0.0, k2 = 0.0;
-        int c1, c2;
-        if (b - a > 2 * pr.W) {
-          warp_far_pair<true>(pr, a, b, spos_dc, spos_dd, npos_far, c1, sS, soffS[i], sJ, soffJ[i]);
-        } else {
-          warp_near_pair<true>(pr, a, b, gS, gJ, pS, pJ, c1, c2, k1, k2, sS, soffS[i], sJ, soffJ[i]);
-        }
-        if (lane == 0 && pr.has_k) {
-          K[p] = k1;
-          K[np + p] = k2;
-        }
-      }
+  const long long u = t - pr.npt;
+  const long long baseD = fo.toff[2 * pr.npt + u];
+  const int lam = (int)(u * (NTHREADS / 32) + wid + 1);
+  const bool valid = lam <= pr.n - 1;
+  const int c = valid ? (cnt[2 * np + lam - 1] & CNT_MASK) : 0;
+  int tot;
+  int ex = block_exclusive_scan(lane == 0 ? c : 0, wtot, tot);
+  ex = __shfl_sync(FULL, ex, 0);
+  if (valid) {
+    if (lane == 0) fo.row_ptr[2 * np + lam - 1] = baseD + ex;
+    const Seg sD = {nullptr, nullptr, fo.col + baseD, fo.val + baseD};
+    double kv;
+    warp_d_row<true>(pr, lam, scr_w, scr_w + WIN_MAX + 2, kv, sD, ex);
+    if (lane == 0 && fo.K) fo.K[2 * np + lam - 1] = kv;
+  }
+}
+
+constexpr int CAPW = 1024;   // per-warp staging capacity (entries) in mode 0 (one row block at a time)
+
+// Copy a warp's staged segment [g0, g1) (tile-local offsets) to global memory, skipping the
+// "holes" of long rows (lanes flagged in `holes`, hole = [hoff, hoff + hlen)) that were
+// written directly.  The stage position advances only over copied entries.
+__device__ __forceinline__ void warp_copy_out(const int* scol, const double* sval, long long gbase, int g0, int g1,
+                                              unsigned holes, int hoff, int hlen, int32_t* __restrict__ col,
+                                              double* __restrict__ val) {
+  const int lane = threadIdx.x & 31;
+  int sp = 0, gp = g0;
+  for (;;) {
+    const bool last = holes == 0;
+    int hs = g1, hl = 0;
+    if (!last) {
+      const int h = __ffs(holes) - 1;
+      holes &= holes - 1;
+      hs = __shfl_sync(FULL, hoff, h);
+      hl = __shfl_sync(FULL, hlen, h);
     }
-  } else {
-    const long long u = t - pr.npt;
-    const long long baseD = toff[2 * pr.npt + u];
-    int lam = (int)(u * nwarps + wid + 1);
-    bool valid = lam <= pr.n - 1;
-    int c = valid ? cnt[2 * np + lam - 1] : 0;
-    int tot;
-    int ex = block_exclusive_scan(lane == 0 ? c : 0, wtot, tot);
-    ex = __shfl_sync(FULL, ex, 0);
-    if (valid) {
-      if (lane == 0) row_ptr[2 * np + lam - 1] = baseD + ex;
-      const Seg sD = {nullptr, nullptr, col + baseD, val + baseD};
-      int cc;
-      double kv;
-      warp_d_row<true>(pr, lam, gS, pS, cc, kv, sD, ex);
-      if (lane == 0 && pr.has_k) K[2 * np + lam - 1] = kv;
+    const int run = hs - gp;
+    int32_t* cdst = col + gbase + gp;
+    double* vdst = val + gbase + gp;
+    for (int k = lane; k < run; k += 32) {
+      cdst[k] = scol[sp + k];
+      vdst[k] = sval[sp + k];
+    }
+    sp += run;
+    gp = hs + hl;
+    if (last) break;
+  }
+}
+
+template <int WK, int WL>
+__global__ void __launch_bounds__(128, 4) k_fill0(Prob pr, const int* __restrict__ cnt, FillOut fo) {
+  constexpr int TW = 2 * WK + 1, SW = 4 * WK + 4;
+  static_assert(64 * FarT<WK, WL>::NPOS <= CAPW, "far rows of a warp must fit the staging");
+  extern __shared__ __align__(16) unsigned char dyn[];
+  __shared__ double scr[4][Scr<TW, SW>::PER_WARP];
+  __shared__ int wtot[32];
+  const long long t = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long np = pr.np;
+  if (t == 0 && threadIdx.x == 0) fo.row_ptr[pr.m] = *fo.nnz;
+  if (t >= pr.npt) {
+    fill_d_tile<128>(pr, fo, t, cnt, scr[wid], wtot);
+    return;
+  }
+  double* sval = reinterpret_cast<double*>(dyn) + wid * CAPW;
+  int* scol = reinterpret_cast<int*>(dyn + 4 * CAPW * sizeof(double)) + wid * CAPW;
+  const long long p = t * 128 + threadIdx.x;
+  const bool valid = p < np;
+  const int rawS = valid ? cnt[p] : 0;
+  const int cS = rawS & CNT_MASK, nRe = rawS >> CNT_BITS;
+  const int cJ = valid ? (cnt[np + p] & CNT_MASK) : 0;
+  int a, b;
+  warp_pairs(pr.n, t * 128 + wid * 32, a, b);
+  // tile-local row offsets: warp scans + one exchange of the 4 warp totals
+  int wtS, wtJ;
+  int exS = warp_excl_scan(cS, wtS);
+  int exJ = warp_excl_scan(cJ, wtJ);
+  if (lane == 0) {
+    wtot[wid] = wtS;
+    wtot[4 + wid] = wtJ;
+  }
+  __syncthreads();
+  int pS = 0, pJ = 0;
+#pragma unroll
+  for (int w = 0; w < 4; ++w) {
+    pS += w < wid ? wtot[w] : 0;
+    pJ += w < wid ? wtot[4 + w] : 0;
+  }
+  exS += pS;
+  exJ += pJ;
+  const long long baseS = fo.toff[t], baseJ = fo.toff[pr.npt + t];
+  if (valid) {
+    fo.row_ptr[p] = baseS + exS;
+    fo.row_ptr[np + p] = baseJ + exJ;
+  }
+  const bool far = valid && (b - a > 2 * WK);
+  const bool nearp = valid && !far;
+  // 1) near pairs: both rows written directly (lane-contiguous, coalesced)
+  double kS = 0.0, kJ = 0.0;
+  const unsigned nearmask = __ballot_sync(FULL, nearp);
+  if (nearmask) {
+    const Seg gS = {nullptr, nullptr, fo.col + baseS, fo.val + baseS};
+    const Seg gJ = {nullptr, nullptr, fo.col + baseJ, fo.val + baseJ};
+    unsigned nm = nearmask;
+    do {
+      const int src = __ffs(nm) - 1;
+      nm &= nm - 1;
+      const int aa = __shfl_sync(FULL, a, src), bb = __shfl_sync(FULL, b, src);
+      const int oS = __shfl_sync(FULL, exS, src), oJ = __shfl_sync(FULL, exJ, src);
+      int c1, c2;
+      double k1, k2;
+      warp_near_pair<true, TW, SW>(pr, aa, bb, scr[wid], c1, c2, k1, k2, gS, oS, gJ, oJ);
+      if (lane == src) {
+        kS = k1;
+        kJ = k2;
+      }
+    } while (nm);
+  }
+  if (valid && fo.K) {
+    fo.K[p] = kS;
+    fo.K[np + p] = kJ;
+  }
+  // 2) far pairs: values in registers, rows staged per warp, copied out around the near rows
+  double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
+  if (far) far_values<WK, WL>(pr, a, b, ux, uy);
+#pragma unroll
+  for (int row = 0; row < 2; ++row) {  // S rows of the warp's 32 pairs, then their J rows
+    const int c_me = row ? cJ : cS, ex_me = row ? exJ : exS, w0 = row ? pJ : pS, wt = row ? wtJ : wtS;
+    const long long gbase = row ? baseJ : baseS;
+    int ht;
+    const int hb = warp_excl_scan(nearp ? c_me : 0, ht);
+    if (far) {
+      const int n1 = row ? (cS - nRe) : nRe;
+      far_emit_row<WK, WL>(pr.n, (int)np, pr.tau, a, b, row, ux, uy, n1, SmemSink{scol, sval}, ex_me - w0 - hb);
+    }
+    __syncwarp();
+    warp_copy_out(scol, sval, gbase, w0, w0 + wt, nearmask, ex_me, c_me, fo.col, fo.val);
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(WARP_THREADS) k_fill1(Prob pr, const FarPos* __restrict__ fp, int npos_far,
+                                                        const int* __restrict__ cnt, FillOut fo) {
+  constexpr int SW = WIN_MAX + 2;
+  __shared__ double scr[WARP_THREADS / 32][Scr<0, SW>::PER_WARP];
+  __shared__ int wtot[32];
+  __shared__ int spos_dc[FAR_MAXPOS], spos_dd[FAR_MAXPOS];
+  __shared__ int soffS[WARP_TP], soffJ[WARP_TP];
+  const long long t = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const long long np = pr.np;
+  if (t == 0 && threadIdx.x == 0) fo.row_ptr[pr.m] = *fo.nnz;
+  if (t >= pr.npt) {
+    fill_d_tile<WARP_THREADS>(pr, fo, t, cnt, scr[wid], wtot);
+    return;
+  }
+  for (int i = threadIdx.x; i < npos_far; i += blockDim.x) {
+    spos_dc[i] = fp->dc[i];
+    spos_dd[i] = fp->dd[i];
+  }
+  const long long baseS = fo.toff[t], baseJ = fo.toff[pr.npt + t];
+  const int i0 = threadIdx.x;
+  const long long p0 = t * WARP_TP + i0;
+  const bool valid = i0 < WARP_TP && p0 < np;
+  const int cS = valid ? (cnt[p0] & CNT_MASK) : 0, cJ = valid ? (cnt[np + p0] & CNT_MASK) : 0;
+  int totS, totJ;
+  const int exS = block_exclusive_scan(cS, wtot, totS);
+  const int exJ = block_exclusive_scan(cJ, wtot, totJ);
+  if (i0 < WARP_TP) {
+    soffS[i0] = exS;
+    soffJ[i0] = exJ;
+  }
+  if (valid) {
+    fo.row_ptr[p0] = baseS + exS;
+    fo.row_ptr[np + p0] = baseJ + exJ;
+  }
+  __syncthreads();
+  const Seg sS = {nullptr, nullptr, fo.col + baseS, fo.val + baseS};
+  const Seg sJ = {nullptr, nullptr, fo.col + baseJ, fo.val + baseJ};
+  for (int i = wid; i < WARP_TP; i += nwarps) {
+    const long long p = t * WARP_TP + i;
+    if (p >= np) break;
+    int a, b;
+    pair_decode(pr.n, p, a, b);
+    double k1 = 0.0, k2 = 0.0;
+    if (b - a > 2 * pr.W) {
+      warp_far_pair<true>(pr, a, b, spos_dc, spos_dd, npos_far, sS, soffS[i], sJ, soffJ[i]);
+    } else {
+      int c1, c2;
+      warp_near_pair<true, 0, SW>(pr, a, b, scr[wid], c1, c2, k1, k2, sS, soffS[i], sJ, soffJ[i]);
+    }
+    if (lane == 0 && fo.K) {
+      fo.K[p] = k1;
+      fo.K[np + p] = k2;
     }
   }
 }
@@ -562,7 +737,6 @@ void setup_prob(sun_plan_s* pl, int which) {
     pr.H = {reinterpret_cast<const double2*>(pl->ws + L.hb0), pl->wK};
     pr.L = reinterpret_cast<const double2*>(pl->ws + L.lb);
     pr.tau = pl->tau0;
-    pr.has_k = 1;
   } else {
     pr.P = 0;
     pr.wK = pl->wH1;
@@ -571,9 +745,9 @@ void setup_prob(sun_plan_s* pl, int which) {
     pr.H = pr.K;
     pr.L = nullptr;
     pr.tau = pl->tau1;
-    pr.has_k = 0;
   }
   pr.W = pr.wK > pr.wL ? pr.wK : pr.wL;
+  pr.inv = reinterpret_cast<const double*>(pl->ws + L.inv);
   build_far_positions(pr.W, pr.wL, pr.wK, pl->pos_dc[which], pl->pos_dd[which]);
   int npos = (int)pl->pos_dc[which].size();
   pl->npos_far[which] = npos;
@@ -581,16 +755,71 @@ void setup_prob(sun_plan_s* pl, int which) {
     pl->hfp[which].dc[i] = pl->pos_dc[which][i];
     pl->hfp[which].dd[i] = pl->pos_dd[which][i];
   }
-  // thread-per-pair with shared staging while a pair emits few entries (<= 4 npos); else
-  // warp-per-pair with direct coalesced row stores
-  pr.mode = (npos <= 16) ? 0 : 1;
+  // thread-per-pair with per-warp shared staging for narrow bands (compile-time widths);
+  // else warp-per-pair with direct coalesced row stores
+  pr.mode = mode0_supported(pr.wK, pr.wL) ? 0 : 1;
   pr.tp = pr.mode == 0 ? THREAD_TP : WARP_TP;
   pr.npt = (pr.np + pr.tp - 1) / pr.tp;
   int dpt = (pr.mode == 0 ? THREAD_TP : WARP_THREADS) / 32;
   pr.ndt = (pl->n - 1 + dpt - 1) / dpt;
 }
 
-int stage_cap_entries() { return STAGE_BYTES / (int)(sizeof(double) + sizeof(int)); }
+
+template <int WK, int WL>
+cudaError_t launch_count0(const Prob& pr, int* cnt, int* ts, cudaStream_t st) {
+  k_count0<WK, WL><<<(unsigned)(pr.npt + pr.ndt), 128, 0, st>>>(pr, cnt, ts);
+  return cudaGetLastError();
+}
+
+template <int WK, int WL>
+cudaError_t launch_fill0(const Prob& pr, const int* cnt, const FillOut& fo, cudaStream_t st) {
+  const size_t smem = (size_t)4 * CAPW * (sizeof(double) + sizeof(int));
+  static bool attr_set = false;  // per instantiation
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_fill0<WK, WL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  k_fill0<WK, WL><<<(unsigned)(pr.npt + pr.ndt), 128, smem, st>>>(pr, cnt, fo);
+  return cudaGetLastError();
+}
+
+cudaError_t dispatch_count0(const Prob& pr, int* cnt, int* ts, cudaStream_t st) {
+  if (pr.wK == 0) return launch_count0<0, 0>(pr, cnt, ts, st);
+  if (pr.wK == 1) return launch_count0<1, 0>(pr, cnt, ts, st);
+  if (pr.wK == 2 && pr.wL == 0) return launch_count0<2, 0>(pr, cnt, ts, st);
+  if (pr.wK == 2 && pr.wL == 1) return launch_count0<2, 1>(pr, cnt, ts, st);
+  return launch_count0<3, 0>(pr, cnt, ts, st);
+}
+
+cudaError_t dispatch_fill0(const Prob& pr, const int* cnt, const FillOut& fo, cudaStream_t st) {
+  if (pr.wK == 0) return launch_fill0<0, 0>(pr, cnt, fo, st);
+  if (pr.wK == 1) return launch_fill0<1, 0>(pr, cnt, fo, st);
+  if (pr.wK == 2 && pr.wL == 0) return launch_fill0<2, 0>(pr, cnt, fo, st);
+  if (pr.wK == 2 && pr.wL == 1) return launch_fill0<2, 1>(pr, cnt, fo, st);
+  return launch_fill0<3, 0>(pr, cnt, fo, st);
+}
+
+// exclusive scan of nslots int32 tile sums into int64 offsets; total -> nnz_out
+cudaError_t launch_scan(const int* ts, long long nslots, long long* toff, long long* chunk, long long* nnz_out,
+                        cudaStream_t st) {
+  const size_t smem = SCAN_CHUNK * sizeof(int);
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_scan_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  if (nslots <= SCAN_CHUNK) {
+    k_scan_chunk<<<1, 1024, smem, st>>>(ts, nslots, nullptr, toff, nnz_out);
+    return cudaGetLastError();
+  }
+  const int nchunks = (int)((nslots + SCAN_CHUNK - 1) / SCAN_CHUNK);
+  k_scan_reduce<<<nchunks, 1024, 0, st>>>(ts, nslots, chunk);
+  k_scan_top<<<1, 1024, 0, st>>>(chunk, nchunks);
+  k_scan_chunk<<<nchunks, 1024, smem, st>>>(ts, nslots, chunk, toff, nnz_out);
+  return cudaGetLastError();
+}
 
 }  // namespace
 
@@ -735,8 +964,8 @@ int sun_count(sun_plan pl, void* stream) {
   char* ws = pl->ws;
   DevHeader* hdr = (DevHeader*)(ws + L.hdr);
   // (a1) expand into band storage
-  long long band_doubles = (long long)((L.cnt0 - L.kb0) / sizeof(double));
-  k_zero<<<296, 256, 0, st>>>((double*)(ws + L.kb0), band_doubles);
+  long long zero_doubles = (long long)((L.ts0 - L.kb0) / sizeof(double));
+  k_zero<<<296, 256, 0, st>>>((double*)(ws + L.kb0), zero_doubles);
   CK(cudaGetLastError());
   OpList ops;
   memset(&ops, 0, sizeof(ops));
@@ -751,24 +980,25 @@ int sun_count(sun_plan pl, void* stream) {
       pl->wL, (const double*)(ws + L.sqrtg));
   CK(cudaGetLastError());
   long long nk = (long long)n * (2 * pl->wK + 1);
+  if (nk < n) nk = n;
   k_band_k<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(
       n, pl->P, (const double2*)(ws + L.hb0), (double2*)(ws + L.kb0), pl->wK, (const double2*)(ws + L.lb), pl->wL,
-      (const double2*)(ws + L.hb1), pl->wH1, pl->has_h1, pl->herm_tol0, pl->herm_tol1, hdr);
+      (const double2*)(ws + L.hb1), pl->wH1, pl->has_h1, pl->herm_tol0, pl->herm_tol1, hdr, (double*)(ws + L.inv));
   CK(cudaGetLastError());
   // (a3) count pass + (a4) prefix scan, per output matrix
   for (int which = 0; which < 1 + pl->has_h1; ++which) {
     const Prob& pr = pl->pr[which];
     int* cnt = (int*)(ws + (which ? L.cnt1 : L.cnt0));
-    long long* ts = (long long*)(ws + (which ? L.ts1 : L.ts0));
+    int* ts = (int*)(ws + (which ? L.ts1 : L.ts0));
     const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
-    unsigned grid = (unsigned)(pr.npt + pr.ndt);
-    if (pr.mode == 0)
-      k_count<0><<<grid, THREAD_TP, 0, st>>>(pr, fp, pl->npos_far[which], cnt, ts);
-    else
-      k_count<1><<<grid, WARP_THREADS, 0, st>>>(pr, fp, pl->npos_far[which], cnt, ts);
-    CK(cudaGetLastError());
-    k_scan<<<1, 1024, 0, st>>>(ts, 2 * pr.npt + pr.ndt, &hdr->nnz[which]);
-    CK(cudaGetLastError());
+    if (pr.mode == 0) {
+      CK(dispatch_count0(pr, cnt, ts, st));
+    } else {
+      k_count1<<<(unsigned)(pr.npt + pr.ndt), WARP_THREADS, 0, st>>>(pr, fp, pl->npos_far[which], cnt, ts);
+      CK(cudaGetLastError());
+    }
+    CK(launch_scan(ts, 2 * pr.npt + pr.ndt, (long long*)(ws + (which ? L.toff1 : L.toff0)), (long long*)(ws + L.chunk),
+                   &hdr->nnz[which], st));
   }
   pl->counted = 1;
   pl->count_stream = st;
@@ -779,13 +1009,12 @@ int sun_count(sun_plan pl, void* stream) {
 int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
   if (!pl) return SUN_ERR_ARG;
   if (!pl->counted) return SUN_ERR_STATE;
-  DevHeader* hdr = (DevHeader*)(pl->ws + pl->lay.hdr);
   struct {
     int flags;
     int pad;
     long long nnz[2];
   } h;
-  CK(cudaMemcpyAsync(&h, hdr, sizeof(h), cudaMemcpyDeviceToHost, pl->count_stream));
+  CK(cudaMemcpyAsync(&h, pl->ws + pl->lay.hdr, sizeof(h), cudaMemcpyDeviceToHost, pl->count_stream));
   CK(cudaStreamSynchronize(pl->count_stream));
   if (h.flags & (F_H0_NOT_HERM | F_H1_NOT_HERM)) return SUN_ERR_NOT_HERMITIAN;
   if (h.flags & F_MALFORMED) return SUN_ERR_ARG;
@@ -803,7 +1032,6 @@ int sun_unfold(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream)
   cudaStream_t st = (cudaStream_t)stream;
   const Layout& L = pl->lay;
   char* ws = pl->ws;
-  DevHeader* hdr = (DevHeader*)(ws + L.hdr);
   const long long m = (long long)pl->n * pl->n - 1;
   for (int which = 0; which < 1 + pl->has_h1; ++which) {
     sun_dcsr* Q = which ? Q1 : Q0;
@@ -814,20 +1042,16 @@ int sun_unfold(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream)
     sun_dcsr* Q = which ? Q1 : Q0;
     const Prob& pr = pl->pr[which];
     const int* cnt = (const int*)(ws + (which ? L.cnt1 : L.cnt0));
-    const long long* ts = (const long long*)(ws + (which ? L.ts1 : L.ts0));
     const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
-    unsigned grid = (unsigned)(pr.npt + pr.ndt);
+    DevHeader* hdr = (DevHeader*)(ws + L.hdr);
+    FillOut fo = {Q->row_ptr, Q->col, Q->val, which ? nullptr : K,
+                  (const long long*)(ws + (which ? L.toff1 : L.toff0)), &hdr->nnz[which]};
     if (pr.mode == 0) {
-      int cap = stage_cap_entries();
-      size_t smem = (size_t)cap * (sizeof(double) + sizeof(int));
-      CK(cudaFuncSetAttribute(k_fill<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      k_fill<0><<<grid, THREAD_TP, smem, st>>>(pr, fp, pl->npos_far[which], cnt, ts, &hdr->nnz[which], Q->row_ptr,
-                                                Q->col, Q->val, which ? nullptr : K, cap);
+      CK(dispatch_fill0(pr, cnt, fo, st));
     } else {
-      k_fill<1><<<grid, WARP_THREADS, 0, st>>>(pr, fp, pl->npos_far[which], cnt, ts, &hdr->nnz[which], Q->row_ptr,
-                                                Q->col, Q->val, which ? nullptr : K, 0);
+      k_fill1<<<(unsigned)(pr.npt + pr.ndt), WARP_THREADS, 0, st>>>(pr, fp, pl->npos_far[which], cnt, fo);
+      CK(cudaGetLastError());
     }
-    CK(cudaGetLastError());
   }
   return SUN_OK;
 }

@@ -1,4 +1,4 @@
-// sunfold_kernels.cuh — sm_100a fp64 kernels of the SU(N) unfold (arXiv:1812.11626).
+// sunfold_kernels.cuh — sm_100a fp64 device code of the SU(N) unfold (arXiv:1812.11626).
 //
 // Row s of Q is the generator expansion of the Hermitian matrix G_s = L^+(F_s), where
 //   L^+(X) = i[H, X] + sum_p gamma_p (L_p^+ X L_p - 1/2 {L_p^+ L_p, X})
@@ -7,11 +7,11 @@
 // This is the paper's contraction of Eq. 6 (q_sn = sum_m f_mns h_m) and Eqs. 10-11
 // (R = -1/2 gamma Re(Y^H X), K; P:200-211 with readings R1/R2) evaluated per output row: the
 // structure constants f_mns = -i Tr(F_s[F_m,F_n]) and d_mns = Tr(F_s{F_m,F_n}) (Eq. 4,
-// P:152-158) are products of matrix units E_ab E_cd = delta_bc E_ad, so their nonzero
-// index patterns (the "triangle" class for generators sharing one index, the
-// "pair" class for coincident pairs, and the D^l chains) are enumerated here as the
+// P:152-158) are traces of products of matrix units E_ab E_cd = delta_bc E_ad, so their
+// nonzero index patterns (the "triangle" class for generators sharing one index,
+// the "pair" class for coincident pairs, and the D^l chains) are enumerated here as the
 // support of G_s inside small index windows; no f/d tensor is stored.
-// DESIGN.md gives the derivation and the algebra below.
+// DESIGN.md gives the derivation.
 //
 // Band storage (the GPU form of the paper's coefficient "index map"):
 //   K  = H0 + (i/2) sum_p gamma_p L_p^+ L_p     n x (2 wK + 1) complex, row-major by row
@@ -38,9 +38,11 @@
 
 namespace sunk {
 
-constexpr int WMAX = 15;            // max(wK, wL) supported by the banded kernels
+constexpr int WMAX = 15;               // max(wK, wL) supported by the banded kernels
 constexpr int WIN_MAX = 4 * WMAX + 2;  // near-pair window bound (4W+1), padded
 constexpr unsigned FULL = 0xffffffffu;
+constexpr int CNT_BITS = 20;           // cnt word: bits 0-19 row length, 20-31 nRe (far pairs)
+constexpr int CNT_MASK = (1 << CNT_BITS) - 1;
 
 struct Band {
   const double2* v;  // v[r * (2w+1) + (c - r + w)]
@@ -52,11 +54,11 @@ struct Prob {
   long long np;  // n(n-1)/2
   long long m;   // n^2 - 1
   Band K, H;
-  const double2* L;  // P bands of half-width wL (sqrt(gamma)-scaled)
+  const double2* L;    // P bands of half-width wL (sqrt(gamma)-scaled)
+  const double* inv;   // inv[l] = 1/sqrt(l(l+1)), l = 1..n-1
   double tau;
-  int has_k;  // write K
-  int mode;   // 0 thread-per-pair (staged), 1 warp-per-pair (direct)
-  int tp;     // pairs per tile
+  int mode;            // 0 thread-per-pair (staged), 1 warp-per-pair (direct)
+  int tp;              // pairs per tile
   long long npt, ndt;  // pair tiles, D tiles
 };
 
@@ -72,8 +74,10 @@ __device__ __forceinline__ double2 lget(const Prob& pr, int p, int r, int c) {
   return __ldg(&pr.L[((long long)p * pr.n + r) * (2 * pr.wL + 1) + (o + pr.wL)]);
 }
 
-__device__ __forceinline__ long long pidx(long long n, long long a, long long b) {
-  return a * (2 * n - a - 1) / 2 + (b - a - 1);
+// p(c,d) = c(2n-c-1)/2 + (d-c-1) < 2^31 for n <= 46340 (unsigned intermediate < 2^32)
+__device__ __forceinline__ int pidx32(int n, int c, int d) {
+  const unsigned uc = (unsigned)c;
+  return (int)((uc * (2u * (unsigned)n - uc - 1u)) / 2u + (unsigned)(d - c - 1));
 }
 
 // pair index p -> (a, b), a < b < n, lexicographic (R5)
@@ -89,6 +93,30 @@ __device__ __forceinline__ void pair_decode(long long n, long long p, int& a_out
   b_out = (int)(a + 1 + (p - a * (2 * n - a - 1) / 2));
 }
 
+// Pairs p_first + lane of a warp: decode once (lane 0), then walk.
+__device__ __forceinline__ void warp_pairs(int n, long long p_first, int& a, int& b) {
+  const int lane = threadIdx.x & 31;
+  int a0 = 0, b0 = 1;
+  if (lane == 0) pair_decode(n, p_first, a0, b0);
+  a0 = __shfl_sync(FULL, a0, 0);
+  b0 = __shfl_sync(FULL, b0, 0);
+  int k = lane;
+  a = a0;
+  b = b0;
+  while (b + k >= n) {
+    if (a >= n - 2) {  // past the last pair (caller masks p >= NP)
+      a = n - 2;
+      b = n - 1;
+      k = 0;
+      break;
+    }
+    k -= n - b;
+    a += 1;
+    b = a + 1;
+  }
+  b += k;
+}
+
 // local upper-triangle index k in an nw x nw window -> (i, j), i < j
 __device__ __forceinline__ void win_decode(int nw, int k, int& i, int& j) {
   int r = 0;
@@ -100,9 +128,7 @@ __device__ __forceinline__ void win_decode(int nw, int k, int& i, int& j) {
   j = r + 1 + k;
 }
 
-__device__ __forceinline__ double inv_sqrt_ll1(int l) { return 1.0 / sqrt((double)l * (double)(l + 1)); }
-
-// U = L^+(E_ab) element (c, d)
+// U = L^+(E_ab) element (c, d), general (runtime band widths)
 __device__ __forceinline__ double2 U_elem(const Prob& pr, int a, int b, int c, int d) {
   double ux = 0.0, uy = 0.0;
   if (d == b) {  // + i K_ca
@@ -156,365 +182,41 @@ __device__ __forceinline__ double2 G_elem(const Prob& pr, int lam, double alpha,
   return make_double2(gx, gy);
 }
 
-// Enumerate the far-pair positions (c, d) of U in lexicographic order.
-template <class F>
-__device__ __forceinline__ void far_positions(const Prob& pr, int a, int b, F&& f) {
-  const int n = pr.n, W = pr.W, wL = pr.wL, wK = pr.wK;
-  for (int dc = -W; dc <= W; ++dc) {
-    int c = a + dc;
-    if (c < 0 || c >= n) continue;
-    int adc = dc < 0 ? -dc : dc;
-    if (dc == 0) {
-      for (int dd = -W; dd <= W; ++dd) {
-        int d = b + dd;
-        if (d < n) f(c, d);
-      }
-    } else if (adc <= wL) {
-      for (int dd = -wL; dd <= wL; ++dd) {
-        int d = b + dd;
-        if (d < n) f(c, d);
-      }
-    } else if (adc <= wK) {
-      f(c, b);
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------------------
-// Output sinks
+// Output sink: a contiguous CSR segment in shared staging or global memory.
 // ---------------------------------------------------------------------------------------
-struct Seg {  // one contiguous CSR segment (a row or a tile segment)
-  int* scol;        // shared staging (nullptr: write global)
+struct Seg {
+  int* scol;  // shared staging (nullptr: write global)
   double* sval;
-  int32_t* gcol;    // global col/val base pointers already offset to the segment start
+  int32_t* gcol;  // global col/val base pointers already offset to the segment start
   double* gval;
-  __device__ __forceinline__ void emit(long long off, long long col, double v) const {
+  __device__ __forceinline__ void emit(long long off, int col, double v) const {
     if (scol) {
-      scol[off] = (int)col;
+      scol[off] = col;
       sval[off] = v;
     } else {
-      gcol[off] = (int32_t)col;
+      gcol[off] = col;
       gval[off] = v;
     }
   }
 };
 
 // ---------------------------------------------------------------------------------------
-// Far pair, one thread.  Counts (nre, nim); with EMIT writes both rows.
-//   row S_ab: [Re U_cd > tau at p(c,d)] then [-Im U_cd at NP + p(c,d)]
-//   row J_ab: [Im U_cd at p(c,d)]       then [Re U_cd at NP + p(c,d)]
+// Warp / block helpers
 // ---------------------------------------------------------------------------------------
-template <bool EMIT>
-__device__ __forceinline__ void far_pair_thread(const Prob& pr, int a, int b, int& nre, int& nim,
-                                                const Seg& sS, long long offS, const Seg& sJ,
-                                                long long offJ) {
-  const double tau = pr.tau;
-  if (!EMIT) {
-    int cr = 0, ci = 0;
-    far_positions(pr, a, b, [&](int c, int d) {
-      double2 u = U_elem(pr, a, b, c, d);
-      cr += fabs(u.x) > tau;
-      ci += fabs(u.y) > tau;
-    });
-    nre = cr;
-    nim = ci;
-    return;
-  }
-  const long long n = pr.n, np = pr.np;
-  long long ire = 0, iim = 0;
-  const long long nR = nre, nI = nim;
-  far_positions(pr, a, b, [&](int c, int d) {
-    double2 u = U_elem(pr, a, b, c, d);
-    long long q = pidx(n, c, d);
-    if (fabs(u.x) > tau) {
-      sS.emit(offS + ire, q, u.x);
-      sJ.emit(offJ + nI + ire, np + q, u.x);
-      ++ire;
-    }
-    if (fabs(u.y) > tau) {
-      sS.emit(offS + nR + iim, np + q, -u.y);
-      sJ.emit(offJ + iim, q, u.y);
-      ++iim;
-    }
-  });
-}
-
-// ---------------------------------------------------------------------------------------
-// D^l chain of one row from the diagonal g over window [lo, hi] (warp-cooperative).
-// pre[j] = sum_{i<j} g[i] (j = 0..nw), computed by lane 0 in ascending order.
-// Returns the number of kept entries; with EMIT writes them at seg/off.
-// ---------------------------------------------------------------------------------------
-template <bool EMIT>
-__device__ int warp_dchain(const Prob& pr, int lo, int hi, const double* g, const double* pre,
-                           const Seg& seg, long long off) {
+__device__ __forceinline__ int warp_excl_scan(int v, int& total) {
   const int lane = threadIdx.x & 31;
-  const int n = pr.n;
-  const double tau = pr.tau;
-  const int nw = hi - lo + 1;
-  const double tr = pre[nw];
-  const long long dbase = 2 * pr.np - 1;  // column of D^l is 2NP + l - 1
-  int kept = 0;
-  int lstart = lo < 1 ? 1 : lo;
-  for (int l0 = lstart; l0 < n; l0 += 32) {
-    int l = l0 + lane;
-    bool valid = l < n;
-    double coef = 0.0;
-    if (valid) {
-      double il = inv_sqrt_ll1(l);
-      if (l <= hi)
-        coef = (pre[l - lo] - (double)l * g[l - lo]) * il;
-      else
-        coef = tr * il;
-    }
-    bool keep = valid && fabs(coef) > tau;
-    unsigned km = __ballot_sync(FULL, keep);
-    if (EMIT && keep) seg.emit(off + kept + __popc(km & ((1u << lane) - 1u)), dbase + l, coef);
-    kept += __popc(km);
-    // beyond hi |tr * inv(l)| is non-increasing in l: stop after the first drop there
-    unsigned dropped_beyond = __ballot_sync(FULL, valid && l > hi && !keep);
-    if (dropped_beyond) break;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
   }
-  return kept;
+  total = __shfl_sync(FULL, x, 31);
+  return x - v;
 }
 
-// ---------------------------------------------------------------------------------------
-// Near pair (b - a <= 2W), warp-cooperative.  scratch: per-warp shared arrays of WIN_MAX+1.
-// Outputs counts (cS, cJ) and K values; with EMIT writes rows S_ab (seg sS at offS) and
-// J_ab (seg sJ at offJ).
-// ---------------------------------------------------------------------------------------
-template <bool EMIT>
-__device__ void warp_near_pair(const Prob& pr, int a, int b, double* gS, double* gJ, double* pS,
-                               double* pJ, int& cS, int& cJ, double& kS, double& kJ, const Seg& sS,
-                               long long offS, const Seg& sJ, long long offJ) {
-  const int lane = threadIdx.x & 31;
-  const int n = pr.n, W = pr.W;
-  const long long np = pr.np;
-  const double tau = pr.tau;
-  const int lo = a - W < 0 ? 0 : a - W;
-  const int hi = b + W > n - 1 ? n - 1 : b + W;
-  const int nw = hi - lo + 1;
-  const int npos = nw * (nw - 1) / 2;
-  const unsigned lt = (1u << lane) - 1u;
-  // pass 1: counts of the four parts
-  int nSS = 0, nSJ = 0, nJS = 0, nJJ = 0;
-  for (int k0 = 0; k0 < npos; k0 += 32) {
-    int k = k0 + lane;
-    double vSS = 0, vSJ = 0, vJS = 0, vJJ = 0;
-    if (k < npos) {
-      int i, j;
-      win_decode(nw, k, i, j);
-      int c = lo + i, d = lo + j;
-      double2 ucd = U_elem(pr, a, b, c, d), udc = U_elem(pr, a, b, d, c);
-      vSS = ucd.x + udc.x;
-      vSJ = udc.y - ucd.y;
-      vJS = ucd.y + udc.y;
-      vJJ = ucd.x - udc.x;
-    }
-    nSS += __popc(__ballot_sync(FULL, fabs(vSS) > tau));
-    nSJ += __popc(__ballot_sync(FULL, fabs(vSJ) > tau));
-    nJS += __popc(__ballot_sync(FULL, fabs(vJS) > tau));
-    nJJ += __popc(__ballot_sync(FULL, fabs(vJJ) > tau));
-  }
-  // pass 2 (EMIT only): write the S and J blocks
-  if (EMIT) {
-    int iSS = 0, iSJ = 0, iJS = 0, iJJ = 0;
-    for (int k0 = 0; k0 < npos; k0 += 32) {
-      int k = k0 + lane;
-      double vSS = 0, vSJ = 0, vJS = 0, vJJ = 0;
-      long long q = 0;
-      if (k < npos) {
-        int i, j;
-        win_decode(nw, k, i, j);
-        int c = lo + i, d = lo + j;
-        double2 ucd = U_elem(pr, a, b, c, d), udc = U_elem(pr, a, b, d, c);
-        vSS = ucd.x + udc.x;
-        vSJ = udc.y - ucd.y;
-        vJS = ucd.y + udc.y;
-        vJJ = ucd.x - udc.x;
-        q = pidx(n, c, d);
-      }
-      unsigned m;
-      bool kp;
-      kp = fabs(vSS) > tau; m = __ballot_sync(FULL, kp);
-      if (kp) sS.emit(offS + iSS + __popc(m & lt), q, vSS);
-      iSS += __popc(m);
-      kp = fabs(vSJ) > tau; m = __ballot_sync(FULL, kp);
-      if (kp) sS.emit(offS + nSS + iSJ + __popc(m & lt), np + q, vSJ);
-      iSJ += __popc(m);
-      kp = fabs(vJS) > tau; m = __ballot_sync(FULL, kp);
-      if (kp) sJ.emit(offJ + iJS + __popc(m & lt), q, vJS);
-      iJS += __popc(m);
-      kp = fabs(vJJ) > tau; m = __ballot_sync(FULL, kp);
-      if (kp) sJ.emit(offJ + nJS + iJJ + __popc(m & lt), np + q, vJJ);
-      iJJ += __popc(m);
-    }
-  }
-  // diagonal -> g, prefix sums (lane 0, ascending), D chains
-  const double s2 = 1.4142135623730951;
-  for (int i = lane; i < nw; i += 32) {
-    double2 u = U_elem(pr, a, b, lo + i, lo + i);
-    gS[i] = s2 * u.x;
-    gJ[i] = s2 * u.y;
-  }
-  __syncwarp();
-  if (lane == 0) {
-    double aS = 0.0, aJ = 0.0;
-    for (int i = 0; i < nw; ++i) {
-      pS[i] = aS;
-      pJ[i] = aJ;
-      aS += gS[i];
-      aJ += gJ[i];
-    }
-    pS[nw] = aS;
-    pJ[nw] = aJ;
-  }
-  __syncwarp();
-  int chS = warp_dchain<EMIT>(pr, lo, hi, gS, pS, sS, offS + nSS + nSJ);
-  int chJ = warp_dchain<EMIT>(pr, lo, hi, gJ, pJ, sJ, offJ + nJS + nJJ);
-  cS = nSS + nSJ + chS;
-  cJ = nJS + nJJ + chJ;
-  kS = pS[nw] / (double)n;
-  kJ = pJ[nw] / (double)n;
-  __syncwarp();
-}
-
-// ---------------------------------------------------------------------------------------
-// Far pair, warp-cooperative (warp mode): lane k of each 32-chunk owns far position k
-// (pos_dc/pos_dd: the far_positions() order, relative to (a, b)).  Pass 1 counts the Re and
-// Im parts; with EMIT pass 2 recomputes and writes both rows (same layout as the thread path).
-// ---------------------------------------------------------------------------------------
-template <bool EMIT>
-__device__ void warp_far_pair(const Prob& pr, int a, int b, const int* pos_dc, const int* pos_dd,
-                              int npos, int& cnt, const Seg& sS, long long offS, const Seg& sJ,
-                              long long offJ) {
-  const int lane = threadIdx.x & 31;
-  const int n = pr.n;
-  const long long np = pr.np;
-  const double tau = pr.tau;
-  const unsigned lt = (1u << lane) - 1u;
-  int nR = 0, nI = 0;
-  for (int k0 = 0; k0 < npos; k0 += 32) {
-    int k = k0 + lane;
-    bool okr = false, oki = false;
-    if (k < npos) {
-      int c = a + pos_dc[k], d = b + pos_dd[k];
-      if (c >= 0 && c < n && d < n) {
-        double2 u = U_elem(pr, a, b, c, d);
-        okr = fabs(u.x) > tau;
-        oki = fabs(u.y) > tau;
-      }
-    }
-    nR += __popc(__ballot_sync(FULL, okr));
-    nI += __popc(__ballot_sync(FULL, oki));
-  }
-  cnt = nR + nI;
-  if (!EMIT) return;
-  int iR = 0, iI = 0;
-  for (int k0 = 0; k0 < npos; k0 += 32) {
-    int k = k0 + lane;
-    bool okr = false, oki = false;
-    double2 u = make_double2(0.0, 0.0);
-    long long q = 0;
-    if (k < npos) {
-      int c = a + pos_dc[k], d = b + pos_dd[k];
-      if (c >= 0 && c < n && d < n) {
-        u = U_elem(pr, a, b, c, d);
-        okr = fabs(u.x) > tau;
-        oki = fabs(u.y) > tau;
-        q = pidx(n, c, d);
-      }
-    }
-    unsigned mr = __ballot_sync(FULL, okr), mi = __ballot_sync(FULL, oki);
-    if (okr) {
-      int r = iR + __popc(mr & lt);
-      sS.emit(offS + r, q, u.x);
-      sJ.emit(offJ + nI + r, np + q, u.x);
-    }
-    if (oki) {
-      int r = iI + __popc(mi & lt);
-      sS.emit(offS + nR + r, np + q, -u.y);
-      sJ.emit(offJ + r, q, u.y);
-    }
-    iR += __popc(mr);
-    iI += __popc(mi);
-  }
-}
-
-// ---------------------------------------------------------------------------------------
-// D^lam row, warp-cooperative.
-// ---------------------------------------------------------------------------------------
-template <bool EMIT>
-__device__ void warp_d_row(const Prob& pr, int lam, double* g, double* pre, int& cnt, double& kval,
-                           const Seg& seg, long long off) {
-  const int lane = threadIdx.x & 31;
-  const int n = pr.n;
-  const long long np = pr.np;
-  const double tau = pr.tau;
-  const double alpha = inv_sqrt_ll1(lam);
-  const int lo = lam - pr.wK < 0 ? 0 : lam - pr.wK;
-  const int hi = lam + pr.wK > n - 1 ? n - 1 : lam + pr.wK;
-  const int nw = hi - lo + 1;
-  const int npos = nw * (nw - 1) / 2;
-  const unsigned lt = (1u << lane) - 1u;
-  const double s2 = 1.4142135623730951;
-  int nS = 0, nJ = 0;
-  for (int k0 = 0; k0 < npos; k0 += 32) {
-    int k = k0 + lane;
-    double vS = 0, vJ = 0;
-    if (k < npos) {
-      int i, j;
-      win_decode(nw, k, i, j);
-      double2 gv = G_elem(pr, lam, alpha, lo + i, lo + j);
-      vS = s2 * gv.x;
-      vJ = -s2 * gv.y;
-    }
-    nS += __popc(__ballot_sync(FULL, fabs(vS) > tau));
-    nJ += __popc(__ballot_sync(FULL, fabs(vJ) > tau));
-  }
-  if (EMIT) {
-    int iS = 0, iJ = 0;
-    for (int k0 = 0; k0 < npos; k0 += 32) {
-      int k = k0 + lane;
-      double vS = 0, vJ = 0;
-      long long q = 0;
-      if (k < npos) {
-        int i, j;
-        win_decode(nw, k, i, j);
-        double2 gv = G_elem(pr, lam, alpha, lo + i, lo + j);
-        vS = s2 * gv.x;
-        vJ = -s2 * gv.y;
-        q = pidx(n, lo + i, lo + j);
-      }
-      bool kp = fabs(vS) > tau;
-      unsigned m = __ballot_sync(FULL, kp);
-      if (kp) seg.emit(off + iS + __popc(m & lt), q, vS);
-      iS += __popc(m);
-      kp = fabs(vJ) > tau;
-      m = __ballot_sync(FULL, kp);
-      if (kp) seg.emit(off + nS + iJ + __popc(m & lt), np + q, vJ);
-      iJ += __popc(m);
-    }
-  }
-  for (int i = lane; i < nw; i += 32) g[i] = G_elem(pr, lam, alpha, lo + i, lo + i).x;
-  __syncwarp();
-  if (lane == 0) {
-    double acc = 0.0;
-    for (int i = 0; i < nw; ++i) {
-      pre[i] = acc;
-      acc += g[i];
-    }
-    pre[nw] = acc;
-  }
-  __syncwarp();
-  int ch = warp_dchain<EMIT>(pr, lo, hi, g, pre, seg, off + nS + nJ);
-  cnt = nS + nJ + ch;
-  kval = pre[nw] / (double)n;
-  __syncwarp();
-}
-
-// ---------------------------------------------------------------------------------------
 // Block-wide exclusive scan of one int per thread (blockDim.x <= 1024, multiple of 32).
-// ---------------------------------------------------------------------------------------
 __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int& total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   int x = v;
@@ -539,6 +241,481 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int& t
   total = warp_tot[nwarps - 1];
   __syncthreads();
   return before + x - v;
+}
+
+// ---------------------------------------------------------------------------------------
+// Last l in (hi, n-1] with |tr * inv[l]| > tau (hi if none).  The predicate is monotone
+// (non-increasing) in l, so the answer is unique; it is located from the estimate
+// l ~ |tr|/tau - 1/2 (inv[l] ~ 1/(l + 1/2)) checked by the 32 lanes in parallel, with a
+// binary search as fallback.  Warp-uniform result, identical in the count and fill passes.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int chain_tail_end(const double* inv, int n, int hi, double tr, double tau) {
+  const int lane = threadIdx.x & 31;
+  if (hi + 1 > n - 1) return hi;
+  const double atr = fabs(tr);
+  if (!(atr * __ldg(&inv[hi + 1]) > tau)) return hi;       // nothing kept beyond the window
+  if (atr * __ldg(&inv[n - 1]) > tau) return n - 1;          // everything kept
+  double est = atr / tau - 0.5;
+  long long e = est > (double)(n - 1) ? (long long)(n - 1) : (long long)est;
+  int base = (int)e - 15;
+  if (base < hi + 1) base = hi + 1;
+  if (base > n - 32) base = n - 32 > hi + 1 ? n - 32 : hi + 1;
+  const int l = base + lane;
+  const bool in = l <= n - 1;
+  const bool kept = in && fabs(tr * __ldg(&inv[l])) > tau;
+  const unsigned km = __ballot_sync(FULL, kept), im = __ballot_sync(FULL, in);
+  // kept lanes must form a prefix of the in-range lanes, boundary strictly inside the window
+  if (km != 0u && km != im && (km & (km + 1u)) == 0u) return base + __popc(km) - 1;
+  if (km == 0u && base == hi + 1) return hi;  // (cannot happen: inv[hi+1] kept)
+  int lo_b = hi + 1, hi_b = n - 1;            // fallback: binary search (lo_b kept)
+  while (lo_b < hi_b) {
+    const int mid = (lo_b + hi_b + 1) >> 1;
+    if (fabs(tr * __ldg(&inv[mid])) > tau)
+      lo_b = mid;
+    else
+      hi_b = mid - 1;
+  }
+  return lo_b;
+}
+
+// Exclusive prefix sums pre[0..nw] of g[0..nw-1] (shared, per warp) by warp shuffles in
+// 32-element chunks (fixed tree order: deterministic, same in both passes).
+__device__ __forceinline__ void warp_prefix(const double* g, double* pre, int nw) {
+  const int lane = threadIdx.x & 31;
+  double carry = 0.0;
+  for (int i0 = 0; i0 < nw; i0 += 32) {
+    const int i = i0 + lane;
+    const double v = i < nw ? g[i] : 0.0;
+    double x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (i < nw) pre[i] = carry + (x - v);
+    carry += __shfl_sync(FULL, x, 31);
+  }
+  if (lane == 0) pre[nw] = carry;
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------------------
+// D^l chain of one row from its diagonal g over the window [lo, hi] (warp-cooperative).
+// pre[j] = sum_{i<j} g[i] (j = 0..nw) in ascending order.  For l > hi the coefficient is
+// tr * inv[l] with |tr * inv[l]| non-increasing in l (correctly rounded sqrt, division and
+// product are monotone), so the kept tail is (hi, lend], found by binary search -- identical
+// in the count and fill passes.  Returns the kept count; with EMIT writes them at seg/off.
+// ---------------------------------------------------------------------------------------
+template <bool EMIT>
+__device__ __forceinline__ int warp_dchain(const Prob& pr, int lo, int hi, const double* g, const double* pre,
+                                           const Seg& seg, long long off) {
+  const int lane = threadIdx.x & 31;
+  const int n = pr.n;
+  const double tau = pr.tau;
+  const int nw = hi - lo + 1;
+  const double tr = pre[nw];
+  const int dbase = (int)(2 * pr.np - 1);  // column of D^l is 2NP + l - 1
+  const double* inv = pr.inv;
+  int kept = 0;
+  const int lstart = lo < 1 ? 1 : lo;
+  for (int l0 = lstart; l0 <= hi; l0 += 32) {  // inside the window
+    const int l = l0 + lane;
+    double coef = 0.0;
+    const bool valid = l <= hi;
+    if (valid) coef = (pre[l - lo] - (double)l * g[l - lo]) * __ldg(&inv[l]);
+    const bool keep = valid && fabs(coef) > tau;
+    const unsigned km = __ballot_sync(FULL, keep);
+    if (EMIT && keep) seg.emit(off + kept + __popc(km & ((1u << lane) - 1u)), dbase + l, coef);
+    kept += __popc(km);
+  }
+  const int lend = chain_tail_end(inv, n, hi, tr, tau);  // tail beyond the window: l in (hi, lend]
+  if (EMIT) {
+    for (int l = hi + 1 + lane; l <= lend; l += 32)
+      seg.emit(off + kept + (l - hi - 1), dbase + l, tr * __ldg(&inv[l]));
+  }
+  return kept + (lend - hi);
+}
+
+// ---------------------------------------------------------------------------------------
+// Both rows (S_ab, J_ab) of a near pair (b - a <= 2W), warp-cooperative.
+// TW > 0: U = L^+(E_ab) is first evaluated once on its support tile [a-W, a+W] x [b-W, b+W]
+//         (TW = 2W + 1 entries per side, one lane per entry) into shared memory; the window
+//         positions then read the tile.  TW == 0: every value through U_elem (wide bands).
+// scr: per-warp shared scratch: tile (TW*TW double2) | gS | gJ | pS | pJ (each SW doubles).
+// Returns the row lengths (cS, cJ) and K values (kS, kJ); with EMIT writes the rows.
+// ---------------------------------------------------------------------------------------
+template <bool EMIT, int TW, int SW>
+__device__ __noinline__ void warp_near_pair(const Prob& pr, int a, int b, double* scr, int& cS, int& cJ, double& kS,
+                                            double& kJ, Seg sS, long long offS, Seg sJ, long long offJ) {
+  const int lane = threadIdx.x & 31;
+  const int n = pr.n, W = pr.W;
+  const int np = (int)pr.np;
+  const double tau = pr.tau;
+  double2* tile = reinterpret_cast<double2*>(scr);
+  double* gS = scr + 2 * TW * TW;
+  double* gJ = gS + SW;
+  double* pS = gJ + SW;
+  double* pJ = pS + SW;
+  const int lo = a - W < 0 ? 0 : a - W;
+  const int hi = b + W > n - 1 ? n - 1 : b + W;
+  const int nw = hi - lo + 1;
+  const int npos = nw * (nw - 1) / 2;
+  const unsigned lt = (1u << lane) - 1u;
+  if constexpr (TW > 0) {
+    for (int k = lane; k < TW * TW; k += 32) {
+      const int c = a - W + k / TW, d = b - W + k % TW;
+      tile[k] = (c >= 0 && d < n) ? U_elem(pr, a, b, c, d) : make_double2(0.0, 0.0);
+    }
+    __syncwarp();
+  }
+  auto U = [&](int c, int d) -> double2 {
+    if constexpr (TW > 0) {
+      const int i = c - (a - W), j = d - (b - W);
+      return (i >= 0 && i < TW && j >= 0 && j < TW) ? tile[i * TW + j] : make_double2(0.0, 0.0);
+    } else {
+      return U_elem(pr, a, b, c, d);
+    }
+  };
+  int n1S = 0, n2S = 0, n1J = 0, n2J = 0;
+  for (int k0 = 0; k0 < npos; k0 += 32) {
+    const int k = k0 + lane;
+    double v1S = 0, v2S = 0, v1J = 0, v2J = 0;
+    if (k < npos) {
+      int i, j;
+      win_decode(nw, k, i, j);
+      const double2 ucd = U(lo + i, lo + j), udc = U(lo + j, lo + i);
+      v1S = ucd.x + udc.x;
+      v2S = udc.y - ucd.y;
+      v1J = ucd.y + udc.y;
+      v2J = ucd.x - udc.x;
+    }
+    n1S += __popc(__ballot_sync(FULL, fabs(v1S) > tau));
+    n2S += __popc(__ballot_sync(FULL, fabs(v2S) > tau));
+    n1J += __popc(__ballot_sync(FULL, fabs(v1J) > tau));
+    n2J += __popc(__ballot_sync(FULL, fabs(v2J) > tau));
+  }
+  if (EMIT) {
+    int i1S = 0, i2S = 0, i1J = 0, i2J = 0;
+    for (int k0 = 0; k0 < npos; k0 += 32) {
+      const int k = k0 + lane;
+      double v1S = 0, v2S = 0, v1J = 0, v2J = 0;
+      int q = 0;
+      if (k < npos) {
+        int i, j;
+        win_decode(nw, k, i, j);
+        const double2 ucd = U(lo + i, lo + j), udc = U(lo + j, lo + i);
+        v1S = ucd.x + udc.x;
+        v2S = udc.y - ucd.y;
+        v1J = ucd.y + udc.y;
+        v2J = ucd.x - udc.x;
+        q = pidx32(n, lo + i, lo + j);
+      }
+      bool kp;
+      unsigned m;
+      kp = fabs(v1S) > tau; m = __ballot_sync(FULL, kp);
+      if (kp) sS.emit(offS + i1S + __popc(m & lt), q, v1S);
+      i1S += __popc(m);
+      kp = fabs(v2S) > tau; m = __ballot_sync(FULL, kp);
+      if (kp) sS.emit(offS + n1S + i2S + __popc(m & lt), np + q, v2S);
+      i2S += __popc(m);
+      kp = fabs(v1J) > tau; m = __ballot_sync(FULL, kp);
+      if (kp) sJ.emit(offJ + i1J + __popc(m & lt), q, v1J);
+      i1J += __popc(m);
+      kp = fabs(v2J) > tau; m = __ballot_sync(FULL, kp);
+      if (kp) sJ.emit(offJ + n1J + i2J + __popc(m & lt), np + q, v2J);
+      i2J += __popc(m);
+    }
+  }
+  const double s2 = 1.4142135623730951;
+  for (int i = lane; i < nw; i += 32) {
+    const double2 u = U(lo + i, lo + i);
+    gS[i] = s2 * u.x;
+    gJ[i] = s2 * u.y;
+  }
+  __syncwarp();
+  warp_prefix(gS, pS, nw);
+  warp_prefix(gJ, pJ, nw);
+  const int chS = warp_dchain<EMIT>(pr, lo, hi, gS, pS, sS, offS + n1S + n2S);
+  const int chJ = warp_dchain<EMIT>(pr, lo, hi, gJ, pJ, sJ, offJ + n1J + n2J);
+  cS = n1S + n2S + chS;
+  cJ = n1J + n2J + chJ;
+  kS = pS[nw] / (double)n;
+  kJ = pJ[nw] / (double)n;
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------------------
+// D^lam row, warp-cooperative.
+// ---------------------------------------------------------------------------------------
+template <bool EMIT>
+__device__ __noinline__ int warp_d_row(const Prob& pr, int lam, double* g, double* pre, double& kval, Seg seg,
+                                       long long off) {
+  const int lane = threadIdx.x & 31;
+  const int n = pr.n;
+  const int np = (int)pr.np;
+  const double tau = pr.tau;
+  const double alpha = __ldg(&pr.inv[lam]);
+  const int lo = lam - pr.wK < 0 ? 0 : lam - pr.wK;
+  const int hi = lam + pr.wK > n - 1 ? n - 1 : lam + pr.wK;
+  const int nw = hi - lo + 1;
+  const int npos = nw * (nw - 1) / 2;
+  const unsigned lt = (1u << lane) - 1u;
+  const double s2 = 1.4142135623730951;
+  int nS = 0, nJ = 0;
+  for (int k0 = 0; k0 < npos; k0 += 32) {
+    const int k = k0 + lane;
+    double vS = 0, vJ = 0;
+    if (k < npos) {
+      int i, j;
+      win_decode(nw, k, i, j);
+      const double2 gv = G_elem(pr, lam, alpha, lo + i, lo + j);
+      vS = s2 * gv.x;
+      vJ = -s2 * gv.y;
+    }
+    nS += __popc(__ballot_sync(FULL, fabs(vS) > tau));
+    nJ += __popc(__ballot_sync(FULL, fabs(vJ) > tau));
+  }
+  if (EMIT) {
+    int iS = 0, iJ = 0;
+    for (int k0 = 0; k0 < npos; k0 += 32) {
+      const int k = k0 + lane;
+      double vS = 0, vJ = 0;
+      int q = 0;
+      if (k < npos) {
+        int i, j;
+        win_decode(nw, k, i, j);
+        const double2 gv = G_elem(pr, lam, alpha, lo + i, lo + j);
+        vS = s2 * gv.x;
+        vJ = -s2 * gv.y;
+        q = pidx32(n, lo + i, lo + j);
+      }
+      bool kp = fabs(vS) > tau;
+      unsigned m = __ballot_sync(FULL, kp);
+      if (kp) seg.emit(off + iS + __popc(m & lt), q, vS);
+      iS += __popc(m);
+      kp = fabs(vJ) > tau;
+      m = __ballot_sync(FULL, kp);
+      if (kp) seg.emit(off + nS + iJ + __popc(m & lt), np + q, vJ);
+      iJ += __popc(m);
+    }
+  }
+  for (int i = lane; i < nw; i += 32) g[i] = G_elem(pr, lam, alpha, lo + i, lo + i).x;
+  __syncwarp();
+  warp_prefix(g, pre, nw);
+  const int ch = warp_dchain<EMIT>(pr, lo, hi, g, pre, seg, off + nS + nJ);
+  kval = pre[nw] / (double)n;
+  __syncwarp();
+  return nS + nJ + ch;
+}
+
+// ---------------------------------------------------------------------------------------
+// Far pair with compile-time half-bandwidths (WK >= WL): all band values the pair needs are
+// loaded up front (independent loads) and the npos U values stay in registers.
+// Position order == lexicographic in (c, d).
+// ---------------------------------------------------------------------------------------
+template <int WK, int WL>
+struct FarT {
+  static constexpr int W = WK;
+  static constexpr int NPOS = (2 * W + 1) + 2 * WL * (2 * WL + 1) + 2 * (W - WL);
+};
+
+template <int WK, int WL, class F>
+__device__ __forceinline__ void far_foreach(F&& f) {
+  int k = 0;
+#pragma unroll
+  for (int dc = -WK; dc <= WK; ++dc) {
+    const int adc = dc < 0 ? -dc : dc;
+    if (dc == 0) {
+#pragma unroll
+      for (int dd = -WK; dd <= WK; ++dd) {
+        f(k, dc, dd);
+        ++k;
+      }
+    } else if (adc <= WL) {
+#pragma unroll
+      for (int dd = -WL; dd <= WL; ++dd) {
+        f(k, dc, dd);
+        ++k;
+      }
+    } else {
+      f(k, dc, 0);
+      ++k;
+    }
+  }
+}
+
+template <int WK, int WL>
+__device__ __forceinline__ void far_values(const Prob& pr, int a, int b, double (&ux)[FarT<WK, WL>::NPOS],
+                                           double (&uy)[FarT<WK, WL>::NPOS]) {
+  constexpr int W = WK;
+  constexpr int SK = 2 * WK + 1, SL = 2 * WL + 1;
+  const int n = pr.n;
+  double2 kc[2 * W + 1], kr[2 * W + 1];
+#pragma unroll
+  for (int i = 0; i <= 2 * W; ++i) {
+    const int c = a + i - W;  // K(c, a): row c, offset a - c = W - i
+    kc[i] = c >= 0 ? __ldg(&pr.K.v[(long long)c * SK + (2 * W - i)]) : make_double2(0.0, 0.0);
+    const int d = b + i - W;  // K(d, b): row d, offset b - d = W - i
+    kr[i] = d < n ? __ldg(&pr.K.v[(long long)d * SK + (2 * W - i)]) : make_double2(0.0, 0.0);
+  }
+  double ox[SL][SL], oy[SL][SL];
+#pragma unroll
+  for (int i = 0; i < SL; ++i)
+#pragma unroll
+    for (int j = 0; j < SL; ++j) ox[i][j] = oy[i][j] = 0.0;
+  for (int p = 0; p < pr.P; ++p) {
+    const double2* La = pr.L + ((long long)p * n + a) * SL;  // row a: L(a, a - WL + i)
+    const double2* Lb = pr.L + ((long long)p * n + b) * SL;
+    double2 la[SL], lb[SL];
+#pragma unroll
+    for (int i = 0; i < SL; ++i) {
+      la[i] = __ldg(&La[i]);
+      lb[i] = __ldg(&Lb[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < SL; ++i)
+#pragma unroll
+      for (int j = 0; j < SL; ++j) {
+        ox[i][j] += la[i].x * lb[j].x + la[i].y * lb[j].y;  // conj(la) lb
+        oy[i][j] += la[i].x * lb[j].y - la[i].y * lb[j].x;
+      }
+  }
+  far_foreach<WK, WL>([&](int k, int dc, int dd) {
+    double x = 0.0, y = 0.0;
+    if (dd == 0) {  // + i K_ca
+      x -= kc[dc + W].y;
+      y += kc[dc + W].x;
+    }
+    if (dc == 0) {  // - i conj(K_db)
+      x -= kr[dd + W].y;
+      y -= kr[dd + W].x;
+    }
+    const int adc = dc < 0 ? -dc : dc, add = dd < 0 ? -dd : dd;
+    if (adc <= WL && add <= WL) {
+      x += ox[dc + WL][dd + WL];
+      y += oy[dc + WL][dd + WL];
+    }
+    ux[k] = x;
+    uy[k] = y;
+  });
+}
+
+template <int WK, int WL>
+__device__ __forceinline__ void far_counts(int n, double tau, int a, int b, const double (&ux)[FarT<WK, WL>::NPOS],
+                                           const double (&uy)[FarT<WK, WL>::NPOS], int& nR, int& nI) {
+  int r = 0, i = 0;
+  far_foreach<WK, WL>([&](int k, int dc, int dd) {
+    const bool ok = (a + dc >= 0) && (b + dd < n);
+    r += (ok && fabs(ux[k]) > tau);
+    i += (ok && fabs(uy[k]) > tau);
+  });
+  nR = r;
+  nI = i;
+}
+
+// Emit one row of a far pair (row 0 = S_ab, row 1 = J_ab) through `sink(index, col, value)`.
+//   row S_ab: [Re U > tau at q] [-Im U at NP + q];   row J_ab: [Im U at q] [Re U at NP + q]
+// n1 = number of entries of the first part (nRe for S_ab, nIm for J_ab).
+template <int WK, int WL, class SINK>
+__device__ __forceinline__ void far_emit_row(int n, int np, double tau, int a, int b, int row,
+                                             const double (&ux)[FarT<WK, WL>::NPOS],
+                                             const double (&uy)[FarT<WK, WL>::NPOS], int n1, const SINK& sink,
+                                             int off) {
+  int i1 = 0, i2 = 0;
+  far_foreach<WK, WL>([&](int k, int dc, int dd) {
+    const int c = a + dc, d = b + dd;
+    const bool ok = (c >= 0) && (d < n);
+    const int q = pidx32(n, c, d);
+    const double v1 = row == 0 ? ux[k] : uy[k];
+    const double v2 = row == 0 ? -uy[k] : ux[k];
+    if (ok && fabs(v1) > tau) {
+      sink(off + i1, q, v1);
+      ++i1;
+    }
+    if (ok && fabs(v2) > tau) {
+      sink(off + n1 + i2, np + q, v2);
+      ++i2;
+    }
+  });
+}
+
+struct SmemSink {
+  int* col;
+  double* val;
+  __device__ __forceinline__ void operator()(int i, int c, double v) const {
+    col[i] = c;
+    val[i] = v;
+  }
+};
+struct GlobalSink {
+  int32_t* col;
+  double* val;
+  __device__ __forceinline__ void operator()(int i, int c, double v) const {
+    col[i] = c;
+    val[i] = v;
+  }
+};
+
+// ---------------------------------------------------------------------------------------
+// Far pair, warp-cooperative (mode 1): lane k of each 32-chunk owns far position k
+// (pos_dc/pos_dd: offsets in lexicographic order).  Pass 1 counts; EMIT pass 2 writes.
+// ---------------------------------------------------------------------------------------
+template <bool EMIT>
+__device__ __forceinline__ int warp_far_pair(const Prob& pr, int a, int b, const int* pos_dc, const int* pos_dd,
+                                             int npos, const Seg& sS, long long offS, const Seg& sJ,
+                                             long long offJ) {
+  const int lane = threadIdx.x & 31;
+  const int n = pr.n;
+  const int np = (int)pr.np;
+  const double tau = pr.tau;
+  const unsigned lt = (1u << lane) - 1u;
+  int nR = 0, nI = 0;
+  for (int k0 = 0; k0 < npos; k0 += 32) {
+    const int k = k0 + lane;
+    bool okr = false, oki = false;
+    if (k < npos) {
+      const int c = a + pos_dc[k], d = b + pos_dd[k];
+      if (c >= 0 && c < n && d < n) {
+        const double2 u = U_elem(pr, a, b, c, d);
+        okr = fabs(u.x) > tau;
+        oki = fabs(u.y) > tau;
+      }
+    }
+    nR += __popc(__ballot_sync(FULL, okr));
+    nI += __popc(__ballot_sync(FULL, oki));
+  }
+  if (EMIT) {
+    int iR = 0, iI = 0;
+    for (int k0 = 0; k0 < npos; k0 += 32) {
+      const int k = k0 + lane;
+      bool okr = false, oki = false;
+      double2 u = make_double2(0.0, 0.0);
+      int q = 0;
+      if (k < npos) {
+        const int c = a + pos_dc[k], d = b + pos_dd[k];
+        if (c >= 0 && c < n && d < n) {
+          u = U_elem(pr, a, b, c, d);
+          okr = fabs(u.x) > tau;
+          oki = fabs(u.y) > tau;
+          q = pidx32(n, c, d);
+        }
+      }
+      const unsigned mr = __ballot_sync(FULL, okr), mi = __ballot_sync(FULL, oki);
+      if (okr) {
+        const int r = iR + __popc(mr & lt);
+        sS.emit(offS + r, q, u.x);
+        sJ.emit(offJ + nI + r, np + q, u.x);
+      }
+      if (oki) {
+        const int r = iI + __popc(mi & lt);
+        sS.emit(offS + nR + r, np + q, -u.y);
+        sJ.emit(offJ + r, q, u.y);
+      }
+      iR += __popc(mr);
+      iI += __popc(mi);
+    }
+  }
+  return nR + nI;
 }
 
 }  // namespace sunk
