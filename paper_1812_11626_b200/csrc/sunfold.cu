@@ -52,10 +52,7 @@ struct OpList {
 };
 
 // mode-0 instantiations (compile-time band widths); anything else runs in mode 1
-bool mode0_supported(int wK, int wL) {
-  return (wK == 0 && wL == 0) || (wK == 1 && wL == 0) || (wK == 2 && wL == 0) || (wK == 2 && wL == 1) ||
-         (wK == 3 && wL == 0);
-}
+bool mode0_supported(int wK, int wL) { return (wK <= 3 && wL == 0) || (wK == 2 && wL == 1); }
 
 thread_local char g_errbuf[512];
 
@@ -266,55 +263,73 @@ struct Scr {
   static constexpr int PER_WARP = A > 2 * (WIN_MAX + 2) ? A : 2 * (WIN_MAX + 2);
 };
 
-template <int WK, int WL>
-__global__ void __launch_bounds__(128, 4) k_count0(Prob pr, int* __restrict__ cnt, int* __restrict__ tsum) {
-  constexpr int TW = 2 * WK + 1, SW = 4 * WK + 4;
-  __shared__ double scr[4][Scr<TW, SW>::PER_WARP];
-  __shared__ int wtot[32];
+// mode 0, far pairs only (b - a > 2 WK): thread per pair, values in registers.  Near pairs
+// and D rows are counted by k_count_near.  Tile sums here cover the far rows; k_count_near
+// adds the near rows' counts to the same slots.
+template <int WK, int WL, int PT>
+__global__ void __launch_bounds__(128) k_count_far(Prob pr, int* __restrict__ cnt, int* __restrict__ tsum) {
+  __shared__ int wred[8];
   const long long t = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (t >= pr.npt) {
-    count_d_tile<128>(pr, t, cnt, tsum, scr[wid], wtot);
-    return;
-  }
-  const Seg none = {nullptr, nullptr, nullptr, nullptr};
   const long long p = t * 128 + threadIdx.x;
   const bool valid = p < pr.np;
   int a, b;
   warp_pairs(pr.n, t * 128 + wid * 32, a, b);
   const bool far = valid && (b - a > 2 * WK);
-  int cS = 0, cJ = 0, packS = 0;
-  unsigned nm = __ballot_sync(FULL, valid && !far);
-  while (nm) {  // near pairs first (no far values live across the calls)
-    const int src = __ffs(nm) - 1;
-    nm &= nm - 1;
-    const int aa = __shfl_sync(FULL, a, src), bb = __shfl_sync(FULL, b, src);
-    int c1, c2;
-    double k1, k2;
-    warp_near_pair<false, TW, SW>(pr, aa, bb, scr[wid], c1, c2, k1, k2, none, 0, none, 0);
-    if (lane == src) {
-      cS = c1;
-      cJ = c2;
-    }
-  }
+  int c = 0;
   if (far) {
     double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
-    far_values<WK, WL>(pr, a, b, ux, uy);
+    far_values<WK, WL, PT>(pr, a, b, ux, uy);
     int nR, nI;
     far_counts<WK, WL>(pr.n, pr.tau, a, b, ux, uy, nR, nI);
-    cS = cJ = nR + nI;
-    packS = nR << CNT_BITS;
+    c = nR + nI;
+    cnt[p] = c | (nR << CNT_BITS);
+    cnt[pr.np + p] = c;
   }
-  if (valid) {
-    cnt[p] = cS | packS;
-    cnt[pr.np + p] = cJ;
-  }
-  int totS, totJ;
-  block_exclusive_scan(cS, wtot, totS);
-  block_exclusive_scan(cJ, wtot, totJ);
+  int x = c;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+  if (lane == 0) wred[wid] = x;
+  __syncthreads();
   if (threadIdx.x == 0) {
-    tsum[t] = totS;
-    tsum[pr.npt + t] = totJ;
+    const int tot = wred[0] + wred[1] + wred[2] + wred[3];
+    tsum[t] = tot;  // S rows and J rows of a far pair have the same length
+    tsum[pr.npt + t] = tot;
+  }
+}
+
+// mode 0, near pairs (b - a <= 2W) and D rows: one warp per item; counts added to the tile
+// slots with integer atomics (order-independent).  D rows have one slot each.
+template <int TW>
+__global__ void __launch_bounds__(128) k_count_near(Prob pr, int* __restrict__ cnt, int* __restrict__ tsum) {
+  constexpr int SW = 2 * TW + 2;
+  __shared__ double scr[4][Scr<TW, SW>::PER_WARP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long item = (long long)blockIdx.x * 4 + wid;
+  const int W2 = 2 * pr.W;
+  const long long nnear = (long long)pr.n * W2;
+  const Seg none = {nullptr, nullptr, nullptr, nullptr};
+  if (item < nnear) {
+    const int a = (int)(item / W2), b = a + 1 + (int)(item % W2);
+    if (b >= pr.n) return;
+    int c1, c2;
+    double k1, k2;
+    warp_near_pair<false, TW, SW>(pr, a, b, scr[wid], c1, c2, k1, k2, none, 0, none, 0);
+    if (lane == 0) {
+      const long long p = (long long)pidx32(pr.n, a, b);
+      cnt[p] = c1;
+      cnt[pr.np + p] = c2;
+      atomicAdd(&tsum[p / 128], c1);
+      atomicAdd(&tsum[pr.npt + p / 128], c2);
+    }
+  } else if (item < nnear + pr.n - 1) {
+    const int lam = (int)(item - nnear) + 1;
+    double kv;
+    const int c = warp_d_row<false>(pr, lam, scr[wid], scr[wid] + WIN_MAX + 2, kv, none, 0);
+    if (lane == 0) {
+      cnt[2 * pr.np + lam - 1] = c;
+      tsum[2 * pr.npt + lam - 1] = c;
+    }
   }
 }
 
@@ -515,21 +530,19 @@ __device__ __forceinline__ void warp_copy_out(const int* scol, const double* sva
   }
 }
 
-template <int WK, int WL>
-__global__ void __launch_bounds__(128, 4) k_fill0(Prob pr, const int* __restrict__ cnt, FillOut fo) {
-  constexpr int TW = 2 * WK + 1, SW = 4 * WK + 4;
+// mode 0 fill, far pairs: thread per pair computes its values in registers and writes its
+// two rows into per-warp shared staging (S rows of the warp's 32 pairs, then their J rows);
+// the warp copies each staged block out with coalesced stores, skipping the near rows
+// (written by k_fill_near).  Also writes row_ptr of all pair rows and K = 0 for far pairs.
+template <int WK, int WL, int PT>
+__global__ void __launch_bounds__(128) k_fill_far(Prob pr, const int* __restrict__ cnt, FillOut fo) {
   static_assert(64 * FarT<WK, WL>::NPOS <= CAPW, "far rows of a warp must fit the staging");
   extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ double scr[4][Scr<TW, SW>::PER_WARP];
-  __shared__ int wtot[32];
+  __shared__ int wtot[8];
   const long long t = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long np = pr.np;
   if (t == 0 && threadIdx.x == 0) fo.row_ptr[pr.m] = *fo.nnz;
-  if (t >= pr.npt) {
-    fill_d_tile<128>(pr, fo, t, cnt, scr[wid], wtot);
-    return;
-  }
   double* sval = reinterpret_cast<double*>(dyn) + wid * CAPW;
   int* scol = reinterpret_cast<int*>(dyn + 4 * CAPW * sizeof(double)) + wid * CAPW;
   const long long p = t * 128 + threadIdx.x;
@@ -539,7 +552,6 @@ __global__ void __launch_bounds__(128, 4) k_fill0(Prob pr, const int* __restrict
   const int cJ = valid ? (cnt[np + p] & CNT_MASK) : 0;
   int a, b;
   warp_pairs(pr.n, t * 128 + wid * 32, a, b);
-  // tile-local row offsets: warp scans + one exchange of the 4 warp totals
   int wtS, wtJ;
   int exS = warp_excl_scan(cS, wtS);
   int exJ = warp_excl_scan(cJ, wtJ);
@@ -563,34 +575,13 @@ __global__ void __launch_bounds__(128, 4) k_fill0(Prob pr, const int* __restrict
   }
   const bool far = valid && (b - a > 2 * WK);
   const bool nearp = valid && !far;
-  // 1) near pairs: both rows written directly (lane-contiguous, coalesced)
-  double kS = 0.0, kJ = 0.0;
+  if (far && fo.K) {
+    fo.K[p] = 0.0;
+    fo.K[np + p] = 0.0;
+  }
   const unsigned nearmask = __ballot_sync(FULL, nearp);
-  if (nearmask) {
-    const Seg gS = {nullptr, nullptr, fo.col + baseS, fo.val + baseS};
-    const Seg gJ = {nullptr, nullptr, fo.col + baseJ, fo.val + baseJ};
-    unsigned nm = nearmask;
-    do {
-      const int src = __ffs(nm) - 1;
-      nm &= nm - 1;
-      const int aa = __shfl_sync(FULL, a, src), bb = __shfl_sync(FULL, b, src);
-      const int oS = __shfl_sync(FULL, exS, src), oJ = __shfl_sync(FULL, exJ, src);
-      int c1, c2;
-      double k1, k2;
-      warp_near_pair<true, TW, SW>(pr, aa, bb, scr[wid], c1, c2, k1, k2, gS, oS, gJ, oJ);
-      if (lane == src) {
-        kS = k1;
-        kJ = k2;
-      }
-    } while (nm);
-  }
-  if (valid && fo.K) {
-    fo.K[p] = kS;
-    fo.K[np + p] = kJ;
-  }
-  // 2) far pairs: values in registers, rows staged per warp, copied out around the near rows
   double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
-  if (far) far_values<WK, WL>(pr, a, b, ux, uy);
+  if (far) far_values<WK, WL, PT>(pr, a, b, ux, uy);
 #pragma unroll
   for (int row = 0; row < 2; ++row) {  // S rows of the warp's 32 pairs, then their J rows
     const int c_me = row ? cJ : cS, ex_me = row ? exJ : exS, w0 = row ? pJ : pS, wt = row ? wtJ : wtS;
@@ -604,6 +595,42 @@ __global__ void __launch_bounds__(128, 4) k_fill0(Prob pr, const int* __restrict
     __syncwarp();
     warp_copy_out(scol, sval, gbase, w0, w0 + wt, nearmask, ex_me, c_me, fo.col, fo.val);
     __syncwarp();
+  }
+}
+
+// mode 0 fill, near pairs and D rows (one warp per item, rows written directly).  Runs after
+// k_fill_far, whose row_ptr entries give the near rows' offsets.
+template <int TW>
+__global__ void __launch_bounds__(128) k_fill_near(Prob pr, FillOut fo) {
+  constexpr int SW = 2 * TW + 2;
+  __shared__ double scr[4][Scr<TW, SW>::PER_WARP];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long item = (long long)blockIdx.x * 4 + wid;
+  const int W2 = 2 * pr.W;
+  const long long nnear = (long long)pr.n * W2;
+  const long long np = pr.np;
+  if (item < nnear) {
+    const int a = (int)(item / W2), b = a + 1 + (int)(item % W2);
+    if (b >= pr.n) return;
+    const long long p = (long long)pidx32(pr.n, a, b);
+    const long long oS = fo.row_ptr[p], oJ = fo.row_ptr[np + p];
+    const Seg sS = {nullptr, nullptr, fo.col + oS, fo.val + oS};
+    const Seg sJ = {nullptr, nullptr, fo.col + oJ, fo.val + oJ};
+    int c1, c2;
+    double k1, k2;
+    warp_near_pair<true, TW, SW>(pr, a, b, scr[wid], c1, c2, k1, k2, sS, 0, sJ, 0);
+    if (lane == 0 && fo.K) {
+      fo.K[p] = k1;
+      fo.K[np + p] = k2;
+    }
+  } else if (item < nnear + pr.n - 1) {
+    const int lam = (int)(item - nnear) + 1;
+    const long long off = fo.toff[2 * pr.npt + lam - 1];
+    if (lane == 0) fo.row_ptr[2 * np + lam - 1] = off;
+    const Seg sD = {nullptr, nullptr, fo.col + off, fo.val + off};
+    double kv;
+    warp_d_row<true>(pr, lam, scr[wid], scr[wid] + WIN_MAX + 2, kv, sD, 0);
+    if (lane == 0 && fo.K) fo.K[2 * np + lam - 1] = kv;
   }
 }
 
@@ -760,44 +787,58 @@ void setup_prob(sun_plan_s* pl, int which) {
   pr.mode = mode0_supported(pr.wK, pr.wL) ? 0 : 1;
   pr.tp = pr.mode == 0 ? THREAD_TP : WARP_TP;
   pr.npt = (pr.np + pr.tp - 1) / pr.tp;
-  int dpt = (pr.mode == 0 ? THREAD_TP : WARP_THREADS) / 32;
-  pr.ndt = (pl->n - 1 + dpt - 1) / dpt;
+  pr.ndt = pr.mode == 0 ? (pl->n - 1) : (pl->n - 1 + WARP_THREADS / 32 - 1) / (WARP_THREADS / 32);
 }
 
 
-template <int WK, int WL>
-cudaError_t launch_count0(const Prob& pr, int* cnt, int* ts, cudaStream_t st) {
-  k_count0<WK, WL><<<(unsigned)(pr.npt + pr.ndt), 128, 0, st>>>(pr, cnt, ts);
-  return cudaGetLastError();
-}
-
-template <int WK, int WL>
-cudaError_t launch_fill0(const Prob& pr, const int* cnt, const FillOut& fo, cudaStream_t st) {
+template <int WK, int WL, int PT>
+cudaError_t launch_far(const Prob& pr, int* cnt, int* ts, const FillOut* fo, cudaStream_t st) {
+  if (!fo) {
+    k_count_far<WK, WL, PT><<<(unsigned)pr.npt, 128, 0, st>>>(pr, cnt, ts);
+    return cudaGetLastError();
+  }
   const size_t smem = (size_t)4 * CAPW * (sizeof(double) + sizeof(int));
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_fill0<WK, WL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k_fill_far<WK, WL, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  k_fill0<WK, WL><<<(unsigned)(pr.npt + pr.ndt), 128, smem, st>>>(pr, cnt, fo);
+  k_fill_far<WK, WL, PT><<<(unsigned)pr.npt, 128, smem, st>>>(pr, cnt, *fo);
   return cudaGetLastError();
 }
 
-cudaError_t dispatch_count0(const Prob& pr, int* cnt, int* ts, cudaStream_t st) {
-  if (pr.wK == 0) return launch_count0<0, 0>(pr, cnt, ts, st);
-  if (pr.wK == 1) return launch_count0<1, 0>(pr, cnt, ts, st);
-  if (pr.wK == 2 && pr.wL == 0) return launch_count0<2, 0>(pr, cnt, ts, st);
-  if (pr.wK == 2 && pr.wL == 1) return launch_count0<2, 1>(pr, cnt, ts, st);
-  return launch_count0<3, 0>(pr, cnt, ts, st);
+// (WK, WL, PT) instantiations of the mode-0 far kernels
+#define SUN_MODE0_LIST(X) \
+  X(0, 0, 0) X(1, 0, 0) X(2, 0, 0) X(3, 0, 0) X(0, 0, 1) X(1, 0, 1) X(2, 0, 1) X(3, 0, 1) X(2, 1, 1) \
+  X(0, 0, -1) X(1, 0, -1) X(2, 0, -1) X(3, 0, -1) X(2, 1, -1)
+
+int mode0_pt(const Prob& pr) { return pr.P == 0 ? 0 : (pr.P == 1 ? 1 : -1); }
+
+cudaError_t dispatch_far(const Prob& pr, int* cnt, int* ts, const FillOut* fo, cudaStream_t st) {
+  const int pt = mode0_pt(pr);
+#define SUN_X(WK, WL, PT) \
+  if (pr.wK == WK && pr.wL == WL && pt == PT) return launch_far<WK, WL, PT>(pr, cnt, ts, fo, st);
+  SUN_MODE0_LIST(SUN_X)
+#undef SUN_X
+  return cudaErrorInvalidValue;
 }
 
-cudaError_t dispatch_fill0(const Prob& pr, const int* cnt, const FillOut& fo, cudaStream_t st) {
-  if (pr.wK == 0) return launch_fill0<0, 0>(pr, cnt, fo, st);
-  if (pr.wK == 1) return launch_fill0<1, 0>(pr, cnt, fo, st);
-  if (pr.wK == 2 && pr.wL == 0) return launch_fill0<2, 0>(pr, cnt, fo, st);
-  if (pr.wK == 2 && pr.wL == 1) return launch_fill0<2, 1>(pr, cnt, fo, st);
-  return launch_fill0<3, 0>(pr, cnt, fo, st);
+cudaError_t dispatch_near(const Prob& pr, int* cnt, int* ts, const FillOut* fo, cudaStream_t st) {
+  const long long items = (long long)pr.n * 2 * pr.W + (pr.n - 1);
+  const unsigned grid = (unsigned)((items + 3) / 4);
+  if (grid == 0) return cudaSuccess;
+#define SUN_NEAR(TW)                                                            \
+  if (2 * pr.W + 1 == TW) {                                                     \
+    if (!fo)                                                                    \
+      k_count_near<TW><<<grid, 128, 0, st>>>(pr, cnt, ts);                      \
+    else                                                                        \
+      k_fill_near<TW><<<grid, 128, 0, st>>>(pr, *fo);                           \
+    return cudaGetLastError();                                                  \
+  }
+  SUN_NEAR(1) SUN_NEAR(3) SUN_NEAR(5) SUN_NEAR(7)
+#undef SUN_NEAR
+  return cudaErrorInvalidValue;
 }
 
 // exclusive scan of nslots int32 tile sums into int64 offsets; total -> nnz_out
@@ -992,7 +1033,8 @@ int sun_count(sun_plan pl, void* stream) {
     int* ts = (int*)(ws + (which ? L.ts1 : L.ts0));
     const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
     if (pr.mode == 0) {
-      CK(dispatch_count0(pr, cnt, ts, st));
+      CK(dispatch_far(pr, cnt, ts, nullptr, st));   // far pairs (writes the tile sums)
+      CK(dispatch_near(pr, cnt, ts, nullptr, st));  // near pairs + D rows (atomic adds)
     } else {
       k_count1<<<(unsigned)(pr.npt + pr.ndt), WARP_THREADS, 0, st>>>(pr, fp, pl->npos_far[which], cnt, ts);
       CK(cudaGetLastError());
@@ -1047,7 +1089,8 @@ int sun_unfold(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream)
     FillOut fo = {Q->row_ptr, Q->col, Q->val, which ? nullptr : K,
                   (const long long*)(ws + (which ? L.toff1 : L.toff0)), &hdr->nnz[which]};
     if (pr.mode == 0) {
-      CK(dispatch_fill0(pr, cnt, fo, st));
+      CK(dispatch_far(pr, const_cast<int*>(cnt), nullptr, &fo, st));
+      CK(dispatch_near(pr, nullptr, nullptr, &fo, st));
     } else {
       k_fill1<<<(unsigned)(pr.npt + pr.ndt), WARP_THREADS, 0, st>>>(pr, fp, pl->npos_far[which], cnt, fo);
       CK(cudaGetLastError());

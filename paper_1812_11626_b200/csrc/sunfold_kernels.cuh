@@ -544,7 +544,8 @@ __device__ __forceinline__ void far_foreach(F&& f) {
   }
 }
 
-template <int WK, int WL>
+// PT: number of dissipators if known at compile time (0 or 1), -1 = runtime pr.P.
+template <int WK, int WL, int PT>
 __device__ __forceinline__ void far_values(const Prob& pr, int a, int b, double (&ux)[FarT<WK, WL>::NPOS],
                                            double (&uy)[FarT<WK, WL>::NPOS]) {
   constexpr int W = WK;
@@ -558,14 +559,16 @@ __device__ __forceinline__ void far_values(const Prob& pr, int a, int b, double 
     const int d = b + i - W;  // K(d, b): row d, offset b - d = W - i
     kr[i] = d < n ? __ldg(&pr.K.v[(long long)d * SK + (2 * W - i)]) : make_double2(0.0, 0.0);
   }
+  // outer block O_ij = sum_p conj(Lt_p(a, a-WL+i)) Lt_p(b, b-WL+j)
   double ox[SL][SL], oy[SL][SL];
+  if constexpr (PT == 0) {
 #pragma unroll
-  for (int i = 0; i < SL; ++i)
+    for (int i = 0; i < SL; ++i)
 #pragma unroll
-    for (int j = 0; j < SL; ++j) ox[i][j] = oy[i][j] = 0.0;
-  for (int p = 0; p < pr.P; ++p) {
-    const double2* La = pr.L + ((long long)p * n + a) * SL;  // row a: L(a, a - WL + i)
-    const double2* Lb = pr.L + ((long long)p * n + b) * SL;
+      for (int j = 0; j < SL; ++j) ox[i][j] = oy[i][j] = 0.0;  // unused (no dissipators)
+  } else if constexpr (PT == 1) {
+    const double2* La = pr.L + (long long)a * SL;
+    const double2* Lb = pr.L + (long long)b * SL;
     double2 la[SL], lb[SL];
 #pragma unroll
     for (int i = 0; i < SL; ++i) {
@@ -576,24 +579,60 @@ __device__ __forceinline__ void far_values(const Prob& pr, int a, int b, double 
     for (int i = 0; i < SL; ++i)
 #pragma unroll
       for (int j = 0; j < SL; ++j) {
-        ox[i][j] += la[i].x * lb[j].x + la[i].y * lb[j].y;  // conj(la) lb
-        oy[i][j] += la[i].x * lb[j].y - la[i].y * lb[j].x;
+        ox[i][j] = la[i].x * lb[j].x + la[i].y * lb[j].y;
+        oy[i][j] = la[i].x * lb[j].y - la[i].y * lb[j].x;
       }
+  } else if constexpr (PT == -1) {
+#pragma unroll
+    for (int i = 0; i < SL; ++i)
+#pragma unroll
+      for (int j = 0; j < SL; ++j) ox[i][j] = oy[i][j] = 0.0;
+    for (int p = 0; p < pr.P; ++p) {
+      const double2* La = pr.L + ((long long)p * n + a) * SL;
+      const double2* Lb = pr.L + ((long long)p * n + b) * SL;
+      double2 la[SL], lb[SL];
+#pragma unroll
+      for (int i = 0; i < SL; ++i) {
+        la[i] = __ldg(&La[i]);
+        lb[i] = __ldg(&Lb[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < SL; ++i)
+#pragma unroll
+        for (int j = 0; j < SL; ++j) {
+          ox[i][j] += la[i].x * lb[j].x + la[i].y * lb[j].y;
+          oy[i][j] += la[i].x * lb[j].y - la[i].y * lb[j].x;
+        }
+    }
   }
   far_foreach<WK, WL>([&](int k, int dc, int dd) {
+    const int adc = dc < 0 ? -dc : dc, add = dd < 0 ? -dd : dd;
+    const bool hasO = PT != 0 && adc <= WL && add <= WL;
     double x = 0.0, y = 0.0;
+    bool init = false;
+    if (hasO) {
+      x = ox[dc + WL][dd + WL];
+      y = oy[dc + WL][dd + WL];
+      init = true;
+    }
     if (dd == 0) {  // + i K_ca
-      x -= kc[dc + W].y;
-      y += kc[dc + W].x;
+      if (init) {
+        x -= kc[dc + W].y;
+        y += kc[dc + W].x;
+      } else {
+        x = -kc[dc + W].y;
+        y = kc[dc + W].x;
+        init = true;
+      }
     }
     if (dc == 0) {  // - i conj(K_db)
-      x -= kr[dd + W].y;
-      y -= kr[dd + W].x;
-    }
-    const int adc = dc < 0 ? -dc : dc, add = dd < 0 ? -dd : dd;
-    if (adc <= WL && add <= WL) {
-      x += ox[dc + WL][dd + WL];
-      y += oy[dc + WL][dd + WL];
+      if (init) {
+        x -= kr[dd + W].y;
+        y -= kr[dd + W].x;
+      } else {
+        x = -kr[dd + W].y;
+        y = -kr[dd + W].x;
+      }
     }
     ux[k] = x;
     uy[k] = y;
