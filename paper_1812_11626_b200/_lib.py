@@ -40,6 +40,8 @@ SIGNATURES = {
     "sun_plan_nnz": (ctypes.c_int, [P, P, P]),
     "sun_unfold": (ctypes.c_int, [P, P, P, P, P]),
     "sun_apply": (ctypes.c_int, [P, P, ctypes.c_double, P, P, P, P]),
+    "sun_run": (ctypes.c_int, [P, P, P, P, P]),
+    "sun_nnz_bound": (ctypes.c_int64, [P, ctypes.c_int32]),
     "sun_plan_info": (ctypes.c_int, [P, P]),
     "sun_plan_destroy": (None, [P]),
     "sun_status_string": (ctypes.c_char_p, [ctypes.c_int]),

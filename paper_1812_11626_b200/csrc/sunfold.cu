@@ -26,7 +26,7 @@ namespace {
 
 constexpr int MAXOPS = 66;     // H0, H1 and up to 64 dissipators
 constexpr int WLMAX = WMAX / 2;  // wK >= 2 wL
-constexpr int F_MALFORMED = 1, F_H0_NOT_HERM = 2, F_H1_NOT_HERM = 4;
+constexpr int F_MALFORMED = 1, F_H0_NOT_HERM = 2, F_H1_NOT_HERM = 4, F_PATTERN = 8;
 constexpr int THREAD_TP = 128;   // mode 0: pairs per tile == threads per CTA (4 warps)
 constexpr int WARP_TP = 64;      // mode 1: pairs per tile
 constexpr int WARP_THREADS = 256;
@@ -36,6 +36,7 @@ struct DevHeader {
   int flags;
   int pad;
   long long nnz[2];  // written by the scan of each output matrix
+  double tau[2];     // drop thresholds of Q0 / Q1 (R6), computed on the device
   int bw[MAXOPS];
   double nrm2[MAXOPS];
 };
@@ -47,12 +48,20 @@ struct OpDesc {
 };
 struct OpList {
   OpDesc op[MAXOPS];
+  int wplan[MAXOPS];     // planned half-bandwidth per operator (-1: no check)
+  double sqrtg[MAXOPS];  // sqrt(gamma_p) for the dissipators (ops 2..)
+  double gamma[MAXOPS];
   int nops;
   int n;
+  int has_h1;
 };
 
 // mode-0 instantiations (compile-time band widths); anything else runs in mode 1
 bool mode0_supported(int wK, int wL) { return (wK <= 3 && wL == 0) || (wK == 2 && wL == 1); }
+
+struct Gammas {
+  double g[MAXOPS];
+};
 
 thread_local char g_errbuf[512];
 
@@ -99,6 +108,8 @@ Layout make_layout(int n, int P) {
 
 struct sun_plan_s {
   int n, P, has_h1;
+  OpList ops;      // operator descriptors (+ planned widths, rates) passed to the expand kernels
+  Gammas gam;
   FarPos hfp[2];   // far-position tables (host copies; uploaded in sun_plan_create)
   double hsqrtg[MAXOPS];
   sun_zcsr H0, H1;
@@ -111,6 +122,8 @@ struct sun_plan_s {
   double tau0, tau1, herm_tol0, herm_tol1;
   Prob pr[2];
   int counted;
+  int ran;            // last fill was enqueued by sun_run (capacity checked at sun_plan_nnz)
+  long long cap[2];   // capacities passed to the last fill
   cudaStream_t count_stream;
   long long nnz[2];
   int npos_far[2];
@@ -147,6 +160,7 @@ __global__ void k_analyze(OpList ops, DevHeader* hdr) {
     }
   }
   if (bad) atomicOr(&hdr->flags, F_MALFORMED);
+  if (ops.wplan[op] >= 0 && bw > ops.wplan[op]) atomicOr(&hdr->flags, F_PATTERN);
   atomicMax(&bwmax, bw);
   red[threadIdx.x] = acc;
   __syncthreads();
@@ -160,7 +174,8 @@ __global__ void k_analyze(OpList ops, DevHeader* hdr) {
   }
 }
 
-__global__ void k_zero(double* p, long long count) {
+__global__ void k_zero(double* p, long long count, int* flags) {
+  if (flags && blockIdx.x == 0 && threadIdx.x == 0) *flags = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
     p[i] = 0.0;
 }
@@ -168,7 +183,7 @@ __global__ void k_zero(double* p, long long count) {
 // (a1) CSR -> band storage.  ops: 0 = H0 (into Hb0, width wK), 1 = H1 (Hb1, width wH1),
 // 2+p = L_p (Lb[p], width wL, scaled by sqrt(gamma_p)).  One thread per (operator, row).
 __global__ void k_scatter(OpList ops, int has_h1, double2* hb0, int wK, double2* hb1, int wH1, double2* lb,
-                          int wL, const double* __restrict__ sqrtg) {
+                          int wL) {
   const int n = ops.n;
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t >= (long long)ops.nops * n) return;
@@ -180,7 +195,7 @@ __global__ void k_scatter(OpList ops, int has_h1, double2* hb0, int wK, double2*
   double s = 1.0;
   if (op == 0) { dst = hb0; w = wK; }
   else if (op == 1) { dst = hb1; w = wH1; }
-  else { dst = lb + (long long)(op - 2) * n * (2 * wL + 1); w = wL; s = sqrtg[op - 2]; }
+  else { dst = lb + (long long)(op - 2) * n * (2 * wL + 1); w = wL; s = ops.sqrtg[op]; }
   for (int64_t k = d.rp[r]; k < d.rp[r + 1]; ++k) {
     int o = d.ci[k] - r;
     if (o < -w || o > w) continue;  // only exact zeros can lie outside (bandwidth from k_analyze)
@@ -193,8 +208,17 @@ __global__ void k_scatter(OpList ops, int has_h1, double2* hb0, int wK, double2*
 // Also writes inv[l] = 1/sqrt(l(l+1)) (normalisation of D^l) for the D-chain kernels.
 __global__ void k_band_k(int n, int P, const double2* __restrict__ hb0, double2* kb0, int wK,
                          const double2* __restrict__ lb, int wL, const double2* __restrict__ hb1, int wH1,
-                         int has_h1, double tol0, double tol1, DevHeader* hdr, double* inv) {
+                         int has_h1, Gammas gam, DevHeader* hdr, double* inv) {
   long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // drop thresholds (R6) and Hermiticity tolerances from this call's norms
+  const double nh0 = sqrt(hdr->nrm2[0]), nh1 = has_h1 ? sqrt(hdr->nrm2[1]) : 0.0;
+  const double tol0 = 1e-12 * nh0, tol1 = 1e-12 * nh1;
+  if (t == 0) {
+    double s0 = nh0;
+    for (int p = 0; p < P; ++p) s0 += gam.g[p] * hdr->nrm2[2 + p];
+    hdr->tau[0] = 1e-14 * s0;
+    hdr->tau[1] = 1e-14 * nh1;
+  }
   if (t < n) inv[t] = t > 0 ? 1.0 / sqrt((double)t * (double)(t + 1)) : 0.0;
   const int sw = 2 * wK + 1;
   if (t >= (long long)n * sw) return;
@@ -241,7 +265,7 @@ template <int NTHREADS>
 __device__ __forceinline__ void count_d_tile(const Prob& pr, long long t, int* cnt, int* tsum, double* scr_w,
                                              int* wtot) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const Seg none = {nullptr, nullptr, nullptr, nullptr};
+  const Seg none = {nullptr, nullptr, 0};
   const long long u = t - pr.npt;
   int c = 0;
   const int lam = (int)(u * (NTHREADS / 32) + wid + 1);
@@ -268,6 +292,7 @@ struct Scr {
 // adds the near rows' counts to the same slots.
 template <int WK, int WL, int PT>
 __global__ void __launch_bounds__(128) k_count_far(Prob pr, int* __restrict__ cnt, int* __restrict__ tsum) {
+  pr.tau = *pr.tau_ptr;
   __shared__ int wred[8];
   const long long t = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -302,13 +327,14 @@ __global__ void __launch_bounds__(128) k_count_far(Prob pr, int* __restrict__ cn
 // slots with integer atomics (order-independent).  D rows have one slot each.
 template <int TW>
 __global__ void __launch_bounds__(128) k_count_near(Prob pr, int* __restrict__ cnt, int* __restrict__ tsum) {
+  pr.tau = *pr.tau_ptr;
   constexpr int SW = 2 * TW + 2;
   __shared__ double scr[4][Scr<TW, SW>::PER_WARP];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long item = (long long)blockIdx.x * 4 + wid;
   const int W2 = 2 * pr.W;
   const long long nnear = (long long)pr.n * W2;
-  const Seg none = {nullptr, nullptr, nullptr, nullptr};
+  const Seg none = {nullptr, nullptr, 0};
   if (item < nnear) {
     const int a = (int)(item / W2), b = a + 1 + (int)(item % W2);
     if (b >= pr.n) return;
@@ -335,6 +361,7 @@ __global__ void __launch_bounds__(128) k_count_near(Prob pr, int* __restrict__ c
 
 __global__ void __launch_bounds__(WARP_THREADS) k_count1(Prob pr, const FarPos* __restrict__ fp, int npos_far,
                                                          int* __restrict__ cnt, int* __restrict__ tsum) {
+  pr.tau = *pr.tau_ptr;
   constexpr int SW = WIN_MAX + 2;
   __shared__ double scr[WARP_THREADS / 32][Scr<0, SW>::PER_WARP];
   __shared__ int wtot[32];
@@ -350,7 +377,7 @@ __global__ void __launch_bounds__(WARP_THREADS) k_count1(Prob pr, const FarPos* 
     spos_dd[i] = fp->dd[i];
   }
   __syncthreads();
-  const Seg none = {nullptr, nullptr, nullptr, nullptr};
+  const Seg none = {nullptr, nullptr, 0};
   int cS = 0, cJ = 0;
   for (int i = wid; i < WARP_TP; i += nwarps) {
     const long long p = t * WARP_TP + i;
@@ -471,6 +498,7 @@ struct FillOut {
   int64_t* row_ptr;
   int32_t* col;
   double* val;
+  long long cap;  // capacity of col/val (writes at or beyond it are dropped; see sun_run)
   double* K;  // nullptr: not written (Q1)
   const long long* toff;
   const long long* nnz;
@@ -491,7 +519,7 @@ __device__ __forceinline__ void fill_d_tile(const Prob& pr, const FillOut& fo, l
   ex = __shfl_sync(FULL, ex, 0);
   if (valid) {
     if (lane == 0) fo.row_ptr[2 * np + lam - 1] = baseD + ex;
-    const Seg sD = {nullptr, nullptr, fo.col + baseD, fo.val + baseD};
+    const Seg sD = {fo.col + baseD, fo.val + baseD, fo.cap - baseD};
     double kv;
     warp_d_row<true>(pr, lam, scr_w, scr_w + WIN_MAX + 2, kv, sD, ex);
     if (lane == 0 && fo.K) fo.K[2 * np + lam - 1] = kv;
@@ -505,7 +533,7 @@ constexpr int CAPW = 1024;   // per-warp staging capacity (entries) in mode 0 (o
 // written directly.  The stage position advances only over copied entries.
 __device__ __forceinline__ void warp_copy_out(const int* scol, const double* sval, long long gbase, int g0, int g1,
                                               unsigned holes, int hoff, int hlen, int32_t* __restrict__ col,
-                                              double* __restrict__ val) {
+                                              double* __restrict__ val, long long cap) {
   const int lane = threadIdx.x & 31;
   int sp = 0, gp = g0;
   for (;;) {
@@ -517,7 +545,9 @@ __device__ __forceinline__ void warp_copy_out(const int* scol, const double* sva
       hs = __shfl_sync(FULL, hoff, h);
       hl = __shfl_sync(FULL, hlen, h);
     }
-    const int run = hs - gp;
+    long long run_l = hs - gp;
+    if (gbase + gp + run_l > cap) run_l = cap - (gbase + gp) > 0 ? cap - (gbase + gp) : 0;
+    const int run = (int)run_l;
     int32_t* cdst = col + gbase + gp;
     double* vdst = val + gbase + gp;
     for (int k = lane; k < run; k += 32) {
@@ -536,6 +566,7 @@ __device__ __forceinline__ void warp_copy_out(const int* scol, const double* sva
 // (written by k_fill_near).  Also writes row_ptr of all pair rows and K = 0 for far pairs.
 template <int WK, int WL, int PT>
 __global__ void __launch_bounds__(128) k_fill_far(Prob pr, const int* __restrict__ cnt, FillOut fo) {
+  pr.tau = *pr.tau_ptr;
   static_assert(64 * FarT<WK, WL>::NPOS <= CAPW, "far rows of a warp must fit the staging");
   extern __shared__ __align__(16) unsigned char dyn[];
   __shared__ int wtot[8];
@@ -593,7 +624,7 @@ __global__ void __launch_bounds__(128) k_fill_far(Prob pr, const int* __restrict
       far_emit_row<WK, WL>(pr.n, (int)np, pr.tau, a, b, row, ux, uy, n1, SmemSink{scol, sval}, ex_me - w0 - hb);
     }
     __syncwarp();
-    warp_copy_out(scol, sval, gbase, w0, w0 + wt, nearmask, ex_me, c_me, fo.col, fo.val);
+    warp_copy_out(scol, sval, gbase, w0, w0 + wt, nearmask, ex_me, c_me, fo.col, fo.val, fo.cap);
     __syncwarp();
   }
 }
@@ -602,6 +633,7 @@ __global__ void __launch_bounds__(128) k_fill_far(Prob pr, const int* __restrict
 // k_fill_far, whose row_ptr entries give the near rows' offsets.
 template <int TW>
 __global__ void __launch_bounds__(128) k_fill_near(Prob pr, FillOut fo) {
+  pr.tau = *pr.tau_ptr;
   constexpr int SW = 2 * TW + 2;
   __shared__ double scr[4][Scr<TW, SW>::PER_WARP];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -614,8 +646,8 @@ __global__ void __launch_bounds__(128) k_fill_near(Prob pr, FillOut fo) {
     if (b >= pr.n) return;
     const long long p = (long long)pidx32(pr.n, a, b);
     const long long oS = fo.row_ptr[p], oJ = fo.row_ptr[np + p];
-    const Seg sS = {nullptr, nullptr, fo.col + oS, fo.val + oS};
-    const Seg sJ = {nullptr, nullptr, fo.col + oJ, fo.val + oJ};
+    const Seg sS = {fo.col + oS, fo.val + oS, fo.cap - oS};
+    const Seg sJ = {fo.col + oJ, fo.val + oJ, fo.cap - oJ};
     int c1, c2;
     double k1, k2;
     warp_near_pair<true, TW, SW>(pr, a, b, scr[wid], c1, c2, k1, k2, sS, 0, sJ, 0);
@@ -627,7 +659,7 @@ __global__ void __launch_bounds__(128) k_fill_near(Prob pr, FillOut fo) {
     const int lam = (int)(item - nnear) + 1;
     const long long off = fo.toff[2 * pr.npt + lam - 1];
     if (lane == 0) fo.row_ptr[2 * np + lam - 1] = off;
-    const Seg sD = {nullptr, nullptr, fo.col + off, fo.val + off};
+    const Seg sD = {fo.col + off, fo.val + off, fo.cap - off};
     double kv;
     warp_d_row<true>(pr, lam, scr[wid], scr[wid] + WIN_MAX + 2, kv, sD, 0);
     if (lane == 0 && fo.K) fo.K[2 * np + lam - 1] = kv;
@@ -636,6 +668,7 @@ __global__ void __launch_bounds__(128) k_fill_near(Prob pr, FillOut fo) {
 
 __global__ void __launch_bounds__(WARP_THREADS) k_fill1(Prob pr, const FarPos* __restrict__ fp, int npos_far,
                                                         const int* __restrict__ cnt, FillOut fo) {
+  pr.tau = *pr.tau_ptr;
   constexpr int SW = WIN_MAX + 2;
   __shared__ double scr[WARP_THREADS / 32][Scr<0, SW>::PER_WARP];
   __shared__ int wtot[32];
@@ -670,8 +703,8 @@ __global__ void __launch_bounds__(WARP_THREADS) k_fill1(Prob pr, const FarPos* _
     fo.row_ptr[np + p0] = baseJ + exJ;
   }
   __syncthreads();
-  const Seg sS = {nullptr, nullptr, fo.col + baseS, fo.val + baseS};
-  const Seg sJ = {nullptr, nullptr, fo.col + baseJ, fo.val + baseJ};
+  const Seg sS = {fo.col + baseS, fo.val + baseS, fo.cap - baseS};
+  const Seg sJ = {fo.col + baseJ, fo.val + baseJ, fo.cap - baseJ};
   for (int i = wid; i < WARP_TP; i += nwarps) {
     const long long p = t * WARP_TP + i;
     if (p >= np) break;
@@ -764,6 +797,7 @@ void setup_prob(sun_plan_s* pl, int which) {
     pr.H = {reinterpret_cast<const double2*>(pl->ws + L.hb0), pl->wK};
     pr.L = reinterpret_cast<const double2*>(pl->ws + L.lb);
     pr.tau = pl->tau0;
+    pr.tau_ptr = &reinterpret_cast<DevHeader*>(pl->ws + L.hdr)->tau[0];
   } else {
     pr.P = 0;
     pr.wK = pl->wH1;
@@ -772,6 +806,7 @@ void setup_prob(sun_plan_s* pl, int which) {
     pr.H = pr.K;
     pr.L = nullptr;
     pr.tau = pl->tau1;
+    pr.tau_ptr = &reinterpret_cast<DevHeader*>(pl->ws + L.hdr)->tau[1];
   }
   pr.W = pr.wK > pr.wL ? pr.wK : pr.wL;
   pr.inv = reinterpret_cast<const double*>(pl->ws + L.inv);
@@ -933,9 +968,15 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
   memset(&ops, 0, sizeof(ops));
   ops.n = n;
   ops.nops = 2 + P;
+  ops.has_h1 = H1 != nullptr;
   ops.op[0] = {H0->row_ptr, H0->col, (const double2*)H0->val};
   ops.op[1] = H1 ? OpDesc{H1->row_ptr, H1->col, (const double2*)H1->val} : ops.op[0];
-  for (int p = 0; p < P; ++p) ops.op[2 + p] = {L[p]->row_ptr, L[p]->col, (const double2*)L[p]->val};
+  for (int p = 0; p < P; ++p) {
+    ops.op[2 + p] = {L[p]->row_ptr, L[p]->col, (const double2*)L[p]->val};
+    ops.sqrtg[2 + p] = sqrt(gamma[p]);
+    ops.gamma[2 + p] = gamma[p];
+  }
+  for (int i = 0; i < MAXOPS; ++i) ops.wplan[i] = -1;
   CK(cudaMemsetAsync(hdr, 0, sizeof(DevHeader), st));
   k_analyze<<<ops.nops, 256, 0, st>>>(ops, hdr);
   CK(cudaGetLastError());
@@ -973,20 +1014,25 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
   for (int p = 0; p < P; ++p) s0 += gamma[p] * h.nrm2[2 + p];
   pl->tau0 = 1e-14 * s0;
   pl->tau1 = H1 ? 1e-14 * sqrt(h.nrm2[1]) : 0.0;
-  pl->herm_tol0 = 1e-12 * sqrt(h.nrm2[0]);
-  pl->herm_tol1 = H1 ? 1e-12 * sqrt(h.nrm2[1]) : 0.0;
+  pl->ops = ops;
+  pl->ops.wplan[0] = pl->wH0;
+  pl->ops.wplan[1] = H1 ? pl->wH1 : -1;
+  for (int p = 0; p < P; ++p) {
+    pl->ops.wplan[2 + p] = pl->wL;
+    pl->gam.g[p] = gamma[p];
+  }
   setup_prob(pl, 0);
   if (pl->has_h1) setup_prob(pl, 1);
   if (pl->npos_far[0] > FAR_MAXPOS || (pl->has_h1 && pl->npos_far[1] > FAR_MAXPOS)) {
     delete pl;
     return SUN_ERR_BANDWIDTH;
   }
-  // constant per-plan tables
-  cudaError_t e = cudaMemcpyAsync(ws + lay.fp0, &pl->hfp[0], sizeof(FarPos), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess && pl->has_h1)
+  // far-position tables (used by the warp-per-pair mode only)
+  cudaError_t e = cudaSuccess;
+  if (pl->pr[0].mode == 1)
+    e = cudaMemcpyAsync(ws + lay.fp0, &pl->hfp[0], sizeof(FarPos), cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess && pl->has_h1 && pl->pr[1].mode == 1)
     e = cudaMemcpyAsync(ws + lay.fp1, &pl->hfp[1], sizeof(FarPos), cudaMemcpyHostToDevice, st);
-  if (e == cudaSuccess && P > 0)
-    e = cudaMemcpyAsync(ws + lay.sqrtg, pl->hsqrtg, P * sizeof(double), cudaMemcpyHostToDevice, st);
   if (e != cudaSuccess) {
     delete pl;
     return cuda_fail(e);
@@ -1004,27 +1050,22 @@ int sun_count(sun_plan pl, void* stream) {
   const int n = pl->n;
   char* ws = pl->ws;
   DevHeader* hdr = (DevHeader*)(ws + L.hdr);
-  // (a1) expand into band storage
+  // (a1) expand: norms + pattern check, band storage, K = H0 + i/2 M, tau (all on the device)
   long long zero_doubles = (long long)((L.ts0 - L.kb0) / sizeof(double));
-  k_zero<<<296, 256, 0, st>>>((double*)(ws + L.kb0), zero_doubles);
+  k_zero<<<296, 256, 0, st>>>((double*)(ws + L.kb0), zero_doubles, &hdr->flags);
   CK(cudaGetLastError());
-  OpList ops;
-  memset(&ops, 0, sizeof(ops));
-  ops.n = n;
-  ops.nops = 2 + pl->P;
-  ops.op[0] = {pl->H0.row_ptr, pl->H0.col, (const double2*)pl->H0.val};
-  ops.op[1] = pl->has_h1 ? OpDesc{pl->H1.row_ptr, pl->H1.col, (const double2*)pl->H1.val} : ops.op[0];
-  for (int p = 0; p < pl->P; ++p) ops.op[2 + p] = {pl->L[p].row_ptr, pl->L[p].col, (const double2*)pl->L[p].val};
-  long long nthreads = (long long)ops.nops * n;
+  k_analyze<<<pl->ops.nops, 256, 0, st>>>(pl->ops, hdr);
+  CK(cudaGetLastError());
+  long long nthreads = (long long)pl->ops.nops * n;
   k_scatter<<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(
-      ops, pl->has_h1, (double2*)(ws + L.hb0), pl->wK, (double2*)(ws + L.hb1), pl->wH1, (double2*)(ws + L.lb),
-      pl->wL, (const double*)(ws + L.sqrtg));
+      pl->ops, pl->has_h1, (double2*)(ws + L.hb0), pl->wK, (double2*)(ws + L.hb1), pl->wH1, (double2*)(ws + L.lb),
+      pl->wL);
   CK(cudaGetLastError());
   long long nk = (long long)n * (2 * pl->wK + 1);
   if (nk < n) nk = n;
   k_band_k<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(
       n, pl->P, (const double2*)(ws + L.hb0), (double2*)(ws + L.kb0), pl->wK, (const double2*)(ws + L.lb), pl->wL,
-      (const double2*)(ws + L.hb1), pl->wH1, pl->has_h1, pl->herm_tol0, pl->herm_tol1, hdr, (double*)(ws + L.inv));
+      (const double2*)(ws + L.hb1), pl->wH1, pl->has_h1, pl->gam, hdr, (double*)(ws + L.inv));
   CK(cudaGetLastError());
   // (a3) count pass + (a4) prefix scan, per output matrix
   for (int which = 0; which < 1 + pl->has_h1; ++which) {
@@ -1043,6 +1084,7 @@ int sun_count(sun_plan pl, void* stream) {
                    &hdr->nnz[which], st));
   }
   pl->counted = 1;
+  pl->ran = 0;
   pl->count_stream = st;
   pl->nnz[0] = pl->nnz[1] = -1;
   return SUN_OK;
@@ -1055,38 +1097,36 @@ int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
     int flags;
     int pad;
     long long nnz[2];
+    double tau[2];
   } h;
   CK(cudaMemcpyAsync(&h, pl->ws + pl->lay.hdr, sizeof(h), cudaMemcpyDeviceToHost, pl->count_stream));
   CK(cudaStreamSynchronize(pl->count_stream));
   if (h.flags & (F_H0_NOT_HERM | F_H1_NOT_HERM)) return SUN_ERR_NOT_HERMITIAN;
+  if (h.flags & F_PATTERN) return SUN_ERR_BANDWIDTH;
+  pl->tau0 = h.tau[0];
+  pl->tau1 = pl->has_h1 ? h.tau[1] : 0.0;
   if (h.flags & F_MALFORMED) return SUN_ERR_ARG;
   pl->nnz[0] = h.nnz[0];
   pl->nnz[1] = pl->has_h1 ? h.nnz[1] : 0;
   if (nnz_q0) *nnz_q0 = pl->nnz[0];
   if (nnz_q1) *nnz_q1 = pl->nnz[1];
+  if (pl->ran) {
+    pl->ran = 0;
+    if (pl->nnz[0] > pl->cap[0] || pl->nnz[1] > pl->cap[1]) return SUN_ERR_CAPACITY;
+  }
   return SUN_OK;
 }
 
-int sun_unfold(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream) {
-  if (!pl || !Q0 || !K) return SUN_ERR_ARG;
-  if (!pl->counted || pl->nnz[0] < 0) return SUN_ERR_STATE;
-  if (pl->has_h1 && !Q1) return SUN_ERR_ARG;
-  cudaStream_t st = (cudaStream_t)stream;
+static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st) {
   const Layout& L = pl->lay;
   char* ws = pl->ws;
-  const long long m = (long long)pl->n * pl->n - 1;
-  for (int which = 0; which < 1 + pl->has_h1; ++which) {
-    sun_dcsr* Q = which ? Q1 : Q0;
-    if (Q->m != m || !Q->row_ptr || (pl->nnz[which] > 0 && (!Q->col || !Q->val))) return SUN_ERR_ARG;
-    if (Q->nnz < pl->nnz[which]) return SUN_ERR_CAPACITY;
-  }
   for (int which = 0; which < 1 + pl->has_h1; ++which) {
     sun_dcsr* Q = which ? Q1 : Q0;
     const Prob& pr = pl->pr[which];
     const int* cnt = (const int*)(ws + (which ? L.cnt1 : L.cnt0));
     const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
     DevHeader* hdr = (DevHeader*)(ws + L.hdr);
-    FillOut fo = {Q->row_ptr, Q->col, Q->val, which ? nullptr : K,
+    FillOut fo = {Q->row_ptr, Q->col, Q->val, (long long)Q->nnz, which ? nullptr : K,
                   (const long long*)(ws + (which ? L.toff1 : L.toff0)), &hdr->nnz[which]};
     if (pr.mode == 0) {
       CK(dispatch_far(pr, const_cast<int*>(cnt), nullptr, &fo, st));
@@ -1097,6 +1137,55 @@ int sun_unfold(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream)
     }
   }
   return SUN_OK;
+}
+
+static int check_outputs(sun_plan pl, const sun_dcsr* Q0, const sun_dcsr* Q1, const double* K) {
+  if (!Q0 || !K) return SUN_ERR_ARG;
+  if (pl->has_h1 && !Q1) return SUN_ERR_ARG;
+  const long long m = (long long)pl->n * pl->n - 1;
+  for (int which = 0; which < 1 + pl->has_h1; ++which) {
+    const sun_dcsr* Q = which ? Q1 : Q0;
+    if (Q->m != m || !Q->row_ptr || Q->nnz < 0 || (Q->nnz > 0 && (!Q->col || !Q->val))) return SUN_ERR_ARG;
+  }
+  return SUN_OK;
+}
+
+int sun_unfold(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream) {
+  if (!pl) return SUN_ERR_ARG;
+  if (!pl->counted || pl->nnz[0] < 0) return SUN_ERR_STATE;
+  int st = check_outputs(pl, Q0, Q1, K);
+  if (st != SUN_OK) return st;
+  for (int which = 0; which < 1 + pl->has_h1; ++which)
+    if ((which ? Q1 : Q0)->nnz < pl->nnz[which]) return SUN_ERR_CAPACITY;
+  pl->cap[0] = Q0->nnz;
+  pl->cap[1] = Q1 ? Q1->nnz : 0;
+  return enqueue_fill(pl, Q0, Q1, K, (cudaStream_t)stream);
+}
+
+int sun_run(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream) {
+  if (!pl) return SUN_ERR_ARG;
+  int st = check_outputs(pl, Q0, Q1, K);
+  if (st != SUN_OK) return st;
+  st = sun_count(pl, stream);
+  if (st != SUN_OK) return st;
+  pl->cap[0] = Q0->nnz;
+  pl->cap[1] = Q1 ? Q1->nnz : 0;
+  pl->ran = 1;
+  return enqueue_fill(pl, Q0, Q1, K, (cudaStream_t)stream);
+}
+
+int64_t sun_nnz_bound(sun_plan pl, int32_t which) {
+  if (!pl || which < 0 || which > 1 || (which == 1 && !pl->has_h1)) return -1;
+  const Prob& pr = pl->pr[which];
+  const long long n = pl->n;
+  const long long W = pr.W;
+  const long long nw = 4 * W + 1 < n ? 4 * W + 1 : n;          // near-pair window
+  const long long nwd = 2 * pr.wK + 1 < n ? 2 * pr.wK + 1 : n;  // D-row window
+  const long long nnear = n * 2 * W < pr.np ? n * 2 * W : pr.np;
+  long long far_row = 2LL * pl->npos_far[which];
+  long long near_row = nw * (nw - 1) + (n - 1);
+  if (far_row > near_row) far_row = near_row;
+  return 2 * (pr.np - nnear) * far_row + 2 * nnear * near_row + (n - 1) * (nwd * (nwd - 1) + (n - 1));
 }
 
 int sun_apply(const sun_dcsr* Q0, const sun_dcsr* Q1, double eps, const double* K, const double* v, double* dvdt,
@@ -1128,8 +1217,8 @@ int sun_plan_info(sun_plan pl, sun_plan_info_t* info) {
   info->mode_q1 = pl->has_h1 ? pl->pr[1].mode : -1;
   info->pairs_per_tile_q0 = pl->pr[0].tp;
   info->pairs_per_tile_q1 = pl->has_h1 ? pl->pr[1].tp : 0;
-  info->tiles_q0 = pl->pr[0].npt + pl->pr[0].ndt;
-  info->tiles_q1 = pl->has_h1 ? pl->pr[1].npt + pl->pr[1].ndt : 0;
+  info->tiles_q0 = 2 * pl->pr[0].npt + pl->pr[0].ndt;
+  info->tiles_q1 = pl->has_h1 ? 2 * pl->pr[1].npt + pl->pr[1].ndt : 0;
   info->has_h1 = pl->has_h1;
   info->npos_far_q0 = pl->npos_far[0];
   info->npos_far_q1 = pl->has_h1 ? pl->npos_far[1] : 0;

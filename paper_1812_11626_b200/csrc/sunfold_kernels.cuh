@@ -56,7 +56,8 @@ struct Prob {
   Band K, H;
   const double2* L;    // P bands of half-width wL (sqrt(gamma)-scaled)
   const double* inv;   // inv[l] = 1/sqrt(l(l+1)), l = 1..n-1
-  double tau;
+  const double* tau_ptr;  // drop threshold in device memory (computed by the expand step)
+  double tau;             // loaded from tau_ptr at kernel entry
   int mode;            // 0 thread-per-pair (staged), 1 warp-per-pair (direct)
   int tp;              // pairs per tile
   long long npt, ndt;  // pair tiles, D tiles
@@ -183,18 +184,14 @@ __device__ __forceinline__ double2 G_elem(const Prob& pr, int lam, double alpha,
 }
 
 // ---------------------------------------------------------------------------------------
-// Output sink: a contiguous CSR segment in shared staging or global memory.
+// Output sink: a contiguous CSR segment in global memory (writes beyond the capacity dropped).
 // ---------------------------------------------------------------------------------------
 struct Seg {
-  int* scol;  // shared staging (nullptr: write global)
-  double* sval;
-  int32_t* gcol;  // global col/val base pointers already offset to the segment start
+  int32_t* gcol;  // global col/val pointers already offset to the segment start
   double* gval;
+  long long lim;  // entries writable from the segment start (output capacity - start)
   __device__ __forceinline__ void emit(long long off, int col, double v) const {
-    if (scol) {
-      scol[off] = col;
-      sval[off] = v;
-    } else {
+    if (off < lim) {
       gcol[off] = col;
       gval[off] = v;
     }

@@ -195,3 +195,24 @@ def test_error_codes():
     with pytest.raises(sun.SunError, match="dimension"):
         sun.Plan(p.H0, None, other.Ls, other.gammas)
     plan.close()
+
+
+def test_run_single_pass_matches_two_pass_and_capacity_fallback():
+    """sun_run (no host round trip) == sun_count/sun_plan_nnz/sun_unfold, byte for byte; an
+    undersized output is reported (SUN_ERR_CAPACITY) and refilled exactly."""
+    sun = _gpu()
+    prob = config(2)
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    b0, b1 = plan.nnz_bound()
+    A = plan.run()  # first call: capacity = structural bound
+    B = plan.run_two_pass()
+    torch.cuda.synchronize()
+    assert A[0].nnz <= b0 and A[1].nnz <= b1
+    for x, y in ((A[0], B[0]), (A[1], B[1])):
+        assert torch.equal(x.row_ptr, y.row_ptr) and torch.equal(x.col, y.col) and torch.equal(x.val, y.val)
+    assert torch.equal(A[2], B[2])
+    small = plan._alloc(A[0].nnz - 7, A[1].nnz)
+    C = plan.run(out=small)
+    torch.cuda.synchronize()
+    assert torch.equal(C[0].col, B[0].col) and torch.equal(C[0].val, B[0].val)
+    plan.close()
