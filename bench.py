@@ -236,12 +236,18 @@ def main():
         e1.record(stream)
         return e0, e1, q
 
+    # warm-up with the timed loop's allocation pattern (two previous outputs kept alive), so
+    # the caching allocator holds every block the timed steps use (no cudaMalloc inside)
+    keep = []
     for _ in range(args.warmup):
-        nnz_total, _ = one_step([])
+        flush.fill_(1.0)
+        nnz_total, out = one_step([])
+        keep.append(out)
+        if len(keep) > 2:
+            keep.pop(0)
     torch.cuda.synchronize()
 
     timings = []
-    keep = []
     barrier(world)
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:

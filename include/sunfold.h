@@ -92,11 +92,13 @@ typedef struct {
   int32_t n, P;
   int32_t w_h0, w_h1, w_l, w_k; /* half-bandwidths: H0, H1, max_p L_p, K = H0 + i/2 sum gamma L^+L */
   double tau_q0, tau_q1;        /* drop thresholds (R6) */
-  int32_t mode_q0, mode_q1;     /* 0: thread-per-pair with shared-memory staging; 1: warp-per-pair */
+  int32_t mode_q0, mode_q1;     /* 0: group-per-pair kernels, compile-time widths; 1: warp-per-pair */
   int32_t pairs_per_tile_q0, pairs_per_tile_q1;
-  int64_t tiles_q0, tiles_q1;   /* row-tile scan slots (S tiles, J tiles, D tiles/rows) */
+  int64_t tiles_q0, tiles_q1;   /* scan slots (S tiles, J tiles, D slots) */
   int32_t has_h1;
   int32_t npos_far_q0, npos_far_q1; /* candidate positions per far pair */
+  int32_t launches_count;       /* kernels enqueued by sun_count (expand, count, scan) */
+  int32_t launches_fill;        /* kernels enqueued by sun_unfold (sun_run = both) */
 } sun_plan_info_t;
 
 /* Bytes of device workspace a plan for dimension n with P dissipators needs (0 if n or P is

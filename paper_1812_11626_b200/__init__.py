@@ -219,17 +219,9 @@ class Plan:
         return self.fill(nnz0, nnz1, out)
 
     def launches_per_run(self) -> int:
-        """Kernels of this library launched by one run() (count + fill), from the plan geometry."""
+        """Kernels of this library launched by one run() (sun_run: count + fill)."""
         inf = self.info()
-        total = 4  # expand: k_zero, k_analyze, k_scatter, k_band_k (first-call sizing adds no kernels)
-        for q in ("q0", "q1") if inf["has_h1"] else ("q0",):
-            nslots_large = inf[f"tiles_{q}"] > 16384  # multi-level scan
-            scan = 3 if nslots_large else 1
-            if inf[f"mode_{q}"] == 0:
-                total += 2 + scan + 2  # count_far, count_near, scan, fill_far, fill_near
-            else:
-                total += 1 + scan + 1  # count1, scan, fill1
-        return total
+        return int(inf["launches_count"] + inf["launches_fill"])
 
     def info(self) -> dict:
         inf = _lib.SunPlanInfo()

@@ -30,6 +30,7 @@ class SunPlanInfo(ctypes.Structure):
         ("tiles_q0", ctypes.c_int64), ("tiles_q1", ctypes.c_int64),
         ("has_h1", ctypes.c_int32),
         ("npos_far_q0", ctypes.c_int32), ("npos_far_q1", ctypes.c_int32),
+        ("launches_count", ctypes.c_int32), ("launches_fill", ctypes.c_int32),
     ]
 
 
@@ -62,8 +63,8 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    path = _build.LIB
-    if _build.stale():
+    path = os.environ.get("SUNFOLD_LIB") or _build.LIB  # SUNFOLD_LIB: diagnostics builds only
+    if path == _build.LIB and _build.stale():
         try:
             _build.build()
         except Exception as e:  # no fallback: the product path needs the CUDA library

@@ -1,13 +1,19 @@
 // sunfold.cu — C-ABI and launch logic of the B200 SU(N) unfold (include/sunfold.h).
 //
-// Pipeline (Table I Step 2; two-step CRS fill P:369-370):
-//   sun_plan_create : k_analyze   bandwidths, Frobenius norms, CSR validation  -> 1 readback
-//   sun_count       : k_zero, k_scatter, k_band_k   (a1) expand to band storage, K = H + i/2 M
-//                     k_count0<WK,WL> / k_count1     (a3) per-row counts (values thresholded) and
-//                                                    (a4) tile offsets by decoupled look-back
-//   sun_plan_nnz    : readback of the chain totals (nnz Q0, Q1) + validation flags
-//   sun_unfold      : k_fill0<WK,WL> / k_fill1       (a5) row_ptr, col, val, K; (a6) Q1
-//   sun_apply       : k_apply                        (a7) dv/dt = Q0 v + eps Q1 v + K
+// Pipeline (Table I Step 2; two-step CRS fill P:369-370), launches per sun_run:
+//   sun_plan_create : k_analyze         bandwidths, Frobenius norms, CSR validation -> 1 readback
+//   sun_count       : k_expand_rows     (a1) CSR -> band storage, per-block norms / flags, zeroing
+//                     k_expand_k        (a1) K = H0 + i/2 sum gamma L^+L, tau, inv[l], Hermiticity
+//                     k_count0 / k_count1 (a3) per-row counts (values thresholded), tile sums;
+//                                        one launch per output matrix (near items + far tiles),
+//                                        Q1's on an auxiliary stream
+//                     k_scan_chain      (a4) chained (decoupled look-back) scan of the tile sums of
+//                                        both matrices -> int64 tile offsets and nnz
+//   sun_plan_nnz    : readback of nnz + validation flags (16 B + header)
+//   sun_unfold      : k_fill_far0 + k_fill_near0 / k_fill1  (a5) row_ptr, col, val, K; (a6) Q1
+//                                        Q0 far tiles on the caller's stream, Q0 near items and Q1
+//                                        on two auxiliary streams (fork/join with events)
+//   sun_apply       : k_apply           (a7) dv/dt = Q0 v + eps Q1 v + K
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -24,21 +30,37 @@ using namespace sunk;
 
 namespace {
 
-constexpr int MAXOPS = 66;     // H0, H1 and up to 64 dissipators
+constexpr int MAXOPS = 66;       // H0, H1 and up to 64 dissipators
 constexpr int WLMAX = WMAX / 2;  // wK >= 2 wL
-constexpr int F_MALFORMED = 1, F_H0_NOT_HERM = 2, F_H1_NOT_HERM = 4, F_PATTERN = 8;
-constexpr int THREAD_TP = 128;   // mode 0: pairs per tile == threads per CTA (4 warps)
-constexpr int WARP_TP = 64;      // mode 1: pairs per tile
+constexpr int F_MALFORMED = 1, F_PATTERN = 8;
+constexpr int TP0 = 256;          // mode 0: pairs per tile == threads per CTA (8 warps)
+constexpr int WARP_TP = 64;       // mode 1: pairs per tile
 constexpr int WARP_THREADS = 256;
 constexpr int FAR_MAXPOS = 1024;
+constexpr int EXP_THREADS = 256;  // k_expand_rows rows per CTA
+constexpr int SCAN_THREADS = 1024, SCAN_IPT = 4, SCAN_TILE = SCAN_THREADS * SCAN_IPT;
+constexpr unsigned long long SCAN_A = 1ull << 62, SCAN_P = 2ull << 62, SCAN_V = (1ull << 62) - 1;
 
+// Device header.  The prefix up to `ticket` is read back by sun_plan_nnz.
 struct DevHeader {
   int flags;
   int pad;
-  long long nnz[2];  // written by the scan of each output matrix
-  double tau[2];     // drop thresholds of Q0 / Q1 (R6), computed on the device
+  long long nnz[2];                  // written by the scan of each output matrix
+  double tau[2];                     // drop thresholds of Q0 / Q1 (R6), on the device
+  unsigned long long herm_dev[2];    // max |H - H^+| (component-wise) of H0, H1 (bits of a double >= 0)
+  double nrm2_h[2];                  // ||H0||_F^2, ||H1||_F^2 (this call's values)
+  unsigned int ticket[2];            // chained-scan chunk tickets
+  unsigned int done;                 // count-pass CTA completion counter (scan by the last CTA)
   int bw[MAXOPS];
   double nrm2[MAXOPS];
+};
+struct HeaderPrefix {
+  int flags;
+  int pad;
+  long long nnz[2];
+  double tau[2];
+  unsigned long long herm_dev[2];
+  double nrm2_h[2];
 };
 
 struct OpDesc {
@@ -56,8 +78,11 @@ struct OpList {
   int has_h1;
 };
 
-// mode-0 instantiations (compile-time band widths); anything else runs in mode 1
-bool mode0_supported(int wK, int wL) { return (wK <= 3 && wL == 0) || (wK == 2 && wL == 1); }
+struct BlkInfo {  // k_expand_rows -> k_expand_k, one per (operator, row block)
+  double nrm2;
+  int bw;
+  int flags;
+};
 
 struct Gammas {
   double g[MAXOPS];
@@ -68,39 +93,56 @@ thread_local char g_errbuf[512];
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct FarPos {
-  int dc[1024];
-  int dd[1024];
+  int dc[FAR_MAXPOS];
+  int dd[FAR_MAXPOS];
 };
 
 struct Layout {
-  size_t hdr, fp0, fp1, sqrtg, inv, kb0, hb0, hb1, lb, ts0, ts1, toff0, toff1, chunk, cnt0, cnt1, total;
-  long long maxslots;
+  size_t hdr, fp0, fp1, inv, kb0, hb0, hb1, lb, blk, ts0, ts1, st0, st1, toff0, toff1, cnt0, cnt1;
+  size_t side_col[2], side_val[2], side_meta[2], total;
+  long long side_rows;
+  long long maxslots, maxchunks, nrb;
 };
 
 Layout make_layout(int n, int P) {
   Layout L;
   long long m = (long long)n * n - 1;
   long long np = (long long)n * (n - 1) / 2;
-  long long maxslots = 2 * (np / 32 + 2) + n + 2;
+  // slots: S tiles + J tiles + D slots; the smallest tile is mode 1's 64 pairs
+  long long maxslots = 2 * (np / WARP_TP + 2) + n + 2;
+  long long maxchunks = (maxslots + SCAN_TILE - 1) / SCAN_TILE + 1;
+  long long nrb = (n + EXP_THREADS - 1) / EXP_THREADS;
   size_t off = 0;
   L.hdr = off; off = align256(off + sizeof(DevHeader));
   L.fp0 = off; off = align256(off + sizeof(FarPos));
   L.fp1 = off; off = align256(off + sizeof(FarPos));
-  L.sqrtg = off; off = align256(off + MAXOPS * sizeof(double));
   L.inv = off; off = align256(off + (size_t)n * sizeof(double));
-  L.kb0 = off; off = align256(off + (size_t)n * (2 * WMAX + 1) * sizeof(double2));  // [kb0, lb end) zeroed per count
+  L.kb0 = off; off = align256(off + (size_t)n * (2 * WMAX + 1) * sizeof(double2));
   L.hb0 = off; off = align256(off + (size_t)n * (2 * WMAX + 1) * sizeof(double2));
   L.hb1 = off; off = align256(off + (size_t)n * (2 * WMAX + 1) * sizeof(double2));
   L.lb = off;  off = align256(off + (size_t)(P > 0 ? P : 1) * n * (2 * WLMAX + 1) * sizeof(double2));
-  L.ts0 = off; off = align256(off + (size_t)maxslots * sizeof(int));
+  L.blk = off; off = align256(off + (size_t)(2 + P) * nrb * sizeof(BlkInfo));
+  L.ts0 = off; off = align256(off + (size_t)maxslots * sizeof(int));   // [ts0, toff0) zeroed per count
   L.ts1 = off; off = align256(off + (size_t)maxslots * sizeof(int));
+  L.st0 = off; off = align256(off + (size_t)maxchunks * sizeof(unsigned long long));
+  L.st1 = off; off = align256(off + (size_t)maxchunks * sizeof(unsigned long long));
   L.toff0 = off; off = align256(off + (size_t)maxslots * sizeof(long long));
   L.toff1 = off; off = align256(off + (size_t)maxslots * sizeof(long long));
-  L.chunk = off; off = align256(off + (size_t)(maxslots / 16384 + 2) * sizeof(long long));
   L.cnt0 = off; off = align256(off + (size_t)m * sizeof(int));
   L.cnt1 = off; off = align256(off + (size_t)m * sizeof(int));
+  // near-row side buffers of mode 0 (W <= 3): 2 rows per near item, (4W + 1)^2 entries per row
+  const long long side_rows = 2 * ((long long)n * 2 * 3 + n);
+  const long long ncmax = 13 * 13;
+  for (int k = 0; k < 2; ++k) {
+    L.side_col[k] = off; off = align256(off + (size_t)(side_rows * ncmax) * sizeof(int32_t));
+    L.side_val[k] = off; off = align256(off + (size_t)(side_rows * ncmax) * sizeof(double));
+    L.side_meta[k] = off; off = align256(off + (size_t)side_rows * 32);
+  }
+  L.side_rows = side_rows;
   L.total = off;
   L.maxslots = maxslots;
+  L.maxchunks = maxchunks;
+  L.nrb = nrb;
   return L;
 }
 
@@ -111,7 +153,6 @@ struct sun_plan_s {
   OpList ops;      // operator descriptors (+ planned widths, rates) passed to the expand kernels
   Gammas gam;
   FarPos hfp[2];   // far-position tables (host copies; uploaded in sun_plan_create)
-  double hsqrtg[MAXOPS];
   sun_zcsr H0, H1;
   std::vector<sun_zcsr> L;
   std::vector<double> gamma;
@@ -119,7 +160,7 @@ struct sun_plan_s {
   size_t ws_bytes;
   Layout lay;
   int wH0, wH1, wL, wK;
-  double tau0, tau1, herm_tol0, herm_tol1;
+  double tau0, tau1;
   Prob pr[2];
   int counted;
   int ran;            // last fill was enqueued by sun_run (capacity checked at sun_plan_nnz)
@@ -127,14 +168,62 @@ struct sun_plan_s {
   cudaStream_t count_stream;
   long long nnz[2];
   int npos_far[2];
+  int launches_count, launches_fill;
   std::vector<int> pos_dc[2], pos_dd[2];
+  NearSide side[2];
+  int combined;         // mode 0 with Q1 absent or Q1 = Q_H[diagonal H1]: one launch per pass
+  int scan_in_count;    // the count kernel's last CTA scans the tile sums (small problems)
+  long long fill_grid[2];
+  // auxiliary streams: the Q1 passes and the near-item fill run concurrently with Q0's far
+  // tiles (fork/join with events on the caller's stream; also valid under graph capture)
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  // CUDA graphs of the enqueue sequences (captured on cap_stream, launched on the caller's
+  // stream), keyed by kind and output buffers; small LRU cache
+  struct GraphEntry {
+    uintptr_t key[12];
+    cudaGraphExec_t exec;
+    unsigned long long used;
+  };
+  cudaStream_t cap_stream = nullptr;
+  std::vector<GraphEntry> graphs;
+  unsigned long long graph_clock = 0;
+  bool use_graphs = true;
+  ~sun_plan_s() {
+    for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    for (int i = 0; i < 2; ++i) {
+      if (aux[i]) cudaStreamDestroy(aux[i]);
+      if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+    }
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+  }
 };
+
+namespace {
+// fork `n` auxiliary streams off `st`
+cudaError_t fork_aux(sun_plan_s* pl, cudaStream_t st, int n) {
+  cudaError_t e = cudaEventRecord(pl->ev_fork, st);
+  for (int i = 0; i < n && e == cudaSuccess; ++i) e = cudaStreamWaitEvent(pl->aux[i], pl->ev_fork, 0);
+  return e;
+}
+// join `n` auxiliary streams back into `st`
+cudaError_t join_aux(sun_plan_s* pl, cudaStream_t st, int n) {
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < n && e == cudaSuccess; ++i) {
+    e = cudaEventRecord(pl->ev_join[i], pl->aux[i]);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, pl->ev_join[i], 0);
+  }
+  return e;
+}
+}  // namespace
 
 // =========================================================================================
 // Kernels
 // =========================================================================================
 
-// (validation + pattern analysis) one CTA per operator: half-bandwidth, ||.||_F^2, CSR checks.
+// (validation + pattern analysis, sun_plan_create) one CTA per operator: half-bandwidth,
+// ||.||_F^2, CSR checks.
 __global__ void k_analyze(OpList ops, DevHeader* hdr) {
   const int op = blockIdx.x;
   const OpDesc d = ops.op[op];
@@ -160,7 +249,6 @@ __global__ void k_analyze(OpList ops, DevHeader* hdr) {
     }
   }
   if (bad) atomicOr(&hdr->flags, F_MALFORMED);
-  if (ops.wplan[op] >= 0 && bw > ops.wplan[op]) atomicOr(&hdr->flags, F_PATTERN);
   atomicMax(&bwmax, bw);
   red[threadIdx.x] = acc;
   __syncthreads();
@@ -174,21 +262,28 @@ __global__ void k_analyze(OpList ops, DevHeader* hdr) {
   }
 }
 
-__global__ void k_zero(double* p, long long count, int* flags) {
-  if (flags && blockIdx.x == 0 && threadIdx.x == 0) *flags = 0;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count; i += (long long)gridDim.x * blockDim.x)
-    p[i] = 0.0;
-}
-
-// (a1) CSR -> band storage.  ops: 0 = H0 (into Hb0, width wK), 1 = H1 (Hb1, width wH1),
-// 2+p = L_p (Lb[p], width wL, scaled by sqrt(gamma_p)).  One thread per (operator, row).
-__global__ void k_scatter(OpList ops, int has_h1, double2* hb0, int wK, double2* hb1, int wH1, double2* lb,
-                          int wL) {
+// (a1) CSR -> band storage, one thread per (operator, row); grid (row blocks, operators).
+//   op 0 = H0 -> Hb0 (width wK), op 1 = H1 -> Hb1 (width wH1), op 2+p = L_p -> Lb[p] (width wL,
+//   scaled by sqrt(gamma_p)).  Also: CSR validation, values beyond the planned bandwidth,
+//   ||.||_F^2 per row block (fixed-order tree), and zeroing of the scan buffers used later
+//   in the same sun_count (tile sums, chained-scan status, tickets, Hermiticity maxima).
+__global__ void __launch_bounds__(EXP_THREADS) k_expand_rows(OpList ops, double2* hb0, int wK, double2* hb1, int wH1,
+                                                             double2* lb, int wL, BlkInfo* blk, int* zero32,
+                                                             long long nzero32, unsigned long long* zero64,
+                                                             long long nzero64, DevHeader* hdr) {
+  const long long gtid = ((long long)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long gstride = (long long)gridDim.x * gridDim.y * blockDim.x;
+  for (long long i = gtid; i < nzero32; i += gstride) zero32[i] = 0;
+  for (long long i = gtid; i < nzero64; i += gstride) zero64[i] = 0ull;
+  if (gtid == 0) {
+    hdr->herm_dev[0] = hdr->herm_dev[1] = 0ull;
+    hdr->ticket[0] = hdr->ticket[1] = 0u;
+    hdr->done = 0u;
+  }
+  const int op = blockIdx.y;
+  if (op == 1 && !ops.has_h1) return;  // block-uniform
   const int n = ops.n;
-  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t >= (long long)ops.nops * n) return;
-  int op = (int)(t / n), r = (int)(t % n);
-  if (op == 1 && !has_h1) return;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
   const OpDesc d = ops.op[op];
   double2* dst;
   int w;
@@ -196,34 +291,105 @@ __global__ void k_scatter(OpList ops, int has_h1, double2* hb0, int wK, double2*
   if (op == 0) { dst = hb0; w = wK; }
   else if (op == 1) { dst = hb1; w = wH1; }
   else { dst = lb + (long long)(op - 2) * n * (2 * wL + 1); w = wL; s = ops.sqrtg[op]; }
-  for (int64_t k = d.rp[r]; k < d.rp[r + 1]; ++k) {
-    int o = d.ci[k] - r;
-    if (o < -w || o > w) continue;  // only exact zeros can lie outside (bandwidth from k_analyze)
-    double2 v = d.v[k];
-    dst[(long long)r * (2 * w + 1) + (o + w)] = make_double2(s * v.x, s * v.y);
+  double acc = 0.0;
+  int bw = 0, flags = 0;
+  if (r < n) {
+    double2* row = dst + (long long)r * (2 * w + 1);
+    for (int o = 0; o <= 2 * w; ++o) row[o] = make_double2(0.0, 0.0);
+    const int64_t lo = d.rp[r], hi = d.rp[r + 1];
+    if (hi < lo) flags |= F_MALFORMED;
+    int prev = -1;
+    for (int64_t k = lo; k < hi; ++k) {
+      const int c = d.ci[k];
+      if (c < 0 || c >= n || c <= prev) { flags |= F_MALFORMED; break; }
+      prev = c;
+      const double2 v = d.v[k];
+      const int o = c - r;
+      const int ao = o < 0 ? -o : o;
+      if (v.x != 0.0 || v.y != 0.0) bw = ao > bw ? ao : bw;
+      acc += v.x * v.x + v.y * v.y;
+      if (ao <= w) row[o + w] = make_double2(s * v.x, s * v.y);
+    }
+    if (ops.wplan[op] >= 0 && bw > ops.wplan[op]) flags |= F_PATTERN;
+  }
+  __shared__ double red[EXP_THREADS];
+  __shared__ int sbw[EXP_THREADS / 32], sfl[EXP_THREADS / 32];
+  red[threadIdx.x] = acc;
+  int wb = bw, wf = flags;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    wb = max(wb, __shfl_xor_sync(FULL, wb, o));
+    wf |= __shfl_xor_sync(FULL, wf, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sbw[threadIdx.x >> 5] = wb;
+    sfl[threadIdx.x >> 5] = wf;
+  }
+  __syncthreads();
+  for (int st = EXP_THREADS / 2; st > 0; st >>= 1) {  // fixed-order tree: deterministic
+    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    int b = 0, f = 0;
+    for (int i = 0; i < EXP_THREADS / 32; ++i) {
+      b = max(b, sbw[i]);
+      f |= sfl[i];
+    }
+    blk[(long long)op * gridDim.x + blockIdx.x] = BlkInfo{red[0], b, f};
   }
 }
 
-// (a1) K = H0 + (i/2) M, M = sum_p Lt_p^+ Lt_p (Lt = sqrt(gamma) L); Hermiticity checks of H0, H1.
-// Also writes inv[l] = 1/sqrt(l(l+1)) (normalisation of D^l) for the D-chain kernels.
-__global__ void k_band_k(int n, int P, const double2* __restrict__ hb0, double2* kb0, int wK,
-                         const double2* __restrict__ lb, int wL, const double2* __restrict__ hb1, int wH1,
-                         int has_h1, Gammas gam, DevHeader* hdr, double* inv) {
-  long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  // drop thresholds (R6) and Hermiticity tolerances from this call's norms
-  const double nh0 = sqrt(hdr->nrm2[0]), nh1 = has_h1 ? sqrt(hdr->nrm2[1]) : 0.0;
-  const double tol0 = 1e-12 * nh0, tol1 = 1e-12 * nh1;
-  if (t == 0) {
-    double s0 = nh0;
-    for (int p = 0; p < P; ++p) s0 += gam.g[p] * hdr->nrm2[2 + p];
-    hdr->tau[0] = 1e-14 * s0;
-    hdr->tau[1] = 1e-14 * nh1;
+// (a1) K = H0 + (i/2) M, M = sum_p Lt_p^+ Lt_p (Lt = sqrt(gamma) L), one thread per band entry;
+// inv[l] = 1/sqrt(l(l+1)) (normalisation of D^l); Hermiticity deviations of H0, H1.
+// Block 0 also reduces the k_expand_rows block records (fixed order) into the header: norms,
+// bandwidths, flags, and the drop thresholds tau (R6).
+__global__ void k_expand_k(int n, int P, int nops, int has_h1, int nrb, const BlkInfo* __restrict__ blk,
+                           const double2* __restrict__ hb0, double2* kb0, int wK, const double2* __restrict__ lb,
+                           int wL, const double2* __restrict__ hb1, int wH1, Gammas gam, DevHeader* hdr,
+                           double* inv) {
+  if (blockIdx.x == 0 && threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int flags = 0;
+    double s0 = 0.0;
+    for (int op = 0; op < nops; ++op) {
+      if (op == 1 && !has_h1) continue;
+      double acc = 0.0;
+      int b = 0;
+      for (int i = lane; i < nrb; i += 32) {  // fixed order per lane, then a fixed tree
+        const BlkInfo bi = blk[(long long)op * nrb + i];
+        acc += bi.nrm2;
+        b = max(b, bi.bw);
+        flags |= bi.flags;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc += __shfl_xor_sync(FULL, acc, o);
+        b = max(b, __shfl_xor_sync(FULL, b, o));
+      }
+      if (lane == 0) {
+        hdr->nrm2[op] = acc;
+        hdr->bw[op] = b;
+        if (op == 0) s0 += sqrt(acc);
+        if (op >= 2) s0 += gam.g[op - 2] * acc;
+        if (op < 2) hdr->nrm2_h[op] = acc;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) flags |= __shfl_xor_sync(FULL, flags, o);
+    if (lane == 0) {
+      hdr->flags = flags;
+      hdr->tau[0] = 1e-14 * s0;
+      hdr->tau[1] = has_h1 ? 1e-14 * sqrt(hdr->nrm2_h[1]) : 0.0;
+      if (!has_h1) hdr->nrm2_h[1] = 0.0;
+    }
   }
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (t < n) inv[t] = t > 0 ? 1.0 / sqrt((double)t * (double)(t + 1)) : 0.0;
   const int sw = 2 * wK + 1;
   if (t >= (long long)n * sw) return;
-  int r = (int)(t / sw), o = (int)(t % sw) - wK;
-  int c = r + o;
+  const int r = (int)(t / sw), o = (int)(t % sw) - wK;
+  const int c = r + o;
   if (c < 0 || c >= n) {
     kb0[t] = make_double2(0.0, 0.0);
     return;
@@ -235,31 +401,710 @@ __global__ void k_band_k(int n, int P, const double2* __restrict__ hb0, double2*
   for (int p = 0; p < P; ++p) {
     const double2* Lp = lb + (long long)p * n * (2 * wL + 1);
     for (int x = lo; x <= hi; ++x) {
-      double2 a = Lp[(long long)x * (2 * wL + 1) + (r - x + wL)];  // L_xr
-      double2 b = Lp[(long long)x * (2 * wL + 1) + (c - x + wL)];  // L_xc
+      const double2 a = Lp[(long long)x * (2 * wL + 1) + (r - x + wL)];  // L_xr
+      const double2 b = Lp[(long long)x * (2 * wL + 1) + (c - x + wL)];  // L_xc
       mx += a.x * b.x + a.y * b.y;  // conj(L_xr) L_xc
       my += a.x * b.y - a.y * b.x;
     }
   }
-  double2 h = hb0[t];
+  const double2 h = hb0[t];
   kb0[t] = make_double2(h.x - 0.5 * my, h.y + 0.5 * mx);
-  double2 ht = hb0[(long long)c * sw + (r - c + wK)];
-  if (fabs(h.x - ht.x) > tol0 || fabs(h.y + ht.y) > tol0) atomicOr(&hdr->flags, F_H0_NOT_HERM);
+  const double2 ht = hb0[(long long)c * sw + (r - c + wK)];
+  const double dev0 = fmax(fabs(h.x - ht.x), fabs(h.y + ht.y));
+  if (dev0 > 0.0) atomicMax(&hdr->herm_dev[0], (unsigned long long)__double_as_longlong(dev0));
   if (has_h1 && o >= -wH1 && o <= wH1) {
-    double2 g = hb1[(long long)r * (2 * wH1 + 1) + (o + wH1)];
-    double2 gt = hb1[(long long)c * (2 * wH1 + 1) + (r - c + wH1)];
-    if (fabs(g.x - gt.x) > tol1 || fabs(g.y + gt.y) > tol1) atomicOr(&hdr->flags, F_H1_NOT_HERM);
+    const double2 g = hb1[(long long)r * (2 * wH1 + 1) + (o + wH1)];
+    const double2 gt = hb1[(long long)c * (2 * wH1 + 1) + (r - c + wH1)];
+    const double dev1 = fmax(fabs(g.x - gt.x), fabs(g.y + gt.y));
+    if (dev1 > 0.0) atomicMax(&hdr->herm_dev[1], (unsigned long long)__double_as_longlong(dev1));
+  }
+}
+
+// per-warp scratch (doubles): near-pair U tile (2 TW^2) + gS, gJ, pS, pJ (4 SW); D rows use
+// the first 2 (WIN_MAX + 2)
+template <int TW, int SW>
+struct Scr {
+  static constexpr int A = 2 * TW * TW + 4 * SW;
+  static constexpr int PER_WARP = A > 2 * (WIN_MAX + 2) ? A : 2 * (WIN_MAX + 2);
+};
+
+// ---------------------------------------------------------------------------------------
+// Mode 0 (compile-time widths).  One launch per output matrix and pass.
+//   count: units = far tiles (TP0 = 256 consecutive pairs, thread per pair, values in
+//          registers) and near units (8 near-pair / D-row items, one warp each), interleaved
+//          evenly in blockIdx order so latency-bound near work overlaps the far work.  A near
+//          unit also stores its rows' window entries (all S/J entries and the D entries
+//          inside the window) and the D-chain tail data in a side buffer (NearSide).
+//   fill:  far tiles write their far rows (staging + TMA bulk stores) and copy their near
+//          rows from the side buffer, generating the chain tails; D units do the D rows.
+// Tile sums (S tile t, J tile t, D slot l) are accumulated with integer atomics into zeroed
+// slots (order-independent, deterministic).
+// ---------------------------------------------------------------------------------------
+template <int WK, int WL>
+struct Mode0 {
+  static constexpr int W = WK;
+  static constexpr int TW = 2 * W + 1;
+  static constexpr int SW = 2 * TW + 2;
+  static constexpr int PER_WARP = Scr<TW, SW>::PER_WARP;
+};
+
+// Pairs per tile: staging-free configurations (W = 0, rows of <= 2 entries) take 8 pairs per
+// thread (tile = 2048 pairs) to amortise the per-tile prologue; others one pair per thread.
+template <int WK, int WL>
+struct Tiling {
+  static constexpr bool DIRECT = FarT<WK, WL>::NPOS <= 2;
+  static constexpr int PPT = DIRECT ? 8 : 1;
+  static constexpr int TP = 256 * PPT;
+};
+
+// (a, b) -> the pair k positions later in lexicographic order (k >= 0; past the end: a > n-2)
+__device__ __forceinline__ void pair_advance(int n, int& a, int& b, int k) {
+  b += k;
+  while (b >= n && a < n - 2) {
+    b -= n;
+    ++a;
+    b += a + 1;
+  }
+}
+
+// near item -> (a, b) of a near pair (b - a <= 2W) or a D row lam; returns 0 none, 1 pair, 2 D
+__device__ __forceinline__ int near_item(const Prob& pr, long long item, int& a, int& b, int& lam) {
+  const int W2 = 2 * pr.W;
+  const long long nnear = (long long)pr.n * W2;
+  if (item < nnear) {
+    a = (int)(item / W2);
+    b = a + 1 + (int)(item % W2);
+    return b < pr.n ? 1 : 0;
+  }
+  if (item < nnear + pr.n - 1) {
+    lam = (int)(item - nnear) + 1;
+    return 2;
+  }
+  return 0;
+}
+
+// unit u of U: near units at evenly spread positions (Bresenham)
+__device__ __forceinline__ bool unit_decode(long long u, long long U, long long nnear_units, long long& idx) {
+  const long long k0 = u * nnear_units / U, k1 = (u + 1) * nnear_units / U;
+  const bool is_near = k1 > k0;
+  idx = is_near ? k0 : u - k0;
+  return is_near;
+}
+
+// ---- count pass ------------------------------------------------------------------------
+template <int WK, int WL>
+__device__ __forceinline__ void count_near_unit(const Prob& pr, long long j, double* scr_w, int* __restrict__ cnt,
+                                                int* __restrict__ tsum, const NearSide& side) {
+  using MC = Mode0<WK, WL>;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long np = pr.np;
+  const long long item = j * 8 + wid;
+  int a, b, lam;
+  const int kind = near_item(pr, item, a, b, lam);
+  const long long r0 = 2 * item * side.nc, r1 = r0 + side.nc;
+  if (kind == 1) {
+    int c1, c2;
+    double k1, k2;
+    TailInfo tS, tJ;
+    const Seg sS = {side.col + r0, side.val + r0, side.nc}, sJ = {side.col + r1, side.val + r1, side.nc};
+    warp_near_pair<true, MC::TW, MC::SW, false>(pr, a, b, scr_w, c1, c2, k1, k2, sS, 0, sJ, 0, &tS, &tJ);
+    if (lane == 0) {
+      side.meta[2 * item] = NearMeta{tS.tr, k1, tS.nwin, tS.hi, tS.lend, 0};
+      side.meta[2 * item + 1] = NearMeta{tJ.tr, k2, tJ.nwin, tJ.hi, tJ.lend, 0};
+      const long long p = (long long)pidx32(pr.n, a, b);
+      cnt[p] = c1;
+      cnt[np + p] = c2;
+      atomicAdd(&tsum[p / pr.tp], c1);
+      atomicAdd(&tsum[pr.npt + p / pr.tp], c2);
+    }
+  } else if (kind == 2) {
+    double kv;
+    TailInfo t;
+    const Seg sD = {side.col + r0, side.val + r0, side.nc};
+    const int c = warp_d_row<true, false>(pr, lam, scr_w, scr_w + WIN_MAX + 2, kv, sD, 0, &t);
+    if (lane == 0) {
+      side.meta[2 * item] = NearMeta{t.tr, kv, t.nwin, t.hi, t.lend, 0};
+      cnt[2 * np + lam - 1] = c;
+      tsum[2 * pr.npt + lam - 1] = c;
+    }
+  }
+}
+
+template <int WK, int WL, int PT>
+__device__ __forceinline__ void count_far_tile(const FarCtx& pr, long long npt, long long t, int* __restrict__ cnt,
+                                               int* __restrict__ tsum, int* red) {
+  using MC = Mode0<WK, WL>;
+  using TL = Tiling<WK, WL>;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long np = pr.np;
+  const long long pw = t * TL::TP + (long long)wid * 32 * TL::PPT;  // the warp's first pair
+  int a, b;
+  warp_pairs(pr.n, pw, a, b);
+  int c = 0;
+#pragma unroll 1
+  for (int j = 0; j < TL::PPT; ++j) {
+    const long long p = pw + j * 32 + lane;
+    if (j) pair_advance(pr.n, a, b, 32);
+    const bool far = p < np && (b - a > 2 * MC::W);
+    if (far) {
+      double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
+      far_values<WK, WL, PT>(pr, a, b, ux, uy);
+      unsigned mr, mi;
+      far_masks<WK, WL>(pr.n, pr.tau, a, b, ux, uy, mr, mi);
+      const int cp = __popc(mr) + __popc(mi);
+      cnt[p] = cp;
+      cnt[np + p] = cp;
+      c += cp;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
+  if (lane == 0) red[wid] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int w = 0; w < 8; ++w) tot += red[w];
+    if (tot) {
+      atomicAdd(&tsum[t], tot);  // S rows and J rows of a far pair have the same length
+      atomicAdd(&tsum[npt + t], tot);
+    }
+  }
+}
+
+__device__ __forceinline__ long long block_scan_ll(long long v, long long* wsum, long long& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    long long s = lane < nwarps ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(FULL, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nwarps) wsum[lane] = s;
+  }
+  __syncthreads();
+  total = wsum[nwarps - 1];
+  long long before = wid > 0 ? wsum[wid - 1] : 0;
+  __syncthreads();
+  return before + x - v;
+}
+
+// One output matrix's arguments of the count pass.
+struct MatCount {
+  Prob pr;
+  int* cnt;
+  int* tsum;
+  NearSide side;
+};
+// Prefix scan of the tile sums done by the count kernel's last CTA (small problems).
+struct ScanIn {
+  const int* ts[2];
+  long long* toff[2];
+  long long* nnz[2];
+  long long nslots[2];
+  unsigned int* done;  // CTA completion counter (zeroed by the expand step)
+  int nmat;            // 0: no scan in the count kernel (k_scan_chain runs instead)
+};
+
+template <int WK, int WL, int PT>
+__device__ __forceinline__ void count_unit(const MatCount& mc, long long u, double* scr_w, int* red) {
+  const long long U = mc.pr.npt + mc.pr.nb_near;
+  long long idx;
+  if (unit_decode(u, U, mc.pr.nb_near, idx)) {  // block-uniform
+    Prob prn = mc.pr;
+    prn.tau = *mc.pr.tau_ptr;
+    count_near_unit<WK, WL>(prn, idx, scr_w, mc.cnt, mc.tsum, mc.side);
+  } else {
+    const FarCtx prf{mc.pr.K.v, mc.pr.L, *mc.pr.tau_ptr, mc.pr.np, mc.pr.n, mc.pr.P};
+    count_far_tile<WK, WL, PT>(prf, mc.pr.npt, idx, mc.cnt, mc.tsum, red);
+  }
+}
+
+// exclusive scan of ns int32 tile sums into int64 offsets by one CTA (fixed order)
+__device__ __forceinline__ void cta_scan_slots(const int* ts, long long ns, long long* toff, long long* nnz,
+                                               long long* wsum) {
+  const long long per = (ns + blockDim.x - 1) / blockDim.x;
+  const long long lo = threadIdx.x * per, hi = lo + per < ns ? lo + per : ns;
+  long long local = 0;
+  for (long long i = lo; i < hi; ++i) local += __ldcg(&ts[i]);
+  long long total;
+  long long run = block_scan_ll(local, wsum, total);
+  for (long long i = lo; i < hi; ++i) {
+    toff[i] = run;
+    run += __ldcg(&ts[i]);
+  }
+  if (threadIdx.x == 0) *nnz = total;
+}
+
+// Count pass of Q0 (compile-time widths WK, WL, PT) and, with Q1W >= 0, of Q1 (widths Q1W, 0,
+// no dissipators) in one launch: one CTA per unit, Q0's units first.  With sc.nmat > 0 the
+// last CTA to finish scans the tile sums (a4).
+template <int WK, int WL, int PT, int Q1W>
+__global__ void __launch_bounds__(256) k_count0(const MatCount m0, const MatCount m1, const ScanIn sc) {
+  using MC = Mode0<WK, WL>;
+  constexpr int PW1 = Q1W >= 0 ? Mode0<(Q1W > 0 ? Q1W : 0), 0>::PER_WARP : 0;
+  constexpr int PW = MC::PER_WARP > PW1 ? MC::PER_WARP : PW1;
+  __shared__ double scr[8][PW];
+  __shared__ int red[8];
+  __shared__ long long wsum[32];
+  __shared__ int last;
+  const long long U0 = m0.pr.npt + m0.pr.nb_near;
+  const long long u = blockIdx.x;
+  if (u < U0) {
+    count_unit<WK, WL, PT>(m0, u, scr[threadIdx.x >> 5], red);
+  } else {
+    if constexpr (Q1W >= 0) count_unit<(Q1W > 0 ? Q1W : 0), 0, 0>(m1, u - U0, scr[threadIdx.x >> 5], red);
+  }
+  if (sc.nmat == 0) return;  // grid-uniform
+  __threadfence();  // this CTA's counts and tile sums are visible device-wide
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(sc.done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int y = 0; y < sc.nmat; ++y) {
+    cta_scan_slots(sc.ts[y], sc.nslots[y], sc.toff[y], sc.nnz[y], wsum);
+    __syncthreads();
   }
 }
 
 // ---------------------------------------------------------------------------------------
-// (a3) count pass.  One CTA per row tile: pair tiles (S and J rows of tp consecutive pairs),
-// then D tiles (one warp per D^lam row).  Writes per-row counts and one int32 sum per tile
-// slot; slots are in global row order (S tiles, J tiles, D tiles).
-//   mode 0: thread per pair, far pairs from compile-time band widths (WK, WL) held in
-//           registers (the S-row count word also carries nRe in bits 20-31); near pairs
-//           warp-cooperative.  128 threads, 128 pairs per tile.
-//   mode 1: warp per pair (wide bands / many positions).  256 threads, 64 pairs per tile.
+// (a5) fill pass outputs
+// ---------------------------------------------------------------------------------------
+struct FillOut {
+  int64_t* row_ptr;
+  int32_t* col;
+  double* val;
+  long long cap;  // capacity of col/val (writes at or beyond it are dropped; see sun_run)
+  double* K;      // nullptr: not written (Q1)
+  const long long* toff;
+  const long long* nnz;
+};
+
+// Near rows of a tile (or a D unit), written by the whole CTA: the rows are listed in shared
+// memory, their lengths prefix-summed, and every thread walks the flattened entry range with
+// a monotone row cursor, so all warps share the work (no warp-serial latency chains).
+// Window entries are copied from the side buffer; chain-tail entries tr * inv[l], l in
+// (hi, lend], are generated with the count pass's expression (bitwise identical).
+constexpr int MAXNR = 2 * TP0;  // rows per tile: 2 per pair
+struct NearRowRef {
+  long long out;  // output index of the row's first entry
+  double tr;
+  int side_row, nwin, hi, lend;
+};
+struct NearRows {
+  NearRowRef r[MAXNR];
+  int start[MAXNR + 1];
+  int2 wtot[8];
+  int nr;
+};
+
+__device__ __forceinline__ void cta_near_rows_out(NearRows& L, const NearSide& side, const double* __restrict__ inv,
+                                                  int dbase, const FillOut& fo) {
+  __syncthreads();  // list complete
+  const int nr = L.nr;
+  if (nr == 0) return;  // block-uniform
+  // prefix of row lengths: thread i owns rows 2i, 2i+1
+  const int i0 = 2 * threadIdx.x, i1 = i0 + 1;
+  const int l0 = i0 < nr ? L.r[i0].nwin + (L.r[i0].lend - L.r[i0].hi) : 0;
+  const int l1 = i1 < nr ? L.r[i1].nwin + (L.r[i1].lend - L.r[i1].hi) : 0;
+  int2 tot;
+  const int2 ex = block_exclusive_scan2(l0 + l1, 0, L.wtot, tot);
+  if (i0 < nr) L.start[i0] = ex.x;
+  if (i1 < nr) L.start[i1] = ex.x + l0;
+  if (threadIdx.x == 0) L.start[nr] = tot.x;
+  __syncthreads();
+  const int total = tot.x;
+  int r = 0;
+  for (int e = threadIdx.x; e < total; e += blockDim.x) {
+    while (L.start[r + 1] <= e) ++r;
+    const NearRowRef& R = L.r[r];
+    const int k = e - L.start[r];
+    const long long o = R.out + k;
+    if (o >= fo.cap) continue;
+    if (k < R.nwin) {
+      const long long sidx = (long long)R.side_row * side.nc + k;
+      fo.col[o] = side.col[sidx];
+      fo.val[o] = side.val[sidx];
+    } else {
+      const int l = R.hi + 1 + (k - R.nwin);
+      fo.col[o] = dbase + l;
+      fo.val[o] = R.tr * __ldg(&inv[l]);
+    }
+  }
+}
+
+// Copy a warp's staged segment [g0, g1) (tile-local offsets) to global memory, skipping the
+// "holes" of near rows (lanes flagged in `holes`, hole = [hoff, hoff + hlen)).  The stage
+// position advances only over copied entries.
+__device__ __forceinline__ void warp_copy_out(const int* scol, const double* sval, long long gbase, int g0, int g1,
+                                              unsigned holes, int hoff, int hlen, int32_t* __restrict__ col,
+                                              double* __restrict__ val, long long cap) {
+  const int lane = threadIdx.x & 31;
+  int sp = 0, gp = g0;
+  for (;;) {
+    const bool last = holes == 0;
+    int hs = g1, hl = 0;
+    if (!last) {
+      const int h = __ffs(holes) - 1;
+      holes &= holes - 1;
+      hs = __shfl_sync(FULL, hoff, h);
+      hl = __shfl_sync(FULL, hlen, h);
+    }
+    long long run_l = hs - gp;
+    if (gbase + gp + run_l > cap) run_l = cap - (gbase + gp) > 0 ? cap - (gbase + gp) : 0;
+    const int run = (int)run_l;
+    int32_t* cdst = col + gbase + gp;
+    double* vdst = val + gbase + gp;
+    for (int k = lane; k < run; k += 32) {
+      cdst[k] = scol[sp + k];
+      vdst[k] = sval[sp + k];
+    }
+    sp += run;
+    gp = hs + hl;
+    if (last) break;
+  }
+}
+
+template <int WK, int WL>
+struct FillFar {
+  static constexpr int NPOS = FarT<WK, WL>::NPOS;
+  static constexpr bool DIRECT = NPOS <= 2;             // rows of <= 4 entries: no staging
+  static constexpr int CAPW = DIRECT ? 0 : 64 * NPOS;   // entries of one 32-row block, worst case
+  static constexpr int COLW = DIRECT ? 0 : (CAPW + 4 + 3) & ~3;  // int32 slots (+ pad), 16-B multiple
+  static constexpr int VALW = DIRECT ? 0 : (CAPW + 2 + 1) & ~1;  // fp64 slots (+ pad)
+  static constexpr int BYTES_PER_WARP = COLW * 4 + VALW * 8;
+  static constexpr int SMEM = 8 * BYTES_PER_WARP;
+};
+
+// Far tile t (256 pairs, thread per pair): row_ptr of all the tile's rows, K of its pairs;
+// each warp stages its 32 far S rows (then J rows) in shared memory and writes the block out
+// with TMA bulk stores (cp.async.bulk) when the block has no near-row holes (16-byte phase
+// matched in the staging, head/tail entries by lanes), else with coalesced warp stores; the
+// warp then writes its near rows from the side buffer.
+// per-tile inputs, loaded one unit ahead (software pipelining of the persistent loop)
+struct TileIn {
+  int cS, cJ;
+  long long baseS, baseJ;
+};
+__device__ __forceinline__ TileIn load_tile_in(long long np, long long npt, long long t, const int* __restrict__ cnt,
+                                               const long long* __restrict__ toff) {
+  const long long p = t * TP0 + threadIdx.x;
+  TileIn ti;
+  ti.cS = p < np ? cnt[p] : 0;
+  ti.cJ = p < np ? cnt[np + p] : 0;
+  ti.baseS = toff[t];
+  ti.baseJ = toff[npt + t];
+  return ti;
+}
+
+template <int WK, int WL, int PT>
+__device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, long long t, const TileIn& ti,
+                                              const FillOut& fo, const NearSide& side, const double* __restrict__ inv,
+                                              int* scol, double* sval, NearRows& L) {
+  using MC = Mode0<WK, WL>;
+  using FF = FillFar<WK, WL>;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long np = pr.np;
+  const long long p = t * TP0 + threadIdx.x;
+  const bool valid = p < np;
+  const int cS = ti.cS, cJ = ti.cJ;
+  int2 tot2;
+  if (threadIdx.x == 0) L.nr = 0;
+  const int2 ex2 = block_exclusive_scan2(cS, cJ, L.wtot, tot2);
+  const int exS = ex2.x, exJ = ex2.y;
+  int a, b;
+  warp_pairs(pr.n, t * TP0 + wid * 32, a, b);
+  const bool far = valid && (b - a > 2 * MC::W);
+  const bool nearp = valid && !far;
+  const long long baseS = ti.baseS, baseJ = ti.baseJ;
+  if (valid) {
+    fo.row_ptr[p] = baseS + exS;
+    fo.row_ptr[np + p] = baseJ + exJ;
+    if (fo.K && far) {
+      fo.K[p] = 0.0;
+      fo.K[np + p] = 0.0;
+    }
+  }
+#ifdef SUN_EXP_PROLOGUE_ONLY
+  return;
+#endif
+  double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
+  int q[FarT<WK, WL>::NPOS];
+  unsigned mr = 0u, mi = 0u;
+  if (far) {
+#ifdef SUN_EXP_NO_COMPUTE
+#pragma unroll
+    for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
+      ux[k] = 1.0 + k;
+      uy[k] = k < 9 ? 1.0 : 0.0;
+    }
+#else
+    far_values<WK, WL, PT>(pr, a, b, ux, uy);
+#endif
+    far_masks<WK, WL>(pr.n, pr.tau, a, b, ux, uy, mr, mi);
+    far_cols<WK, WL>(pr.n, a, b, q);
+  }
+  const unsigned nearmask = __ballot_sync(FULL, nearp);
+  if constexpr (FF::DIRECT) {
+    // rows of <= 4 entries: each thread writes its rows directly (adjacent lanes write
+    // adjacent rows, so the stores are already coalesced)
+    if (far) {
+      const Seg seg = {fo.col, fo.val, fo.cap};
+#pragma unroll
+      for (int row = 0; row < 2; ++row) {
+        const long long o = (row ? baseJ + exJ : baseS + exS);
+        const unsigned m1 = row ? mi : mr, m2 = row ? mr : mi;
+        int o1 = 0, o2 = __popc(m1);
+#pragma unroll
+        for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
+          if ((m1 >> k) & 1u) seg.emit(o + o1++, q[k], row ? uy[k] : ux[k]);
+          if ((m2 >> k) & 1u) seg.emit(o + o2++, (int)np + q[k], row ? ux[k] : -uy[k]);
+        }
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int row = 0; row < 2; ++row) {  // the warp's 32 S rows, then its 32 J rows
+      const int c_me = row ? cJ : cS, ex_me = row ? exJ : exS;
+      const long long gbase = row ? baseJ : baseS;
+      const int w0 = __shfl_sync(FULL, ex_me, 0);
+      const int wt = __shfl_sync(FULL, ex_me + c_me, 31) - w0;  // rows of invalid lanes have c = 0
+      const long long g = gbase + w0;                              // global index of the block's first entry
+      const bool bulk = nearmask == 0u && g + wt <= fo.cap;
+      if (lane == 0) bulk_wait_read0();  // earlier bulk reads of this warp's staging are done
+      __syncwarp();
+      int pc = 0, pv = 0, hb = 0;
+      if (bulk) {  // stage with the global 16-byte phase of the block's first entry
+        pc = (int)(((uintptr_t)(fo.col + g) >> 2) & 3);
+        pv = (int)(((uintptr_t)(fo.val + g) >> 3) & 1);
+      } else {
+        int ht;
+        hb = warp_excl_scan(nearp ? c_me : 0, ht);
+      }
+#ifndef SUN_EXP_NO_STAGE
+      if (far) far_stage_row<WK, WL>((int)np, row, q, ux, uy, mr, mi, scol + pc, sval + pv, ex_me - w0 - hb);
+#endif
+      if (bulk) fence_async_smem();  // make the staged entries visible to the async (TMA) proxy
+      __syncwarp();
+      if (bulk) {
+        // col: int32, 16 B = 4 entries; val: fp64, 16 B = 2 entries
+        const long long end = g + wt;
+        const long long ca = g + ((4 - pc) & 3), ce = ca <= end ? ca + ((end - ca) & ~3ll) : ca;
+        const long long va = g + pv, ve = va <= end ? va + ((end - va) & ~1ll) : va;
+#ifndef SUN_EXP_NO_STORE
+        if (lane == 0) {
+          if (ce > ca) bulk_s2g(fo.col + ca, scol + pc + (ca - g), (unsigned)((ce - ca) * 4));
+          if (ve > va) bulk_s2g(fo.val + va, sval + pv + (va - g), (unsigned)((ve - va) * 8));
+          bulk_commit();
+        }
+#endif
+        // head / tail entries outside the aligned middles (at most 3 + 3 col, 1 + 1 val)
+        if (ce > ca) {
+          const long long k = lane < 4 ? g + lane : ce + (lane - 4);
+          if ((lane < 4 && k < ca) || (lane >= 4 && lane < 8 && k < end)) fo.col[k] = scol[pc + (k - g)];
+        } else if (lane < wt) {
+          fo.col[g + lane] = scol[pc + lane];
+        }
+        if (ve > va) {
+          const long long k = lane < 2 ? g + lane : ve + (lane - 2);
+          if ((lane < 2 && k < va) || (lane >= 2 && lane < 4 && k < end)) fo.val[k] = sval[pv + (k - g)];
+        } else if (lane < wt) {
+          fo.val[g + lane] = sval[pv + lane];
+        }
+      } else {
+        warp_copy_out(scol, sval, gbase, w0, w0 + wt, nearmask, ex_me, c_me, fo.col, fo.val, fo.cap);
+      }
+      __syncwarp();
+    }
+  }
+  // near rows of the tile: from the side buffer, by the whole CTA
+  if (nearp) {
+    const long long item = (long long)a * (2 * MC::W) + (b - a - 1);
+    const NearMeta mS = side.meta[2 * item], mJ = side.meta[2 * item + 1];
+    const int slot = atomicAdd(&L.nr, 2);
+    L.r[slot] = NearRowRef{baseS + exS, mS.tr, (int)(2 * item), mS.nwin, mS.hi, mS.lend};
+    L.r[slot + 1] = NearRowRef{baseJ + exJ, mJ.tr, (int)(2 * item + 1), mJ.nwin, mJ.hi, mJ.lend};
+    if (fo.K) {
+      fo.K[p] = mS.k;
+      fo.K[np + p] = mJ.k;
+    }
+  }
+#ifndef SUN_EXP_NO_NEAR
+  cta_near_rows_out(L, side, inv, (int)(2 * np - 1), fo);
+#endif
+}
+
+// Staging-free far tile (W = 0: every pair is far, rows of <= 2 entries), TP = 2048 pairs:
+// warp w owns pairs [t TP + 256 w, + 256), 8 coalesced iterations of 32 pairs; row offsets
+// from warp scans with a running carry and a block scan of the warp totals.
+template <int WK, int WL, int PT>
+__device__ __forceinline__ void fill_direct_tile(const FarCtx& pr, long long npt, long long t,
+                                                 const int* __restrict__ cnt, const FillOut& fo, int2* wtot) {
+  using TL = Tiling<WK, WL>;
+  static_assert(TL::DIRECT && WK == 0, "direct tile: W = 0");
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long np = pr.np;
+  const long long pw = t * TL::TP + (long long)wid * 32 * TL::PPT;
+  int cS[TL::PPT], cJ[TL::PPT];
+  int sS = 0, sJ = 0;
+#pragma unroll
+  for (int j = 0; j < TL::PPT; ++j) {
+    const long long p = pw + j * 32 + lane;
+    cS[j] = p < np ? cnt[p] : 0;
+    cJ[j] = p < np ? cnt[np + p] : 0;
+    sS += cS[j];
+    sJ += cJ[j];
+  }
+  int2 tot2;
+  const int2 ex2 = block_exclusive_scan2(sS, sJ, wtot, tot2);  // per-thread totals, block order
+  // the warp's base = exclusive prefix of its lane 0 (threads ordered as warps x lanes)
+  const long long baseS = fo.toff[t] + __shfl_sync(FULL, ex2.x, 0);
+  const long long baseJ = fo.toff[npt + t] + __shfl_sync(FULL, ex2.y, 0);
+  long long carryS = 0, carryJ = 0;
+  int a, b;
+  warp_pairs(pr.n, pw, a, b);
+  const Seg seg = {fo.col, fo.val, fo.cap};
+#pragma unroll 1
+  for (int j = 0; j < TL::PPT; ++j) {
+    const long long p = pw + j * 32 + lane;
+    if (j) pair_advance(pr.n, a, b, 32);
+    int tS, tJ;
+    const int eS = warp_excl_scan(cS[j], tS), eJ = warp_excl_scan(cJ[j], tJ);
+    const long long rS = baseS + carryS + eS, rJ = baseJ + carryJ + eJ;
+    carryS += tS;
+    carryJ += tJ;
+    if (p >= np) continue;
+    fo.row_ptr[p] = rS;
+    fo.row_ptr[np + p] = rJ;
+    if (fo.K) {
+      fo.K[p] = 0.0;
+      fo.K[np + p] = 0.0;
+    }
+    double ux[1], uy[1];
+    far_values<WK, WL, PT>(pr, a, b, ux, uy);
+    unsigned mr, mi;
+    far_masks<WK, WL>(pr.n, pr.tau, a, b, ux, uy, mr, mi);
+    const int q = pidx32(pr.n, a, b);
+    // S row: [Re U at q] [-Im U at NP + q];  J row: [Im U at q] [Re U at NP + q]
+    int o = 0;
+    if (mr & 1u) seg.emit(rS + o++, q, ux[0]);
+    if (mi & 1u) seg.emit(rS + o, (int)np + q, -uy[0]);
+    o = 0;
+    if (mi & 1u) seg.emit(rJ + o++, q, uy[0]);
+    if (mr & 1u) seg.emit(rJ + o, (int)np + q, ux[0]);
+  }
+}
+
+// D unit: DU D rows from the side buffer, by the whole CTA
+constexpr int DU = 32;
+template <int WK, int WL>
+__device__ __forceinline__ void fill_d_unit(const Prob& pr, long long u, const FillOut& fo, const NearSide& side,
+                                            NearRows& L) {
+  const long long np = pr.np;
+  const int lam = (int)(u * DU + threadIdx.x + 1);
+  if (threadIdx.x == 0) L.nr = 0;
+  __syncthreads();
+  if (threadIdx.x < DU && lam <= pr.n - 1) {
+    const long long off = fo.toff[2 * pr.npt + lam - 1];
+    fo.row_ptr[2 * np + lam - 1] = off;
+    const long long item = (long long)pr.n * 2 * pr.W + lam - 1;
+    const NearMeta m = side.meta[2 * item];
+    const int slot = atomicAdd(&L.nr, 1);
+    L.r[slot] = NearRowRef{off, m.tr, (int)(2 * item), m.nwin, m.hi, m.lend};
+    if (fo.K) fo.K[2 * np + lam - 1] = m.k;
+  }
+  cta_near_rows_out(L, side, pr.inv, (int)(2 * np - 1), fo);
+}
+
+// One output matrix's arguments of the fill pass.
+struct MatFill {
+  Prob pr;
+  const int* cnt;
+  FillOut fo;
+  NearSide side;
+};
+
+// Fill pass of Q0 and, with Q1W >= 0, of Q1 (widths Q1W, 0, no dissipators; staging-free
+// rows only, i.e. Q1W = 0) in one persistent launch: units u = blockIdx.x + k gridDim.x over
+//   [Q0 D units][Q1 D units][Q0 far tiles, last first][Q1 far tiles]
+// D units and the near-heavy last tiles start first; Q1's light tiles fill the tail.  The
+// next far tile's counts and offsets are loaded before the current unit runs.
+template <int WK, int WL, int PT, int Q1W>
+__global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFill m1) {
+  using FF = FillFar<WK, WL>;
+  static_assert(Q1W <= 0, "combined fill: Q1 rows must be staging-free");
+  extern __shared__ __align__(128) unsigned char dyn[];
+  __shared__ NearRows L;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr bool HAS1 = Q1W >= 0;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    m0.fo.row_ptr[m0.pr.m] = *m0.fo.nnz;
+    if (HAS1) m1.fo.row_ptr[m1.pr.m] = *m1.fo.nnz;
+  }
+  const long long nd0 = (m0.pr.n - 1 + DU - 1) / DU;
+  const long long nd1 = HAS1 ? (m1.pr.n - 1 + DU - 1) / DU : 0;
+  const long long nt0 = m0.pr.npt, nt1 = HAS1 ? m1.pr.npt : 0;
+  const long long D = nd0 + nd1, U = D + nt0 + nt1;
+  int* scol = reinterpret_cast<int*>(dyn + wid * FF::BYTES_PER_WARP);
+  double* sval = reinterpret_cast<double*>(dyn + wid * FF::BYTES_PER_WARP + FF::COLW * 4);
+  const FarCtx prf0{m0.pr.K.v, m0.pr.L, *m0.pr.tau_ptr, m0.pr.np, m0.pr.n, m0.pr.P};
+  FarCtx prf1{};
+  if (HAS1) prf1 = FarCtx{m1.pr.K.v, m1.pr.L, *m1.pr.tau_ptr, m1.pr.np, m1.pr.n, m1.pr.P};
+  // tile of unit u >= D: (matrix, tile)
+  auto tile_of = [&](long long v, int& mat) -> long long {
+    if (v < D + nt0) {
+      mat = 0;
+      return nt0 - 1 - (v - D);
+    }
+    mat = 1;
+    return v - D - nt0;
+  };
+  auto load = [&](long long v) -> TileIn {
+    int mat;
+    const long long t = tile_of(v, mat);
+    if (mat == 0 && !FF::DIRECT) return load_tile_in(m0.pr.np, nt0, t, m0.cnt, m0.fo.toff);
+    return TileIn{0, 0, 0, 0};  // direct tiles load their own inputs
+  };
+  long long u = blockIdx.x;
+  TileIn nxt{0, 0, 0, 0};
+  if (u < U && u >= D) nxt = load(u);
+  for (; u < U; u += gridDim.x) {  // block-uniform
+    const TileIn cur = nxt;
+    const long long un = u + gridDim.x;
+    if (un < U && un >= D) nxt = load(un);
+    __syncthreads();  // shared state of the previous unit consumed
+    if (u < nd0) {
+      fill_d_unit<WK, WL>(m0.pr, u, m0.fo, m0.side, L);
+    } else if (u < D) {
+      if constexpr (HAS1) fill_d_unit<0, 0>(m1.pr, u - nd0, m1.fo, m1.side, L);
+    } else {
+      int mat;
+      const long long t = tile_of(u, mat);
+      if (mat == 0) {
+        if constexpr (FF::DIRECT)
+          fill_direct_tile<WK, WL, PT>(prf0, nt0, t, m0.cnt, m0.fo, L.wtot);
+        else
+          fill_far_tile<WK, WL, PT>(prf0, nt0, t, cur, m0.fo, m0.side, m0.pr.inv, scol, sval, L);
+      } else {
+        if constexpr (HAS1) fill_direct_tile<0, 0, 0>(prf1, nt1, t, m1.cnt, m1.fo, L.wtot);
+      }
+    }
+  }
+  if (!FF::DIRECT && lane == 0) bulk_wait0();  // staging must outlive the bulk reads
+}
+
+// ---------------------------------------------------------------------------------------
+// Mode 1 (runtime widths): warp per pair, far positions from a table in shared memory.
+// Tiles of WARP_TP pairs (S and J), then D tiles of 8 rows.  Sole owner of each slot.
 // ---------------------------------------------------------------------------------------
 template <int NTHREADS>
 __device__ __forceinline__ void count_d_tile(const Prob& pr, long long t, int* cnt, int* tsum, double* scr_w,
@@ -277,86 +1122,6 @@ __device__ __forceinline__ void count_d_tile(const Prob& pr, long long t, int* c
   int tot;
   block_exclusive_scan(lane == 0 ? c : 0, wtot, tot);
   if (threadIdx.x == 0) tsum[2 * pr.npt + u] = tot;
-}
-
-// per-warp scratch (doubles): near-pair U tile (2 TW^2) + gS, gJ, pS, pJ (4 SW); D rows use
-// the first 2 (WIN_MAX + 2)
-template <int TW, int SW>
-struct Scr {
-  static constexpr int A = 2 * TW * TW + 4 * SW;
-  static constexpr int PER_WARP = A > 2 * (WIN_MAX + 2) ? A : 2 * (WIN_MAX + 2);
-};
-
-// mode 0, far pairs only (b - a > 2 WK): thread per pair, values in registers.  Near pairs
-// and D rows are counted by k_count_near.  Tile sums here cover the far rows; k_count_near
-// adds the near rows' counts to the same slots.
-template <int WK, int WL, int PT>
-__global__ void __launch_bounds__(128) k_count_far(Prob pr, int* __restrict__ cnt, int* __restrict__ tsum) {
-  pr.tau = *pr.tau_ptr;
-  __shared__ int wred[8];
-  const long long t = blockIdx.x;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long p = t * 128 + threadIdx.x;
-  const bool valid = p < pr.np;
-  int a, b;
-  warp_pairs(pr.n, t * 128 + wid * 32, a, b);
-  const bool far = valid && (b - a > 2 * WK);
-  int c = 0;
-  if (far) {
-    double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
-    far_values<WK, WL, PT>(pr, a, b, ux, uy);
-    int nR, nI;
-    far_counts<WK, WL>(pr.n, pr.tau, a, b, ux, uy, nR, nI);
-    c = nR + nI;
-    cnt[p] = c | (nR << CNT_BITS);
-    cnt[pr.np + p] = c;
-  }
-  int x = c;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
-  if (lane == 0) wred[wid] = x;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const int tot = wred[0] + wred[1] + wred[2] + wred[3];
-    tsum[t] = tot;  // S rows and J rows of a far pair have the same length
-    tsum[pr.npt + t] = tot;
-  }
-}
-
-// mode 0, near pairs (b - a <= 2W) and D rows: one warp per item; counts added to the tile
-// slots with integer atomics (order-independent).  D rows have one slot each.
-template <int TW>
-__global__ void __launch_bounds__(128) k_count_near(Prob pr, int* __restrict__ cnt, int* __restrict__ tsum) {
-  pr.tau = *pr.tau_ptr;
-  constexpr int SW = 2 * TW + 2;
-  __shared__ double scr[4][Scr<TW, SW>::PER_WARP];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long item = (long long)blockIdx.x * 4 + wid;
-  const int W2 = 2 * pr.W;
-  const long long nnear = (long long)pr.n * W2;
-  const Seg none = {nullptr, nullptr, 0};
-  if (item < nnear) {
-    const int a = (int)(item / W2), b = a + 1 + (int)(item % W2);
-    if (b >= pr.n) return;
-    int c1, c2;
-    double k1, k2;
-    warp_near_pair<false, TW, SW>(pr, a, b, scr[wid], c1, c2, k1, k2, none, 0, none, 0);
-    if (lane == 0) {
-      const long long p = (long long)pidx32(pr.n, a, b);
-      cnt[p] = c1;
-      cnt[pr.np + p] = c2;
-      atomicAdd(&tsum[p / 128], c1);
-      atomicAdd(&tsum[pr.npt + p / 128], c2);
-    }
-  } else if (item < nnear + pr.n - 1) {
-    const int lam = (int)(item - nnear) + 1;
-    double kv;
-    const int c = warp_d_row<false>(pr, lam, scr[wid], scr[wid] + WIN_MAX + 2, kv, none, 0);
-    if (lane == 0) {
-      cnt[2 * pr.np + lam - 1] = c;
-      tsum[2 * pr.npt + lam - 1] = c;
-    }
-  }
 }
 
 __global__ void __launch_bounds__(WARP_THREADS) k_count1(Prob pr, const FarPos* __restrict__ fp, int npos_far,
@@ -407,103 +1172,6 @@ __global__ void __launch_bounds__(WARP_THREADS) k_count1(Prob pr, const FarPos* 
   }
 }
 
-// ---------------------------------------------------------------------------------------
-// (a4) exclusive scan of the tile sums -> int64 tile offsets and nnz.  Fixed order
-// (deterministic).  Small: one CTA through shared memory.  Large: chunk sums, a scan of
-// the chunk sums, then per-chunk scans.
-// ---------------------------------------------------------------------------------------
-constexpr int SCAN_CHUNK = 16384;
-
-template <typename T>
-__device__ __forceinline__ long long block_scan_ll(long long v, long long* wsum, long long& total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  long long x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    long long y = __shfl_up_sync(FULL, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    long long s = lane < nwarps ? wsum[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      long long y = __shfl_up_sync(FULL, s, o);
-      if (lane >= o) s += y;
-    }
-    if (lane < nwarps) wsum[lane] = s;
-  }
-  __syncthreads();
-  total = wsum[nwarps - 1];
-  long long before = wid > 0 ? wsum[wid - 1] : 0;
-  __syncthreads();
-  return before + x - v;
-}
-
-// scan of one chunk [c0, c0 + len) of int32 values with base offset; writes int64 exclusive
-__global__ void __launch_bounds__(1024) k_scan_chunk(const int* __restrict__ ts, long long nslots,
-                                                     const long long* __restrict__ chunk_base, long long* out,
-                                                     long long* nnz_out) {
-  extern __shared__ int sv[];
-  __shared__ long long wsum[32];
-  const long long c0 = (long long)blockIdx.x * SCAN_CHUNK;
-  const int len = (int)(nslots - c0 < SCAN_CHUNK ? nslots - c0 : SCAN_CHUNK);
-  for (int i = threadIdx.x; i < len; i += blockDim.x) sv[i] = ts[c0 + i];
-  __syncthreads();
-  const int per = (len + blockDim.x - 1) / blockDim.x;
-  const int lo = threadIdx.x * per, hi = lo + per < len ? lo + per : len;
-  long long local = 0;
-  for (int i = lo; i < hi; ++i) local += sv[i];
-  long long total;
-  long long run = block_scan_ll<long long>(local, wsum, total) + (chunk_base ? chunk_base[blockIdx.x] : 0);
-  for (int i = lo; i < hi; ++i) {
-    out[c0 + i] = run;
-    run += sv[i];
-  }
-  if (nnz_out && threadIdx.x == blockDim.x - 1 && blockIdx.x == gridDim.x - 1) *nnz_out = run;
-}
-
-__global__ void __launch_bounds__(1024) k_scan_reduce(const int* __restrict__ ts, long long nslots,
-                                                      long long* __restrict__ chunk_sum) {
-  __shared__ long long wsum[32];
-  const long long c0 = (long long)blockIdx.x * SCAN_CHUNK;
-  const int len = (int)(nslots - c0 < SCAN_CHUNK ? nslots - c0 : SCAN_CHUNK);
-  long long local = 0;
-  for (int i = threadIdx.x; i < len; i += blockDim.x) local += ts[c0 + i];
-  long long total;
-  block_scan_ll<long long>(local, wsum, total);
-  if (threadIdx.x == 0) chunk_sum[blockIdx.x] = total;
-}
-
-__global__ void __launch_bounds__(1024) k_scan_top(long long* chunk, int nchunks) {
-  __shared__ long long wsum[32];
-  const int per = (nchunks + blockDim.x - 1) / blockDim.x;
-  const int lo = threadIdx.x * per, hi = lo + per < nchunks ? lo + per : nchunks;
-  long long local = 0;
-  for (int i = lo; i < hi; ++i) local += chunk[i];
-  long long total;
-  long long run = block_scan_ll<long long>(local, wsum, total);
-  for (int i = lo; i < hi; ++i) {
-    long long v = chunk[i];
-    chunk[i] = run;
-    run += v;
-  }
-}
-
-// ---------------------------------------------------------------------------------------
-// (a5) fill pass (+ K).  Same tiling as the count pass.
-// ---------------------------------------------------------------------------------------
-struct FillOut {
-  int64_t* row_ptr;
-  int32_t* col;
-  double* val;
-  long long cap;  // capacity of col/val (writes at or beyond it are dropped; see sun_run)
-  double* K;  // nullptr: not written (Q1)
-  const long long* toff;
-  const long long* nnz;
-};
-
 template <int NTHREADS>
 __device__ __forceinline__ void fill_d_tile(const Prob& pr, const FillOut& fo, long long t, const int* cnt,
                                             double* scr_w, int* wtot) {
@@ -513,7 +1181,7 @@ __device__ __forceinline__ void fill_d_tile(const Prob& pr, const FillOut& fo, l
   const long long baseD = fo.toff[2 * pr.npt + u];
   const int lam = (int)(u * (NTHREADS / 32) + wid + 1);
   const bool valid = lam <= pr.n - 1;
-  const int c = valid ? (cnt[2 * np + lam - 1] & CNT_MASK) : 0;
+  const int c = valid ? cnt[2 * np + lam - 1] : 0;
   int tot;
   int ex = block_exclusive_scan(lane == 0 ? c : 0, wtot, tot);
   ex = __shfl_sync(FULL, ex, 0);
@@ -522,146 +1190,6 @@ __device__ __forceinline__ void fill_d_tile(const Prob& pr, const FillOut& fo, l
     const Seg sD = {fo.col + baseD, fo.val + baseD, fo.cap - baseD};
     double kv;
     warp_d_row<true>(pr, lam, scr_w, scr_w + WIN_MAX + 2, kv, sD, ex);
-    if (lane == 0 && fo.K) fo.K[2 * np + lam - 1] = kv;
-  }
-}
-
-constexpr int CAPW = 1024;   // per-warp staging capacity (entries) in mode 0 (one row block at a time)
-
-// Copy a warp's staged segment [g0, g1) (tile-local offsets) to global memory, skipping the
-// "holes" of long rows (lanes flagged in `holes`, hole = [hoff, hoff + hlen)) that were
-// written directly.  The stage position advances only over copied entries.
-__device__ __forceinline__ void warp_copy_out(const int* scol, const double* sval, long long gbase, int g0, int g1,
-                                              unsigned holes, int hoff, int hlen, int32_t* __restrict__ col,
-                                              double* __restrict__ val, long long cap) {
-  const int lane = threadIdx.x & 31;
-  int sp = 0, gp = g0;
-  for (;;) {
-    const bool last = holes == 0;
-    int hs = g1, hl = 0;
-    if (!last) {
-      const int h = __ffs(holes) - 1;
-      holes &= holes - 1;
-      hs = __shfl_sync(FULL, hoff, h);
-      hl = __shfl_sync(FULL, hlen, h);
-    }
-    long long run_l = hs - gp;
-    if (gbase + gp + run_l > cap) run_l = cap - (gbase + gp) > 0 ? cap - (gbase + gp) : 0;
-    const int run = (int)run_l;
-    int32_t* cdst = col + gbase + gp;
-    double* vdst = val + gbase + gp;
-    for (int k = lane; k < run; k += 32) {
-      cdst[k] = scol[sp + k];
-      vdst[k] = sval[sp + k];
-    }
-    sp += run;
-    gp = hs + hl;
-    if (last) break;
-  }
-}
-
-// mode 0 fill, far pairs: thread per pair computes its values in registers and writes its
-// two rows into per-warp shared staging (S rows of the warp's 32 pairs, then their J rows);
-// the warp copies each staged block out with coalesced stores, skipping the near rows
-// (written by k_fill_near).  Also writes row_ptr of all pair rows and K = 0 for far pairs.
-template <int WK, int WL, int PT>
-__global__ void __launch_bounds__(128) k_fill_far(Prob pr, const int* __restrict__ cnt, FillOut fo) {
-  pr.tau = *pr.tau_ptr;
-  static_assert(64 * FarT<WK, WL>::NPOS <= CAPW, "far rows of a warp must fit the staging");
-  extern __shared__ __align__(16) unsigned char dyn[];
-  __shared__ int wtot[8];
-  const long long t = blockIdx.x;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long np = pr.np;
-  if (t == 0 && threadIdx.x == 0) fo.row_ptr[pr.m] = *fo.nnz;
-  double* sval = reinterpret_cast<double*>(dyn) + wid * CAPW;
-  int* scol = reinterpret_cast<int*>(dyn + 4 * CAPW * sizeof(double)) + wid * CAPW;
-  const long long p = t * 128 + threadIdx.x;
-  const bool valid = p < np;
-  const int rawS = valid ? cnt[p] : 0;
-  const int cS = rawS & CNT_MASK, nRe = rawS >> CNT_BITS;
-  const int cJ = valid ? (cnt[np + p] & CNT_MASK) : 0;
-  int a, b;
-  warp_pairs(pr.n, t * 128 + wid * 32, a, b);
-  int wtS, wtJ;
-  int exS = warp_excl_scan(cS, wtS);
-  int exJ = warp_excl_scan(cJ, wtJ);
-  if (lane == 0) {
-    wtot[wid] = wtS;
-    wtot[4 + wid] = wtJ;
-  }
-  __syncthreads();
-  int pS = 0, pJ = 0;
-#pragma unroll
-  for (int w = 0; w < 4; ++w) {
-    pS += w < wid ? wtot[w] : 0;
-    pJ += w < wid ? wtot[4 + w] : 0;
-  }
-  exS += pS;
-  exJ += pJ;
-  const long long baseS = fo.toff[t], baseJ = fo.toff[pr.npt + t];
-  if (valid) {
-    fo.row_ptr[p] = baseS + exS;
-    fo.row_ptr[np + p] = baseJ + exJ;
-  }
-  const bool far = valid && (b - a > 2 * WK);
-  const bool nearp = valid && !far;
-  if (far && fo.K) {
-    fo.K[p] = 0.0;
-    fo.K[np + p] = 0.0;
-  }
-  const unsigned nearmask = __ballot_sync(FULL, nearp);
-  double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
-  if (far) far_values<WK, WL, PT>(pr, a, b, ux, uy);
-#pragma unroll
-  for (int row = 0; row < 2; ++row) {  // S rows of the warp's 32 pairs, then their J rows
-    const int c_me = row ? cJ : cS, ex_me = row ? exJ : exS, w0 = row ? pJ : pS, wt = row ? wtJ : wtS;
-    const long long gbase = row ? baseJ : baseS;
-    int ht;
-    const int hb = warp_excl_scan(nearp ? c_me : 0, ht);
-    if (far) {
-      const int n1 = row ? (cS - nRe) : nRe;
-      far_emit_row<WK, WL>(pr.n, (int)np, pr.tau, a, b, row, ux, uy, n1, SmemSink{scol, sval}, ex_me - w0 - hb);
-    }
-    __syncwarp();
-    warp_copy_out(scol, sval, gbase, w0, w0 + wt, nearmask, ex_me, c_me, fo.col, fo.val, fo.cap);
-    __syncwarp();
-  }
-}
-
-// mode 0 fill, near pairs and D rows (one warp per item, rows written directly).  Runs after
-// k_fill_far, whose row_ptr entries give the near rows' offsets.
-template <int TW>
-__global__ void __launch_bounds__(128) k_fill_near(Prob pr, FillOut fo) {
-  pr.tau = *pr.tau_ptr;
-  constexpr int SW = 2 * TW + 2;
-  __shared__ double scr[4][Scr<TW, SW>::PER_WARP];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long item = (long long)blockIdx.x * 4 + wid;
-  const int W2 = 2 * pr.W;
-  const long long nnear = (long long)pr.n * W2;
-  const long long np = pr.np;
-  if (item < nnear) {
-    const int a = (int)(item / W2), b = a + 1 + (int)(item % W2);
-    if (b >= pr.n) return;
-    const long long p = (long long)pidx32(pr.n, a, b);
-    const long long oS = fo.row_ptr[p], oJ = fo.row_ptr[np + p];
-    const Seg sS = {fo.col + oS, fo.val + oS, fo.cap - oS};
-    const Seg sJ = {fo.col + oJ, fo.val + oJ, fo.cap - oJ};
-    int c1, c2;
-    double k1, k2;
-    warp_near_pair<true, TW, SW>(pr, a, b, scr[wid], c1, c2, k1, k2, sS, 0, sJ, 0);
-    if (lane == 0 && fo.K) {
-      fo.K[p] = k1;
-      fo.K[np + p] = k2;
-    }
-  } else if (item < nnear + pr.n - 1) {
-    const int lam = (int)(item - nnear) + 1;
-    const long long off = fo.toff[2 * pr.npt + lam - 1];
-    if (lane == 0) fo.row_ptr[2 * np + lam - 1] = off;
-    const Seg sD = {fo.col + off, fo.val + off, fo.cap - off};
-    double kv;
-    warp_d_row<true>(pr, lam, scr[wid], scr[wid] + WIN_MAX + 2, kv, sD, 0);
     if (lane == 0 && fo.K) fo.K[2 * np + lam - 1] = kv;
   }
 }
@@ -690,7 +1218,7 @@ __global__ void __launch_bounds__(WARP_THREADS) k_fill1(Prob pr, const FarPos* _
   const int i0 = threadIdx.x;
   const long long p0 = t * WARP_TP + i0;
   const bool valid = i0 < WARP_TP && p0 < np;
-  const int cS = valid ? (cnt[p0] & CNT_MASK) : 0, cJ = valid ? (cnt[np + p0] & CNT_MASK) : 0;
+  const int cS = valid ? cnt[p0] : 0, cJ = valid ? cnt[np + p0] : 0;
   int totS, totJ;
   const int exS = block_exclusive_scan(cS, wtot, totS);
   const int exJ = block_exclusive_scan(cJ, wtot, totJ);
@@ -721,6 +1249,89 @@ __global__ void __launch_bounds__(WARP_THREADS) k_fill1(Prob pr, const FarPos* _
       fo.K[p] = k1;
       fo.K[np + p] = k2;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// (a4) exclusive scan of the int32 tile sums of both matrices (blockIdx.y) into int64 tile
+// offsets and nnz, in one launch: chained scan with decoupled look-back.  Chunks are taken
+// in ticket order, so every predecessor of a running chunk is resident or done.  Integer
+// sums: the result does not depend on the order (deterministic).
+// ---------------------------------------------------------------------------------------
+struct ScanArgs {
+  const int* ts[2];
+  long long* toff[2];
+  unsigned long long* status[2];
+  long long* nnz[2];
+  long long nslots[2];
+  unsigned int* ticket;
+};
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_chain(ScanArgs A) {
+  const int y = blockIdx.y;
+  __shared__ unsigned int chunk_s;
+  __shared__ long long wsum[32];
+  __shared__ long long prefix_s;
+  if (threadIdx.x == 0) chunk_s = atomicAdd(&A.ticket[y], 1u);
+  __syncthreads();
+  const long long chunk = chunk_s;
+  const long long nslots = A.nslots[y];
+  const long long nchunks = (nslots + SCAN_TILE - 1) / SCAN_TILE;
+  if (chunk >= (nchunks > 0 ? nchunks : 1)) return;  // block-uniform
+  const long long c0 = chunk * SCAN_TILE + (long long)threadIdx.x * SCAN_IPT;
+  const int* ts = A.ts[y];
+  int v[SCAN_IPT];
+  if (c0 + SCAN_IPT <= nslots) {
+    const int4 q = *reinterpret_cast<const int4*>(ts + c0);  // 16-byte aligned (c0 % 4 == 0)
+    v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+  } else {
+#pragma unroll
+    for (int i = 0; i < SCAN_IPT; ++i) v[i] = c0 + i < nslots ? ts[c0 + i] : 0;
+  }
+  long long local = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_IPT; ++i) local += v[i];
+  long long total;
+  const long long ex = block_scan_ll(local, wsum, total);
+  unsigned long long* st = A.status[y];
+  if (threadIdx.x == 0) {
+    long long prefix = 0;
+    if (chunk == 0) {
+      __threadfence();
+      atomicExch(&st[0], SCAN_P | (unsigned long long)total);
+    } else {
+      __threadfence();
+      atomicExch(&st[chunk], SCAN_A | (unsigned long long)total);
+      for (long long k = chunk - 1; k >= 0; --k) {
+        unsigned long long s;
+        do {
+          s = atomicAdd(&st[k], 0ull);
+        } while ((s & ~SCAN_V) == 0ull);
+        prefix += (long long)(s & SCAN_V);
+        if ((s & ~SCAN_V) == SCAN_P) break;
+      }
+      __threadfence();
+      atomicExch(&st[chunk], SCAN_P | (unsigned long long)(prefix + total));
+    }
+    prefix_s = prefix;
+    if (chunk == nchunks - 1 || nchunks == 0) *A.nnz[y] = prefix + total;
+  }
+  __syncthreads();
+  long long run = prefix_s + ex;
+  long long o[SCAN_IPT];
+#pragma unroll
+  for (int i = 0; i < SCAN_IPT; ++i) {
+    o[i] = run;
+    run += v[i];
+  }
+  long long* out = A.toff[y];
+  if (c0 + SCAN_IPT <= nslots) {
+    reinterpret_cast<longlong2*>(out + c0)[0] = make_longlong2(o[0], o[1]);
+    reinterpret_cast<longlong2*>(out + c0)[1] = make_longlong2(o[2], o[3]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < SCAN_IPT; ++i)
+      if (c0 + i < nslots) out[c0 + i] = o[i];
   }
 }
 
@@ -766,7 +1377,7 @@ bool zcsr_ok(const sun_zcsr* A, int n) {
   return A && A->n == n && A->nnz >= 0 && A->row_ptr && (A->nnz == 0 || (A->col && A->val));
 }
 
-// far-pair position list in far_positions() order (relative offsets to (a, b))
+// far-pair position list (relative offsets to (a, b)), lexicographic; same as far_pos()
 void build_far_positions(int W, int wL, int wK, std::vector<int>& dc, std::vector<int>& dd) {
   dc.clear();
   dd.clear();
@@ -783,6 +1394,23 @@ void build_far_positions(int W, int wL, int wK, std::vector<int>& dc, std::vecto
   }
 }
 
+// ---- mode-0 instantiations: (WK, WL, PT) ----
+#define SUN_MODE0_LIST(X)                                        \
+  X(0, 0, 0) X(1, 0, 0) X(2, 0, 0) X(3, 0, 0)                    \
+  X(0, 0, 1) X(1, 0, 1) X(2, 0, 1) X(3, 0, 1) X(2, 1, 1)         \
+  X(0, 0, -1) X(1, 0, -1) X(2, 0, -1) X(3, 0, -1) X(2, 1, -1)
+
+int mode0_pt(int P) { return P == 0 ? 0 : (P == 1 ? 1 : -1); }
+
+bool mode0_supported(int wK, int wL, int P) {
+  const int pt = mode0_pt(P);
+#define SUN_X(WK, WL, PT) \
+  if (wK == WK && wL == WL && pt == PT) return true;
+  SUN_MODE0_LIST(SUN_X)
+#undef SUN_X
+  return false;
+}
+
 void setup_prob(sun_plan_s* pl, int which) {
   Prob& pr = pl->pr[which];
   const Layout& L = pl->lay;
@@ -796,7 +1424,6 @@ void setup_prob(sun_plan_s* pl, int which) {
     pr.K = {reinterpret_cast<const double2*>(pl->ws + L.kb0), pl->wK};
     pr.H = {reinterpret_cast<const double2*>(pl->ws + L.hb0), pl->wK};
     pr.L = reinterpret_cast<const double2*>(pl->ws + L.lb);
-    pr.tau = pl->tau0;
     pr.tau_ptr = &reinterpret_cast<DevHeader*>(pl->ws + L.hdr)->tau[0];
   } else {
     pr.P = 0;
@@ -805,9 +1432,9 @@ void setup_prob(sun_plan_s* pl, int which) {
     pr.K = {reinterpret_cast<const double2*>(pl->ws + L.hb1), pl->wH1};
     pr.H = pr.K;
     pr.L = nullptr;
-    pr.tau = pl->tau1;
     pr.tau_ptr = &reinterpret_cast<DevHeader*>(pl->ws + L.hdr)->tau[1];
   }
+  pr.tau = 0.0;
   pr.W = pr.wK > pr.wL ? pr.wK : pr.wL;
   pr.inv = reinterpret_cast<const double*>(pl->ws + L.inv);
   build_far_positions(pr.W, pr.wL, pr.wK, pl->pos_dc[which], pl->pos_dd[which]);
@@ -817,91 +1444,104 @@ void setup_prob(sun_plan_s* pl, int which) {
     pl->hfp[which].dc[i] = pl->pos_dc[which][i];
     pl->hfp[which].dd[i] = pl->pos_dd[which][i];
   }
-  // thread-per-pair with per-warp shared staging for narrow bands (compile-time widths);
-  // else warp-per-pair with direct coalesced row stores
-  pr.mode = mode0_supported(pr.wK, pr.wL) ? 0 : 1;
-  pr.tp = pr.mode == 0 ? THREAD_TP : WARP_TP;
-  pr.npt = (pr.np + pr.tp - 1) / pr.tp;
-  pr.ndt = pr.mode == 0 ? (pl->n - 1) : (pl->n - 1 + WARP_THREADS / 32 - 1) / (WARP_THREADS / 32);
+  pr.mode = mode0_supported(pr.wK, pr.wL, pr.P) ? 0 : 1;
+  pl->side[which] = NearSide{reinterpret_cast<int32_t*>(pl->ws + L.side_col[which]),
+                             reinterpret_cast<double*>(pl->ws + L.side_val[which]),
+                             reinterpret_cast<NearMeta*>(pl->ws + L.side_meta[which]), (4 * pr.W + 1) * (4 * pr.W + 1)};
+  if (pr.mode == 0) {
+    pr.tp = pr.wK == 0 ? 2048 : TP0;  // Tiling<WK, WL>::TP (staging-free W = 0: 8 pairs per thread)
+    pr.npt = (pr.np + pr.tp - 1) / pr.tp;
+    pr.ndt = pl->n - 1;
+    const long long items = (long long)pl->n * 2 * pr.W + (pl->n - 1);
+    pr.nb_near = (items + 7) / 8;
+  } else {
+    pr.tp = WARP_TP;
+    pr.npt = (pr.np + WARP_TP - 1) / WARP_TP;
+    pr.ndt = (pl->n - 1 + WARP_THREADS / 32 - 1) / (WARP_THREADS / 32);
+    pr.nb_near = 0;
+  }
 }
 
-
-template <int WK, int WL, int PT>
-cudaError_t launch_far(const Prob& pr, int* cnt, int* ts, const FillOut* fo, cudaStream_t st) {
-  if (!fo) {
-    k_count_far<WK, WL, PT><<<(unsigned)pr.npt, 128, 0, st>>>(pr, cnt, ts);
-    return cudaGetLastError();
-  }
-  const size_t smem = (size_t)4 * CAPW * (sizeof(double) + sizeof(int));
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_fill_far<WK, WL, PT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  k_fill_far<WK, WL, PT><<<(unsigned)pr.npt, 128, smem, st>>>(pr, cnt, *fo);
+// ---- mode-0 launchers.  Q1W = -1: one matrix per launch; Q1W = 0: Q0 + Q1 (Q1 = (0, 0, 0)).
+template <int WK, int WL, int PT, int Q1W>
+cudaError_t launch_count0(const MatCount& m0, const MatCount& m1, const ScanIn& sc, cudaStream_t st) {
+  const long long U = m0.pr.npt + m0.pr.nb_near + (Q1W >= 0 ? m1.pr.npt + m1.pr.nb_near : 0);
+  if (U > 0) k_count0<WK, WL, PT, Q1W><<<(unsigned)U, 256, 0, st>>>(m0, m1, sc);
   return cudaGetLastError();
 }
 
-// (WK, WL, PT) instantiations of the mode-0 far kernels
-#define SUN_MODE0_LIST(X) \
-  X(0, 0, 0) X(1, 0, 0) X(2, 0, 0) X(3, 0, 0) X(0, 0, 1) X(1, 0, 1) X(2, 0, 1) X(3, 0, 1) X(2, 1, 1) \
-  X(0, 0, -1) X(1, 0, -1) X(2, 0, -1) X(3, 0, -1) X(2, 1, -1)
-
-int mode0_pt(const Prob& pr) { return pr.P == 0 ? 0 : (pr.P == 1 ? 1 : -1); }
-
-cudaError_t dispatch_far(const Prob& pr, int* cnt, int* ts, const FillOut* fo, cudaStream_t st) {
-  const int pt = mode0_pt(pr);
-#define SUN_X(WK, WL, PT) \
-  if (pr.wK == WK && pr.wL == WL && pt == PT) return launch_far<WK, WL, PT>(pr, cnt, ts, fo, st);
-  SUN_MODE0_LIST(SUN_X)
-#undef SUN_X
-  return cudaErrorInvalidValue;
+// called at plan creation (outside any graph capture): dynamic shared memory limit and the
+// persistent fill grid (resident CTAs x SMs, capped by the number of units)
+template <int WK, int WL, int PT, int Q1W>
+cudaError_t attr_fill0(const Prob& p0, const Prob* p1, long long& grid) {
+  const int smem = FillFar<WK, WL>::SMEM;
+  cudaError_t e = cudaFuncSetAttribute(k_fill0<WK, WL, PT, Q1W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int dev = 0, sms = 0, nb = 0;
+  if (e == cudaSuccess) e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fill0<WK, WL, PT, Q1W>, 256, smem);
+  if (e != cudaSuccess) return e;
+  long long U = p0.npt + (p0.n - 1 + DU - 1) / DU;
+  if (Q1W >= 0 && p1) U += p1->npt + (p1->n - 1 + DU - 1) / DU;
+  grid = (long long)(nb > 0 ? nb : 1) * sms;
+  if (grid > U) grid = U;
+  return cudaSuccess;
 }
 
-cudaError_t dispatch_near(const Prob& pr, int* cnt, int* ts, const FillOut* fo, cudaStream_t st) {
-  const long long items = (long long)pr.n * 2 * pr.W + (pr.n - 1);
-  const unsigned grid = (unsigned)((items + 3) / 4);
-  if (grid == 0) return cudaSuccess;
-#define SUN_NEAR(TW)                                                            \
-  if (2 * pr.W + 1 == TW) {                                                     \
-    if (!fo)                                                                    \
-      k_count_near<TW><<<grid, 128, 0, st>>>(pr, cnt, ts);                      \
-    else                                                                        \
-      k_fill_near<TW><<<grid, 128, 0, st>>>(pr, *fo);                           \
-    return cudaGetLastError();                                                  \
-  }
-  SUN_NEAR(1) SUN_NEAR(3) SUN_NEAR(5) SUN_NEAR(7)
-#undef SUN_NEAR
-  return cudaErrorInvalidValue;
-}
-
-// exclusive scan of nslots int32 tile sums into int64 offsets; total -> nnz_out
-cudaError_t launch_scan(const int* ts, long long nslots, long long* toff, long long* chunk, long long* nnz_out,
-                        cudaStream_t st) {
-  const size_t smem = SCAN_CHUNK * sizeof(int);
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_scan_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  if (nslots <= SCAN_CHUNK) {
-    k_scan_chunk<<<1, 1024, smem, st>>>(ts, nslots, nullptr, toff, nnz_out);
-    return cudaGetLastError();
-  }
-  const int nchunks = (int)((nslots + SCAN_CHUNK - 1) / SCAN_CHUNK);
-  k_scan_reduce<<<nchunks, 1024, 0, st>>>(ts, nslots, chunk);
-  k_scan_top<<<1, 1024, 0, st>>>(chunk, nchunks);
-  k_scan_chunk<<<nchunks, 1024, smem, st>>>(ts, nslots, chunk, toff, nnz_out);
+template <int WK, int WL, int PT, int Q1W>
+cudaError_t launch_fill0(const MatFill& m0, const MatFill& m1, long long grid, cudaStream_t st) {
+  k_fill0<WK, WL, PT, Q1W><<<(unsigned)grid, 256, FillFar<WK, WL>::SMEM, st>>>(m0, m1);
   return cudaGetLastError();
 }
+
+#define SUN_DISPATCH0(pr, q1w, CALL)                              \
+  do {                                                            \
+    const int pt_ = mode0_pt((pr).P);                             \
+    if ((q1w) == 0) {                                             \
+      SUN_MODE0_LIST(SUN_X0)                                      \
+    } else {                                                      \
+      SUN_MODE0_LIST(SUN_X1)                                      \
+    }                                                             \
+    return cudaErrorInvalidValue;                                 \
+  } while (0)
+
+cudaError_t dispatch_attr0(const Prob& p0, const Prob* p1, int q1w, long long& grid) {
+#define SUN_X0(WK, WL, PT) \
+  if (p0.wK == WK && p0.wL == WL && pt_ == PT) return attr_fill0<WK, WL, PT, 0>(p0, p1, grid);
+#define SUN_X1(WK, WL, PT) \
+  if (p0.wK == WK && p0.wL == WL && pt_ == PT) return attr_fill0<WK, WL, PT, -1>(p0, p1, grid);
+  SUN_DISPATCH0(p0, q1w, 0);
+#undef SUN_X0
+#undef SUN_X1
+}
+
+cudaError_t dispatch_count0(const MatCount& m0, const MatCount& m1, int q1w, const ScanIn& sc, cudaStream_t st) {
+#define SUN_X0(WK, WL, PT) \
+  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_count0<WK, WL, PT, 0>(m0, m1, sc, st);
+#define SUN_X1(WK, WL, PT) \
+  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_count0<WK, WL, PT, -1>(m0, m1, sc, st);
+  SUN_DISPATCH0(m0.pr, q1w, 0);
+#undef SUN_X0
+#undef SUN_X1
+}
+
+cudaError_t dispatch_fill0(const MatFill& m0, const MatFill& m1, int q1w, long long grid, cudaStream_t st) {
+#define SUN_X0(WK, WL, PT) \
+  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_fill0<WK, WL, PT, 0>(m0, m1, grid, st);
+#define SUN_X1(WK, WL, PT) \
+  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_fill0<WK, WL, PT, -1>(m0, m1, grid, st);
+  SUN_DISPATCH0(m0.pr, q1w, 0);
+#undef SUN_X0
+#undef SUN_X1
+}
+
+long long nslots_of(const Prob& pr) { return 2 * pr.npt + pr.ndt; }
 
 }  // namespace
 
 extern "C" {
 
-const char* sun_version(void) { return "sunfold 0.1 (sm_100a, fp64)"; }
+const char* sun_version(void) { return "sunfold 0.2 (sm_100a, fp64)"; }
 
 const char* sun_status_string(int status) {
   switch (status) {
@@ -993,7 +1633,6 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
   for (int p = 0; p < P; ++p) {
     pl->L.push_back(*L[p]);
     pl->gamma.push_back(gamma[p]);
-    pl->hsqrtg[p] = sqrt(gamma[p]);
   }
   pl->ws = ws;
   pl->ws_bytes = workspace_bytes;
@@ -1027,6 +1666,43 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
     delete pl;
     return SUN_ERR_BANDWIDTH;
   }
+  const int nmat = 1 + pl->has_h1;
+  {
+    const Prob& p0 = pl->pr[0];
+    const Prob& p1 = pl->pr[1];
+    pl->combined = p0.mode == 0 && (!pl->has_h1 || (p1.mode == 0 && p1.wK == 0 && p1.wL == 0 && p1.P == 0));
+    pl->scan_in_count = 0;  // a one-CTA scan is a long serial chain: the chained-scan kernel is faster
+  }
+  pl->launches_count = 2 + (pl->combined ? 1 : nmat) + (pl->scan_in_count ? 0 : 1);  // expand x2, count, scan
+  pl->launches_fill = pl->combined ? 1 : nmat;
+  for (int i = 0; i < 2; ++i) {
+    cudaError_t e1 = cudaStreamCreateWithFlags(&pl->aux[i], cudaStreamNonBlocking);
+    if (e1 == cudaSuccess) e1 = cudaEventCreateWithFlags(&pl->ev_join[i], cudaEventDisableTiming);
+    if (e1 != cudaSuccess) {
+      delete pl;
+      return cuda_fail(e1);
+    }
+  }
+  {
+    cudaError_t e1 = cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming);
+    if (e1 == cudaSuccess) e1 = cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking);
+    if (e1 != cudaSuccess) {
+      delete pl;
+      return cuda_fail(e1);
+    }
+    const char* ng = getenv("SUNFOLD_NO_GRAPHS");
+    pl->use_graphs = !(ng && ng[0] && ng[0] != '0');
+    if (pl->combined) {
+      e1 = dispatch_attr0(pl->pr[0], pl->has_h1 ? &pl->pr[1] : nullptr, pl->has_h1 ? 0 : -1, pl->fill_grid[0]);
+    } else {
+      for (int which = 0; which < nmat && e1 == cudaSuccess; ++which)
+        if (pl->pr[which].mode == 0) e1 = dispatch_attr0(pl->pr[which], nullptr, -1, pl->fill_grid[which]);
+    }
+    if (e1 != cudaSuccess) {
+      delete pl;
+      return cuda_fail(e1);
+    }
+  }
   // far-position tables (used by the warp-per-pair mode only)
   cudaError_t e = cudaSuccess;
   if (pl->pr[0].mode == 1)
@@ -1043,69 +1719,94 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
   return SUN_OK;
 }
 
-int sun_count(sun_plan pl, void* stream) {
-  if (!pl) return SUN_ERR_ARG;
-  cudaStream_t st = (cudaStream_t)stream;
+static int enqueue_count(sun_plan pl, cudaStream_t st) {
   const Layout& L = pl->lay;
   const int n = pl->n;
   char* ws = pl->ws;
   DevHeader* hdr = (DevHeader*)(ws + L.hdr);
-  // (a1) expand: norms + pattern check, band storage, K = H0 + i/2 M, tau (all on the device)
-  long long zero_doubles = (long long)((L.ts0 - L.kb0) / sizeof(double));
-  k_zero<<<296, 256, 0, st>>>((double*)(ws + L.kb0), zero_doubles, &hdr->flags);
+  // (a1) expand: band storage + norms/flags per row block; zero the scan state
+  const long long nz32 = (long long)((L.st0 - L.ts0) / sizeof(int));
+  const long long nz64 = (long long)((L.toff0 - L.st0) / sizeof(unsigned long long));
+  dim3 g1((unsigned)L.nrb, (unsigned)pl->ops.nops);
+  k_expand_rows<<<g1, EXP_THREADS, 0, st>>>(pl->ops, (double2*)(ws + L.hb0), pl->wK, (double2*)(ws + L.hb1), pl->wH1,
+                                            (double2*)(ws + L.lb), pl->wL, (BlkInfo*)(ws + L.blk), (int*)(ws + L.ts0),
+                                            nz32, (unsigned long long*)(ws + L.st0), nz64, hdr);
   CK(cudaGetLastError());
-  k_analyze<<<pl->ops.nops, 256, 0, st>>>(pl->ops, hdr);
-  CK(cudaGetLastError());
-  long long nthreads = (long long)pl->ops.nops * n;
-  k_scatter<<<(unsigned)((nthreads + 255) / 256), 256, 0, st>>>(
-      pl->ops, pl->has_h1, (double2*)(ws + L.hb0), pl->wK, (double2*)(ws + L.hb1), pl->wH1, (double2*)(ws + L.lb),
-      pl->wL);
-  CK(cudaGetLastError());
+  // (a1) K = H0 + i/2 sum gamma L^+L, reductions -> tau, inv[l], Hermiticity
   long long nk = (long long)n * (2 * pl->wK + 1);
   if (nk < n) nk = n;
-  k_band_k<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(
-      n, pl->P, (const double2*)(ws + L.hb0), (double2*)(ws + L.kb0), pl->wK, (const double2*)(ws + L.lb), pl->wL,
-      (const double2*)(ws + L.hb1), pl->wH1, pl->has_h1, pl->gam, hdr, (double*)(ws + L.inv));
+  k_expand_k<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(
+      n, pl->P, pl->ops.nops, pl->has_h1, (int)L.nrb, (const BlkInfo*)(ws + L.blk), (const double2*)(ws + L.hb0),
+      (double2*)(ws + L.kb0), pl->wK, (const double2*)(ws + L.lb), pl->wL, (const double2*)(ws + L.hb1), pl->wH1,
+      pl->gam, hdr, (double*)(ws + L.inv));
   CK(cudaGetLastError());
-  // (a3) count pass + (a4) prefix scan, per output matrix
-  for (int which = 0; which < 1 + pl->has_h1; ++which) {
+  // (a3) count pass (+ (a4) prefix scan in the last CTA when small)
+  const int nmat = 1 + pl->has_h1;
+  MatCount mc[2];
+  ScanArgs sa;
+  ScanIn sc;
+  memset(&sa, 0, sizeof(sa));
+  memset(&sc, 0, sizeof(sc));
+  long long maxchunks = 1;
+  for (int which = 0; which < nmat; ++which) {
     const Prob& pr = pl->pr[which];
     int* cnt = (int*)(ws + (which ? L.cnt1 : L.cnt0));
     int* ts = (int*)(ws + (which ? L.ts1 : L.ts0));
-    const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
-    if (pr.mode == 0) {
-      CK(dispatch_far(pr, cnt, ts, nullptr, st));   // far pairs (writes the tile sums)
-      CK(dispatch_near(pr, cnt, ts, nullptr, st));  // near pairs + D rows (atomic adds)
-    } else {
-      k_count1<<<(unsigned)(pr.npt + pr.ndt), WARP_THREADS, 0, st>>>(pr, fp, pl->npos_far[which], cnt, ts);
-      CK(cudaGetLastError());
-    }
-    CK(launch_scan(ts, 2 * pr.npt + pr.ndt, (long long*)(ws + (which ? L.toff1 : L.toff0)), (long long*)(ws + L.chunk),
-                   &hdr->nnz[which], st));
+    mc[which] = MatCount{pr, cnt, ts, pl->side[which]};
+    sa.ts[which] = sc.ts[which] = ts;
+    sa.toff[which] = sc.toff[which] = (long long*)(ws + (which ? L.toff1 : L.toff0));
+    sa.status[which] = (unsigned long long*)(ws + (which ? L.st1 : L.st0));
+    sa.nnz[which] = sc.nnz[which] = &hdr->nnz[which];
+    sa.nslots[which] = sc.nslots[which] = nslots_of(pr);
+    const long long nc = (sa.nslots[which] + SCAN_TILE - 1) / SCAN_TILE;
+    if (nc > maxchunks) maxchunks = nc;
   }
-  pl->counted = 1;
-  pl->ran = 0;
-  pl->count_stream = st;
-  pl->nnz[0] = pl->nnz[1] = -1;
+  if (nmat == 1) mc[1] = mc[0];
+  sa.ticket = hdr->ticket;
+  sc.done = &hdr->done;
+  if (pl->combined) {
+    sc.nmat = pl->scan_in_count ? nmat : 0;
+    CK(dispatch_count0(mc[0], mc[1], pl->has_h1 ? 0 : -1, sc, st));
+  } else {
+    ScanIn none;
+    memset(&none, 0, sizeof(none));
+    if (pl->has_h1) CK(fork_aux(pl, st, 1));  // Q1's count pass runs concurrently on aux[0]
+    for (int which = 0; which < nmat; ++which) {
+      const Prob& pr = pl->pr[which];
+      cudaStream_t s = which ? pl->aux[0] : st;
+      if (pr.mode == 0) {
+        CK(dispatch_count0(mc[which], mc[which], -1, none, s));
+      } else {
+        const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
+        k_count1<<<(unsigned)(pr.npt + pr.ndt), WARP_THREADS, 0, s>>>(pr, fp, pl->npos_far[which], mc[which].cnt,
+                                                                        mc[which].tsum);
+        CK(cudaGetLastError());
+      }
+    }
+    if (pl->has_h1) CK(join_aux(pl, st, 1));
+  }
+  if (!pl->scan_in_count) {  // (a4) chained scan of both matrices' tile sums
+    k_scan_chain<<<dim3((unsigned)maxchunks, nmat), SCAN_THREADS, 0, st>>>(sa);
+    CK(cudaGetLastError());
+  }
   return SUN_OK;
 }
 
 int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
   if (!pl) return SUN_ERR_ARG;
   if (!pl->counted) return SUN_ERR_STATE;
-  struct {
-    int flags;
-    int pad;
-    long long nnz[2];
-    double tau[2];
-  } h;
+  HeaderPrefix h;
   CK(cudaMemcpyAsync(&h, pl->ws + pl->lay.hdr, sizeof(h), cudaMemcpyDeviceToHost, pl->count_stream));
   CK(cudaStreamSynchronize(pl->count_stream));
-  if (h.flags & (F_H0_NOT_HERM | F_H1_NOT_HERM)) return SUN_ERR_NOT_HERMITIAN;
+  if (h.flags & F_MALFORMED) return SUN_ERR_ARG;
+  for (int k = 0; k < 1 + pl->has_h1; ++k) {
+    double dev;
+    memcpy(&dev, &h.herm_dev[k], sizeof(dev));
+    if (dev > 1e-12 * sqrt(h.nrm2_h[k])) return SUN_ERR_NOT_HERMITIAN;
+  }
   if (h.flags & F_PATTERN) return SUN_ERR_BANDWIDTH;
   pl->tau0 = h.tau[0];
   pl->tau1 = pl->has_h1 ? h.tau[1] : 0.0;
-  if (h.flags & F_MALFORMED) return SUN_ERR_ARG;
   pl->nnz[0] = h.nnz[0];
   pl->nnz[1] = pl->has_h1 ? h.nnz[1] : 0;
   if (nnz_q0) *nnz_q0 = pl->nnz[0];
@@ -1120,22 +1821,105 @@ int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
 static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st) {
   const Layout& L = pl->lay;
   char* ws = pl->ws;
-  for (int which = 0; which < 1 + pl->has_h1; ++which) {
+  DevHeader* hdr = (DevHeader*)(ws + L.hdr);
+  const int nmat = 1 + pl->has_h1;
+  MatFill mf[2];
+  for (int which = 0; which < nmat; ++which) {
     sun_dcsr* Q = which ? Q1 : Q0;
-    const Prob& pr = pl->pr[which];
-    const int* cnt = (const int*)(ws + (which ? L.cnt1 : L.cnt0));
-    const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
-    DevHeader* hdr = (DevHeader*)(ws + L.hdr);
     FillOut fo = {Q->row_ptr, Q->col, Q->val, (long long)Q->nnz, which ? nullptr : K,
                   (const long long*)(ws + (which ? L.toff1 : L.toff0)), &hdr->nnz[which]};
+    mf[which] = MatFill{pl->pr[which], (const int*)(ws + (which ? L.cnt1 : L.cnt0)), fo, pl->side[which]};
+  }
+  if (nmat == 1) mf[1] = mf[0];
+  if (pl->combined) {
+    CK(dispatch_fill0(mf[0], mf[1], pl->has_h1 ? 0 : -1, pl->fill_grid[0], st));
+    return SUN_OK;
+  }
+  // Q0 on st; Q1 concurrently on aux[0]
+  if (pl->has_h1) CK(fork_aux(pl, st, 1));
+  for (int which = pl->has_h1; which >= 0; --which) {  // Q1 (small) first
+    const Prob& pr = pl->pr[which];
+    cudaStream_t s = which ? pl->aux[0] : st;
     if (pr.mode == 0) {
-      CK(dispatch_far(pr, const_cast<int*>(cnt), nullptr, &fo, st));
-      CK(dispatch_near(pr, nullptr, nullptr, &fo, st));
+      CK(dispatch_fill0(mf[which], mf[which], -1, pl->fill_grid[which], s));
     } else {
-      k_fill1<<<(unsigned)(pr.npt + pr.ndt), WARP_THREADS, 0, st>>>(pr, fp, pl->npos_far[which], cnt, fo);
+      const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
+      k_fill1<<<(unsigned)(pr.npt + pr.ndt), WARP_THREADS, 0, s>>>(pr, fp, pl->npos_far[which], mf[which].cnt,
+                                                                  mf[which].fo);
       CK(cudaGetLastError());
     }
   }
+  if (pl->has_h1) CK(join_aux(pl, st, 1));
+  return SUN_OK;
+}
+
+// Enqueue kind 0 (count), 1 (fill) or 2 (count + fill) on `st`: replay a cached CUDA graph of
+// the sequence (captured on the plan's capture stream; kernel arguments, including the output
+// pointers and capacities, are part of the key), or enqueue directly if graphs are disabled.
+static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st) {
+  auto direct = [&](cudaStream_t s) -> int {
+    int rc = SUN_OK;
+    if (kind != 1) rc = enqueue_count(pl, s);
+    if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s);
+    return rc;
+  };
+  if (!pl->use_graphs) return direct(st);
+  uintptr_t key[12] = {(uintptr_t)kind, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  if (kind != 0) {
+    key[1] = (uintptr_t)Q0->row_ptr; key[2] = (uintptr_t)Q0->col; key[3] = (uintptr_t)Q0->val;
+    key[4] = (uintptr_t)Q0->nnz;     key[5] = (uintptr_t)K;
+    if (Q1) {
+      key[6] = (uintptr_t)Q1->row_ptr; key[7] = (uintptr_t)Q1->col; key[8] = (uintptr_t)Q1->val;
+      key[9] = (uintptr_t)Q1->nnz;
+    }
+  }
+  cudaGraphExec_t exec = nullptr;
+  for (auto& g : pl->graphs)
+    if (memcmp(g.key, key, sizeof(key)) == 0) {
+      exec = g.exec;
+      g.used = ++pl->graph_clock;
+      break;
+    }
+  if (!exec) {
+    CK(cudaStreamBeginCapture(pl->cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = direct(pl->cap_stream);
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(pl->cap_stream, &graph);
+    if (rc != SUN_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return cuda_fail(e);
+    constexpr size_t MAXG = 8;
+    if (pl->graphs.size() >= MAXG) {  // evict the least recently used
+      size_t v = 0;
+      for (size_t i = 1; i < pl->graphs.size(); ++i)
+        if (pl->graphs[i].used < pl->graphs[v].used) v = i;
+      cudaGraphExecDestroy(pl->graphs[v].exec);
+      pl->graphs.erase(pl->graphs.begin() + v);
+    }
+    sun_plan_s::GraphEntry ge;
+    memcpy(ge.key, key, sizeof(key));
+    ge.exec = exec;
+    ge.used = ++pl->graph_clock;
+    pl->graphs.push_back(ge);
+  }
+  CK(cudaGraphLaunch(exec, st));
+  return SUN_OK;
+}
+
+int sun_count(sun_plan pl, void* stream) {
+  if (!pl) return SUN_ERR_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int rc = enqueue_kind(pl, 0, nullptr, nullptr, nullptr, st);
+  if (rc != SUN_OK) return rc;
+  pl->counted = 1;
+  pl->ran = 0;
+  pl->count_stream = st;
+  pl->nnz[0] = pl->nnz[1] = -1;
   return SUN_OK;
 }
 
@@ -1159,19 +1943,23 @@ int sun_unfold(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream)
     if ((which ? Q1 : Q0)->nnz < pl->nnz[which]) return SUN_ERR_CAPACITY;
   pl->cap[0] = Q0->nnz;
   pl->cap[1] = Q1 ? Q1->nnz : 0;
-  return enqueue_fill(pl, Q0, Q1, K, (cudaStream_t)stream);
+  return enqueue_kind(pl, 1, Q0, pl->has_h1 ? Q1 : nullptr, K, (cudaStream_t)stream);
 }
 
 int sun_run(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, void* stream) {
   if (!pl) return SUN_ERR_ARG;
   int st = check_outputs(pl, Q0, Q1, K);
   if (st != SUN_OK) return st;
-  st = sun_count(pl, stream);
+  cudaStream_t s = (cudaStream_t)stream;
+  st = enqueue_kind(pl, 2, Q0, pl->has_h1 ? Q1 : nullptr, K, s);
   if (st != SUN_OK) return st;
+  pl->counted = 1;
+  pl->count_stream = s;
+  pl->nnz[0] = pl->nnz[1] = -1;
   pl->cap[0] = Q0->nnz;
-  pl->cap[1] = Q1 ? Q1->nnz : 0;
+  pl->cap[1] = pl->has_h1 ? Q1->nnz : 0;
   pl->ran = 1;
-  return enqueue_fill(pl, Q0, Q1, K, (cudaStream_t)stream);
+  return SUN_OK;
 }
 
 int64_t sun_nnz_bound(sun_plan pl, int32_t which) {
@@ -1217,11 +2005,13 @@ int sun_plan_info(sun_plan pl, sun_plan_info_t* info) {
   info->mode_q1 = pl->has_h1 ? pl->pr[1].mode : -1;
   info->pairs_per_tile_q0 = pl->pr[0].tp;
   info->pairs_per_tile_q1 = pl->has_h1 ? pl->pr[1].tp : 0;
-  info->tiles_q0 = 2 * pl->pr[0].npt + pl->pr[0].ndt;
-  info->tiles_q1 = pl->has_h1 ? 2 * pl->pr[1].npt + pl->pr[1].ndt : 0;
+  info->tiles_q0 = nslots_of(pl->pr[0]);
+  info->tiles_q1 = pl->has_h1 ? nslots_of(pl->pr[1]) : 0;
   info->has_h1 = pl->has_h1;
   info->npos_far_q0 = pl->npos_far[0];
   info->npos_far_q1 = pl->has_h1 ? pl->npos_far[1] : 0;
+  info->launches_count = pl->launches_count;
+  info->launches_fill = pl->launches_fill;
   return SUN_OK;
 }
 

@@ -41,8 +41,6 @@ namespace sunk {
 constexpr int WMAX = 15;               // max(wK, wL) supported by the banded kernels
 constexpr int WIN_MAX = 4 * WMAX + 2;  // near-pair window bound (4W+1), padded
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int CNT_BITS = 20;           // cnt word: bits 0-19 row length, 20-31 nRe (far pairs)
-constexpr int CNT_MASK = (1 << CNT_BITS) - 1;
 
 struct Band {
   const double2* v;  // v[r * (2w+1) + (c - r + w)]
@@ -58,9 +56,10 @@ struct Prob {
   const double* inv;   // inv[l] = 1/sqrt(l(l+1)), l = 1..n-1
   const double* tau_ptr;  // drop threshold in device memory (computed by the expand step)
   double tau;             // loaded from tau_ptr at kernel entry
-  int mode;            // 0 thread-per-pair (staged), 1 warp-per-pair (direct)
-  int tp;              // pairs per tile
-  long long npt, ndt;  // pair tiles, D tiles
+  int mode;            // 0 group-per-pair far kernels (compile-time widths), 1 warp-per-pair (runtime widths)
+  int tp;              // pairs per tile (one scan slot per tile for the S rows, one for the J rows)
+  long long npt, ndt;  // pair tiles, D slots
+  long long nb_near;   // mode 0: units of 8 near-pair / D-row items (one warp each)
 };
 
 __device__ __forceinline__ double2 bget(const Band B, int r, int c) {
@@ -240,6 +239,35 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int& t
   return before + x - v;
 }
 
+// Block-wide exclusive scans of two ints per thread at once (one pass, two barriers).
+// Assumes every warp of the block is converged and blockDim.x <= 1024.
+__device__ __forceinline__ int2 block_exclusive_scan2(int v1, int v2, int2* warp_tot, int2& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  int x = v1, y = v2;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int a = __shfl_up_sync(FULL, x, o), b = __shfl_up_sync(FULL, y, o);
+    if (lane >= o) {
+      x += a;
+      y += b;
+    }
+  }
+  if (lane == 31) warp_tot[wid] = make_int2(x, y);
+  __syncthreads();
+  int2 before = make_int2(0, 0), tot = make_int2(0, 0);
+  for (int w = 0; w < nwarps; ++w) {  // <= 32 broadcast reads
+    const int2 t = warp_tot[w];
+    if (w < wid) {
+      before.x += t.x;
+      before.y += t.y;
+    }
+    tot.x += t.x;
+    tot.y += t.y;
+  }
+  total = tot;
+  return make_int2(before.x + x - v1, before.y + y - v2);
+}
+
 // ---------------------------------------------------------------------------------------
 // Last l in (hi, n-1] with |tr * inv[l]| > tau (hi if none).  The predicate is monotone
 // (non-increasing) in l, so the answer is unique; it is located from the estimate
@@ -303,9 +331,29 @@ __device__ __forceinline__ void warp_prefix(const double* g, double* pre, int nw
 // product are monotone), so the kept tail is (hi, lend], found by binary search -- identical
 // in the count and fill passes.  Returns the kept count; with EMIT writes them at seg/off.
 // ---------------------------------------------------------------------------------------
-template <bool EMIT>
+// Tail of a row's D-chain: entries tr * inv[l] for l in (hi, lend], after `nwin` entries
+// (the row's S/J window entries and its D entries inside the window).
+struct TailInfo {
+  double tr;
+  int nwin, hi, lend;
+};
+
+// Side buffer of the near rows (row 2i = S row / D row of near item i, 2i+1 = J row).
+struct NearMeta {
+  double tr, k;       // D-chain trace (tail value tr * inv[l]) and the row's K value
+  int nwin, hi, lend;  // window entries; tail l in (hi, lend]
+  int pad;
+};
+struct NearSide {
+  int32_t* col;  // [2 * items * nc]
+  double* val;   // [2 * items * nc]
+  NearMeta* meta;
+  int nc;        // entries per row slot: (4W + 1)^2 >= any row's window entries
+};
+
+template <bool EMIT, bool TAIL = true>
 __device__ __forceinline__ int warp_dchain(const Prob& pr, int lo, int hi, const double* g, const double* pre,
-                                           const Seg& seg, long long off) {
+                                           const Seg& seg, long long off, int nbefore = 0, TailInfo* ti = nullptr) {
   const int lane = threadIdx.x & 31;
   const int n = pr.n;
   const double tau = pr.tau;
@@ -326,10 +374,11 @@ __device__ __forceinline__ int warp_dchain(const Prob& pr, int lo, int hi, const
     kept += __popc(km);
   }
   const int lend = chain_tail_end(inv, n, hi, tr, tau);  // tail beyond the window: l in (hi, lend]
-  if (EMIT) {
+  if (EMIT && TAIL) {
     for (int l = hi + 1 + lane; l <= lend; l += 32)
       seg.emit(off + kept + (l - hi - 1), dbase + l, tr * __ldg(&inv[l]));
   }
+  if (ti) *ti = TailInfo{tr, nbefore + kept, hi, lend};
   return kept + (lend - hi);
 }
 
@@ -341,9 +390,10 @@ __device__ __forceinline__ int warp_dchain(const Prob& pr, int lo, int hi, const
 // scr: per-warp shared scratch: tile (TW*TW double2) | gS | gJ | pS | pJ (each SW doubles).
 // Returns the row lengths (cS, cJ) and K values (kS, kJ); with EMIT writes the rows.
 // ---------------------------------------------------------------------------------------
-template <bool EMIT, int TW, int SW>
-__device__ __noinline__ void warp_near_pair(const Prob& pr, int a, int b, double* scr, int& cS, int& cJ, double& kS,
-                                            double& kJ, Seg sS, long long offS, Seg sJ, long long offJ) {
+template <bool EMIT, int TW, int SW, bool TAIL = true>
+__device__ __forceinline__ void warp_near_pair(const Prob& pr, int a, int b, double* scr, int& cS, int& cJ, double& kS,
+                                            double& kJ, Seg sS, long long offS, Seg sJ, long long offJ,
+                                            TailInfo* tS = nullptr, TailInfo* tJ = nullptr) {
   const int lane = threadIdx.x & 31;
   const int n = pr.n, W = pr.W;
   const int np = (int)pr.np;
@@ -432,8 +482,8 @@ __device__ __noinline__ void warp_near_pair(const Prob& pr, int a, int b, double
   __syncwarp();
   warp_prefix(gS, pS, nw);
   warp_prefix(gJ, pJ, nw);
-  const int chS = warp_dchain<EMIT>(pr, lo, hi, gS, pS, sS, offS + n1S + n2S);
-  const int chJ = warp_dchain<EMIT>(pr, lo, hi, gJ, pJ, sJ, offJ + n1J + n2J);
+  const int chS = warp_dchain<EMIT, TAIL>(pr, lo, hi, gS, pS, sS, offS + n1S + n2S, n1S + n2S, tS);
+  const int chJ = warp_dchain<EMIT, TAIL>(pr, lo, hi, gJ, pJ, sJ, offJ + n1J + n2J, n1J + n2J, tJ);
   cS = n1S + n2S + chS;
   cJ = n1J + n2J + chJ;
   kS = pS[nw] / (double)n;
@@ -444,9 +494,9 @@ __device__ __noinline__ void warp_near_pair(const Prob& pr, int a, int b, double
 // ---------------------------------------------------------------------------------------
 // D^lam row, warp-cooperative.
 // ---------------------------------------------------------------------------------------
-template <bool EMIT>
-__device__ __noinline__ int warp_d_row(const Prob& pr, int lam, double* g, double* pre, double& kval, Seg seg,
-                                       long long off) {
+template <bool EMIT, bool TAIL = true>
+__device__ __forceinline__ int warp_d_row(const Prob& pr, int lam, double* g, double* pre, double& kval, Seg seg,
+                                       long long off, TailInfo* ti = nullptr) {
   const int lane = threadIdx.x & 31;
   const int n = pr.n;
   const int np = (int)pr.np;
@@ -499,21 +549,23 @@ __device__ __noinline__ int warp_d_row(const Prob& pr, int lam, double* g, doubl
   for (int i = lane; i < nw; i += 32) g[i] = G_elem(pr, lam, alpha, lo + i, lo + i).x;
   __syncwarp();
   warp_prefix(g, pre, nw);
-  const int ch = warp_dchain<EMIT>(pr, lo, hi, g, pre, seg, off + nS + nJ);
+  const int ch = warp_dchain<EMIT, TAIL>(pr, lo, hi, g, pre, seg, off + nS + nJ, nS + nJ, ti);
   kval = pre[nw] / (double)n;
   __syncwarp();
   return nS + nJ + ch;
 }
 
 // ---------------------------------------------------------------------------------------
-// Far pair with compile-time half-bandwidths (WK >= WL): all band values the pair needs are
-// loaded up front (independent loads) and the npos U values stay in registers.
-// Position order == lexicographic in (c, d).
+// Far pair (b - a > 2W) with compile-time half-bandwidths (WK >= WL), thread per pair: the
+// band values the pair needs are loaded up front (independent loads) and the NPOS values of
+// U = L^+(E_ab) stay in registers.  Far positions, in lexicographic (dc, dd) order, which is
+// ascending column order q(a + dc, b + dd):
+//   dc = 0: dd in [-WK, WK];  0 < |dc| <= WL: dd in [-WL, WL];  WL < |dc| <= WK: dd = 0
 // ---------------------------------------------------------------------------------------
 template <int WK, int WL>
 struct FarT {
-  static constexpr int W = WK;
-  static constexpr int NPOS = (2 * W + 1) + 2 * WL * (2 * WL + 1) + 2 * (W - WL);
+  static_assert(WK >= WL, "far-pair kernels need wK >= wL");
+  static constexpr int NPOS = (2 * WK + 1) + 2 * WL * (2 * WL + 1) + 2 * (WK - WL);
 };
 
 template <int WK, int WL, class F>
@@ -522,28 +574,28 @@ __device__ __forceinline__ void far_foreach(F&& f) {
 #pragma unroll
   for (int dc = -WK; dc <= WK; ++dc) {
     const int adc = dc < 0 ? -dc : dc;
-    if (dc == 0) {
+    const int w = dc == 0 ? WK : (adc <= WL ? WL : 0);
 #pragma unroll
-      for (int dd = -WK; dd <= WK; ++dd) {
-        f(k, dc, dd);
-        ++k;
-      }
-    } else if (adc <= WL) {
-#pragma unroll
-      for (int dd = -WL; dd <= WL; ++dd) {
-        f(k, dc, dd);
-        ++k;
-      }
-    } else {
-      f(k, dc, 0);
+    for (int dd = -w; dd <= w; ++dd) {
+      f(k, dc, dd);
       ++k;
     }
   }
 }
 
-// PT: number of dissipators if known at compile time (0 or 1), -1 = runtime pr.P.
+// The far-pair kernels' view of the problem (kept in registers).
+struct FarCtx {
+  const double2* K;  // band K, half-width WK
+  const double2* L;  // P bands Lt_p, half-width WL
+  double tau;
+  long long np;
+  int n, P;
+};
+
+// U_cd = i K_ca [d = b] - i conj(K_db) [c = a] + sum_p conj(Lt_p,ac) Lt_p,bd at all far positions.
+// PT: dissipators known at compile time (0 or 1), -1 = runtime P.
 template <int WK, int WL, int PT>
-__device__ __forceinline__ void far_values(const Prob& pr, int a, int b, double (&ux)[FarT<WK, WL>::NPOS],
+__device__ __forceinline__ void far_values(const FarCtx& pr, int a, int b, double (&ux)[FarT<WK, WL>::NPOS],
                                            double (&uy)[FarT<WK, WL>::NPOS]) {
   constexpr int W = WK;
   constexpr int SK = 2 * WK + 1, SL = 2 * WL + 1;
@@ -552,39 +604,19 @@ __device__ __forceinline__ void far_values(const Prob& pr, int a, int b, double 
 #pragma unroll
   for (int i = 0; i <= 2 * W; ++i) {
     const int c = a + i - W;  // K(c, a): row c, offset a - c = W - i
-    kc[i] = c >= 0 ? __ldg(&pr.K.v[(long long)c * SK + (2 * W - i)]) : make_double2(0.0, 0.0);
+    kc[i] = c >= 0 ? __ldg(&pr.K[(long long)c * SK + (2 * W - i)]) : make_double2(0.0, 0.0);
     const int d = b + i - W;  // K(d, b): row d, offset b - d = W - i
-    kr[i] = d < n ? __ldg(&pr.K.v[(long long)d * SK + (2 * W - i)]) : make_double2(0.0, 0.0);
+    kr[i] = d < n ? __ldg(&pr.K[(long long)d * SK + (2 * W - i)]) : make_double2(0.0, 0.0);
   }
   // outer block O_ij = sum_p conj(Lt_p(a, a-WL+i)) Lt_p(b, b-WL+j)
   double ox[SL][SL], oy[SL][SL];
-  if constexpr (PT == 0) {
 #pragma unroll
-    for (int i = 0; i < SL; ++i)
+  for (int i = 0; i < SL; ++i)
 #pragma unroll
-      for (int j = 0; j < SL; ++j) ox[i][j] = oy[i][j] = 0.0;  // unused (no dissipators)
-  } else if constexpr (PT == 1) {
-    const double2* La = pr.L + (long long)a * SL;
-    const double2* Lb = pr.L + (long long)b * SL;
-    double2 la[SL], lb[SL];
-#pragma unroll
-    for (int i = 0; i < SL; ++i) {
-      la[i] = __ldg(&La[i]);
-      lb[i] = __ldg(&Lb[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < SL; ++i)
-#pragma unroll
-      for (int j = 0; j < SL; ++j) {
-        ox[i][j] = la[i].x * lb[j].x + la[i].y * lb[j].y;
-        oy[i][j] = la[i].x * lb[j].y - la[i].y * lb[j].x;
-      }
-  } else if constexpr (PT == -1) {
-#pragma unroll
-    for (int i = 0; i < SL; ++i)
-#pragma unroll
-      for (int j = 0; j < SL; ++j) ox[i][j] = oy[i][j] = 0.0;
-    for (int p = 0; p < pr.P; ++p) {
+    for (int j = 0; j < SL; ++j) ox[i][j] = oy[i][j] = 0.0;
+  if constexpr (PT != 0) {
+    const int np_ = PT < 0 ? pr.P : PT;
+    for (int p = 0; p < np_; ++p) {
       const double2* La = pr.L + ((long long)p * n + a) * SL;
       const double2* Lb = pr.L + ((long long)p * n + b) * SL;
       double2 la[SL], lb[SL];
@@ -604,93 +636,95 @@ __device__ __forceinline__ void far_values(const Prob& pr, int a, int b, double 
   }
   far_foreach<WK, WL>([&](int k, int dc, int dd) {
     const int adc = dc < 0 ? -dc : dc, add = dd < 0 ? -dd : dd;
-    const bool hasO = PT != 0 && adc <= WL && add <= WL;
     double x = 0.0, y = 0.0;
-    bool init = false;
-    if (hasO) {
+    if (PT != 0 && adc <= WL && add <= WL) {
       x = ox[dc + WL][dd + WL];
       y = oy[dc + WL][dd + WL];
-      init = true;
     }
     if (dd == 0) {  // + i K_ca
-      if (init) {
-        x -= kc[dc + W].y;
-        y += kc[dc + W].x;
-      } else {
-        x = -kc[dc + W].y;
-        y = kc[dc + W].x;
-        init = true;
-      }
+      x -= kc[dc + W].y;
+      y += kc[dc + W].x;
     }
     if (dc == 0) {  // - i conj(K_db)
-      if (init) {
-        x -= kr[dd + W].y;
-        y -= kr[dd + W].x;
-      } else {
-        x = -kr[dd + W].y;
-        y = -kr[dd + W].x;
-      }
+      x -= kr[dd + W].y;
+      y -= kr[dd + W].x;
     }
     ux[k] = x;
     uy[k] = y;
   });
 }
 
+// kept bits of the far positions: bit k of mr (Re U) / mi (Im U), |.| > tau and in range
 template <int WK, int WL>
-__device__ __forceinline__ void far_counts(int n, double tau, int a, int b, const double (&ux)[FarT<WK, WL>::NPOS],
-                                           const double (&uy)[FarT<WK, WL>::NPOS], int& nR, int& nI) {
-  int r = 0, i = 0;
+__device__ __forceinline__ void far_masks(int n, double tau, int a, int b, const double (&ux)[FarT<WK, WL>::NPOS],
+                                          const double (&uy)[FarT<WK, WL>::NPOS], unsigned& mr, unsigned& mi) {
+  static_assert(FarT<WK, WL>::NPOS <= 32, "mask width");
+  unsigned r = 0u, i = 0u;
   far_foreach<WK, WL>([&](int k, int dc, int dd) {
-    const bool ok = (a + dc >= 0) && (b + dd < n);
-    r += (ok && fabs(ux[k]) > tau);
-    i += (ok && fabs(uy[k]) > tau);
+    const bool ok = (dc >= 0 || a + dc >= 0) && (dd <= 0 || b + dd < n);
+    r |= (unsigned)(ok && fabs(ux[k]) > tau) << k;
+    i |= (unsigned)(ok && fabs(uy[k]) > tau) << k;
   });
-  nR = r;
-  nI = i;
+  mr = r;
+  mi = i;
 }
 
-// Emit one row of a far pair (row 0 = S_ab, row 1 = J_ab) through `sink(index, col, value)`.
-//   row S_ab: [Re U > tau at q] [-Im U at NP + q];   row J_ab: [Im U at q] [Re U at NP + q]
-// n1 = number of entries of the first part (nRe for S_ab, nIm for J_ab).
-template <int WK, int WL, class SINK>
-__device__ __forceinline__ void far_emit_row(int n, int np, double tau, int a, int b, int row,
-                                             const double (&ux)[FarT<WK, WL>::NPOS],
-                                             const double (&uy)[FarT<WK, WL>::NPOS], int n1, const SINK& sink,
-                                             int off) {
-  int i1 = 0, i2 = 0;
+// column indices q(a + dc, b + dd) of the far positions (S_cd; J_cd is NP + q)
+template <int WK, int WL>
+__device__ __forceinline__ void far_cols(int n, int a, int b, int (&q)[FarT<WK, WL>::NPOS]) {
+  const int q0 = pidx32(n, a, b);
   far_foreach<WK, WL>([&](int k, int dc, int dd) {
-    const int c = a + dc, d = b + dd;
-    const bool ok = (c >= 0) && (d < n);
-    const int q = pidx32(n, c, d);
-    const double v1 = row == 0 ? ux[k] : uy[k];
-    const double v2 = row == 0 ? -uy[k] : ux[k];
-    if (ok && fabs(v1) > tau) {
-      sink(off + i1, q, v1);
-      ++i1;
-    }
-    if (ok && fabs(v2) > tau) {
-      sink(off + n1 + i2, np + q, v2);
-      ++i2;
-    }
+    // rows c = a + dc < 0 are masked out; clamp keeps the arithmetic in range
+    const int c = a + dc < 0 ? 0 : a + dc;
+    q[k] = dc == 0 ? q0 + dd : pidx32(n, c, b + dd);
   });
 }
 
-struct SmemSink {
-  int* col;
-  double* val;
-  __device__ __forceinline__ void operator()(int i, int c, double v) const {
-    col[i] = c;
-    val[i] = v;
+// Predicated shared stores of one staged entry (col, val) at 32-bit shared addresses; the
+// addresses advance by the kept bit (branch-free: no divergence, no reconvergence code).
+__device__ __forceinline__ void sts_entry(unsigned keep, unsigned& pc, unsigned& pv, int col, double val) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.shared.u32 [%1], %2;\n\t@p st.shared.f64 [%3], %4;\n\t}" ::"r"(keep),
+      "r"(pc), "r"(col), "r"(pv), "d"(val)
+      : "memory");
+  pc += keep << 2;
+  pv += keep << 3;
+}
+
+// Stage one row of a far pair (row 0 = S_ab, row 1 = J_ab) at scol/sval[off ..]:
+//   row S_ab: [Re U at q] [-Im U at NP + q];   row J_ab: [Im U at q] [Re U at NP + q]
+// Two running pointers (first and second half of the row), one predicated store pair per
+// position and half.
+template <int WK, int WL>
+__device__ __forceinline__ void far_stage_row(int np, int row, const int (&q)[FarT<WK, WL>::NPOS],
+                                              const double (&ux)[FarT<WK, WL>::NPOS],
+                                              const double (&uy)[FarT<WK, WL>::NPOS], unsigned mr, unsigned mi,
+                                              int* scol, double* sval, int off) {
+  const unsigned m1 = row ? mi : mr, m2 = row ? mr : mi;
+  const int off2 = off + __popc(m1);
+  unsigned pc1 = (unsigned)__cvta_generic_to_shared(scol + off), pv1 = (unsigned)__cvta_generic_to_shared(sval + off);
+  unsigned pc2 = (unsigned)__cvta_generic_to_shared(scol + off2), pv2 = (unsigned)__cvta_generic_to_shared(sval + off2);
+#pragma unroll
+  for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
+    const double v1 = row ? uy[k] : ux[k];
+    const double v2 = row ? ux[k] : -uy[k];
+    sts_entry((m1 >> k) & 1u, pc1, pv1, q[k], v1);
+    sts_entry((m2 >> k) & 1u, pc2, pv2, np + q[k], v2);
   }
-};
-struct GlobalSink {
-  int32_t* col;
-  double* val;
-  __device__ __forceinline__ void operator()(int i, int c, double v) const {
-    col[i] = c;
-    val[i] = v;
-  }
-};
+}
+
+// ---------------------------------------------------------------------------------------
+// TMA 1D bulk store (cp.async.bulk, sm_90+): shared -> global, 16-byte aligned, bulk_group
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, unsigned bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // ---------------------------------------------------------------------------------------
 // Far pair, warp-cooperative (mode 1): lane k of each 32-chunk owns far position k
