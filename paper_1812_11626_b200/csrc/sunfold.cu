@@ -689,56 +689,72 @@ struct FillOut {
   const long long* nnz;
 };
 
-// Near rows of a tile (or a D unit), written by the whole CTA: the rows are listed in shared
-// memory, their lengths prefix-summed, and every thread walks the flattened entry range with
-// a monotone row cursor, so all warps share the work (no warp-serial latency chains).
-// Window entries are copied from the side buffer; chain-tail entries tr * inv[l], l in
-// (hi, lend], are generated with the count pass's expression (bitwise identical).
-constexpr int MAXNR = 2 * TP0;  // rows per tile: 2 per pair
-struct NearRowRef {
-  long long out;  // output index of the row's first entry
-  double tr;
-  int side_row, nwin, hi, lend;
-};
-struct NearRows {
-  NearRowRef r[MAXNR];
-  int start[MAXNR + 1];
-  int2 wtot[8];
-  int nr;
-};
-
-__device__ __forceinline__ void cta_near_rows_out(NearRows& L, const NearSide& side, const double* __restrict__ inv,
-                                                  int dbase, const FillOut& fo) {
-  __syncthreads();  // list complete
-  const int nr = L.nr;
-  if (nr == 0) return;  // block-uniform
-  // prefix of row lengths: thread i owns rows 2i, 2i+1
-  const int i0 = 2 * threadIdx.x, i1 = i0 + 1;
-  const int l0 = i0 < nr ? L.r[i0].nwin + (L.r[i0].lend - L.r[i0].hi) : 0;
-  const int l1 = i1 < nr ? L.r[i1].nwin + (L.r[i1].lend - L.r[i1].hi) : 0;
-  int2 tot;
-  const int2 ex = block_exclusive_scan2(l0 + l1, 0, L.wtot, tot);
-  if (i0 < nr) L.start[i0] = ex.x;
-  if (i1 < nr) L.start[i1] = ex.x + l0;
-  if (threadIdx.x == 0) L.start[nr] = tot.x;
-  __syncthreads();
-  const int total = tot.x;
-  int r = 0;
-  for (int e = threadIdx.x; e < total; e += blockDim.x) {
-    while (L.start[r + 1] <= e) ++r;
-    const NearRowRef& R = L.r[r];
-    const int k = e - L.start[r];
-    const long long o = R.out + k;
-    if (o >= fo.cap) continue;
-    if (k < R.nwin) {
-      const long long sidx = (long long)R.side_row * side.nc + k;
-      fo.col[o] = side.col[sidx];
-      fo.val[o] = side.val[sidx];
-    } else {
-      const int l = R.hi + 1 + (k - R.nwin);
-      fo.col[o] = dbase + l;
-      fo.val[o] = R.tr * __ldg(&inv[l]);
+// Near rows (the S and J rows of near pairs, and the D rows) are written by near units, one
+// warp per row, from the count pass's side buffer: window entries copied, chain-tail entries
+// tr * inv[l], l in (hi, lend], generated with the count pass's expression (bitwise
+// identical).  Row offset = tile offset + the tile's earlier counts (warp reduction); D rows
+// have a scan slot of their own.  Loops are unrolled so the loads of several iterations are in
+// flight together.
+__device__ __forceinline__ void warp_near_row_write(const NearSide& side, long long srow, const NearMeta& m,
+                                                   const double* __restrict__ inv, int dbase, const FillOut& fo,
+                                                   long long o) {
+  const int lane = threadIdx.x & 31;
+  const long long lim = fo.cap - o;
+  const int32_t* sc = side.col + srow * side.nc;
+  const double* sv = side.val + srow * side.nc;
+#pragma unroll 3
+  for (int k = lane; k < m.nwin; k += 32) {
+    const int c = __ldg(&sc[k]);
+    const double v = __ldg(&sv[k]);
+    if (k < lim) {
+      fo.col[o + k] = c;
+      fo.val[o + k] = v;
     }
+  }
+  const long long ot = o + m.nwin;
+  const long long limt = lim - m.nwin;
+#pragma unroll 4
+  for (int l = m.hi + 1 + lane; l <= m.lend; l += 32) {
+    const int k = l - m.hi - 1;
+    const double v = m.tr * __ldg(&inv[l]);
+    if (k < limt) {
+      fo.col[ot + k] = dbase + l;
+      fo.val[ot + k] = v;
+    }
+  }
+}
+
+// near unit j: side rows 8j .. 8j + 7 (row 2i = S row / D row of near item i, 2i + 1 = J row)
+__device__ __forceinline__ void fill_near_unit(const Prob& pr, long long j, const int* __restrict__ cnt,
+                                               const FillOut& fo, const NearSide& side) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long np = pr.np;
+  const long long srow = j * 8 + wid;
+  const long long item = srow >> 1;
+  const int half = (int)(srow & 1);
+  int a, b, lam;
+  const int kind = near_item(pr, item, a, b, lam);
+  long long o;
+  if (kind == 1) {
+    const long long p = (long long)pidx32(pr.n, a, b);
+    const long long tb = p / pr.tp, ts = tb * pr.tp;
+    const int* c = cnt + (half ? np : 0);
+    int s1 = 0;
+    for (long long q = ts + lane; q < p; q += 32) s1 += __ldg(&c[q]);
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) s1 += __shfl_xor_sync(FULL, s1, sh);
+    o = fo.toff[(half ? pr.npt : 0) + tb] + s1;
+    const NearMeta m = side.meta[srow];
+    if (lane == 0 && fo.K) fo.K[(half ? np : 0) + p] = m.k;
+    warp_near_row_write(side, srow, m, pr.inv, (int)(2 * np - 1), fo, o);
+  } else if (kind == 2 && half == 0) {
+    o = fo.toff[2 * pr.npt + lam - 1];
+    const NearMeta m = side.meta[srow];
+    if (lane == 0) {
+      fo.row_ptr[2 * np + lam - 1] = o;
+      if (fo.K) fo.K[2 * np + lam - 1] = m.k;
+    }
+    warp_near_row_write(side, srow, m, pr.inv, (int)(2 * np - 1), fo, o);
   }
 }
 
@@ -808,8 +824,7 @@ __device__ __forceinline__ TileIn load_tile_in(long long np, long long npt, long
 
 template <int WK, int WL, int PT>
 __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, long long t, const TileIn& ti,
-                                              const FillOut& fo, const NearSide& side, const double* __restrict__ inv,
-                                              int* scol, double* sval, NearRows& L) {
+                                              const FillOut& fo, int* scol, double* sval, int2* wtot) {
   using MC = Mode0<WK, WL>;
   using FF = FillFar<WK, WL>;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -818,8 +833,7 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
   const bool valid = p < np;
   const int cS = ti.cS, cJ = ti.cJ;
   int2 tot2;
-  if (threadIdx.x == 0) L.nr = 0;
-  const int2 ex2 = block_exclusive_scan2(cS, cJ, L.wtot, tot2);
+  const int2 ex2 = block_exclusive_scan2(cS, cJ, wtot, tot2);
   const int exS = ex2.x, exJ = ex2.y;
   int a, b;
   warp_pairs(pr.n, t * TP0 + wid * 32, a, b);
@@ -926,21 +940,6 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
       __syncwarp();
     }
   }
-  // near rows of the tile: from the side buffer, by the whole CTA
-  if (nearp) {
-    const long long item = (long long)a * (2 * MC::W) + (b - a - 1);
-    const NearMeta mS = side.meta[2 * item], mJ = side.meta[2 * item + 1];
-    const int slot = atomicAdd(&L.nr, 2);
-    L.r[slot] = NearRowRef{baseS + exS, mS.tr, (int)(2 * item), mS.nwin, mS.hi, mS.lend};
-    L.r[slot + 1] = NearRowRef{baseJ + exJ, mJ.tr, (int)(2 * item + 1), mJ.nwin, mJ.hi, mJ.lend};
-    if (fo.K) {
-      fo.K[p] = mS.k;
-      fo.K[np + p] = mJ.k;
-    }
-  }
-#ifndef SUN_EXP_NO_NEAR
-  cta_near_rows_out(L, side, inv, (int)(2 * np - 1), fo);
-#endif
 }
 
 // Staging-free far tile (W = 0: every pair is far, rows of <= 2 entries), TP = 2048 pairs:
@@ -1004,27 +1003,6 @@ __device__ __forceinline__ void fill_direct_tile(const FarCtx& pr, long long npt
   }
 }
 
-// D unit: DU D rows from the side buffer, by the whole CTA
-constexpr int DU = 32;
-template <int WK, int WL>
-__device__ __forceinline__ void fill_d_unit(const Prob& pr, long long u, const FillOut& fo, const NearSide& side,
-                                            NearRows& L) {
-  const long long np = pr.np;
-  const int lam = (int)(u * DU + threadIdx.x + 1);
-  if (threadIdx.x == 0) L.nr = 0;
-  __syncthreads();
-  if (threadIdx.x < DU && lam <= pr.n - 1) {
-    const long long off = fo.toff[2 * pr.npt + lam - 1];
-    fo.row_ptr[2 * np + lam - 1] = off;
-    const long long item = (long long)pr.n * 2 * pr.W + lam - 1;
-    const NearMeta m = side.meta[2 * item];
-    const int slot = atomicAdd(&L.nr, 1);
-    L.r[slot] = NearRowRef{off, m.tr, (int)(2 * item), m.nwin, m.hi, m.lend};
-    if (fo.K) fo.K[2 * np + lam - 1] = m.k;
-  }
-  cta_near_rows_out(L, side, pr.inv, (int)(2 * np - 1), fo);
-}
-
 // One output matrix's arguments of the fill pass.
 struct MatFill {
   Prob pr;
@@ -1035,68 +1013,70 @@ struct MatFill {
 
 // Fill pass of Q0 and, with Q1W >= 0, of Q1 (widths Q1W, 0, no dissipators; staging-free
 // rows only, i.e. Q1W = 0) in one persistent launch: units u = blockIdx.x + k gridDim.x over
-//   [Q0 D units][Q1 D units][Q0 far tiles, last first][Q1 far tiles]
-// D units and the near-heavy last tiles start first; Q1's light tiles fill the tail.  The
-// next far tile's counts and offsets are loaded before the current unit runs.
+//   [Q0 far tiles, last first, with Q0 near units spread evenly among them][Q1 near][Q1 tiles]
+// The next far tile's counts and offsets are loaded before the current unit runs.
 template <int WK, int WL, int PT, int Q1W>
 __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFill m1) {
   using FF = FillFar<WK, WL>;
   static_assert(Q1W <= 0, "combined fill: Q1 rows must be staging-free");
   extern __shared__ __align__(128) unsigned char dyn[];
-  __shared__ NearRows L;
+  __shared__ int2 wtot[8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr bool HAS1 = Q1W >= 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     m0.fo.row_ptr[m0.pr.m] = *m0.fo.nnz;
     if (HAS1) m1.fo.row_ptr[m1.pr.m] = *m1.fo.nnz;
   }
-  const long long nd0 = (m0.pr.n - 1 + DU - 1) / DU;
-  const long long nd1 = HAS1 ? (m1.pr.n - 1 + DU - 1) / DU : 0;
+  // near units: 8 side rows each (2 per near item)
+  const long long nn0 = (2 * (m0.pr.n * 2LL * m0.pr.W + m0.pr.n - 1) + 7) / 8;
+  const long long nn1 = HAS1 ? (2 * (m1.pr.n * 2LL * m1.pr.W + m1.pr.n - 1) + 7) / 8 : 0;
   const long long nt0 = m0.pr.npt, nt1 = HAS1 ? m1.pr.npt : 0;
-  const long long D = nd0 + nd1, U = D + nt0 + nt1;
+  const long long U0 = nt0 + nn0, U = U0 + nn1 + nt1;
   int* scol = reinterpret_cast<int*>(dyn + wid * FF::BYTES_PER_WARP);
   double* sval = reinterpret_cast<double*>(dyn + wid * FF::BYTES_PER_WARP + FF::COLW * 4);
   const FarCtx prf0{m0.pr.K.v, m0.pr.L, *m0.pr.tau_ptr, m0.pr.np, m0.pr.n, m0.pr.P};
   FarCtx prf1{};
   if (HAS1) prf1 = FarCtx{m1.pr.K.v, m1.pr.L, *m1.pr.tau_ptr, m1.pr.np, m1.pr.n, m1.pr.P};
-  // tile of unit u >= D: (matrix, tile)
-  auto tile_of = [&](long long v, int& mat) -> long long {
-    if (v < D + nt0) {
-      mat = 0;
-      return nt0 - 1 - (v - D);
+  // unit -> kind: 0 Q0 far tile, 1 Q0 near unit, 2 Q1 near unit, 3 Q1 tile; idx
+  auto decode = [&](long long v, long long& idx) -> int {
+    if (v < U0) {
+      if (unit_decode(v, U0, nn0, idx)) return 1;
+      idx = nt0 - 1 - idx;  // far tiles, last first
+      return 0;
     }
-    mat = 1;
-    return v - D - nt0;
-  };
-  auto load = [&](long long v) -> TileIn {
-    int mat;
-    const long long t = tile_of(v, mat);
-    if (mat == 0 && !FF::DIRECT) return load_tile_in(m0.pr.np, nt0, t, m0.cnt, m0.fo.toff);
-    return TileIn{0, 0, 0, 0};  // direct tiles load their own inputs
+    v -= U0;
+    if (v < nn1) {
+      idx = v;
+      return 2;
+    }
+    idx = v - nn1;
+    return 3;
   };
   long long u = blockIdx.x;
   TileIn nxt{0, 0, 0, 0};
-  if (u < U && u >= D) nxt = load(u);
+  auto prefetch = [&](long long v) {
+    long long idx;
+    if (v < U && decode(v, idx) == 0 && !FF::DIRECT) nxt = load_tile_in(m0.pr.np, nt0, idx, m0.cnt, m0.fo.toff);
+  };
+  prefetch(u);
   for (; u < U; u += gridDim.x) {  // block-uniform
     const TileIn cur = nxt;
-    const long long un = u + gridDim.x;
-    if (un < U && un >= D) nxt = load(un);
-    __syncthreads();  // shared state of the previous unit consumed
-    if (u < nd0) {
-      fill_d_unit<WK, WL>(m0.pr, u, m0.fo, m0.side, L);
-    } else if (u < D) {
-      if constexpr (HAS1) fill_d_unit<0, 0>(m1.pr, u - nd0, m1.fo, m1.side, L);
+    prefetch(u + gridDim.x);
+    long long idx;
+    const int kind = decode(u, idx);
+    if (kind == 0) {
+      __syncthreads();  // wtot of the previous unit consumed
+      if constexpr (FF::DIRECT)
+        fill_direct_tile<WK, WL, PT>(prf0, nt0, idx, m0.cnt, m0.fo, wtot);
+      else
+        fill_far_tile<WK, WL, PT>(prf0, nt0, idx, cur, m0.fo, scol, sval, wtot);
+    } else if (kind == 1) {
+      fill_near_unit(m0.pr, idx, m0.cnt, m0.fo, m0.side);
+    } else if (kind == 2) {
+      if constexpr (HAS1) fill_near_unit(m1.pr, idx, m1.cnt, m1.fo, m1.side);
     } else {
-      int mat;
-      const long long t = tile_of(u, mat);
-      if (mat == 0) {
-        if constexpr (FF::DIRECT)
-          fill_direct_tile<WK, WL, PT>(prf0, nt0, t, m0.cnt, m0.fo, L.wtot);
-        else
-          fill_far_tile<WK, WL, PT>(prf0, nt0, t, cur, m0.fo, m0.side, m0.pr.inv, scol, sval, L);
-      } else {
-        if constexpr (HAS1) fill_direct_tile<0, 0, 0>(prf1, nt1, t, m1.cnt, m1.fo, L.wtot);
-      }
+      __syncthreads();
+      if constexpr (HAS1) fill_direct_tile<0, 0, 0>(prf1, nt1, idx, m1.cnt, m1.fo, wtot);
     }
   }
   if (!FF::DIRECT && lane == 0) bulk_wait0();  // staging must outlive the bulk reads
@@ -1481,8 +1461,8 @@ cudaError_t attr_fill0(const Prob& p0, const Prob* p1, long long& grid) {
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fill0<WK, WL, PT, Q1W>, 256, smem);
   if (e != cudaSuccess) return e;
-  long long U = p0.npt + (p0.n - 1 + DU - 1) / DU;
-  if (Q1W >= 0 && p1) U += p1->npt + (p1->n - 1 + DU - 1) / DU;
+  long long U = p0.npt + (2 * (p0.n * 2LL * p0.W + p0.n - 1) + 7) / 8;
+  if (Q1W >= 0 && p1) U += p1->npt + (2 * (p1->n * 2LL * p1->W + p1->n - 1) + 7) / 8;
   grid = (long long)(nb > 0 ? nb : 1) * sms;
   if (grid > U) grid = U;
   return cudaSuccess;
