@@ -21,6 +21,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <type_traits>
 #include <vector>
 
 #include "../../include/sunfold.h"
@@ -483,9 +484,14 @@ __device__ __forceinline__ int near_item(const Prob& pr, long long item, int& a,
   return 0;
 }
 
-// unit u of U: near units at evenly spread positions (Bresenham)
+// unit u of U: near units at evenly spread positions (Bresenham).  floor(u nn / U) in double
+// precision is exact here: u nn < 2^53 is exact, the quotient is < 2^31, and a non-integer
+// quotient is at least 1/U < 2^-20 away from the next integer, far above the rounding error.
 __device__ __forceinline__ bool unit_decode(long long u, long long U, long long nnear_units, long long& idx) {
-  const long long k0 = u * nnear_units / U, k1 = (u + 1) * nnear_units / U;
+  const double r = (double)nnear_units / (double)U;
+  const long long k0 = (long long)floor((double)u * (double)nnear_units / (double)U);
+  const long long k1 = (long long)floor((double)(u + 1) * (double)nnear_units / (double)U);
+  (void)r;
   const bool is_near = k1 > k0;
   idx = is_near ? k0 : u - k0;
   return is_near;
@@ -886,8 +892,9 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
       }
     }
   } else {
-#pragma unroll 1
-    for (int row = 0; row < 2; ++row) {  // the warp's 32 S rows, then its 32 J rows
+    // the warp's 32 S rows, then its 32 J rows
+    auto do_row = [&](auto row_c) {
+      constexpr int row = decltype(row_c)::value;
       const int c_me = row ? cJ : cS, ex_me = row ? exJ : exS;
       const long long gbase = row ? baseJ : baseS;
       const int w0 = __shfl_sync(FULL, ex_me, 0);
@@ -905,9 +912,11 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
         hb = warp_excl_scan(nearp ? c_me : 0, ht);
       }
 #ifndef SUN_EXP_NO_STAGE
-      if (far) far_stage_row<WK, WL>((int)np, row, q, ux, uy, mr, mi, scol + pc, sval + pv, ex_me - w0 - hb);
+      if (far) far_stage_row<WK, WL, row>((int)np, q, ux, uy, mr, mi, scol + pc, sval + pv, ex_me - w0 - hb);
 #endif
+#ifndef SUN_EXP_NO_FENCE
       if (bulk) fence_async_smem();  // make the staged entries visible to the async (TMA) proxy
+#endif
       __syncwarp();
       if (bulk) {
         // col: int32, 16 B = 4 entries; val: fp64, 16 B = 2 entries
@@ -938,7 +947,9 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
         warp_copy_out(scol, sval, gbase, w0, w0 + wt, nearmask, ex_me, c_me, fo.col, fo.val, fo.cap);
       }
       __syncwarp();
-    }
+    };
+    do_row(std::integral_constant<int, 0>{});
+    do_row(std::integral_constant<int, 1>{});
   }
 }
 

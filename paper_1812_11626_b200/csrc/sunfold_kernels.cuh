@@ -691,25 +691,27 @@ __device__ __forceinline__ void sts_entry(unsigned keep, unsigned& pc, unsigned&
   pv += keep << 3;
 }
 
-// Stage one row of a far pair (row 0 = S_ab, row 1 = J_ab) at scol/sval[off ..]:
+// Stage one row of a far pair (ROW 0 = S_ab, ROW 1 = J_ab) at scol/sval[off ..]:
 //   row S_ab: [Re U at q] [-Im U at NP + q];   row J_ab: [Im U at q] [Re U at NP + q]
 // Two running pointers (first and second half of the row), one predicated store pair per
-// position and half.
-template <int WK, int WL>
-__device__ __forceinline__ void far_stage_row(int np, int row, const int (&q)[FarT<WK, WL>::NPOS],
+// position and half; the masks are consumed bit by bit.
+template <int WK, int WL, int ROW>
+__device__ __forceinline__ void far_stage_row(int np, const int (&q)[FarT<WK, WL>::NPOS],
                                               const double (&ux)[FarT<WK, WL>::NPOS],
                                               const double (&uy)[FarT<WK, WL>::NPOS], unsigned mr, unsigned mi,
                                               int* scol, double* sval, int off) {
-  const unsigned m1 = row ? mi : mr, m2 = row ? mr : mi;
+  unsigned m1 = ROW ? mi : mr, m2 = ROW ? mr : mi;
   const int off2 = off + __popc(m1);
   unsigned pc1 = (unsigned)__cvta_generic_to_shared(scol + off), pv1 = (unsigned)__cvta_generic_to_shared(sval + off);
   unsigned pc2 = (unsigned)__cvta_generic_to_shared(scol + off2), pv2 = (unsigned)__cvta_generic_to_shared(sval + off2);
 #pragma unroll
   for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
-    const double v1 = row ? uy[k] : ux[k];
-    const double v2 = row ? ux[k] : -uy[k];
-    sts_entry((m1 >> k) & 1u, pc1, pv1, q[k], v1);
-    sts_entry((m2 >> k) & 1u, pc2, pv2, np + q[k], v2);
+    const double v1 = ROW ? uy[k] : ux[k];
+    const double v2 = ROW ? ux[k] : -uy[k];
+    sts_entry(m1 & 1u, pc1, pv1, q[k], v1);
+    sts_entry(m2 & 1u, pc2, pv2, np + q[k], v2);
+    m1 >>= 1;
+    m2 >>= 1;
   }
 }
 
