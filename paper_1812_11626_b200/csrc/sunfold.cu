@@ -34,7 +34,8 @@ namespace {
 constexpr int MAXOPS = 66;       // H0, H1 and up to 64 dissipators
 constexpr int WLMAX = WMAX / 2;  // wK >= 2 wL
 constexpr int F_MALFORMED = 1, F_PATTERN = 8;
-constexpr int TP0 = 256;          // mode 0: pairs per tile == threads per CTA (8 warps)
+constexpr int TP0 = 256;          // mode 0: pairs per fill tile (scan slot) == threads per fill CTA
+constexpr int SLOTS_PER_TILE = 8;  // mode 0: count warps (single-warp CTAs) per fill tile
 constexpr int WARP_TP = 64;       // mode 1: pairs per tile
 constexpr int WARP_THREADS = 256;
 constexpr int FAR_MAXPOS = 1024;
@@ -109,8 +110,8 @@ Layout make_layout(int n, int P) {
   Layout L;
   long long m = (long long)n * n - 1;
   long long np = (long long)n * (n - 1) / 2;
-  // slots: S tiles + J tiles + D slots; the smallest tile is mode 1's 64 pairs
-  long long maxslots = 2 * (np / WARP_TP + 2) + n + 2;
+  // slots: S tiles + J tiles + D slots
+  long long maxslots = 2 * (np / WARP_TP + 2) + n + 2;  // smallest slot: mode 1's 64-pair tile
   long long maxchunks = (maxslots + SCAN_TILE - 1) / SCAN_TILE + 1;
   long long nrb = (n + EXP_THREADS - 1) / EXP_THREADS;
   size_t off = 0;
@@ -137,7 +138,7 @@ Layout make_layout(int n, int P) {
   for (int k = 0; k < 2; ++k) {
     L.side_col[k] = off; off = align256(off + (size_t)(side_rows * ncmax) * sizeof(int32_t));
     L.side_val[k] = off; off = align256(off + (size_t)(side_rows * ncmax) * sizeof(double));
-    L.side_meta[k] = off; off = align256(off + (size_t)side_rows * 32);
+    L.side_meta[k] = off; off = align256(off + (size_t)side_rows * sizeof(NearMeta));
   }
   L.side_rows = side_rows;
   L.total = off;
@@ -173,7 +174,6 @@ struct sun_plan_s {
   std::vector<int> pos_dc[2], pos_dd[2];
   NearSide side[2];
   int combined;         // mode 0 with Q1 absent or Q1 = Q_H[diagonal H1]: one launch per pass
-  int scan_in_count;    // the count kernel's last CTA scans the tile sums (small problems)
   long long fill_grid[2];
   // auxiliary streams: the Q1 passes and the near-item fill run concurrently with Q0's far
   // tiles (fork/join with events on the caller's stream; also valid under graph capture)
@@ -498,13 +498,18 @@ __device__ __forceinline__ bool unit_decode(long long u, long long U, long long 
 }
 
 // ---- count pass ------------------------------------------------------------------------
+// Every count CTA is a single warp, so no unit waits on a slow sibling warp:
+//   near item i: a near pair (both rows) or a D row, warp-cooperative; its window entries and
+//               chain-tail data go to the side buffer (the fill pass copies them)
+//   far slot s:  the far pairs of pairs [s tp, (s + 1) tp), thread per pair (PPT rounds)
+// Scan slots: S slot s, J slot s (tp pairs each), one slot per D row.  Slot sums are
+// accumulated with integer atomics into zeroed slots (order-independent, deterministic).
 template <int WK, int WL>
-__device__ __forceinline__ void count_near_unit(const Prob& pr, long long j, double* scr_w, int* __restrict__ cnt,
+__device__ __forceinline__ void count_near_item(const Prob& pr, long long item, double* scr, int* __restrict__ cnt,
                                                 int* __restrict__ tsum, const NearSide& side) {
   using MC = Mode0<WK, WL>;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const long long np = pr.np;
-  const long long item = j * 8 + wid;
   int a, b, lam;
   const int kind = near_item(pr, item, a, b, lam);
   const long long r0 = 2 * item * side.nc, r1 = r0 + side.nc;
@@ -513,7 +518,7 @@ __device__ __forceinline__ void count_near_unit(const Prob& pr, long long j, dou
     double k1, k2;
     TailInfo tS, tJ;
     const Seg sS = {side.col + r0, side.val + r0, side.nc}, sJ = {side.col + r1, side.val + r1, side.nc};
-    warp_near_pair<true, MC::TW, MC::SW, false>(pr, a, b, scr_w, c1, c2, k1, k2, sS, 0, sJ, 0, &tS, &tJ);
+    warp_near_pair<true, MC::TW, MC::SW, false>(pr, a, b, scr, c1, c2, k1, k2, sS, 0, sJ, 0, &tS, &tJ);
     if (lane == 0) {
       side.meta[2 * item] = NearMeta{tS.tr, k1, tS.nwin, tS.hi, tS.lend, 0};
       side.meta[2 * item + 1] = NearMeta{tJ.tr, k2, tJ.nwin, tJ.hi, tJ.lend, 0};
@@ -527,7 +532,7 @@ __device__ __forceinline__ void count_near_unit(const Prob& pr, long long j, dou
     double kv;
     TailInfo t;
     const Seg sD = {side.col + r0, side.val + r0, side.nc};
-    const int c = warp_d_row<true, false>(pr, lam, scr_w, scr_w + WIN_MAX + 2, kv, sD, 0, &t);
+    const int c = warp_d_row<true, false>(pr, lam, scr, scr + WIN_MAX + 2, kv, sD, 0, &t);
     if (lane == 0) {
       side.meta[2 * item] = NearMeta{t.tr, kv, t.nwin, t.hi, t.lend, 0};
       cnt[2 * np + lam - 1] = c;
@@ -537,13 +542,13 @@ __device__ __forceinline__ void count_near_unit(const Prob& pr, long long j, dou
 }
 
 template <int WK, int WL, int PT>
-__device__ __forceinline__ void count_far_tile(const FarCtx& pr, long long npt, long long t, int* __restrict__ cnt,
-                                               int* __restrict__ tsum, int* red) {
+__device__ __forceinline__ void count_far_slot(const FarCtx& pr, long long npt, long long s, int* __restrict__ cnt,
+                                               int* __restrict__ tsum) {
   using MC = Mode0<WK, WL>;
   using TL = Tiling<WK, WL>;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const long long np = pr.np;
-  const long long pw = t * TL::TP + (long long)wid * 32 * TL::PPT;  // the warp's first pair
+  const long long pw = s * (32 * TL::PPT);  // the slot's first pair
   int a, b;
   warp_pairs(pr.n, pw, a, b);
   int c = 0;
@@ -565,42 +570,10 @@ __device__ __forceinline__ void count_far_tile(const FarCtx& pr, long long npt, 
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
-  if (lane == 0) red[wid] = c;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int tot = 0;
-    for (int w = 0; w < 8; ++w) tot += red[w];
-    if (tot) {
-      atomicAdd(&tsum[t], tot);  // S rows and J rows of a far pair have the same length
-      atomicAdd(&tsum[npt + t], tot);
-    }
+  if (lane == 0 && c) {  // into the scan slot (fill tile) of this count warp
+    atomicAdd(&tsum[s / SLOTS_PER_TILE], c);  // S rows and J rows of a far pair have the same length
+    atomicAdd(&tsum[npt + s / SLOTS_PER_TILE], c);
   }
-}
-
-__device__ __forceinline__ long long block_scan_ll(long long v, long long* wsum, long long& total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  long long x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    long long y = __shfl_up_sync(FULL, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    long long s = lane < nwarps ? wsum[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      long long y = __shfl_up_sync(FULL, s, o);
-      if (lane >= o) s += y;
-    }
-    if (lane < nwarps) wsum[lane] = s;
-  }
-  __syncthreads();
-  total = wsum[nwarps - 1];
-  long long before = wid > 0 ? wsum[wid - 1] : 0;
-  __syncthreads();
-  return before + x - v;
 }
 
 // One output matrix's arguments of the count pass.
@@ -610,75 +583,44 @@ struct MatCount {
   int* tsum;
   NearSide side;
 };
-// Prefix scan of the tile sums done by the count kernel's last CTA (small problems).
-struct ScanIn {
-  const int* ts[2];
-  long long* toff[2];
-  long long* nnz[2];
-  long long nslots[2];
-  unsigned int* done;  // CTA completion counter (zeroed by the expand step)
-  int nmat;            // 0: no scan in the count kernel (k_scan_chain runs instead)
-};
-
-template <int WK, int WL, int PT>
-__device__ __forceinline__ void count_unit(const MatCount& mc, long long u, double* scr_w, int* red) {
-  const long long U = mc.pr.npt + mc.pr.nb_near;
-  long long idx;
-  if (unit_decode(u, U, mc.pr.nb_near, idx)) {  // block-uniform
-    Prob prn = mc.pr;
-    prn.tau = *mc.pr.tau_ptr;
-    count_near_unit<WK, WL>(prn, idx, scr_w, mc.cnt, mc.tsum, mc.side);
-  } else {
-    const FarCtx prf{mc.pr.K.v, mc.pr.L, *mc.pr.tau_ptr, mc.pr.np, mc.pr.n, mc.pr.P};
-    count_far_tile<WK, WL, PT>(prf, mc.pr.npt, idx, mc.cnt, mc.tsum, red);
-  }
-}
-
-// exclusive scan of ns int32 tile sums into int64 offsets by one CTA (fixed order)
-__device__ __forceinline__ void cta_scan_slots(const int* ts, long long ns, long long* toff, long long* nnz,
-                                               long long* wsum) {
-  const long long per = (ns + blockDim.x - 1) / blockDim.x;
-  const long long lo = threadIdx.x * per, hi = lo + per < ns ? lo + per : ns;
-  long long local = 0;
-  for (long long i = lo; i < hi; ++i) local += __ldcg(&ts[i]);
-  long long total;
-  long long run = block_scan_ll(local, wsum, total);
-  for (long long i = lo; i < hi; ++i) {
-    toff[i] = run;
-    run += __ldcg(&ts[i]);
-  }
-  if (threadIdx.x == 0) *nnz = total;
-}
 
 // Count pass of Q0 (compile-time widths WK, WL, PT) and, with Q1W >= 0, of Q1 (widths Q1W, 0,
-// no dissipators) in one launch: one CTA per unit, Q0's units first.  With sc.nmat > 0 the
-// last CTA to finish scans the tile sums (a4).
+// no dissipators) in one launch of single-warp CTAs:
+//   [Q0 near items][Q1 near items][Q0 far slots][Q1 far slots]   (long near items first)
 template <int WK, int WL, int PT, int Q1W>
-__global__ void __launch_bounds__(256) k_count0(const MatCount m0, const MatCount m1, const ScanIn sc) {
-  using MC = Mode0<WK, WL>;
-  constexpr int PW1 = Q1W >= 0 ? Mode0<(Q1W > 0 ? Q1W : 0), 0>::PER_WARP : 0;
-  constexpr int PW = MC::PER_WARP > PW1 ? MC::PER_WARP : PW1;
-  __shared__ double scr[8][PW];
-  __shared__ int red[8];
-  __shared__ long long wsum[32];
-  __shared__ int last;
-  const long long U0 = m0.pr.npt + m0.pr.nb_near;
-  const long long u = blockIdx.x;
-  if (u < U0) {
-    count_unit<WK, WL, PT>(m0, u, scr[threadIdx.x >> 5], red);
-  } else {
-    if constexpr (Q1W >= 0) count_unit<(Q1W > 0 ? Q1W : 0), 0, 0>(m1, u - U0, scr[threadIdx.x >> 5], red);
+__global__ void __launch_bounds__(32) k_count0(const MatCount m0, const MatCount m1) {
+  constexpr int Q1K = Q1W > 0 ? Q1W : 0;
+  constexpr int PW0 = Mode0<WK, WL>::PER_WARP, PW1 = Mode0<Q1K, 0>::PER_WARP;
+  __shared__ double scr[PW0 > PW1 ? PW0 : PW1];
+  constexpr bool HAS1 = Q1W >= 0;
+  const long long nn0 = m0.pr.nb_near, nn1 = HAS1 ? m1.pr.nb_near : 0;
+  long long u = blockIdx.x;
+  if (u < nn0) {
+    Prob prn = m0.pr;
+    prn.tau = *m0.pr.tau_ptr;
+    count_near_item<WK, WL>(prn, u, scr, m0.cnt, m0.tsum, m0.side);
+    return;
   }
-  if (sc.nmat == 0) return;  // grid-uniform
-  __threadfence();  // this CTA's counts and tile sums are visible device-wide
-  __syncthreads();
-  if (threadIdx.x == 0) last = atomicAdd(sc.done, 1u) == gridDim.x - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int y = 0; y < sc.nmat; ++y) {
-    cta_scan_slots(sc.ts[y], sc.nslots[y], sc.toff[y], sc.nnz[y], wsum);
-    __syncthreads();
+  u -= nn0;
+  if (u < nn1) {
+    if constexpr (HAS1) {
+      Prob prn = m1.pr;
+      prn.tau = *m1.pr.tau_ptr;
+      count_near_item<Q1K, 0>(prn, u, scr, m1.cnt, m1.tsum, m1.side);
+    }
+    return;
+  }
+  u -= nn1;
+  const long long nw0 = (m0.pr.np + m0.pr.tp / SLOTS_PER_TILE - 1) / (m0.pr.tp / SLOTS_PER_TILE);
+  if (u < nw0) {
+    const FarCtx prf{m0.pr.K.v, m0.pr.L, *m0.pr.tau_ptr, m0.pr.np, m0.pr.n, m0.pr.P};
+    count_far_slot<WK, WL, PT>(prf, m0.pr.npt, u, m0.cnt, m0.tsum);
+    return;
+  }
+  u -= nw0;
+  if constexpr (HAS1) {
+    const FarCtx prf{m1.pr.K.v, m1.pr.L, *m1.pr.tau_ptr, m1.pr.np, m1.pr.n, m1.pr.P};
+    count_far_slot<Q1K, 0, 0>(prf, m1.pr.npt, u, m1.cnt, m1.tsum);
   }
 }
 
@@ -1041,7 +983,7 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
   // near units: 8 side rows each (2 per near item)
   const long long nn0 = (2 * (m0.pr.n * 2LL * m0.pr.W + m0.pr.n - 1) + 7) / 8;
   const long long nn1 = HAS1 ? (2 * (m1.pr.n * 2LL * m1.pr.W + m1.pr.n - 1) + 7) / 8 : 0;
-  const long long nt0 = m0.pr.npt, nt1 = HAS1 ? m1.pr.npt : 0;
+  const long long nt0 = m0.pr.npt, nt1 = HAS1 ? m1.pr.npt : 0;  // fill tiles = scan slots
   const long long U0 = nt0 + nn0, U = U0 + nn1 + nt1;
   int* scol = reinterpret_cast<int*>(dyn + wid * FF::BYTES_PER_WARP);
   double* sval = reinterpret_cast<double*>(dyn + wid * FF::BYTES_PER_WARP + FF::COLW * 4);
@@ -1067,7 +1009,7 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
   TileIn nxt{0, 0, 0, 0};
   auto prefetch = [&](long long v) {
     long long idx;
-    if (v < U && decode(v, idx) == 0 && !FF::DIRECT) nxt = load_tile_in(m0.pr.np, nt0, idx, m0.cnt, m0.fo.toff);
+    if (v < U && decode(v, idx) == 0 && !FF::DIRECT) nxt = load_tile_in(m0.pr.np, m0.pr.npt, idx, m0.cnt, m0.fo.toff);
   };
   prefetch(u);
   for (; u < U; u += gridDim.x) {  // block-uniform
@@ -1078,16 +1020,16 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
     if (kind == 0) {
       __syncthreads();  // wtot of the previous unit consumed
       if constexpr (FF::DIRECT)
-        fill_direct_tile<WK, WL, PT>(prf0, nt0, idx, m0.cnt, m0.fo, wtot);
+        fill_direct_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, m0.cnt, m0.fo, wtot);
       else
-        fill_far_tile<WK, WL, PT>(prf0, nt0, idx, cur, m0.fo, scol, sval, wtot);
+        fill_far_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, cur, m0.fo, scol, sval, wtot);
     } else if (kind == 1) {
       fill_near_unit(m0.pr, idx, m0.cnt, m0.fo, m0.side);
     } else if (kind == 2) {
       if constexpr (HAS1) fill_near_unit(m1.pr, idx, m1.cnt, m1.fo, m1.side);
     } else {
       __syncthreads();
-      if constexpr (HAS1) fill_direct_tile<0, 0, 0>(prf1, nt1, idx, m1.cnt, m1.fo, wtot);
+      if constexpr (HAS1) fill_direct_tile<0, 0, 0>(prf1, m1.pr.npt, idx, m1.cnt, m1.fo, wtot);
     }
   }
   if (!FF::DIRECT && lane == 0) bulk_wait0();  // staging must outlive the bulk reads
@@ -1249,6 +1191,32 @@ __global__ void __launch_bounds__(WARP_THREADS) k_fill1(Prob pr, const FarPos* _
 // in ticket order, so every predecessor of a running chunk is resident or done.  Integer
 // sums: the result does not depend on the order (deterministic).
 // ---------------------------------------------------------------------------------------
+__device__ __forceinline__ long long block_scan_ll(long long v, long long* wsum, long long& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  long long x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    long long y = __shfl_up_sync(FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    long long s = lane < nwarps ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long y = __shfl_up_sync(FULL, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nwarps) wsum[lane] = s;
+  }
+  __syncthreads();
+  total = wsum[nwarps - 1];
+  long long before = wid > 0 ? wsum[wid - 1] : 0;
+  __syncthreads();
+  return before + x - v;
+}
+
 struct ScanArgs {
   const int* ts[2];
   long long* toff[2];
@@ -1440,11 +1408,12 @@ void setup_prob(sun_plan_s* pl, int which) {
                              reinterpret_cast<double*>(pl->ws + L.side_val[which]),
                              reinterpret_cast<NearMeta*>(pl->ws + L.side_meta[which]), (4 * pr.W + 1) * (4 * pr.W + 1)};
   if (pr.mode == 0) {
-    pr.tp = pr.wK == 0 ? 2048 : TP0;  // Tiling<WK, WL>::TP (staging-free W = 0: 8 pairs per thread)
+    // scan slot = fill tile of Tiling<WK, WL>::TP pairs (staging-free W = 0: 8 pairs per thread)
+    pr.tp = pr.wK == 0 ? 2048 : TP0;
     pr.npt = (pr.np + pr.tp - 1) / pr.tp;
     pr.ndt = pl->n - 1;
     const long long items = (long long)pl->n * 2 * pr.W + (pl->n - 1);
-    pr.nb_near = (items + 7) / 8;
+    pr.nb_near = items;  // count-pass near items: one warp-CTA each
   } else {
     pr.tp = WARP_TP;
     pr.npt = (pr.np + WARP_TP - 1) / WARP_TP;
@@ -1455,9 +1424,10 @@ void setup_prob(sun_plan_s* pl, int which) {
 
 // ---- mode-0 launchers.  Q1W = -1: one matrix per launch; Q1W = 0: Q0 + Q1 (Q1 = (0, 0, 0)).
 template <int WK, int WL, int PT, int Q1W>
-cudaError_t launch_count0(const MatCount& m0, const MatCount& m1, const ScanIn& sc, cudaStream_t st) {
-  const long long U = m0.pr.npt + m0.pr.nb_near + (Q1W >= 0 ? m1.pr.npt + m1.pr.nb_near : 0);
-  if (U > 0) k_count0<WK, WL, PT, Q1W><<<(unsigned)U, 256, 0, st>>>(m0, m1, sc);
+cudaError_t launch_count0(const MatCount& m0, const MatCount& m1, cudaStream_t st) {
+  auto warps = [](const Prob& p) { return (p.np + p.tp / SLOTS_PER_TILE - 1) / (p.tp / SLOTS_PER_TILE); };
+  const long long U = warps(m0.pr) + m0.pr.nb_near + (Q1W >= 0 ? warps(m1.pr) + m1.pr.nb_near : 0);
+  if (U > 0) k_count0<WK, WL, PT, Q1W><<<(unsigned)U, 32, 0, st>>>(m0, m1);
   return cudaGetLastError();
 }
 
@@ -1506,11 +1476,11 @@ cudaError_t dispatch_attr0(const Prob& p0, const Prob* p1, int q1w, long long& g
 #undef SUN_X1
 }
 
-cudaError_t dispatch_count0(const MatCount& m0, const MatCount& m1, int q1w, const ScanIn& sc, cudaStream_t st) {
+cudaError_t dispatch_count0(const MatCount& m0, const MatCount& m1, int q1w, cudaStream_t st) {
 #define SUN_X0(WK, WL, PT) \
-  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_count0<WK, WL, PT, 0>(m0, m1, sc, st);
+  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_count0<WK, WL, PT, 0>(m0, m1, st);
 #define SUN_X1(WK, WL, PT) \
-  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_count0<WK, WL, PT, -1>(m0, m1, sc, st);
+  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_count0<WK, WL, PT, -1>(m0, m1, st);
   SUN_DISPATCH0(m0.pr, q1w, 0);
 #undef SUN_X0
 #undef SUN_X1
@@ -1662,9 +1632,8 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
     const Prob& p0 = pl->pr[0];
     const Prob& p1 = pl->pr[1];
     pl->combined = p0.mode == 0 && (!pl->has_h1 || (p1.mode == 0 && p1.wK == 0 && p1.wL == 0 && p1.P == 0));
-    pl->scan_in_count = 0;  // a one-CTA scan is a long serial chain: the chained-scan kernel is faster
   }
-  pl->launches_count = 2 + (pl->combined ? 1 : nmat) + (pl->scan_in_count ? 0 : 1);  // expand x2, count, scan
+  pl->launches_count = 2 + (pl->combined ? 1 : nmat) + 1;  // expand x2, count, scan
   pl->launches_fill = pl->combined ? 1 : nmat;
   for (int i = 0; i < 2; ++i) {
     cudaError_t e1 = cudaStreamCreateWithFlags(&pl->aux[i], cudaStreamNonBlocking);
@@ -1735,38 +1704,32 @@ static int enqueue_count(sun_plan pl, cudaStream_t st) {
   const int nmat = 1 + pl->has_h1;
   MatCount mc[2];
   ScanArgs sa;
-  ScanIn sc;
   memset(&sa, 0, sizeof(sa));
-  memset(&sc, 0, sizeof(sc));
   long long maxchunks = 1;
   for (int which = 0; which < nmat; ++which) {
     const Prob& pr = pl->pr[which];
     int* cnt = (int*)(ws + (which ? L.cnt1 : L.cnt0));
     int* ts = (int*)(ws + (which ? L.ts1 : L.ts0));
     mc[which] = MatCount{pr, cnt, ts, pl->side[which]};
-    sa.ts[which] = sc.ts[which] = ts;
-    sa.toff[which] = sc.toff[which] = (long long*)(ws + (which ? L.toff1 : L.toff0));
+    sa.ts[which] = ts;
+    sa.toff[which] = (long long*)(ws + (which ? L.toff1 : L.toff0));
     sa.status[which] = (unsigned long long*)(ws + (which ? L.st1 : L.st0));
-    sa.nnz[which] = sc.nnz[which] = &hdr->nnz[which];
-    sa.nslots[which] = sc.nslots[which] = nslots_of(pr);
+    sa.nnz[which] = &hdr->nnz[which];
+    sa.nslots[which] = nslots_of(pr);
     const long long nc = (sa.nslots[which] + SCAN_TILE - 1) / SCAN_TILE;
     if (nc > maxchunks) maxchunks = nc;
   }
   if (nmat == 1) mc[1] = mc[0];
   sa.ticket = hdr->ticket;
-  sc.done = &hdr->done;
   if (pl->combined) {
-    sc.nmat = pl->scan_in_count ? nmat : 0;
-    CK(dispatch_count0(mc[0], mc[1], pl->has_h1 ? 0 : -1, sc, st));
+    CK(dispatch_count0(mc[0], mc[1], pl->has_h1 ? 0 : -1, st));
   } else {
-    ScanIn none;
-    memset(&none, 0, sizeof(none));
     if (pl->has_h1) CK(fork_aux(pl, st, 1));  // Q1's count pass runs concurrently on aux[0]
     for (int which = 0; which < nmat; ++which) {
       const Prob& pr = pl->pr[which];
       cudaStream_t s = which ? pl->aux[0] : st;
       if (pr.mode == 0) {
-        CK(dispatch_count0(mc[which], mc[which], -1, none, s));
+        CK(dispatch_count0(mc[which], mc[which], -1, s));
       } else {
         const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
         k_count1<<<(unsigned)(pr.npt + pr.ndt), WARP_THREADS, 0, s>>>(pr, fp, pl->npos_far[which], mc[which].cnt,
@@ -1776,10 +1739,9 @@ static int enqueue_count(sun_plan pl, cudaStream_t st) {
     }
     if (pl->has_h1) CK(join_aux(pl, st, 1));
   }
-  if (!pl->scan_in_count) {  // (a4) chained scan of both matrices' tile sums
-    k_scan_chain<<<dim3((unsigned)maxchunks, nmat), SCAN_THREADS, 0, st>>>(sa);
-    CK(cudaGetLastError());
-  }
+  // (a4) chained scan of both matrices' slot sums
+  k_scan_chain<<<dim3((unsigned)maxchunks, nmat), SCAN_THREADS, 0, st>>>(sa);
+  CK(cudaGetLastError());
   return SUN_OK;
 }
 

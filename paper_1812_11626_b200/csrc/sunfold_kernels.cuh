@@ -340,7 +340,7 @@ struct TailInfo {
 
 // Side buffer of the near rows (row 2i = S row / D row of near item i, 2i+1 = J row).
 struct NearMeta {
-  double tr, k;       // D-chain trace (tail value tr * inv[l]) and the row's K value
+  double tr, k;        // D-chain trace (tail value tr * inv[l]) and the row's K value
   int nwin, hi, lend;  // window entries; tail l in (hi, lend]
   int pad;
 };
@@ -350,6 +350,7 @@ struct NearSide {
   NearMeta* meta;
   int nc;        // entries per row slot: (4W + 1)^2 >= any row's window entries
 };
+
 
 template <bool EMIT, bool TAIL = true>
 __device__ __forceinline__ int warp_dchain(const Prob& pr, int lo, int hi, const double* g, const double* pre,
