@@ -11,10 +11,11 @@ Q1 (a6)), on a plan (pattern analysis) built once before timing.  `unfold_cold_m
 the first-call cost including sun_plan_create.  Inputs are resident in HBM when a timed
 step starts; L2 is flushed (a 512 MiB write) between timed steps, outside the step events.
 
-value = (nnz(Q0) + nnz(Q1)) x ranks / max-over-ranks(mean step time)   [nnz/s]
-Multi-GPU: replicas only: every rank unfolds its own copy; there is
-no data-path collective.  `--impl reference` times the CPU oracle (oracle/sparse_o2.c) on the
-host cores (rank 0 only).
+value = sum over ranks of (nnz(Q0) + nnz(Q1)) x steps / max over ranks of the timed region
+Multi-GPU: rank r unfolds the dimer at U = 2 + 0.25 r (a U scan, the
+paper's bifurcation-diagram axis); ranks are independent (no data-path collective, weak
+scaling); NCCL carries only the barrier and the max-over-ranks time.  `--impl reference` times
+the CPU oracle (oracle/sparse_o2.c) on the host cores (rank 0 only).
 """
 from __future__ import annotations
 
@@ -37,7 +38,7 @@ UNIT = "nnz/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -49,7 +50,7 @@ def parse():
 # ---------------------------------------------------------------------------------------
 # distributed plumbing (replicas only)
 # ---------------------------------------------------------------------------------------
-def dist_init(args):
+def dist_init(args, backend: str = "nccl"):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -57,21 +58,40 @@ def dist_init(args):
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return rank, world, local
 
 
-def max_over_ranks(x: float, world: int) -> float:
+def _reduce(x: float, world: int, op: str) -> float:
     if world == 1:
         return x
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def max_over_ranks(x: float, world: int) -> float:
+    return _reduce(x, world, "max")
+
+
+def sum_over_ranks(x: float, world: int) -> float:
+    return _reduce(x, world, "sum")
+
+
+def aggregate(nnz_per_step: int, steps: int, t_region_s: float, world: int):
+    """Whole-job throughput: all ranks' nonzeros over the slowest rank's timed region."""
+    total = sum_over_ranks(float(nnz_per_step) * steps, world)
+    t = max_over_ranks(t_region_s, world)
+    return total / t, t
 
 
 def barrier(world):
@@ -85,30 +105,56 @@ def barrier(world):
 # clocks sampling during the timed region
 # ---------------------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
-             "clocks_event_reasons.sw_power_cap"
+    """SM clock and throttle reasons sampled every ~5 ms by NVML (nvidia-smi's library) while the
+    timed region runs; falls back to nvidia-smi queries if NVML is unavailable."""
+
+    # NVML clocks-event-reason bits (nvmlClocksEventReason*)
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []
+        self.rows = []  # (sm_mhz, sm_max_mhz, reasons bitmask)
         self._stop = threading.Event()
         self._thr = None
 
-    def _run(self):
+    def _run_nvml(self):
+        import pynvml
+
+        pynvml.nvmlInit()
+        try:
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append((float(sm), float(smax), int(rs)))
+                self._stop.wait(0.005)
+        finally:
+            pynvml.nvmlShutdown()
+
+    def _run_smi(self):
+        fields = "clocks.sm,clocks.max.sm,clocks_throttle_reasons.active"
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={fields}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 if out.returncode == 0 and out.stdout.strip():
-                    self.rows.append([x.strip() for x in out.stdout.strip().split(",")])
+                    r = [x.strip() for x in out.stdout.strip().split(",")]
+                    self.rows.append((float(r[0]), float(r[1]), int(r[2], 16)))
             except Exception:
                 pass
-            self._stop.wait(0.1)
+            self._stop.wait(0.02)
+
+    def _run(self):
+        try:
+            self._run_nvml()
+        except Exception:
+            self._run_smi()
 
     def __enter__(self):
         self._thr = threading.Thread(target=self._run, daemon=True)
         self._thr.start()
+        time.sleep(0.02)  # the first samples precede the timed region's first step
         return self
 
     def __exit__(self, *exc):
@@ -119,16 +165,13 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
-            for nm, v in zip(names, r[4:8]):
-                if v.strip().lower() == "active":
+        for _, _, rs in self.rows:
+            for bit, nm in self.REASONS.items():
+                if rs & bit:
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(self.rows)}
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(reasons), "samples": len(self.rows), "source": "nvml"}
 
 
 # ---------------------------------------------------------------------------------------
@@ -195,9 +238,9 @@ def main():
     rank, world, local = dist_init(args)
     torch.cuda.set_device(local)
     import paper_1812_11626_b200 as sun
-    from workloads import CONFIG_NAMES, config
+    from workloads import CONFIG_NAMES, config, u_scan_problem
 
-    prob = config(args.config)
+    prob = u_scan_problem(args.config, rank, world)
     stream = torch.cuda.current_stream()
     H0 = sun.DeviceZCSR.from_host(prob.H0)
     H1 = sun.DeviceZCSR.from_host(prob.H1) if prob.H1 is not None else None
@@ -263,9 +306,8 @@ def main():
     barrier(world)
     torch.cuda.synchronize()
     step_ms = [e0.elapsed_time(e1) for e0, e1 in timings]
-    ms_local = statistics.mean(step_ms)
-    ms = max_over_ranks(ms_local, world)
-    value = nnz_total * world / (ms * 1e-3)
+    value, t_region = aggregate(nnz_total, args.steps, sum(step_ms) * 1e-3, world)
+    ms = t_region * 1e3 / args.steps
     # the two-step (count -> host nnz -> fill) API on the same plan
     tp = []
     for _ in range(max(3, min(args.steps, 10))):
@@ -294,13 +336,16 @@ def main():
     torch.cuda.synchronize()
     cold_ms = statistics.mean([a.elapsed_time(b) for a, b, _ in cold])
     del cold
-    # isolated fill-pass timing (steady state, inputs counted): repeat the fill on one plan
+    # isolated fill-pass timing (steady state, inputs counted): repeat the fill on one plan,
+    # launched directly (no graph replay) so the events bracket the fill kernel itself
+    plan.set_graphs(False)
     plan.count()
     n0, n1 = plan.nnz()
     outs = plan.fill(n0, n1)
     iso = []
-    for _ in range(max(5, args.steps)):
+    for _ in range(max(5, min(args.steps, 50))):
         flush.fill_(1.0)
+        torch.cuda._sleep(200_000)  # GPU busy while the host enqueues: the events bracket the kernel only
         a, b = ev(), ev()
         a.record(stream)
         plan.fill(n0, n1, out=outs)
@@ -310,8 +355,9 @@ def main():
     iso_ms = statistics.mean([a.elapsed_time(b) for a, b in iso])
     # count phase alone (expand + count + scan), device time
     cnt_ev = []
-    for _ in range(max(5, args.steps)):
+    for _ in range(max(5, min(args.steps, 50))):
         flush.fill_(1.0)
+        torch.cuda._sleep(200_000)
         a, b = ev(), ev()
         a.record(stream)
         plan.count()
@@ -331,7 +377,7 @@ def main():
             traffic = None
     achieved = fill_bytes / (iso_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src, "kernel": "k_fill (sun_unfold: Q0 + K + Q1)",
+                "traffic": traffic, "peak_source": peak_src, "kernel": "k_fill0 (sun_unfold: Q0 far tiles + near rows + K, Q1; one launch)",
                 "algorithmic_bytes_per_launch": fill_bytes, "launch_ms": iso_ms}
 
     # end to end through the public API with host buffers

@@ -152,6 +152,13 @@ int64_t sun_nnz_bound(sun_plan plan, int32_t which);
 int sun_apply(const sun_dcsr* Q0, const sun_dcsr* Q1, double eps, const double* K, const double* v,
               double* dvdt, void* stream);
 
+/* Enable (1, the default) or disable (0) CUDA-graph replay of this plan's enqueue sequences.
+ * With graphs, sun_count / sun_unfold / sun_run capture their launches once per distinct
+ * output buffer set and replay the graph (one launch); without, every kernel is launched
+ * directly (used to time a kernel alone).  The environment variable SUNFOLD_NO_GRAPHS=1
+ * sets the default to 0.  Errors: SUN_ERR_ARG. */
+int sun_plan_set_graphs(sun_plan plan, int32_t enable);
+
 /* Fill a diagnostics struct for the plan. */
 int sun_plan_info(sun_plan plan, sun_plan_info_t* info);
 

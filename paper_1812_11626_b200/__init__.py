@@ -223,6 +223,10 @@ class Plan:
         inf = self.info()
         return int(inf["launches_count"] + inf["launches_fill"])
 
+    def set_graphs(self, enable: bool):
+        """CUDA-graph replay of the enqueue sequences on (default) or off (sun_plan_set_graphs)."""
+        _check(lib().sun_plan_set_graphs(self._plan, 1 if enable else 0), "sun_plan_set_graphs")
+
     def info(self) -> dict:
         inf = _lib.SunPlanInfo()
         _check(lib().sun_plan_info(self._plan, ctypes.addressof(inf)), "sun_plan_info")

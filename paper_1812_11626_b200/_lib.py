@@ -44,6 +44,7 @@ SIGNATURES = {
     "sun_run": (ctypes.c_int, [P, P, P, P, P]),
     "sun_nnz_bound": (ctypes.c_int64, [P, ctypes.c_int32]),
     "sun_plan_info": (ctypes.c_int, [P, P]),
+    "sun_plan_set_graphs": (ctypes.c_int, [P, ctypes.c_int32]),
     "sun_plan_destroy": (None, [P]),
     "sun_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sun_gen_index": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),

@@ -1968,6 +1968,12 @@ int sun_plan_info(sun_plan pl, sun_plan_info_t* info) {
   return SUN_OK;
 }
 
+int sun_plan_set_graphs(sun_plan pl, int32_t enable) {
+  if (!pl) return SUN_ERR_ARG;
+  pl->use_graphs = enable != 0;
+  return SUN_OK;
+}
+
 void sun_plan_destroy(sun_plan pl) { delete pl; }
 
 }  // extern "C"

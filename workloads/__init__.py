@@ -141,11 +141,11 @@ def dimer_dissipator(n: int) -> ZCSR:
     return ZCSR.from_triplets(n, rows, cols, vals)
 
 
-def dimer_problem(n: int, drive: bool, gamma: float = 0.1, name: str = "") -> Problem:
+def dimer_problem(n: int, drive: bool, gamma: float = 0.1, name: str = "", U: float = 2.0) -> Problem:
     return Problem(
         name=name or f"dimer_N{n}",
         n=n,
-        H0=dimer_hamiltonian(n),
+        H0=dimer_hamiltonian(n, U=U),
         H1=dimer_drive(n) if drive else None,
         Ls=[dimer_dissipator(n)],
         gammas=[gamma],
@@ -222,6 +222,19 @@ def config(idx: int) -> Problem:
     if idx == 4:
         return dimer_problem(1000, drive=True, name="c4_dimer_N1000_drive")
     raise ValueError(idx)
+
+
+def u_scan_problem(idx: int, rank: int, world: int, dU: float = 0.25) -> Problem:
+    """Rank `rank`'s share of a U scan (the bifurcation-diagram axis, PAPER.md P:259-261,
+    Fig. 2): the dimer of configs[idx] (1, 2 or 4) at U = 2 + rank * dU.  Every
+    rank's problem has the same pattern sizes; ranks share nothing (multi-GPU = independent
+    unfolds, no data-path collective).  Other configs are not U-parametrised and are
+    replicated."""
+    if world <= 1 or idx not in (1, 2, 4):
+        return config(idx)
+    n = {1: 64, 2: 256, 4: 1000}[idx]
+    U = 2.0 + rank * dU
+    return dimer_problem(n, drive=idx != 1, name=f"{CONFIG_NAMES[idx]}_U{U:g}", U=U)
 
 
 CONFIG_NAMES = {
