@@ -2,8 +2,8 @@
 //
 // Pipeline (Table I Step 2; two-step CRS fill P:369-370), launches per sun_run:
 //   sun_plan_create : k_analyze         bandwidths, Frobenius norms, CSR validation -> 1 readback
-//   sun_count       : k_expand_rows     (a1) CSR -> band storage, per-block norms / flags, zeroing
-//                     k_expand_k        (a1) K = H0 + i/2 sum gamma L^+L, tau, inv[l], Hermiticity
+//   sun_count       : k_expand          (a1) CSR -> band storage, K = H0 + i/2 sum gamma L^+L, inv[l],
+//                                        norms / flags / Hermiticity -> tau (last block), zeroing
 //                     k_count0 / k_count1 (a3) per-row counts (values thresholded), tile sums;
 //                                        one launch per output matrix (near items + far tiles),
 //                                        Q1's on an auxiliary stream
@@ -39,7 +39,7 @@ constexpr int SLOTS_PER_TILE = 8;  // mode 0: count warps (single-warp CTAs) per
 constexpr int WARP_TP = 64;       // mode 1: pairs per tile
 constexpr int WARP_THREADS = 256;
 constexpr int FAR_MAXPOS = 1024;
-constexpr int EXP_THREADS = 256;  // k_expand_rows rows per CTA
+constexpr int EXP_THREADS = 256;  // k_expand rows (or K-band entries) per CTA
 constexpr int SCAN_THREADS = 1024, SCAN_IPT = 4, SCAN_TILE = SCAN_THREADS * SCAN_IPT;
 constexpr unsigned long long SCAN_A = 1ull << 62, SCAN_P = 2ull << 62, SCAN_V = (1ull << 62) - 1;
 
@@ -80,7 +80,7 @@ struct OpList {
   int has_h1;
 };
 
-struct BlkInfo {  // k_expand_rows -> k_expand_k, one per (operator, row block)
+struct BlkInfo {  // k_expand: one per (operator, row block), reduced by the last block
   double nrm2;
   int bw;
   int flags;
@@ -100,7 +100,7 @@ struct FarPos {
 };
 
 struct Layout {
-  size_t hdr, fp0, fp1, inv, kb0, hb0, hb1, lb, blk, ts0, ts1, st0, st1, toff0, toff1, cnt0, cnt1;
+  size_t hdr, fp0, fp1, inv, kb0, hb0, hb1, lb, blk, herm, ts0, ts1, st0, st1, toff0, toff1, cnt0, cnt1;
   size_t side_col[2], side_val[2], side_meta[2], total;
   long long side_rows;
   long long maxslots, maxchunks, nrb;
@@ -124,6 +124,7 @@ Layout make_layout(int n, int P) {
   L.hb1 = off; off = align256(off + (size_t)n * (2 * WMAX + 1) * sizeof(double2));
   L.lb = off;  off = align256(off + (size_t)(P > 0 ? P : 1) * n * (2 * WLMAX + 1) * sizeof(double2));
   L.blk = off; off = align256(off + (size_t)(2 + P) * nrb * sizeof(BlkInfo));
+  L.herm = off; off = align256(off + (size_t)2 * ((long long)n * (2 * WMAX + 1) / EXP_THREADS + 2) * sizeof(unsigned long long));
   L.ts0 = off; off = align256(off + (size_t)maxslots * sizeof(int));   // [ts0, toff0) zeroed per count
   L.ts1 = off; off = align256(off + (size_t)maxslots * sizeof(int));
   L.st0 = off; off = align256(off + (size_t)maxchunks * sizeof(unsigned long long));
@@ -263,161 +264,218 @@ __global__ void k_analyze(OpList ops, DevHeader* hdr) {
   }
 }
 
-// (a1) CSR -> band storage, one thread per (operator, row); grid (row blocks, operators).
-//   op 0 = H0 -> Hb0 (width wK), op 1 = H1 -> Hb1 (width wH1), op 2+p = L_p -> Lb[p] (width wL,
-//   scaled by sqrt(gamma_p)).  Also: CSR validation, values beyond the planned bandwidth,
-//   ||.||_F^2 per row block (fixed-order tree), and zeroing of the scan buffers used later
-//   in the same sun_count (tile sums, chained-scan status, tickets, Hermiticity maxima).
-__global__ void __launch_bounds__(EXP_THREADS) k_expand_rows(OpList ops, double2* hb0, int wK, double2* hb1, int wH1,
-                                                             double2* lb, int wL, BlkInfo* blk, int* zero32,
-                                                             long long nzero32, unsigned long long* zero64,
-                                                             long long nzero64, DevHeader* hdr) {
-  const long long gtid = ((long long)blockIdx.y * gridDim.x + blockIdx.x) * blockDim.x + threadIdx.x;
-  const long long gstride = (long long)gridDim.x * gridDim.y * blockDim.x;
-  for (long long i = gtid; i < nzero32; i += gstride) zero32[i] = 0;
-  for (long long i = gtid; i < nzero64; i += gstride) zero64[i] = 0ull;
-  if (gtid == 0) {
-    hdr->herm_dev[0] = hdr->herm_dev[1] = 0ull;
-    hdr->ticket[0] = hdr->ticket[1] = 0u;
-    hdr->done = 0u;
+// (a1) expand, one launch.  Blocks [0, nA): CSR -> band storage, one thread per (operator,
+// row) (op 0 = H0 -> Hb0 at width wK, op 1 = H1 -> Hb1 at width wH1, op 2+p = L_p -> Lb[p] at
+// width wL scaled by sqrt(gamma_p)), CSR validation, values beyond the planned bandwidth,
+// ||.||_F^2 per row block (fixed-order tree).  Blocks [nA, ..): one thread per entry (r, o) of
+// the K = H0 + (i/2) sum_p gamma_p L_p^+ L_p band, read straight from the CSR inputs (so no
+// block waits for another), the Hermiticity deviations of H0 / H1, inv[l] = 1/sqrt(l(l+1))
+// (D^l normalisation).  The last block to finish reduces the per-block records in
+// fixed order into the header: norms, bandwidths, flags, Hermiticity deviations and the drop
+// thresholds tau (R6).
+struct ExpandArgs {
+  OpList ops;
+  Gammas gam;
+  double2 *hb0, *hb1, *lb, *kb0;
+  double* inv;
+  BlkInfo* blk;             // nA records
+  unsigned long long* herm; // 2 per K block
+  int* zero32;
+  unsigned long long* zero64;
+  long long nz32, nz64;
+  DevHeader* hdr;
+  unsigned int* done;       // completion counter (0 between launches)
+  int wK, wH1, wL, wX;      // wX = max(wK, wH1): width of the K-block grid
+  int nrb, nA, nB, P;
+};
+
+__device__ __forceinline__ double2 csr_get(const OpDesc& d, int r, int c) {
+  for (int64_t k = d.rp[r], e = d.rp[r + 1]; k < e; ++k) {
+    const int cc = d.ci[k];
+    if (cc == c) return d.v[k];
+    if (cc > c) break;
   }
-  const int op = blockIdx.y;
-  if (op == 1 && !ops.has_h1) return;  // block-uniform
-  const int n = ops.n;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  const OpDesc d = ops.op[op];
-  double2* dst;
-  int w;
-  double s = 1.0;
-  if (op == 0) { dst = hb0; w = wK; }
-  else if (op == 1) { dst = hb1; w = wH1; }
-  else { dst = lb + (long long)(op - 2) * n * (2 * wL + 1); w = wL; s = ops.sqrtg[op]; }
-  double acc = 0.0;
-  int bw = 0, flags = 0;
-  if (r < n) {
-    double2* row = dst + (long long)r * (2 * w + 1);
-    for (int o = 0; o <= 2 * w; ++o) row[o] = make_double2(0.0, 0.0);
-    const int64_t lo = d.rp[r], hi = d.rp[r + 1];
-    if (hi < lo) flags |= F_MALFORMED;
-    int prev = -1;
-    for (int64_t k = lo; k < hi; ++k) {
-      const int c = d.ci[k];
-      if (c < 0 || c >= n || c <= prev) { flags |= F_MALFORMED; break; }
-      prev = c;
-      const double2 v = d.v[k];
-      const int o = c - r;
-      const int ao = o < 0 ? -o : o;
-      if (v.x != 0.0 || v.y != 0.0) bw = ao > bw ? ao : bw;
-      acc += v.x * v.x + v.y * v.y;
-      if (ao <= w) row[o + w] = make_double2(s * v.x, s * v.y);
-    }
-    if (ops.wplan[op] >= 0 && bw > ops.wplan[op]) flags |= F_PATTERN;
-  }
-  __shared__ double red[EXP_THREADS];
-  __shared__ int sbw[EXP_THREADS / 32], sfl[EXP_THREADS / 32];
-  red[threadIdx.x] = acc;
-  int wb = bw, wf = flags;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    wb = max(wb, __shfl_xor_sync(FULL, wb, o));
-    wf |= __shfl_xor_sync(FULL, wf, o);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    sbw[threadIdx.x >> 5] = wb;
-    sfl[threadIdx.x >> 5] = wf;
-  }
-  __syncthreads();
-  for (int st = EXP_THREADS / 2; st > 0; st >>= 1) {  // fixed-order tree: deterministic
-    if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    int b = 0, f = 0;
-    for (int i = 0; i < EXP_THREADS / 32; ++i) {
-      b = max(b, sbw[i]);
-      f |= sfl[i];
-    }
-    blk[(long long)op * gridDim.x + blockIdx.x] = BlkInfo{red[0], b, f};
-  }
+  return make_double2(0.0, 0.0);
 }
 
-// (a1) K = H0 + (i/2) M, M = sum_p Lt_p^+ Lt_p (Lt = sqrt(gamma) L), one thread per band entry;
-// inv[l] = 1/sqrt(l(l+1)) (normalisation of D^l); Hermiticity deviations of H0, H1.
-// Block 0 also reduces the k_expand_rows block records (fixed order) into the header: norms,
-// bandwidths, flags, and the drop thresholds tau (R6).
-__global__ void k_expand_k(int n, int P, int nops, int has_h1, int nrb, const BlkInfo* __restrict__ blk,
-                           const double2* __restrict__ hb0, double2* kb0, int wK, const double2* __restrict__ lb,
-                           int wL, const double2* __restrict__ hb1, int wH1, Gammas gam, DevHeader* hdr,
-                           double* inv) {
-  if (blockIdx.x == 0 && threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int flags = 0;
-    double s0 = 0.0;
-    for (int op = 0; op < nops; ++op) {
-      if (op == 1 && !has_h1) continue;
-      double acc = 0.0;
-      int b = 0;
-      for (int i = lane; i < nrb; i += 32) {  // fixed order per lane, then a fixed tree
-        const BlkInfo bi = blk[(long long)op * nrb + i];
-        acc += bi.nrm2;
-        b = max(b, bi.bw);
-        flags |= bi.flags;
+__global__ void __launch_bounds__(EXP_THREADS) k_expand(const ExpandArgs A) {
+  const OpList& ops = A.ops;
+  const int n = ops.n;
+  const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long gstride = (long long)gridDim.x * blockDim.x;
+  for (long long i = gtid; i < A.nz32; i += gstride) A.zero32[i] = 0;
+  for (long long i = gtid; i < A.nz64; i += gstride) A.zero64[i] = 0ull;
+  if (gtid == 0) A.hdr->ticket[0] = A.hdr->ticket[1] = 0u;
+  __shared__ double red[EXP_THREADS];
+  __shared__ int sbw[EXP_THREADS / 32], sfl[EXP_THREADS / 32];
+  __shared__ unsigned long long sh0[EXP_THREADS / 32], sh1[EXP_THREADS / 32];
+  __shared__ int last;
+  if ((int)blockIdx.x < A.nA) {
+    const int op = blockIdx.x / A.nrb, rb = blockIdx.x % A.nrb;
+    double acc = 0.0;
+    int bw = 0, flags = 0;
+    const int r = rb * blockDim.x + threadIdx.x;
+    if (!(op == 1 && !ops.has_h1) && r < n) {
+      const OpDesc d = ops.op[op];
+      double2* dst;
+      int w;
+      double sc = 1.0;
+      if (op == 0) { dst = A.hb0; w = A.wK; }
+      else if (op == 1) { dst = A.hb1; w = A.wH1; }
+      else { dst = A.lb + (long long)(op - 2) * n * (2 * A.wL + 1); w = A.wL; sc = ops.sqrtg[op]; }
+      double2* row = dst + (long long)r * (2 * w + 1);
+      for (int o = 0; o <= 2 * w; ++o) row[o] = make_double2(0.0, 0.0);
+      const int64_t lo = d.rp[r], hi = d.rp[r + 1];
+      if (hi < lo) flags |= F_MALFORMED;
+      int prev = -1;
+      for (int64_t k = lo; k < hi; ++k) {
+        const int c = d.ci[k];
+        if (c < 0 || c >= n || c <= prev) { flags |= F_MALFORMED; break; }
+        prev = c;
+        const double2 v = d.v[k];
+        const int o = c - r;
+        const int ao = o < 0 ? -o : o;
+        if (v.x != 0.0 || v.y != 0.0) bw = ao > bw ? ao : bw;
+        acc += v.x * v.x + v.y * v.y;
+        if (ao <= w) row[o + w] = make_double2(sc * v.x, sc * v.y);
       }
+      if (ops.wplan[op] >= 0 && bw > ops.wplan[op]) flags |= F_PATTERN;
+    }
+    red[threadIdx.x] = acc;
+    int wb = bw, wf = flags;
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        acc += __shfl_xor_sync(FULL, acc, o);
-        b = max(b, __shfl_xor_sync(FULL, b, o));
+    for (int o = 16; o > 0; o >>= 1) {
+      wb = max(wb, __shfl_xor_sync(FULL, wb, o));
+      wf |= __shfl_xor_sync(FULL, wf, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sbw[threadIdx.x >> 5] = wb;
+      sfl[threadIdx.x >> 5] = wf;
+    }
+    __syncthreads();
+    for (int st = EXP_THREADS / 2; st > 0; st >>= 1) {  // fixed-order tree: deterministic
+      if (threadIdx.x < st) red[threadIdx.x] += red[threadIdx.x + st];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      int bb = 0, f = 0;
+      for (int i = 0; i < EXP_THREADS / 32; ++i) {
+        bb = max(bb, sbw[i]);
+        f |= sfl[i];
       }
-      if (lane == 0) {
-        hdr->nrm2[op] = acc;
-        hdr->bw[op] = b;
-        if (op == 0) s0 += sqrt(acc);
-        if (op >= 2) s0 += gam.g[op - 2] * acc;
-        if (op < 2) hdr->nrm2_h[op] = acc;
+      A.blk[blockIdx.x] = BlkInfo{red[0], bb, f};
+    }
+  } else {
+    const long long t = (long long)(blockIdx.x - A.nA) * blockDim.x + threadIdx.x;
+    if (t < n) A.inv[t] = t > 0 ? 1.0 / sqrt((double)t * (double)(t + 1)) : 0.0;
+    unsigned long long d0 = 0ull, d1 = 0ull;
+    const int sw = 2 * A.wX + 1;
+    if (t < (long long)n * sw) {
+      const int r = (int)(t / sw), o = (int)(t % sw) - A.wX;
+      const int c = r + o;
+      const bool in = c >= 0 && c < n;
+      if (o >= -A.wK && o <= A.wK) {
+        double2 kv = make_double2(0.0, 0.0);
+        if (in) {
+          double mx = 0.0, my = 0.0;
+          int lo = max(r, c) - A.wL, hi = min(r, c) + A.wL;
+          if (lo < 0) lo = 0;
+          if (hi > n - 1) hi = n - 1;
+          for (int p = 0; p < A.P; ++p) {
+            const OpDesc L = ops.op[2 + p];
+            double px = 0.0, py = 0.0;
+            for (int x = lo; x <= hi; ++x) {
+              const double2 a = csr_get(L, x, r), b = csr_get(L, x, c);  // conj(L_xr) L_xc
+              px += a.x * b.x + a.y * b.y;
+              py += a.x * b.y - a.y * b.x;
+            }
+            mx += ops.gamma[2 + p] * px;
+            my += ops.gamma[2 + p] * py;
+          }
+          const double2 h = csr_get(ops.op[0], r, c), ht = csr_get(ops.op[0], c, r);
+          kv = make_double2(h.x - 0.5 * my, h.y + 0.5 * mx);
+          d0 = (unsigned long long)__double_as_longlong(fmax(fabs(h.x - ht.x), fabs(h.y + ht.y)));
+        }
+        A.kb0[(long long)r * (2 * A.wK + 1) + (o + A.wK)] = kv;
+      }
+      if (in && ops.has_h1 && o >= -A.wH1 && o <= A.wH1) {
+        const double2 g = csr_get(ops.op[1], r, c), gt = csr_get(ops.op[1], c, r);
+        d1 = (unsigned long long)__double_as_longlong(fmax(fabs(g.x - gt.x), fabs(g.y + gt.y)));
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) flags |= __shfl_xor_sync(FULL, flags, o);
+    for (int o = 16; o > 0; o >>= 1) {
+      d0 = max(d0, __shfl_xor_sync(FULL, d0, o));
+      d1 = max(d1, __shfl_xor_sync(FULL, d1, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sh0[threadIdx.x >> 5] = d0;
+      sh1[threadIdx.x >> 5] = d1;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long m0 = 0ull, m1 = 0ull;
+      for (int i = 0; i < EXP_THREADS / 32; ++i) {
+        m0 = max(m0, sh0[i]);
+        m1 = max(m1, sh1[i]);
+      }
+      A.herm[2 * (blockIdx.x - A.nA)] = m0;
+      A.herm[2 * (blockIdx.x - A.nA) + 1] = m1;
+    }
+  }
+  // the last block reduces the records (fixed order)
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(A.done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last || threadIdx.x >= 32) return;
+  __threadfence();
+  const int lane = threadIdx.x;
+  DevHeader* hdr = A.hdr;
+  int flags = 0;
+  double s0 = 0.0;
+  for (int op = 0; op < ops.nops; ++op) {
+    if (op == 1 && !ops.has_h1) continue;
+    double acc = 0.0;
+    int bb = 0;
+    for (int i = lane; i < A.nrb; i += 32) {  // fixed order per lane, then a fixed tree
+      const BlkInfo bi = A.blk[op * A.nrb + i];
+      acc += bi.nrm2;
+      bb = max(bb, bi.bw);
+      flags |= bi.flags;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc += __shfl_xor_sync(FULL, acc, o);
+      bb = max(bb, __shfl_xor_sync(FULL, bb, o));
+    }
     if (lane == 0) {
-      hdr->flags = flags;
-      hdr->tau[0] = 1e-14 * s0;
-      hdr->tau[1] = has_h1 ? 1e-14 * sqrt(hdr->nrm2_h[1]) : 0.0;
-      if (!has_h1) hdr->nrm2_h[1] = 0.0;
+      hdr->nrm2[op] = acc;
+      hdr->bw[op] = bb;
+      if (op == 0) s0 += sqrt(acc);
+      if (op >= 2) s0 += A.gam.g[op - 2] * acc;
+      if (op < 2) hdr->nrm2_h[op] = acc;
     }
   }
-  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (t < n) inv[t] = t > 0 ? 1.0 / sqrt((double)t * (double)(t + 1)) : 0.0;
-  const int sw = 2 * wK + 1;
-  if (t >= (long long)n * sw) return;
-  const int r = (int)(t / sw), o = (int)(t % sw) - wK;
-  const int c = r + o;
-  if (c < 0 || c >= n) {
-    kb0[t] = make_double2(0.0, 0.0);
-    return;
+  unsigned long long m0 = 0ull, m1 = 0ull;
+  for (int i = lane; i < A.nB; i += 32) {
+    m0 = max(m0, A.herm[2 * i]);
+    m1 = max(m1, A.herm[2 * i + 1]);
   }
-  double mx = 0.0, my = 0.0;
-  int lo = max(r, c) - wL, hi = min(r, c) + wL;
-  if (lo < 0) lo = 0;
-  if (hi > n - 1) hi = n - 1;
-  for (int p = 0; p < P; ++p) {
-    const double2* Lp = lb + (long long)p * n * (2 * wL + 1);
-    for (int x = lo; x <= hi; ++x) {
-      const double2 a = Lp[(long long)x * (2 * wL + 1) + (r - x + wL)];  // L_xr
-      const double2 b = Lp[(long long)x * (2 * wL + 1) + (c - x + wL)];  // L_xc
-      mx += a.x * b.x + a.y * b.y;  // conj(L_xr) L_xc
-      my += a.x * b.y - a.y * b.x;
-    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    flags |= __shfl_xor_sync(FULL, flags, o);
+    m0 = max(m0, __shfl_xor_sync(FULL, m0, o));
+    m1 = max(m1, __shfl_xor_sync(FULL, m1, o));
   }
-  const double2 h = hb0[t];
-  kb0[t] = make_double2(h.x - 0.5 * my, h.y + 0.5 * mx);
-  const double2 ht = hb0[(long long)c * sw + (r - c + wK)];
-  const double dev0 = fmax(fabs(h.x - ht.x), fabs(h.y + ht.y));
-  if (dev0 > 0.0) atomicMax(&hdr->herm_dev[0], (unsigned long long)__double_as_longlong(dev0));
-  if (has_h1 && o >= -wH1 && o <= wH1) {
-    const double2 g = hb1[(long long)r * (2 * wH1 + 1) + (o + wH1)];
-    const double2 gt = hb1[(long long)c * (2 * wH1 + 1) + (r - c + wH1)];
-    const double dev1 = fmax(fabs(g.x - gt.x), fabs(g.y + gt.y));
-    if (dev1 > 0.0) atomicMax(&hdr->herm_dev[1], (unsigned long long)__double_as_longlong(dev1));
+  if (lane == 0) {
+    hdr->flags = flags;
+    hdr->herm_dev[0] = m0;
+    hdr->herm_dev[1] = ops.has_h1 ? m1 : 0ull;
+    hdr->tau[0] = 1e-14 * s0;
+    hdr->tau[1] = ops.has_h1 ? 1e-14 * sqrt(hdr->nrm2_h[1]) : 0.0;
+    if (!ops.has_h1) hdr->nrm2_h[1] = 0.0;
+    *A.done = 0u;  // ready for the next launch
   }
 }
 
@@ -1633,7 +1691,7 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
     const Prob& p1 = pl->pr[1];
     pl->combined = p0.mode == 0 && (!pl->has_h1 || (p1.mode == 0 && p1.wK == 0 && p1.wL == 0 && p1.P == 0));
   }
-  pl->launches_count = 2 + (pl->combined ? 1 : nmat) + 1;  // expand x2, count, scan
+  pl->launches_count = 1 + (pl->combined ? 1 : nmat) + 1;  // expand, count, scan
   pl->launches_fill = pl->combined ? 1 : nmat;
   for (int i = 0; i < 2; ++i) {
     cudaError_t e1 = cudaStreamCreateWithFlags(&pl->aux[i], cudaStreamNonBlocking);
@@ -1687,18 +1745,35 @@ static int enqueue_count(sun_plan pl, cudaStream_t st) {
   // (a1) expand: band storage + norms/flags per row block; zero the scan state
   const long long nz32 = (long long)((L.st0 - L.ts0) / sizeof(int));
   const long long nz64 = (long long)((L.toff0 - L.st0) / sizeof(unsigned long long));
-  dim3 g1((unsigned)L.nrb, (unsigned)pl->ops.nops);
-  k_expand_rows<<<g1, EXP_THREADS, 0, st>>>(pl->ops, (double2*)(ws + L.hb0), pl->wK, (double2*)(ws + L.hb1), pl->wH1,
-                                            (double2*)(ws + L.lb), pl->wL, (BlkInfo*)(ws + L.blk), (int*)(ws + L.ts0),
-                                            nz32, (unsigned long long*)(ws + L.st0), nz64, hdr);
-  CK(cudaGetLastError());
-  // (a1) K = H0 + i/2 sum gamma L^+L, reductions -> tau, inv[l], Hermiticity
-  long long nk = (long long)n * (2 * pl->wK + 1);
-  if (nk < n) nk = n;
-  k_expand_k<<<(unsigned)((nk + 255) / 256), 256, 0, st>>>(
-      n, pl->P, pl->ops.nops, pl->has_h1, (int)L.nrb, (const BlkInfo*)(ws + L.blk), (const double2*)(ws + L.hb0),
-      (double2*)(ws + L.kb0), pl->wK, (const double2*)(ws + L.lb), pl->wL, (const double2*)(ws + L.hb1), pl->wH1,
-      pl->gam, hdr, (double*)(ws + L.inv));
+  ExpandArgs ea;
+  ea.ops = pl->ops;
+  ea.gam = pl->gam;
+  ea.hb0 = (double2*)(ws + L.hb0);
+  ea.hb1 = (double2*)(ws + L.hb1);
+  ea.lb = (double2*)(ws + L.lb);
+  ea.kb0 = (double2*)(ws + L.kb0);
+  ea.inv = (double*)(ws + L.inv);
+  ea.blk = (BlkInfo*)(ws + L.blk);
+  ea.herm = (unsigned long long*)(ws + L.herm);
+  ea.zero32 = (int*)(ws + L.ts0);
+  ea.zero64 = (unsigned long long*)(ws + L.st0);
+  ea.nz32 = nz32;
+  ea.nz64 = nz64;
+  ea.hdr = hdr;
+  ea.done = &hdr->done;
+  ea.wK = pl->wK;
+  ea.wH1 = pl->wH1;
+  ea.wL = pl->wL;
+  ea.wX = pl->wK > pl->wH1 ? pl->wK : pl->wH1;
+  ea.nrb = (int)L.nrb;
+  ea.nA = (int)L.nrb * pl->ops.nops;
+  {
+    long long nk = (long long)n * (2 * ea.wX + 1);
+    if (nk < n) nk = n;
+    ea.nB = (int)((nk + EXP_THREADS - 1) / EXP_THREADS);
+  }
+  ea.P = pl->P;
+  k_expand<<<(unsigned)(ea.nA + ea.nB), EXP_THREADS, 0, st>>>(ea);
   CK(cudaGetLastError());
   // (a3) count pass (+ (a4) prefix scan in the last CTA when small)
   const int nmat = 1 + pl->has_h1;

@@ -602,12 +602,15 @@ __device__ __forceinline__ void far_values(const FarCtx& pr, int a, int b, doubl
   constexpr int SK = 2 * WK + 1, SL = 2 * WL + 1;
   const int n = pr.n;
   double2 kc[2 * W + 1], kr[2 * W + 1];
+  // band rows through base pointers: compile-time offsets (i SK + 2W - i) from K(a - W, .)
+  const double2* Ka = pr.K + (long long)(a - W) * SK;
+  const double2* Kb = pr.K + (long long)(b - W) * SK;
 #pragma unroll
   for (int i = 0; i <= 2 * W; ++i) {
     const int c = a + i - W;  // K(c, a): row c, offset a - c = W - i
-    kc[i] = c >= 0 ? __ldg(&pr.K[(long long)c * SK + (2 * W - i)]) : make_double2(0.0, 0.0);
+    kc[i] = c >= 0 ? __ldg(Ka + (i * SK + 2 * W - i)) : make_double2(0.0, 0.0);
     const int d = b + i - W;  // K(d, b): row d, offset b - d = W - i
-    kr[i] = d < n ? __ldg(&pr.K[(long long)d * SK + (2 * W - i)]) : make_double2(0.0, 0.0);
+    kr[i] = d < n ? __ldg(Kb + (i * SK + 2 * W - i)) : make_double2(0.0, 0.0);
   }
   // outer block O_ij = sum_p conj(Lt_p(a, a-WL+i)) Lt_p(b, b-WL+j)
   double ox[SL][SL], oy[SL][SL];
