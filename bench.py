@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-rk4", action="store_true")
     return ap.parse_args()
 
 
@@ -365,6 +366,36 @@ def main():
         cnt_ev.append((a, b))
     torch.cuda.synchronize()
     count_dev_ms = statistics.mean([a.elapsed_time(b) for a, b in cnt_ev])
+    # F1: RK4 propagation of the unfolded system from rho(0) = |0><0|,
+    # timed on the device (L2 flushed before).  h = 1e-5 keeps RK4 stable: BASELINE's
+    # dissipator has no gamma/(N-1) prefactor (reading R9), |lambda|max ~ gamma N^2.
+    rk4 = None
+    if not args.no_rk4:
+        from workloads import ZCSR as _Z
+
+        v = sun.expand_state(_Z.from_triplets(prob.n, [0], [0], [1.0]))
+        work = torch.empty(3 * m, dtype=torch.float64, device="cuda")
+        h = 1e-5
+        nst = 20
+        sun.rk4(Q0, Q1, K, v, h, 2, eps0=1.0, eps1=1.5, omega=1.0, work=work)  # warm-up
+        flush.fill_(1.0)
+        torch.cuda._sleep(200_000)
+        a, b = ev(), ev()
+        a.record(stream)
+        sun.rk4(Q0, Q1, K, v, h, nst, eps0=1.0, eps1=1.5, omega=1.0, work=work)
+        b.record(stream)
+        torch.cuda.synchronize()
+        rk_ms = a.elapsed_time(b) / nst
+        # algorithmic bytes of one step: 4 SpMV stages over Q0, Q1 (12 B/nnz + 8 B/row each),
+        # K, the gathered v (and k for stages 2-4) read once, k/acc/v' written
+        nz = Q0.nnz + (Q1.nnz if Q1 is not None else 0)
+        rows = (m + 1) * (2 if Q1 is not None else 1)
+        stage = 12 * nz + 8 * rows + 8 * m * 2
+        step_bytes = 4 * stage + 8 * m * (2 + 3 + 3 + 3)
+        rk_gbs = step_bytes / (rk_ms * 1e-3) / 1e9
+        rk4 = {"ms_per_step": rk_ms, "steps": nst, "h": h, "bytes_per_step": step_bytes,
+               "roofline": {"bound": "hbm", "achieved": rk_gbs, "peak": peak, "unit": "GB/s", "frac": rk_gbs / peak},
+               "kernel": "k_rk4_stage (4 fused SpMV stages per RK4 step)"}
     info = plan.info()
     launches_per_step = plan.launches_per_run()
     plan.close()
@@ -444,6 +475,7 @@ def main():
         "gpu_launches": args.steps * launches_per_step,
         "roofline": roofline,
         "cpu_baseline": cpu,
+        "rk4": rk4,
         "plan": {k: info[k] for k in ("w_h0", "w_l", "w_k", "mode_q0", "npos_far_q0", "tiles_q0")},
         "wall_s_timed_region": t_wall,
     }

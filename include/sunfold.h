@@ -152,6 +152,33 @@ int64_t sun_nnz_bound(sun_plan plan, int32_t which);
 int sun_apply(const sun_dcsr* Q0, const sun_dcsr* Q1, double eps, const double* K, const double* v,
               double* dvdt, void* stream);
 
+/* ---- Propagation (PAPER.md Step 3) and states (Step 2.6 P:456-457, Eq. 5) ---- */
+
+/* v(0): the coherence vector of an N x N operator rho (Eq. 5):
+ *   v_s = Re Tr(F_s rho),  s = 0 .. M-1 (generator order R5); for S_ab / J_ab only the
+ *   entries (a, b) and (b, a) contribute, for D^l the diagonal prefix (sum_{c<l} rho_cc -
+ *   l rho_ll) / sqrt(l(l+1)).  rho: CSR (device), any entries; v: device float64[M], written
+ *   (fully overwritten).  Asynchronous on `stream`.  Errors: SUN_ERR_ARG, SUN_ERR_DIM, _CUDA. */
+int sun_expand_state(const sun_zcsr* rho, double* v, void* stream);
+
+/* Populations of the state with coherence vector v (inverse of Eq. 5 on the diagonal):
+ *   diag[a] = <a|rho|a> = 1/N + sum_l v_{D^l} delta_l(a),  delta_l(a) = (D^l)_aa,
+ * i.e. the bifurcation-diagram observable p_n.  v: device float64[N^2 - 1];
+ * diag: device float64[N].  Asynchronous.  Errors: SUN_ERR_ARG, SUN_ERR_DIM, _CUDA. */
+int sun_state_diag(const double* v, int32_t n, double* diag, void* stream);
+
+/* Fixed-step classic fourth-order Runge-Kutta (the paper's integrator, Step 3.1 P:464-470) of
+ *   dv/dt = (Q0 + eps(t) Q1) v + K,   eps(t) = eps0 + eps1 sin(omega t)   (Eq. 9, reading R10)
+ * from t0 over nsteps steps of size h:
+ *   k1 = f(t, v), k2 = f(t + h/2, v + h/2 k1), k3 = f(t + h/2, v + h/2 k2), k4 = f(t + h, v + h k3),
+ *   v <- v + h/6 (k1 + 2 k2 + 2 k3 + k4).
+ * One fused SpMV kernel per stage (the stage input v + c k is formed in the gather; the RK4
+ * sum is accumulated in the epilogue).  Q1 may be NULL (no drive); K may be NULL (= 0).
+ * v: device float64[M], in/out.  work: device float64[3 M] scratch owned by the caller.
+ * Asynchronous on `stream`.  Errors: SUN_ERR_ARG, SUN_ERR_DIM, SUN_ERR_CUDA. */
+int sun_rk4(const sun_dcsr* Q0, const sun_dcsr* Q1, const double* K, double eps0, double eps1, double omega,
+            double t0, double h, int64_t nsteps, double* v, double* work, void* stream);
+
 /* Enable (1, the default) or disable (0) CUDA-graph replay of this plan's enqueue sequences.
  * With graphs, sun_count / sun_unfold / sun_run capture their launches once per distinct
  * output buffer set and replay the graph (one launch); without, every kernel is launched

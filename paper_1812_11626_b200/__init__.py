@@ -25,7 +25,8 @@ import torch
 
 from . import _lib
 
-__all__ = ["CSR", "DeviceZCSR", "Plan", "unfold", "apply", "gen_index", "lib", "SunError"]
+__all__ = ["CSR", "DeviceZCSR", "Plan", "unfold", "apply", "rk4", "expand_state", "state_diag", "gen_index", "lib",
+           "SunError"]
 
 
 class SunError(RuntimeError):
@@ -251,6 +252,41 @@ def unfold(H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), stream=
         return plan.run()
     finally:
         plan.close()
+
+
+def expand_state(rho, stream=None) -> torch.Tensor:
+    """v = Re Tr(F_s rho) (Eq. 5; sun_expand_state).  rho: DeviceZCSR or host CSR object."""
+    R = _to_device(rho)
+    s = _zcsr_struct(R)
+    v = torch.empty(R.n * R.n - 1, dtype=torch.float64, device=R.row_ptr.device)
+    _check(lib().sun_expand_state(ctypes.addressof(s), ctypes.c_void_p(v.data_ptr()),
+                                  ctypes.c_void_p(_stream_handle(stream))), "sun_expand_state")
+    return v
+
+
+def state_diag(v: torch.Tensor, n: int, stream=None) -> torch.Tensor:
+    """Populations <a|rho|a> of the state with coherence vector v (sun_state_diag)."""
+    assert v.is_cuda and v.dtype == torch.float64 and v.shape[0] == n * n - 1
+    d = torch.empty(n, dtype=torch.float64, device=v.device)
+    _check(lib().sun_state_diag(ctypes.c_void_p(v.data_ptr()), n, ctypes.c_void_p(d.data_ptr()),
+                                ctypes.c_void_p(_stream_handle(stream))), "sun_state_diag")
+    return d
+
+
+def rk4(Q0: CSR, Q1: Optional[CSR], K: Optional[torch.Tensor], v: torch.Tensor, h: float, nsteps: int,
+        t0: float = 0.0, eps0: float = 0.0, eps1: float = 0.0, omega: float = 1.0, work=None,
+        stream=None) -> torch.Tensor:
+    """Fixed-step RK4 of dv/dt = (Q0 + eps(t) Q1) v + K in place on v (sun_rk4, Step 3.1)."""
+    assert v.is_cuda and v.dtype == torch.float64 and v.shape[0] == Q0.m
+    w = work if work is not None else torch.empty(3 * Q0.m, dtype=torch.float64, device=v.device)
+    s0 = _dcsr_struct(Q0)
+    s1 = _dcsr_struct(Q1) if Q1 is not None else None
+    _check(lib().sun_rk4(ctypes.addressof(s0), ctypes.addressof(s1) if s1 is not None else None,
+                         ctypes.c_void_p(K.data_ptr()) if K is not None else None, ctypes.c_double(eps0),
+                         ctypes.c_double(eps1), ctypes.c_double(omega), ctypes.c_double(t0), ctypes.c_double(h),
+                         ctypes.c_int64(nsteps), ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                         ctypes.c_void_p(_stream_handle(stream))), "sun_rk4")
+    return v
 
 
 def apply(Q0: CSR, Q1: Optional[CSR], eps: float, K: Optional[torch.Tensor], v: torch.Tensor,

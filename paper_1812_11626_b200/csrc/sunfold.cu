@@ -1375,6 +1375,185 @@ __global__ void k_apply(long long m, const int64_t* __restrict__ rp0, const int3
   if (ok && sub == 0) y[row] = s0 + eps * s1 + (Kv ? Kv[row] : 0.0);
 }
 
+// ---------------------------------------------------------------------------------------
+// Propagation (F1) and states (F2)
+// ---------------------------------------------------------------------------------------
+// One RK4 stage: y = Q0 x + eps Q1 x + K with x = v + c kp (formed in the gather; kp = NULL:
+// x = v), 8 lanes per row (fixed-order reduction).  Epilogue by `mode`:
+//   0: kout = y, acc = y        1: kout = y, acc += 2 y        2: vout = v + h6 (acc + y)
+struct Rk4Stage {
+  const int64_t* rp0;
+  const int32_t* c0;
+  const double* v0;
+  const int64_t* rp1;
+  const int32_t* c1;
+  const double* v1;
+  const double* K;
+  const double* v;
+  const double* kp;
+  double* kout;
+  double* acc;
+  double* vout;
+  double eps, c, h6;
+  long long m;
+  int mode;
+};
+
+__global__ void __launch_bounds__(256) k_rk4_stage(const Rk4Stage S) {
+  const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3;
+  const int sub = threadIdx.x & 7;
+  const bool ok = row < S.m;
+  double s0 = 0.0, s1 = 0.0;
+  if (ok) {
+    const int64_t e0 = S.rp0[row + 1];
+    if (S.kp) {
+      for (int64_t k = S.rp0[row] + sub; k < e0; k += 8) {
+        const int j = S.c0[k];
+        s0 += S.v0[k] * (__ldg(&S.v[j]) + S.c * __ldg(&S.kp[j]));
+      }
+    } else {
+      for (int64_t k = S.rp0[row] + sub; k < e0; k += 8) s0 += S.v0[k] * __ldg(&S.v[S.c0[k]]);
+    }
+    if (S.rp1) {
+      const int64_t e1 = S.rp1[row + 1];
+      for (int64_t k = S.rp1[row] + sub; k < e1; k += 8) {
+        const int j = S.c1[k];
+        s1 += S.v1[k] * (S.kp ? __ldg(&S.v[j]) + S.c * __ldg(&S.kp[j]) : __ldg(&S.v[j]));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(FULL, s0, o);
+    s1 += __shfl_xor_sync(FULL, s1, o);
+  }
+  if (ok && sub == 0) {
+    const double y = s0 + S.eps * s1 + (S.K ? S.K[row] : 0.0);
+    if (S.mode == 0) {
+      S.kout[row] = y;
+      S.acc[row] = y;
+    } else if (S.mode == 1) {
+      S.kout[row] = y;
+      S.acc[row] += 2.0 * y;
+    } else {
+      S.vout[row] = S.v[row] + S.h6 * (S.acc[row] + y);
+    }
+  }
+}
+
+// v = Re Tr(F_s rho): S_ab / J_ab from the off-diagonal entries (two addends per coefficient,
+// added to zero: the result does not depend on their order), then the D^l chain from the
+// diagonal (one CTA, fixed-order scan).
+__global__ void k_state_zero(double* v, long long m) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < m; i += (long long)gridDim.x * blockDim.x)
+    v[i] = 0.0;
+}
+
+__global__ void k_state_offdiag(int n, const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                const double2* __restrict__ val, double* v) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const long long np = (long long)n * (n - 1) / 2;
+  const double is2 = 0.70710678118654752440;
+  for (int64_t k = rp[r]; k < rp[r + 1]; ++k) {
+    const int c = ci[k];
+    if (c == r) continue;
+    const double2 x = val[k];
+    const int a = r < c ? r : c, b = r < c ? c : r;
+    const long long p = (long long)a * (2LL * n - a - 1) / 2 + (b - a - 1);
+    // Tr(S_ab rho) = (rho_ab + rho_ba)/sqrt2;  Tr(J_ab rho) = i (rho_ab - rho_ba)/sqrt2
+    atomicAdd(&v[p], is2 * x.x);
+    atomicAdd(&v[np + p], r < c ? -is2 * x.y : is2 * x.y);
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_state_diag(int n, const int64_t* __restrict__ rp,
+                                                     const int32_t* __restrict__ ci,
+                                                     const double2* __restrict__ val, double* v) {
+  __shared__ double carry_s;
+  __shared__ double wsum[32];
+  const long long dbase = (long long)n * (n - 1) - 1;  // v index of D^l is N(N-1) + l - 1
+  if (threadIdx.x == 0) carry_s = 0.0;
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int c = base + threadIdx.x;
+    double d = 0.0;
+    if (c < n)
+      for (int64_t k = rp[c]; k < rp[c + 1]; ++k)
+        if (ci[k] == c) d = val[k].x;
+    // block inclusive scan of d (fixed order)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double x = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      double t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(FULL, t, o);
+        if (lane >= o) t += y;
+      }
+      wsum[lane] = t;
+    }
+    __syncthreads();
+    const double carry = carry_s;
+    const double incl = carry + (wid > 0 ? wsum[wid - 1] : 0.0) + x;
+    const double pre = incl - d;  // sum_{c' < c} rho_c'c'
+    if (c >= 1 && c < n) v[dbase + c] = (pre - (double)c * d) / sqrt((double)c * (double)(c + 1));
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry_s = incl;
+    __syncthreads();
+  }
+}
+
+// diag[a] = 1/N + sum_{l >= max(a,1)} v_{D^l} delta_l(a): delta_l(a) = 1/sqrt(l(l+1)) for
+// l > a, -a/sqrt(a(a+1)) for l = a.  Suffix sums by one CTA (fixed order).
+__global__ void __launch_bounds__(1024) k_state_pop(int n, const double* __restrict__ v, double* diag) {
+  __shared__ double carry_s;
+  __shared__ double wsum[32];
+  const long long dbase = (long long)n * (n - 1) - 1;
+  if (threadIdx.x == 0) carry_s = 0.0;
+  __syncthreads();
+  // process l from n-1 down in blocks: suffix[a] = sum_{l > a} v_l / sqrt(l(l+1))
+  for (int top = n - 1; top >= 0; top -= blockDim.x) {
+    const int a = top - (int)threadIdx.x;  // descending
+    double w = 0.0;                          // term of l = a + 1 (for the suffix over l > a)
+    if (a >= 0 && a + 1 <= n - 1) w = v[dbase + a + 1] / sqrt((double)(a + 1) * (double)(a + 2));
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    double x = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      double t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(FULL, t, o);
+        if (lane >= o) t += y;
+      }
+      wsum[lane] = t;
+    }
+    __syncthreads();
+    const double suf = carry_s + (wid > 0 ? wsum[wid - 1] : 0.0) + x;  // sum_{l > a}
+    if (a >= 0) {
+      const double self = a >= 1 ? -(double)a * v[dbase + a] / sqrt((double)a * (double)(a + 1)) : 0.0;
+      diag[a] = 1.0 / (double)n + suf + self;
+    }
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry_s = suf;
+    __syncthreads();
+  }
+}
+
 // =========================================================================================
 // Host side
 // =========================================================================================
@@ -2040,6 +2219,70 @@ int sun_plan_info(sun_plan pl, sun_plan_info_t* info) {
   info->npos_far_q1 = pl->has_h1 ? pl->npos_far[1] : 0;
   info->launches_count = pl->launches_count;
   info->launches_fill = pl->launches_fill;
+  return SUN_OK;
+}
+
+int sun_expand_state(const sun_zcsr* rho, double* v, void* stream) {
+  if (!rho || !v || !rho->row_ptr || (rho->nnz > 0 && (!rho->col || !rho->val))) return SUN_ERR_ARG;
+  const int n = rho->n;
+  if (n < 2 || n > 46340) return SUN_ERR_DIM;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long m = (long long)n * n - 1;
+  k_state_zero<<<296, 256, 0, st>>>(v, m);
+  CK(cudaGetLastError());
+  k_state_offdiag<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(n, rho->row_ptr, rho->col,
+                                                                (const double2*)rho->val, v);
+  CK(cudaGetLastError());
+  k_state_diag<<<1, 1024, 0, st>>>(n, rho->row_ptr, rho->col, (const double2*)rho->val, v);
+  CK(cudaGetLastError());
+  return SUN_OK;
+}
+
+int sun_state_diag(const double* v, int32_t n, double* diag, void* stream) {
+  if (!v || !diag) return SUN_ERR_ARG;
+  if (n < 2 || n > 46340) return SUN_ERR_DIM;
+  k_state_pop<<<1, 1024, 0, (cudaStream_t)stream>>>(n, v, diag);
+  CK(cudaGetLastError());
+  return SUN_OK;
+}
+
+int sun_rk4(const sun_dcsr* Q0, const sun_dcsr* Q1, const double* K, double eps0, double eps1, double omega,
+            double t0, double h, int64_t nsteps, double* v, double* work, void* stream) {
+  if (!Q0 || !Q0->row_ptr || !v || !work || nsteps < 0) return SUN_ERR_ARG;
+  if (Q0->nnz > 0 && (!Q0->col || !Q0->val)) return SUN_ERR_ARG;
+  if (Q1 && (Q1->m != Q0->m || !Q1->row_ptr || (Q1->nnz > 0 && (!Q1->col || !Q1->val)))) return SUN_ERR_ARG;
+  const long long m = Q0->m;
+  if (m <= 0) return SUN_ERR_DIM;
+  cudaStream_t st = (cudaStream_t)stream;
+  double* k = work;
+  double* acc = work + m;
+  double* vb = work + 2 * m;
+  double* cur = v;
+  double* nxt = vb;
+  Rk4Stage S;
+  S.rp0 = Q0->row_ptr; S.c0 = Q0->col; S.v0 = Q0->val;
+  S.rp1 = Q1 ? Q1->row_ptr : nullptr; S.c1 = Q1 ? Q1->col : nullptr; S.v1 = Q1 ? Q1->val : nullptr;
+  S.K = K; S.m = m; S.kout = k; S.acc = acc; S.h6 = h / 6.0;
+  const unsigned grid = (unsigned)((m * 8 + 255) / 256);
+  auto eps = [&](double t) { return eps0 + eps1 * sin(omega * t); };
+  for (int64_t i = 0; i < nsteps; ++i) {
+    const double t = t0 + (double)i * h;
+    S.v = cur;
+    S.vout = nxt;
+    S.kp = nullptr; S.c = 0.0; S.eps = eps(t); S.mode = 0;              // k1 = f(t, v)
+    k_rk4_stage<<<grid, 256, 0, st>>>(S);
+    S.kp = k; S.c = 0.5 * h; S.eps = eps(t + 0.5 * h); S.mode = 1;     // k2 = f(t + h/2, v + h/2 k1)
+    k_rk4_stage<<<grid, 256, 0, st>>>(S);
+    S.mode = 1;                                                         // k3 = f(t + h/2, v + h/2 k2)
+    k_rk4_stage<<<grid, 256, 0, st>>>(S);
+    S.c = h; S.eps = eps(t + h); S.mode = 2;                            // k4 = f(t + h, v + h k3); v'
+    k_rk4_stage<<<grid, 256, 0, st>>>(S);
+    CK(cudaGetLastError());
+    double* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+  }
+  if (cur != v) CK(cudaMemcpyAsync(v, cur, (size_t)m * sizeof(double), cudaMemcpyDeviceToDevice, st));
   return SUN_OK;
 }
 

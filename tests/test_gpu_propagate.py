@@ -1,0 +1,101 @@
+"""GPU parity of the propagation rows against oracle.propagate.
+
+F1: sun_rk4 (fixed-step RK4 of dv/dt = (Q0 + eps(t) Q1) v + K) vs RK4 on rho (Eq. 1) projected
+(small N), and vs RK4 on v with the oracle's O2 matrices (BASELINE sizes).  F2: sun_expand_state
+vs Tr(F_s rho); sun_state_diag vs diag(rho).  Tolerance: normwise 1e-12 of max|v| (RK4 adds
+O(steps) roundings of size 1e-16 |Q| |v| h)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+
+from oracle import basis, propagate, sparse
+from workloads import ZCSR, config, dimer_problem
+
+pytestmark = pytest.mark.gpu
+
+
+def _sun():
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    import paper_1812_11626_b200 as sun
+
+    return sun
+
+
+def _dense_random_rho(n, seed):
+    rng = np.random.default_rng(seed)
+    B = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    rho = B @ B.conj().T
+    return rho / np.trace(rho)
+
+
+def test_expand_state_and_populations():
+    sun = _sun()
+    for n, seed in ((2, 0), (6, 1), (33, 2)):
+        rho = _dense_random_rho(n, seed)
+        v = sun.expand_state(ZCSR.from_dense(rho)).cpu().numpy()
+        ref = basis.project(rho).real
+        assert np.abs(v - ref).max() <= 1e-14 * max(1.0, np.abs(ref).max())
+        d = sun.state_diag(torch.tensor(ref, device="cuda"), n).cpu().numpy()
+        assert np.abs(d - np.diag(rho).real).max() <= 1e-14
+    # the paper's initial state |0><0| at N = 1000
+    n = 1000
+    rho0 = ZCSR.from_triplets(n, [0], [0], [1.0])
+    v = sun.expand_state(rho0)
+    d = sun.state_diag(v, n).cpu().numpy()
+    assert abs(d[0] - 1.0) < 1e-13 and np.abs(d[1:]).max() < 1e-13
+
+
+def _csr_np(q, m):
+    return sp.csr_matrix((q["val"], q["col"], q["row_ptr"]), shape=(m, m))
+
+
+@pytest.mark.parametrize("n", [3, 8])
+def test_rk4_matches_rk4_on_rho(n):
+    sun = _sun()
+    prob = dimer_problem(n, True)
+    Q0, Q1, K = sun.unfold(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    rho0 = np.zeros((n, n), complex)
+    rho0[0, 0] = 1.0
+    v = sun.expand_state(ZCSR.from_dense(rho0))
+    h, steps, t0 = 0.05, 20, 0.3
+    sun.rk4(Q0, Q1, K, v, h, steps, t0=t0, eps0=1.0, eps1=1.5, omega=1.0)
+    rho = propagate.rk4_rho(prob.H0.to_dense(), prob.H1.to_dense(), [L.to_dense() for L in prob.Ls], prob.gammas,
+                            rho0, t0, h, steps, eps0=1.0, eps1=1.5, omega=1.0)
+    ref = basis.project(rho).real
+    assert np.abs(v.cpu().numpy() - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("idx", [2, 4])
+def test_rk4_matches_oracle_sparse_rk4_at_baseline_sizes(idx):
+    sun = _sun()
+    prob = config(idx)
+    Q0, Q1, K = sun.unfold(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    ref = sparse.unfold_problem(prob)
+    m = prob.m
+    rho0 = ZCSR.from_triplets(prob.n, [0], [0], [1.0])
+    v0 = sun.expand_state(rho0)
+    v = v0.clone()
+    # BASELINE's dissipator has no gamma/(N-1) prefactor (reading R9): |lambda|max ~ gamma N^2,
+    # so RK4 needs h |lambda| < 2.8; h = 1e-5 is stable at N <= 1000
+    h, steps = 1e-5, 3
+    sun.rk4(Q0, Q1, K, v, h, steps, eps0=1.0, eps1=1.5, omega=1.0)
+    vref = propagate.rk4_v(_csr_np(ref["Q0"], m), _csr_np(ref["Q1"], m), ref["Q0"]["K"], v0.cpu().numpy(), 0.0, h,
+                           steps, eps0=1.0, eps1=1.5, omega=1.0)
+    assert np.abs(v.cpu().numpy() - vref).max() <= 1e-12 * np.abs(vref).max()
+    # populations stay a probability distribution
+    d = sun.state_diag(v, prob.n).cpu().numpy()
+    assert abs(d.sum() - 1.0) < 1e-12
+
+
+def test_rk4_zero_steps_and_errors():
+    sun = _sun()
+    prob = dimer_problem(5, False)
+    Q0, Q1, K = sun.unfold(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    v = torch.arange(24, dtype=torch.float64, device="cuda")
+    w = v.clone()
+    sun.rk4(Q0, None, K, v, 0.1, 0)
+    assert torch.equal(v, w)
+    assert sun.lib().sun_rk4(None, None, None, 0.0, 0.0, 0.0, 0.0, 0.1, 1, None, None, None) == 1  # SUN_ERR_ARG
+    assert sun.lib().sun_state_diag(None, 5, None, None) == 1
