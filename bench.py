@@ -374,7 +374,7 @@ def main():
         from workloads import ZCSR as _Z
 
         v = sun.expand_state(_Z.from_triplets(prob.n, [0], [0], [1.0]))
-        work = torch.empty(3 * m, dtype=torch.float64, device="cuda")
+        work = torch.empty((int(sun.lib().sun_rk4_work_bytes(m)) + 7) // 8, dtype=torch.float64, device="cuda")
         h = 1e-5
         nst = 20
         sun.rk4(Q0, Q1, K, v, h, 2, eps0=1.0, eps1=1.5, omega=1.0, work=work)  # warm-up

@@ -173,11 +173,17 @@ int sun_state_diag(const double* v, int32_t n, double* diag, void* stream);
  *   k1 = f(t, v), k2 = f(t + h/2, v + h/2 k1), k3 = f(t + h/2, v + h/2 k2), k4 = f(t + h, v + h k3),
  *   v <- v + h/6 (k1 + 2 k2 + 2 k3 + k4).
  * One fused SpMV kernel per stage (the stage input v + c k is formed in the gather; the RK4
- * sum is accumulated in the epilogue).  Q1 may be NULL (no drive); K may be NULL (= 0).
- * v: device float64[M], in/out.  work: device float64[3 M] scratch owned by the caller.
- * Asynchronous on `stream`.  Errors: SUN_ERR_ARG, SUN_ERR_DIM, SUN_ERR_CUDA. */
+ * sum is accumulated in the epilogue; the stage vectors k are double-buffered).  Q1 may be NULL (no drive); K may be NULL (= 0).
+ * v: device float64[M], in/out.  work: device scratch of sun_rk4_work_bytes(M) bytes owned by
+ * the caller (8-byte aligned).  Rows of Q0 with more than 64 entries are processed by a warp
+ * each (their list is built at the start of the call: one 4-byte readback, i.e. the call
+ * synchronises once); all else is asynchronous on `stream`.
+ * Errors: SUN_ERR_ARG, SUN_ERR_DIM (M = 0 or M > 2^31 - 1), SUN_ERR_CUDA. */
 int sun_rk4(const sun_dcsr* Q0, const sun_dcsr* Q1, const double* K, double eps0, double eps1, double omega,
-            double t0, double h, int64_t nsteps, double* v, double* work, void* stream);
+            double t0, double h, int64_t nsteps, double* v, void* work, void* stream);
+
+/* Bytes of scratch sun_rk4 needs for an M-row system (4 M doubles + M + 2 ints); 0 if M <= 0. */
+size_t sun_rk4_work_bytes(int64_t m);
 
 /* Enable (1, the default) or disable (0) CUDA-graph replay of this plan's enqueue sequences.
  * With graphs, sun_count / sun_unfold / sun_run capture their launches once per distinct

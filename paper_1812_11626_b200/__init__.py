@@ -278,7 +278,9 @@ def rk4(Q0: CSR, Q1: Optional[CSR], K: Optional[torch.Tensor], v: torch.Tensor, 
         stream=None) -> torch.Tensor:
     """Fixed-step RK4 of dv/dt = (Q0 + eps(t) Q1) v + K in place on v (sun_rk4, Step 3.1)."""
     assert v.is_cuda and v.dtype == torch.float64 and v.shape[0] == Q0.m
-    w = work if work is not None else torch.empty(3 * Q0.m, dtype=torch.float64, device=v.device)
+    nb = int(lib().sun_rk4_work_bytes(Q0.m))
+    w = work if work is not None else torch.empty((nb + 7) // 8, dtype=torch.float64, device=v.device)
+    assert w.numel() * w.element_size() >= nb
     s0 = _dcsr_struct(Q0)
     s1 = _dcsr_struct(Q1) if Q1 is not None else None
     _check(lib().sun_rk4(ctypes.addressof(s0), ctypes.addressof(s1) if s1 is not None else None,

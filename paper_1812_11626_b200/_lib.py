@@ -49,6 +49,7 @@ SIGNATURES = {
     "sun_state_diag": (ctypes.c_int, [P, ctypes.c_int32, P, P]),
     "sun_rk4": (ctypes.c_int, [P, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                ctypes.c_double, ctypes.c_int64, P, P, P]),
+    "sun_rk4_work_bytes": (ctypes.c_size_t, [ctypes.c_int64]),
     "sun_plan_destroy": (None, [P]),
     "sun_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sun_gen_index": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),

@@ -1379,8 +1379,11 @@ __global__ void k_apply(long long m, const int64_t* __restrict__ rp0, const int3
 // Propagation (F1) and states (F2)
 // ---------------------------------------------------------------------------------------
 // One RK4 stage: y = Q0 x + eps Q1 x + K with x = v + c kp (formed in the gather; kp = NULL:
-// x = v), 8 lanes per row (fixed-order reduction).  Epilogue by `mode`:
+// x = v).  Rows of Q0 with at most RK4_LONG entries: one thread per row, entries in order,
+// four independent entries in flight per round; longer rows (the D-chain rows): one warp per
+// row from a list, fixed-order tree reduction.  Epilogue by `mode`:
 //   0: kout = y, acc = y        1: kout = y, acc += 2 y        2: vout = v + h6 (acc + y)
+constexpr int RK4_LONG = 64;
 struct Rk4Stage {
   const int64_t* rp0;
   const int32_t* c0;
@@ -1394,51 +1397,83 @@ struct Rk4Stage {
   double* kout;
   double* acc;
   double* vout;
+  const int* longrows;
   double eps, c, h6;
   long long m;
-  int mode;
+  int nlong, nshort_blocks, mode;
 };
 
-__global__ void __launch_bounds__(256) k_rk4_stage(const Rk4Stage S) {
-  const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 3;
-  const int sub = threadIdx.x & 7;
-  const bool ok = row < S.m;
-  double s0 = 0.0, s1 = 0.0;
-  if (ok) {
-    const int64_t e0 = S.rp0[row + 1];
-    if (S.kp) {
-      for (int64_t k = S.rp0[row] + sub; k < e0; k += 8) {
-        const int j = S.c0[k];
-        s0 += S.v0[k] * (__ldg(&S.v[j]) + S.c * __ldg(&S.kp[j]));
-      }
-    } else {
-      for (int64_t k = S.rp0[row] + sub; k < e0; k += 8) s0 += S.v0[k] * __ldg(&S.v[S.c0[k]]);
-    }
-    if (S.rp1) {
-      const int64_t e1 = S.rp1[row + 1];
-      for (int64_t k = S.rp1[row] + sub; k < e1; k += 8) {
-        const int j = S.c1[k];
-        s1 += S.v1[k] * (S.kp ? __ldg(&S.v[j]) + S.c * __ldg(&S.kp[j]) : __ldg(&S.v[j]));
-      }
-    }
+__device__ __forceinline__ double rk4_x(const Rk4Stage& S, int j) {
+  return S.kp ? __ldg(&S.v[j]) + S.c * __ldg(&S.kp[j]) : __ldg(&S.v[j]);
+}
+
+__device__ __forceinline__ void rk4_epilogue(const Rk4Stage& S, long long row, double y) {
+  if (S.mode == 0) {
+    S.kout[row] = y;
+    S.acc[row] = y;
+  } else if (S.mode == 1) {
+    S.kout[row] = y;
+    S.acc[row] += 2.0 * y;
+  } else {
+    S.vout[row] = S.v[row] + S.h6 * (S.acc[row] + y);
   }
+}
+
+__global__ void __launch_bounds__(256) k_rk4_stage(const Rk4Stage S) {
+  if ((int)blockIdx.x < S.nshort_blocks) {
+    const long long row = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= S.m) return;
+    const int64_t b0 = S.rp0[row], e0 = S.rp0[row + 1];
+    if (e0 - b0 > RK4_LONG) return;  // a warp of the long-row part does this row
+    double s0 = 0.0;
+    int64_t k = b0;
+    for (; k + 4 <= e0; k += 4) {
+      const int j0 = __ldg(&S.c0[k]), j1 = __ldg(&S.c0[k + 1]), j2 = __ldg(&S.c0[k + 2]), j3 = __ldg(&S.c0[k + 3]);
+      const double a0 = __ldg(&S.v0[k]), a1 = __ldg(&S.v0[k + 1]), a2 = __ldg(&S.v0[k + 2]), a3 = __ldg(&S.v0[k + 3]);
+      const double x0 = rk4_x(S, j0), x1 = rk4_x(S, j1), x2 = rk4_x(S, j2), x3 = rk4_x(S, j3);
+      s0 += a0 * x0;
+      s0 += a1 * x1;
+      s0 += a2 * x2;
+      s0 += a3 * x3;
+    }
+    for (; k < e0; ++k) s0 += __ldg(&S.v0[k]) * rk4_x(S, __ldg(&S.c0[k]));
+    double s1 = 0.0;
+    if (S.rp1)
+      for (int64_t q = S.rp1[row]; q < S.rp1[row + 1]; ++q) s1 += __ldg(&S.v1[q]) * rk4_x(S, __ldg(&S.c1[q]));
+    rk4_epilogue(S, row, s0 + S.eps * s1 + (S.K ? S.K[row] : 0.0));
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const long long w = (long long)(blockIdx.x - S.nshort_blocks) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (w >= S.nlong) return;  // warp-uniform
+  const long long row = S.longrows[w];
+  double s0 = 0.0, s1 = 0.0;
+  const int64_t e0 = S.rp0[row + 1];
+#pragma unroll 4
+  for (int64_t k = S.rp0[row] + lane; k < e0; k += 32) s0 += __ldg(&S.v0[k]) * rk4_x(S, __ldg(&S.c0[k]));
+  if (S.rp1)
+    for (int64_t q = S.rp1[row] + lane; q < S.rp1[row + 1]; q += 32) s1 += __ldg(&S.v1[q]) * rk4_x(S, __ldg(&S.c1[q]));
 #pragma unroll
-  for (int o = 4; o > 0; o >>= 1) {
+  for (int o = 16; o > 0; o >>= 1) {
     s0 += __shfl_xor_sync(FULL, s0, o);
     s1 += __shfl_xor_sync(FULL, s1, o);
   }
-  if (ok && sub == 0) {
-    const double y = s0 + S.eps * s1 + (S.K ? S.K[row] : 0.0);
-    if (S.mode == 0) {
-      S.kout[row] = y;
-      S.acc[row] = y;
-    } else if (S.mode == 1) {
-      S.kout[row] = y;
-      S.acc[row] += 2.0 * y;
-    } else {
-      S.vout[row] = S.v[row] + S.h6 * (S.acc[row] + y);
-    }
-  }
+  if (lane == 0) rk4_epilogue(S, row, s0 + S.eps * s1 + (S.K ? S.K[row] : 0.0));
+}
+
+// rows of Q0 longer than RK4_LONG, listed in ascending order (ballot compaction per warp and
+// an atomic per warp: the list order is fixed by the row order within each warp, the warps'
+// slots may vary, which does not change any row's result)
+__global__ void k_rk4_longrows(long long m, const int64_t* __restrict__ rp, int* list, int* count) {
+  const long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool lg = row < m && rp[row + 1] - rp[row] > RK4_LONG;
+  const unsigned bal = __ballot_sync(FULL, lg);
+  if (!bal) return;
+  const int lane = threadIdx.x & 31;
+  int base = 0;
+  if (lane == 0) base = atomicAdd(count, __popc(bal));
+  base = __shfl_sync(FULL, base, 0);
+  if (lg) list[base + __popc(bal & ((1u << lane) - 1u))] = (int)row;
 }
 
 // v = Re Tr(F_s rho): S_ab / J_ab from the off-diagonal entries (two addends per coefficient,
@@ -2246,36 +2281,56 @@ int sun_state_diag(const double* v, int32_t n, double* diag, void* stream) {
   return SUN_OK;
 }
 
+size_t sun_rk4_work_bytes(int64_t m) {
+  if (m <= 0) return 0;
+  return (size_t)(4 * m) * sizeof(double) + (size_t)(m + 2) * sizeof(int);
+}
+
 int sun_rk4(const sun_dcsr* Q0, const sun_dcsr* Q1, const double* K, double eps0, double eps1, double omega,
-            double t0, double h, int64_t nsteps, double* v, double* work, void* stream) {
+            double t0, double h, int64_t nsteps, double* v, void* work, void* stream) {
   if (!Q0 || !Q0->row_ptr || !v || !work || nsteps < 0) return SUN_ERR_ARG;
   if (Q0->nnz > 0 && (!Q0->col || !Q0->val)) return SUN_ERR_ARG;
   if (Q1 && (Q1->m != Q0->m || !Q1->row_ptr || (Q1->nnz > 0 && (!Q1->col || !Q1->val)))) return SUN_ERR_ARG;
   const long long m = Q0->m;
-  if (m <= 0) return SUN_ERR_DIM;
+  if (m <= 0 || m > 0x7fffffffLL) return SUN_ERR_DIM;
+  if (nsteps == 0) return SUN_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  double* k = work;
-  double* acc = work + m;
-  double* vb = work + 2 * m;
+  // stage vectors are double-buffered: a stage gathers k_{i-1} (other rows) while it writes k_i
+  double* kA = (double*)work;
+  double* kB = kA + m;
+  double* acc = kA + 2 * m;
+  double* vb = kA + 3 * m;
+  int* cntp = (int*)(vb + m);
+  int* list = cntp + 2;
+  // the long-row list of this Q0 (one small readback per call)
+  CK(cudaMemsetAsync(cntp, 0, sizeof(int), st));
+  k_rk4_longrows<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(m, Q0->row_ptr, list, cntp);
+  CK(cudaGetLastError());
+  int nlong = 0;
+  CK(cudaMemcpyAsync(&nlong, cntp, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
   double* cur = v;
   double* nxt = vb;
   Rk4Stage S;
   S.rp0 = Q0->row_ptr; S.c0 = Q0->col; S.v0 = Q0->val;
   S.rp1 = Q1 ? Q1->row_ptr : nullptr; S.c1 = Q1 ? Q1->col : nullptr; S.v1 = Q1 ? Q1->val : nullptr;
-  S.K = K; S.m = m; S.kout = k; S.acc = acc; S.h6 = h / 6.0;
-  const unsigned grid = (unsigned)((m * 8 + 255) / 256);
+  S.K = K; S.m = m; S.acc = acc; S.h6 = h / 6.0;
+  S.longrows = list;
+  S.nlong = nlong;
+  S.nshort_blocks = (int)((m + 255) / 256);
+  const unsigned grid = (unsigned)(S.nshort_blocks + (nlong + 7) / 8);
   auto eps = [&](double t) { return eps0 + eps1 * sin(omega * t); };
   for (int64_t i = 0; i < nsteps; ++i) {
     const double t = t0 + (double)i * h;
     S.v = cur;
     S.vout = nxt;
-    S.kp = nullptr; S.c = 0.0; S.eps = eps(t); S.mode = 0;              // k1 = f(t, v)
+    S.kp = nullptr; S.kout = kA; S.c = 0.0; S.eps = eps(t); S.mode = 0;        // k1 = f(t, v)
     k_rk4_stage<<<grid, 256, 0, st>>>(S);
-    S.kp = k; S.c = 0.5 * h; S.eps = eps(t + 0.5 * h); S.mode = 1;     // k2 = f(t + h/2, v + h/2 k1)
+    S.kp = kA; S.kout = kB; S.c = 0.5 * h; S.eps = eps(t + 0.5 * h); S.mode = 1;  // k2 = f(t + h/2, v + h/2 k1)
     k_rk4_stage<<<grid, 256, 0, st>>>(S);
-    S.mode = 1;                                                         // k3 = f(t + h/2, v + h/2 k2)
+    S.kp = kB; S.kout = kA; S.mode = 1;                                       // k3 = f(t + h/2, v + h/2 k2)
     k_rk4_stage<<<grid, 256, 0, st>>>(S);
-    S.c = h; S.eps = eps(t + h); S.mode = 2;                            // k4 = f(t + h, v + h k3); v'
+    S.kp = kA; S.kout = nullptr; S.c = h; S.eps = eps(t + h); S.mode = 2;     // k4 = f(t + h, v + h k3); v'
     k_rk4_stage<<<grid, 256, 0, st>>>(S);
     CK(cudaGetLastError());
     double* tmp = cur;
