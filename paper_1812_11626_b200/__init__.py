@@ -25,8 +25,8 @@ import torch
 
 from . import _lib
 
-__all__ = ["CSR", "DeviceZCSR", "Plan", "unfold", "apply", "rk4", "expand_state", "state_diag", "gen_index", "lib",
-           "SunError"]
+__all__ = ["CSR", "DeviceZCSR", "Plan", "unfold", "unfold_split", "apply", "rk4", "expand_state", "state_diag",
+           "gen_index", "lib", "SunError"]
 
 
 class SunError(RuntimeError):
@@ -252,6 +252,23 @@ def unfold(H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), stream=
         return plan.run()
     finally:
         plan.close()
+
+
+def unfold_split(H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), stream=None):
+    """The paper's split (Eq. 9): dv/dt = [Q(t) + R] v + K with Q = Q_H[H0] (Eq. 6)
+    and R, K from the dissipators (Eqs. 10-11), as separate CSR matrices.
+    Two unfolds through the same C-ABI: (H0, no dissipators) and (0, {L_p, gamma_p}); a trace of
+    L_p contributes its unitary part to R (reading R3).  Returns (QH, R, Q1 or None, K)."""
+    H0d = _to_device(H0)
+    zero = DeviceZCSR(H0d.n, torch.zeros(H0d.n + 1, dtype=torch.int64, device=H0d.row_ptr.device),
+                      torch.zeros(0, dtype=torch.int32, device=H0d.row_ptr.device),
+                      torch.zeros(0, dtype=torch.complex128, device=H0d.row_ptr.device))
+    QH, Q1, _ = unfold(H0d, H1, (), (), stream)
+    if len(Ls):
+        R, _, K = unfold(zero, None, Ls, gammas, stream)
+    else:
+        R, _, K = unfold(zero, None, (), (), stream)
+    return QH, R, Q1, K
 
 
 def expand_state(rho, stream=None) -> torch.Tensor:

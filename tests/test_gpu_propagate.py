@@ -108,3 +108,25 @@ def test_rk4_zero_steps_and_errors():
     assert torch.equal(v, w)
     assert sun.lib().sun_rk4(None, None, None, 0.0, 0.0, 0.0, 0.0, 0.1, 1, None, None, None) == 1  # SUN_ERR_ARG
     assert sun.lib().sun_state_diag(None, 5, None, None) == 1
+
+
+@pytest.mark.parametrize("idx", [0, 2, 3])
+def test_unfold_split_sums_to_q0(idx):
+    """F4: Q_H (Eq. 6) + R (Eq. 10) == Q0 as matrices; K identical; R = 0 without dissipators."""
+    sun = _sun()
+    prob = config(idx)
+    QH, R, Q1, K = sun.unfold_split(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    Q0, Q1b, K0 = sun.unfold(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    m = prob.m
+    tocsr = lambda q: sp.csr_matrix((q.val.cpu().numpy(), q.col.cpu().numpy(), q.row_ptr.cpu().numpy()), shape=(m, m))  # noqa
+    diff = (tocsr(QH) + tocsr(R) - tocsr(Q0)).toarray() if m < 5000 else None
+    scale = np.abs(Q0.val.cpu().numpy()).max()
+    if diff is not None:
+        assert np.abs(diff).max() <= 1e-12 * scale
+    else:
+        d = tocsr(QH) + tocsr(R) - tocsr(Q0)
+        assert (np.abs(d.data).max() if d.nnz else 0.0) <= 1e-12 * scale
+    assert np.abs(K.cpu().numpy() - K0.cpu().numpy()).max() <= 1e-12 * max(1.0, np.abs(K0.cpu().numpy()).max())
+    # Q_H is skew-symmetric (P:175)
+    A = tocsr(QH)
+    assert abs(A + A.T).max() <= 1e-12 * max(1.0, abs(A).max())
