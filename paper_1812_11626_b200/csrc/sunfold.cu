@@ -1140,15 +1140,15 @@ __global__ void __launch_bounds__(WARP_THREADS) k_count1(Prob pr, const FarPos* 
     if (p >= pr.np) break;
     int a, b;
     pair_decode(pr.n, p, a, b);
-    int c1, c2;
+    int c1, c2, nR = 0;
     if (b - a > 2 * pr.W) {
-      c1 = c2 = warp_far_pair<false>(pr, a, b, spos_dc, spos_dd, npos_far, none, 0, none, 0);
+      c1 = c2 = warp_far_pair<false>(pr, a, b, spos_dc, spos_dd, npos_far, none, 0, none, 0, &nR);
     } else {
       double k1, k2;
       warp_near_pair<false, 0, SW>(pr, a, b, scr[wid], c1, c2, k1, k2, none, 0, none, 0);
     }
     if (lane == 0) {
-      cnt[p] = c1;
+      cnt[p] = c1 | (nR << CNT_BITS);
       cnt[pr.np + p] = c2;
       cS += c1;
       cJ += c2;
@@ -1209,7 +1209,7 @@ __global__ void __launch_bounds__(WARP_THREADS) k_fill1(Prob pr, const FarPos* _
   const int i0 = threadIdx.x;
   const long long p0 = t * WARP_TP + i0;
   const bool valid = i0 < WARP_TP && p0 < np;
-  const int cS = valid ? cnt[p0] : 0, cJ = valid ? cnt[np + p0] : 0;
+  const int cS = valid ? (cnt[p0] & CNT_MASK) : 0, cJ = valid ? cnt[np + p0] : 0;
   int totS, totJ;
   const int exS = block_exclusive_scan(cS, wtot, totS);
   const int exJ = block_exclusive_scan(cJ, wtot, totJ);
@@ -1231,7 +1231,9 @@ __global__ void __launch_bounds__(WARP_THREADS) k_fill1(Prob pr, const FarPos* _
     pair_decode(pr.n, p, a, b);
     double k1 = 0.0, k2 = 0.0;
     if (b - a > 2 * pr.W) {
-      warp_far_pair<true>(pr, a, b, spos_dc, spos_dd, npos_far, sS, soffS[i], sJ, soffJ[i]);
+      const int w = cnt[p];  // row length and nR from the count pass: emit in one pass
+      warp_far_pair<true>(pr, a, b, spos_dc, spos_dd, npos_far, sS, soffS[i], sJ, soffJ[i], nullptr, w >> CNT_BITS,
+                          w & CNT_MASK);
     } else {
       int c1, c2;
       warp_near_pair<true, 0, SW>(pr, a, b, scr[wid], c1, c2, k1, k2, sS, soffS[i], sJ, soffJ[i]);

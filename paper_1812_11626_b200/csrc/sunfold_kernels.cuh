@@ -736,16 +736,27 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // Far pair, warp-cooperative (mode 1): lane k of each 32-chunk owns far position k
 // (pos_dc/pos_dd: offsets in lexicographic order).  Pass 1 counts; EMIT pass 2 writes.
 // ---------------------------------------------------------------------------------------
+// Count word of a mode-1 far pair's S row: bits 0-19 the row length, 20-31 nR (the kept Re
+// parts), so the fill pass emits in one pass.
+constexpr int CNT_BITS = 20;
+constexpr int CNT_MASK = (1 << CNT_BITS) - 1;
+
+// nR_known >= 0 (EMIT only): the kept counts are known (nR, total - nR): pass 1 is skipped.
 template <bool EMIT>
 __device__ __forceinline__ int warp_far_pair(const Prob& pr, int a, int b, const int* pos_dc, const int* pos_dd,
                                              int npos, const Seg& sS, long long offS, const Seg& sJ,
-                                             long long offJ) {
+                                             long long offJ, int* nR_out = nullptr, int nR_known = -1,
+                                             int total_known = 0) {
   const int lane = threadIdx.x & 31;
   const int n = pr.n;
   const int np = (int)pr.np;
   const double tau = pr.tau;
   const unsigned lt = (1u << lane) - 1u;
   int nR = 0, nI = 0;
+  if (EMIT && nR_known >= 0) {
+    nR = nR_known;
+    nI = total_known - nR_known;
+  } else
   for (int k0 = 0; k0 < npos; k0 += 32) {
     const int k = k0 + lane;
     bool okr = false, oki = false;
@@ -791,6 +802,7 @@ __device__ __forceinline__ int warp_far_pair(const Prob& pr, int a, int b, const
       iI += __popc(mi);
     }
   }
+  if (nR_out) *nR_out = nR;
   return nR + nI;
 }
 
