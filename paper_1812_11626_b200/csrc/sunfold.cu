@@ -1115,6 +1115,22 @@ __device__ __forceinline__ void count_d_tile(const Prob& pr, long long t, int* c
   if (threadIdx.x == 0) tsum[2 * pr.npt + u] = tot;
 }
 
+// FK >= 0: compile-time far path far_warp_pair<FK, FL, PT> (else the runtime position table)
+template <int FK, int FL, int PT>
+__device__ __forceinline__ int mode1_far(const Prob& pr, int a, int b, const int* pos_dc, const int* pos_dd, int npos,
+                                         const Seg& sS, long long offS, const Seg& sJ, long long offJ, int* nR_out,
+                                         int nR_known, int total_known, bool emit) {
+  if constexpr (FK >= 0) {
+    if (emit) return far_warp_pair<FK, FL, PT, true>(pr, a, b, sS, offS, sJ, offJ, nR_out);
+    return far_warp_pair<FK, FL, PT, false>(pr, a, b, sS, offS, sJ, offJ, nR_out);
+  } else {
+    if (emit)
+      return warp_far_pair<true>(pr, a, b, pos_dc, pos_dd, npos, sS, offS, sJ, offJ, nR_out, nR_known, total_known);
+    return warp_far_pair<false>(pr, a, b, pos_dc, pos_dd, npos, sS, offS, sJ, offJ, nR_out);
+  }
+}
+
+template <int FK, int FL, int PT>
 __global__ void __launch_bounds__(WARP_THREADS) k_count1(Prob pr, const FarPos* __restrict__ fp, int npos_far,
                                                          int* __restrict__ cnt, int* __restrict__ tsum) {
   pr.tau = *pr.tau_ptr;
@@ -1142,7 +1158,7 @@ __global__ void __launch_bounds__(WARP_THREADS) k_count1(Prob pr, const FarPos* 
     pair_decode(pr.n, p, a, b);
     int c1, c2, nR = 0;
     if (b - a > 2 * pr.W) {
-      c1 = c2 = warp_far_pair<false>(pr, a, b, spos_dc, spos_dd, npos_far, none, 0, none, 0, &nR);
+      c1 = c2 = mode1_far<FK, FL, PT>(pr, a, b, spos_dc, spos_dd, npos_far, none, 0, none, 0, &nR, -1, 0, false);
     } else {
       double k1, k2;
       warp_near_pair<false, 0, SW>(pr, a, b, scr[wid], c1, c2, k1, k2, none, 0, none, 0);
@@ -1185,6 +1201,7 @@ __device__ __forceinline__ void fill_d_tile(const Prob& pr, const FillOut& fo, l
   }
 }
 
+template <int FK, int FL, int PT>
 __global__ void __launch_bounds__(WARP_THREADS) k_fill1(Prob pr, const FarPos* __restrict__ fp, int npos_far,
                                                         const int* __restrict__ cnt, FillOut fo) {
   pr.tau = *pr.tau_ptr;
@@ -1232,8 +1249,8 @@ __global__ void __launch_bounds__(WARP_THREADS) k_fill1(Prob pr, const FarPos* _
     double k1 = 0.0, k2 = 0.0;
     if (b - a > 2 * pr.W) {
       const int w = cnt[p];  // row length and nR from the count pass: emit in one pass
-      warp_far_pair<true>(pr, a, b, spos_dc, spos_dd, npos_far, sS, soffS[i], sJ, soffJ[i], nullptr, w >> CNT_BITS,
-                          w & CNT_MASK);
+      mode1_far<FK, FL, PT>(pr, a, b, spos_dc, spos_dd, npos_far, sS, soffS[i], sJ, soffJ[i], nullptr, w >> CNT_BITS,
+                            w & CNT_MASK, true);
     } else {
       int c1, c2;
       warp_near_pair<true, 0, SW>(pr, a, b, scr[wid], c1, c2, k1, k2, sS, soffS[i], sJ, soffJ[i]);
@@ -1772,6 +1789,28 @@ cudaError_t dispatch_fill0(const MatFill& m0, const MatFill& m1, int q1w, long l
 
 long long nslots_of(const Prob& pr) { return 2 * pr.npt + pr.ndt; }
 
+// mode 1 (warp per pair): compile-time far path for the widths listed, else the runtime table
+template <int FK, int FL, int PT>
+cudaError_t launch_mode1_t(const Prob& pr, const FarPos* fp, int npos, int* cnt, int* ts, const FillOut* fo,
+                           cudaStream_t st) {
+  const unsigned grid = (unsigned)(pr.npt + pr.ndt);
+  if (!fo)
+    k_count1<FK, FL, PT><<<grid, WARP_THREADS, 0, st>>>(pr, fp, npos, cnt, ts);
+  else
+    k_fill1<FK, FL, PT><<<grid, WARP_THREADS, 0, st>>>(pr, fp, npos, cnt, *fo);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_mode1(const Prob& pr, const FarPos* fp, int npos, int* cnt, int* ts, const FillOut* fo,
+                         cudaStream_t st) {
+  const int pt = mode0_pt(pr.P);
+  if (pr.wK == 4 && pr.wL == 2) {
+    if (pt == 1) return launch_mode1_t<4, 2, 1>(pr, fp, npos, cnt, ts, fo, st);
+    if (pt == -1) return launch_mode1_t<4, 2, -1>(pr, fp, npos, cnt, ts, fo, st);
+  }
+  return launch_mode1_t<-1, 0, 0>(pr, fp, npos, cnt, ts, fo, st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -2023,9 +2062,7 @@ static int enqueue_count(sun_plan pl, cudaStream_t st) {
         CK(dispatch_count0(mc[which], mc[which], -1, s));
       } else {
         const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
-        k_count1<<<(unsigned)(pr.npt + pr.ndt), WARP_THREADS, 0, s>>>(pr, fp, pl->npos_far[which], mc[which].cnt,
-                                                                        mc[which].tsum);
-        CK(cudaGetLastError());
+        CK(launch_mode1(pr, fp, pl->npos_far[which], mc[which].cnt, mc[which].tsum, nullptr, s));
       }
     }
     if (pl->has_h1) CK(join_aux(pl, st, 1));
@@ -2088,9 +2125,7 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
       CK(dispatch_fill0(mf[which], mf[which], -1, pl->fill_grid[which], s));
     } else {
       const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
-      k_fill1<<<(unsigned)(pr.npt + pr.ndt), WARP_THREADS, 0, s>>>(pr, fp, pl->npos_far[which], mf[which].cnt,
-                                                                  mf[which].fo);
-      CK(cudaGetLastError());
+      CK(launch_mode1(pr, fp, pl->npos_far[which], const_cast<int*>(mf[which].cnt), nullptr, &mf[which].fo, s));
     }
   }
   if (pl->has_h1) CK(join_aux(pl, st, 1));

@@ -806,4 +806,101 @@ __device__ __forceinline__ int warp_far_pair(const Prob& pr, int a, int b, const
   return nR + nI;
 }
 
+// ---------------------------------------------------------------------------------------
+// Far pair, warp-cooperative with compile-time widths (mode 1 fast path for wide bands):
+// lane j owns far positions k = h 32 + j (h < NCH) of the fixed lexicographic list
+// (far_foreach order).  The values of both rounds stay in registers between the count and
+// the emit, so the fill emits in one pass.  PT: dissipators at compile time (0, 1), -1 runtime.
+// ---------------------------------------------------------------------------------------
+template <int WK, int WL>
+__device__ __forceinline__ void far_pos(int k, int& dc, int& dd) {
+  int idx = 0;
+  dc = 0;
+  dd = 0;
+#pragma unroll
+  for (int c = -WK; c <= WK; ++c) {
+    const int ac = c < 0 ? -c : c;
+    const int w = (c == 0) ? WK : (ac <= WL ? WL : 0);
+    if (k >= idx && k < idx + 2 * w + 1) {
+      dc = c;
+      dd = k - idx - w;
+    }
+    idx += 2 * w + 1;
+  }
+}
+
+template <int WK, int WL, int PT, bool EMIT>
+__device__ __forceinline__ int far_warp_pair(const Prob& pr, int a, int b, const Seg& sS, long long offS,
+                                             const Seg& sJ, long long offJ, int* nR_out = nullptr) {
+  constexpr int NPOS = FarT<WK, WL>::NPOS, NCH = (NPOS + 31) / 32;
+  constexpr int SK = 2 * WK + 1, SL = 2 * WL + 1;
+  const int lane = threadIdx.x & 31;
+  const int n = pr.n, np = (int)pr.np;
+  const double tau = pr.tau;
+  const unsigned lt = (1u << lane) - 1u;
+  double ux[NCH], uy[NCH];
+  unsigned mr[NCH], mi[NCH];
+  int qq[NCH];
+  int nR = 0, nI = 0;
+  const int P = PT < 0 ? pr.P : PT;
+#pragma unroll
+  for (int h = 0; h < NCH; ++h) {
+    const int k = h * 32 + lane;
+    int dc, dd;
+    far_pos<WK, WL>(k < NPOS ? k : 0, dc, dd);
+    const int c = a + dc, d = b + dd;
+    const bool ok = k < NPOS && c >= 0 && d < n;
+    double x = 0.0, y = 0.0;
+    if (ok) {
+      const int adc = dc < 0 ? -dc : dc, add = dd < 0 ? -dd : dd;
+      if (PT != 0 && adc <= WL && add <= WL) {
+        const double2* La = pr.L + (long long)a * SL + (dc + WL);
+        const double2* Lb = pr.L + (long long)b * SL + (dd + WL);
+        const long long ps = (long long)n * SL;
+        for (int p = 0; p < P; ++p) {
+          const double2 la = __ldg(La + p * ps), lb = __ldg(Lb + p * ps);
+          x += la.x * lb.x + la.y * lb.y;  // conj(Lt_p,ac) Lt_p,bd
+          y += la.x * lb.y - la.y * lb.x;
+        }
+      }
+      if (dd == 0) {  // + i K_ca
+        const double2 kv = __ldg(&pr.K.v[(long long)c * SK + (WK - dc)]);
+        x -= kv.y;
+        y += kv.x;
+      }
+      if (dc == 0) {  // - i conj(K_db)
+        const double2 kv = __ldg(&pr.K.v[(long long)d * SK + (WK - dd)]);
+        x -= kv.y;
+        y -= kv.x;
+      }
+    }
+    ux[h] = x;
+    uy[h] = y;
+    qq[h] = ok ? pidx32(n, c, d) : 0;
+    mr[h] = __ballot_sync(FULL, ok && fabs(x) > tau);
+    mi[h] = __ballot_sync(FULL, ok && fabs(y) > tau);
+    nR += __popc(mr[h]);
+    nI += __popc(mi[h]);
+  }
+  if (EMIT) {
+    int bR = 0, bI = 0;
+#pragma unroll
+    for (int h = 0; h < NCH; ++h) {
+      const int rR = bR + __popc(mr[h] & lt), rI = bI + __popc(mi[h] & lt);
+      if ((mr[h] >> lane) & 1u) {
+        sS.emit(offS + rR, qq[h], ux[h]);
+        sJ.emit(offJ + nI + rR, np + qq[h], ux[h]);
+      }
+      if ((mi[h] >> lane) & 1u) {
+        sS.emit(offS + nR + rI, np + qq[h], -uy[h]);
+        sJ.emit(offJ + rI, qq[h], uy[h]);
+      }
+      bR += __popc(mr[h]);
+      bI += __popc(mi[h]);
+    }
+  }
+  if (nR_out) *nR_out = nR;
+  return nR + nI;
+}
+
 }  // namespace sunk
