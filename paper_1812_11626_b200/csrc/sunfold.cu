@@ -505,6 +505,8 @@ struct Mode0 {
   static constexpr int TW = 2 * W + 1;
   static constexpr int SW = 2 * TW + 2;
   static constexpr int PER_WARP = Scr<TW, SW>::PER_WARP;
+  static constexpr int NW = 4 * W + 1;             // near window bound
+  static constexpr int SEG = NW * (NW - 1) / 2;    // side row segment stride (nc = NW^2)
 };
 
 // Pairs per tile: staging-free configurations (W = 0, rows of <= 2 entries) take 8 pairs per
@@ -576,10 +578,10 @@ __device__ __forceinline__ void count_near_item(const Prob& pr, long long item, 
     double k1, k2;
     TailInfo tS, tJ;
     const Seg sS = {side.col + r0, side.val + r0, side.nc}, sJ = {side.col + r1, side.val + r1, side.nc};
-    warp_near_pair<true, MC::TW, MC::SW, false>(pr, a, b, scr, c1, c2, k1, k2, sS, 0, sJ, 0, &tS, &tJ);
+    warp_near_pair<true, MC::TW, MC::SW, false, MC::SEG>(pr, a, b, scr, c1, c2, k1, k2, sS, 0, sJ, 0, &tS, &tJ);
     if (lane == 0) {
-      side.meta[2 * item] = NearMeta{tS.tr, k1, tS.nwin, tS.hi, tS.lend, 0};
-      side.meta[2 * item + 1] = NearMeta{tJ.tr, k2, tJ.nwin, tJ.hi, tJ.lend, 0};
+      side.meta[2 * item] = NearMeta{tS.tr, k1, tS.n1, tS.n2, tS.nwin - tS.n1 - tS.n2, tS.hi, tS.lend, 0};
+      side.meta[2 * item + 1] = NearMeta{tJ.tr, k2, tJ.n1, tJ.n2, tJ.nwin - tJ.n1 - tJ.n2, tJ.hi, tJ.lend, 0};
       const long long p = (long long)pidx32(pr.n, a, b);
       cnt[p] = c1;
       cnt[np + p] = c2;
@@ -590,9 +592,9 @@ __device__ __forceinline__ void count_near_item(const Prob& pr, long long item, 
     double kv;
     TailInfo t;
     const Seg sD = {side.col + r0, side.val + r0, side.nc};
-    const int c = warp_d_row<true, false>(pr, lam, scr, scr + WIN_MAX + 2, kv, sD, 0, &t);
+    const int c = warp_d_row<true, false, MC::SEG>(pr, lam, scr, scr + WIN_MAX + 2, kv, sD, 0, &t);
     if (lane == 0) {
-      side.meta[2 * item] = NearMeta{t.tr, kv, t.nwin, t.hi, t.lend, 0};
+      side.meta[2 * item] = NearMeta{t.tr, kv, t.n1, t.n2, t.nwin - t.n1 - t.n2, t.hi, t.lend, 0};
       cnt[2 * np + lam - 1] = c;
       tsum[2 * pr.npt + lam - 1] = c;
     }
@@ -708,17 +710,20 @@ __device__ __forceinline__ void warp_near_row_write(const NearSide& side, long l
   const long long lim = fo.cap - o;
   const int32_t* sc = side.col + srow * side.nc;
   const double* sv = side.val + srow * side.nc;
+  // window: segments [0, n1), [seg, seg + n2), [2 seg, 2 seg + nd) -> output [0, nwin)
+  const int nwin = m.n1 + m.n2 + m.nd, b2 = m.n1 + m.n2;
 #pragma unroll 3
-  for (int k = lane; k < m.nwin; k += 32) {
-    const int c = __ldg(&sc[k]);
-    const double v = __ldg(&sv[k]);
+  for (int k = lane; k < nwin; k += 32) {
+    const int sidx = k < m.n1 ? k : (k < b2 ? side.seg + (k - m.n1) : 2 * side.seg + (k - b2));
+    const int c = __ldg(&sc[sidx]);
+    const double v = __ldg(&sv[sidx]);
     if (k < lim) {
       fo.col[o + k] = c;
       fo.val[o + k] = v;
     }
   }
-  const long long ot = o + m.nwin;
-  const long long limt = lim - m.nwin;
+  const long long ot = o + nwin;
+  const long long limt = lim - nwin;
 #pragma unroll 4
   for (int l = m.hi + 1 + lane; l <= m.lend; l += 32) {
     const int k = l - m.hi - 1;
@@ -1697,7 +1702,8 @@ void setup_prob(sun_plan_s* pl, int which) {
   pr.mode = mode0_supported(pr.wK, pr.wL, pr.P) ? 0 : 1;
   pl->side[which] = NearSide{reinterpret_cast<int32_t*>(pl->ws + L.side_col[which]),
                              reinterpret_cast<double*>(pl->ws + L.side_val[which]),
-                             reinterpret_cast<NearMeta*>(pl->ws + L.side_meta[which]), (4 * pr.W + 1) * (4 * pr.W + 1)};
+                             reinterpret_cast<NearMeta*>(pl->ws + L.side_meta[which]), (4 * pr.W + 1) * (4 * pr.W + 1),
+                             (4 * pr.W + 1) * (4 * pr.W) / 2};
   if (pr.mode == 0) {
     // scan slot = fill tile of Tiling<WK, WL>::TP pairs (staging-free W = 0: 8 pairs per thread)
     pr.tp = pr.wK == 0 ? 2048 : TP0;

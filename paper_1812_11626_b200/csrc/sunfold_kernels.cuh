@@ -336,19 +336,25 @@ __device__ __forceinline__ void warp_prefix(const double* g, double* pre, int nw
 struct TailInfo {
   double tr;
   int nwin, hi, lend;
+  int n1, n2;  // split side rows (SEG > 0): entries of segments 1 and 2 (segment 3 = nwin - n1 - n2)
 };
 
 // Side buffer of the near rows (row 2i = S row / D row of near item i, 2i+1 = J row).
+// Side row slot of nc = NW^2 entries (NW = 4W + 1), three segments written in one pass:
+// [0, seg) the row's S_cd entries, [seg, 2 seg) its J_cd entries, [2 seg, ..) its D^l entries
+// inside the window; seg = NW (NW - 1) / 2.  The output row is seg 1, seg 2, seg 3, tail.
 struct NearMeta {
-  double tr, k;        // D-chain trace (tail value tr * inv[l]) and the row's K value
-  int nwin, hi, lend;  // window entries; tail l in (hi, lend]
+  double tr, k;     // D-chain trace (tail value tr * inv[l]) and the row's K value
+  int n1, n2, nd;   // entries of the three segments
+  int hi, lend;     // chain tail: l in (hi, lend]
   int pad;
 };
 struct NearSide {
   int32_t* col;  // [2 * items * nc]
   double* val;   // [2 * items * nc]
   NearMeta* meta;
-  int nc;        // entries per row slot: (4W + 1)^2 >= any row's window entries
+  int nc;        // entries per row slot: (4W + 1)^2
+  int seg;       // segment stride: (4W + 1) 4W / 2
 };
 
 
@@ -391,7 +397,8 @@ __device__ __forceinline__ int warp_dchain(const Prob& pr, int lo, int hi, const
 // scr: per-warp shared scratch: tile (TW*TW double2) | gS | gJ | pS | pJ (each SW doubles).
 // Returns the row lengths (cS, cJ) and K values (kS, kJ); with EMIT writes the rows.
 // ---------------------------------------------------------------------------------------
-template <bool EMIT, int TW, int SW, bool TAIL = true>
+// SEG > 0 (with EMIT): split side rows, one pass (segments at offS, offS + SEG, offS + 2 SEG).
+template <bool EMIT, int TW, int SW, bool TAIL = true, int SEG = 0>
 __device__ __forceinline__ void warp_near_pair(const Prob& pr, int a, int b, double* scr, int& cS, int& cJ, double& kS,
                                             double& kJ, Seg sS, long long offS, Seg sJ, long long offJ,
                                             TailInfo* tS = nullptr, TailInfo* tJ = nullptr) {
@@ -425,6 +432,8 @@ __device__ __forceinline__ void warp_near_pair(const Prob& pr, int a, int b, dou
     }
   };
   int n1S = 0, n2S = 0, n1J = 0, n2J = 0;
+  constexpr bool SPLIT = EMIT && SEG > 0;
+  if (!SPLIT)
   for (int k0 = 0; k0 < npos; k0 += 32) {
     const int k = k0 + lane;
     double v1S = 0, v2S = 0, v1J = 0, v2J = 0;
@@ -443,6 +452,8 @@ __device__ __forceinline__ void warp_near_pair(const Prob& pr, int a, int b, dou
     n2J += __popc(__ballot_sync(FULL, fabs(v2J) > tau));
   }
   if (EMIT) {
+    // second halves: after the first (counted above) or at the fixed segment SEG (one pass)
+    const long long o2S = SPLIT ? offS + SEG : offS + n1S, o2J = SPLIT ? offJ + SEG : offJ + n1J;
     int i1S = 0, i2S = 0, i1J = 0, i2J = 0;
     for (int k0 = 0; k0 < npos; k0 += 32) {
       const int k = k0 + lane;
@@ -464,14 +475,20 @@ __device__ __forceinline__ void warp_near_pair(const Prob& pr, int a, int b, dou
       if (kp) sS.emit(offS + i1S + __popc(m & lt), q, v1S);
       i1S += __popc(m);
       kp = fabs(v2S) > tau; m = __ballot_sync(FULL, kp);
-      if (kp) sS.emit(offS + n1S + i2S + __popc(m & lt), np + q, v2S);
+      if (kp) sS.emit(o2S + i2S + __popc(m & lt), np + q, v2S);
       i2S += __popc(m);
       kp = fabs(v1J) > tau; m = __ballot_sync(FULL, kp);
       if (kp) sJ.emit(offJ + i1J + __popc(m & lt), q, v1J);
       i1J += __popc(m);
       kp = fabs(v2J) > tau; m = __ballot_sync(FULL, kp);
-      if (kp) sJ.emit(offJ + n1J + i2J + __popc(m & lt), np + q, v2J);
+      if (kp) sJ.emit(o2J + i2J + __popc(m & lt), np + q, v2J);
       i2J += __popc(m);
+    }
+    if (SPLIT) {
+      n1S = i1S;
+      n2S = i2S;
+      n1J = i1J;
+      n2J = i2J;
     }
   }
   const double s2 = 1.4142135623730951;
@@ -483,8 +500,18 @@ __device__ __forceinline__ void warp_near_pair(const Prob& pr, int a, int b, dou
   __syncwarp();
   warp_prefix(gS, pS, nw);
   warp_prefix(gJ, pJ, nw);
-  const int chS = warp_dchain<EMIT, TAIL>(pr, lo, hi, gS, pS, sS, offS + n1S + n2S, n1S + n2S, tS);
-  const int chJ = warp_dchain<EMIT, TAIL>(pr, lo, hi, gJ, pJ, sJ, offJ + n1J + n2J, n1J + n2J, tJ);
+  const int chS = warp_dchain<EMIT, TAIL>(pr, lo, hi, gS, pS, sS, SPLIT ? offS + 2 * SEG : offS + n1S + n2S,
+                                          n1S + n2S, tS);
+  const int chJ = warp_dchain<EMIT, TAIL>(pr, lo, hi, gJ, pJ, sJ, SPLIT ? offJ + 2 * SEG : offJ + n1J + n2J,
+                                          n1J + n2J, tJ);
+  if (tS) {
+    tS->n1 = n1S;
+    tS->n2 = n2S;
+  }
+  if (tJ) {
+    tJ->n1 = n1J;
+    tJ->n2 = n2J;
+  }
   cS = n1S + n2S + chS;
   cJ = n1J + n2J + chJ;
   kS = pS[nw] / (double)n;
@@ -495,7 +522,7 @@ __device__ __forceinline__ void warp_near_pair(const Prob& pr, int a, int b, dou
 // ---------------------------------------------------------------------------------------
 // D^lam row, warp-cooperative.
 // ---------------------------------------------------------------------------------------
-template <bool EMIT, bool TAIL = true>
+template <bool EMIT, bool TAIL = true, int SEG = 0>
 __device__ __forceinline__ int warp_d_row(const Prob& pr, int lam, double* g, double* pre, double& kval, Seg seg,
                                        long long off, TailInfo* ti = nullptr) {
   const int lane = threadIdx.x & 31;
@@ -510,6 +537,8 @@ __device__ __forceinline__ int warp_d_row(const Prob& pr, int lam, double* g, do
   const unsigned lt = (1u << lane) - 1u;
   const double s2 = 1.4142135623730951;
   int nS = 0, nJ = 0;
+  constexpr bool SPLIT = EMIT && SEG > 0;
+  if (!SPLIT)
   for (int k0 = 0; k0 < npos; k0 += 32) {
     const int k = k0 + lane;
     double vS = 0, vJ = 0;
@@ -524,6 +553,7 @@ __device__ __forceinline__ int warp_d_row(const Prob& pr, int lam, double* g, do
     nJ += __popc(__ballot_sync(FULL, fabs(vJ) > tau));
   }
   if (EMIT) {
+    const long long o2 = SPLIT ? off + SEG : off + nS;
     int iS = 0, iJ = 0;
     for (int k0 = 0; k0 < npos; k0 += 32) {
       const int k = k0 + lane;
@@ -543,14 +573,22 @@ __device__ __forceinline__ int warp_d_row(const Prob& pr, int lam, double* g, do
       iS += __popc(m);
       kp = fabs(vJ) > tau;
       m = __ballot_sync(FULL, kp);
-      if (kp) seg.emit(off + nS + iJ + __popc(m & lt), np + q, vJ);
+      if (kp) seg.emit(o2 + iJ + __popc(m & lt), np + q, vJ);
       iJ += __popc(m);
+    }
+    if (SPLIT) {
+      nS = iS;
+      nJ = iJ;
     }
   }
   for (int i = lane; i < nw; i += 32) g[i] = G_elem(pr, lam, alpha, lo + i, lo + i).x;
   __syncwarp();
   warp_prefix(g, pre, nw);
-  const int ch = warp_dchain<EMIT, TAIL>(pr, lo, hi, g, pre, seg, off + nS + nJ, nS + nJ, ti);
+  const int ch = warp_dchain<EMIT, TAIL>(pr, lo, hi, g, pre, seg, SPLIT ? off + 2 * SEG : off + nS + nJ, nS + nJ, ti);
+  if (ti) {
+    ti->n1 = nS;
+    ti->n2 = nJ;
+  }
   kval = pre[nw] / (double)n;
   __syncwarp();
   return nS + nJ + ch;
