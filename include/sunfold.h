@@ -92,7 +92,8 @@ typedef struct {
   int32_t n, P;
   int32_t w_h0, w_h1, w_l, w_k; /* half-bandwidths: H0, H1, max_p L_p, K = H0 + i/2 sum gamma L^+L */
   double tau_q0, tau_q1;        /* drop thresholds (R6) */
-  int32_t mode_q0, mode_q1;     /* 0: group-per-pair kernels, compile-time widths; 1: warp-per-pair */
+  int32_t mode_q0, mode_q1;     /* 0: thread-per-pair far tiles (compile-time widths); 1: warp-per-pair,
+                                   runtime widths; 2: warp-per-pair far path, compile-time widths */
   int32_t pairs_per_tile_q0, pairs_per_tile_q1;
   int64_t tiles_q0, tiles_q1;   /* scan slots (S tiles, J tiles, D slots) */
   int32_t has_h1;

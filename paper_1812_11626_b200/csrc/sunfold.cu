@@ -134,8 +134,9 @@ Layout make_layout(int n, int P) {
   L.cnt0 = off; off = align256(off + (size_t)m * sizeof(int));
   L.cnt1 = off; off = align256(off + (size_t)m * sizeof(int));
   // near-row side buffers of mode 0 (W <= 3): 2 rows per near item, (4W + 1)^2 entries per row
-  const long long side_rows = 2 * ((long long)n * 2 * 3 + n);
-  const long long ncmax = 13 * 13;
+  // near-row side buffers of modes 0 and 2 (W <= 4): 2 rows per near item, (4W + 1)^2 entries
+  const long long side_rows = 2 * ((long long)n * 2 * 4 + n);
+  const long long ncmax = 17 * 17;
   for (int k = 0; k < 2; ++k) {
     L.side_col[k] = off; off = align256(off + (size_t)(side_rows * ncmax) * sizeof(int32_t));
     L.side_val[k] = off; off = align256(off + (size_t)(side_rows * ncmax) * sizeof(double));
@@ -751,7 +752,7 @@ __device__ __forceinline__ void fill_near_unit(const Prob& pr, long long j, cons
     const long long tb = p / pr.tp, ts = tb * pr.tp;
     const int* c = cnt + (half ? np : 0);
     int s1 = 0;
-    for (long long q = ts + lane; q < p; q += 32) s1 += __ldg(&c[q]);
+    for (long long q = ts + lane; q < p; q += 32) s1 += __ldg(&c[q]) & CNT_MASK;  // mode 2 packs nR above
 #pragma unroll
     for (int sh = 16; sh > 0; sh >>= 1) s1 += __shfl_xor_sync(FULL, s1, sh);
     o = fo.toff[(half ? pr.npt : 0) + tb] + s1;
@@ -1096,6 +1097,114 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
     }
   }
   if (!FF::DIRECT && lane == 0) bulk_wait0();  // staging must outlive the bulk reads
+}
+
+// ---------------------------------------------------------------------------------------
+// Mode 2 (compile-time widths, many far positions: e.g. (wK, wL) = (4, 2), NPOS = 33): mode
+// 0's structure (single-warp count CTAs with the near side buffer; a persistent fill with near
+// units) with the warp-per-pair far path far_warp_pair (rows of ~70 entries are stored
+// coalesced by the warp; no staging).  Scan slot = fill tile of TP0 pairs = 8 count warps.
+// ---------------------------------------------------------------------------------------
+template <int WK, int WL, int PT>
+__global__ void __launch_bounds__(32) k_count2(const MatCount mc) {
+  using MC = Mode0<WK, WL>;
+  __shared__ double scr[MC::PER_WARP];
+  const Prob& p0 = mc.pr;
+  long long u = blockIdx.x;
+  Prob pr = p0;
+  pr.tau = *p0.tau_ptr;
+  if (u < p0.nb_near) {
+    count_near_item<WK, WL>(pr, u, scr, mc.cnt, mc.tsum, mc.side);
+    return;
+  }
+  u -= p0.nb_near;  // far warp u: pairs [32 u, 32 u + 32), one after the other
+  const int lane = threadIdx.x & 31;
+  const long long np = pr.np;
+  const Seg none = {nullptr, nullptr, 0};
+  long long pw = u * 32;
+  int a = 0, b = 1;
+  if (pw < np) pair_decode(pr.n, pw, a, b);
+  int tot = 0;
+  for (int j = 0; j < 32 && pw + j < np; ++j) {
+    if (j) {
+      if (++b == pr.n) {
+        ++a;
+        b = a + 1;
+      }
+    }
+    if (b - a > 2 * MC::W) {
+      int nR;
+      const int c = far_warp_pair<WK, WL, PT, false>(pr, a, b, none, 0, none, 0, &nR);
+      if (lane == 0) {
+        mc.cnt[pw + j] = c | (nR << CNT_BITS);
+        mc.cnt[np + pw + j] = c;
+      }
+      tot += c;
+    }
+  }
+  if (lane == 0 && tot) {
+    atomicAdd(&mc.tsum[pw / TP0], tot);
+    atomicAdd(&mc.tsum[pr.npt + pw / TP0], tot);
+  }
+}
+
+template <int WK, int WL, int PT>
+__device__ __forceinline__ void fill2_far_tile(const Prob& pr, long long t, const int* __restrict__ cnt,
+                                               const FillOut& fo, int2* wtot, int* soff) {
+  using MC = Mode0<WK, WL>;
+  const int wid = threadIdx.x >> 5;
+  const long long np = pr.np;
+  const long long p = t * TP0 + threadIdx.x;
+  const bool valid = p < np;
+  const int w = valid ? cnt[p] : 0;
+  const int cS = w & CNT_MASK, cJ = valid ? cnt[np + p] : 0;
+  __syncthreads();  // soff / wtot of the previous unit consumed
+  int2 tot2;
+  const int2 ex2 = block_exclusive_scan2(cS, cJ, wtot, tot2);
+  const long long baseS = fo.toff[t], baseJ = fo.toff[pr.npt + t];
+  int a, b;
+  warp_pairs(pr.n, t * TP0 + wid * 32, a, b);
+  const bool far = valid && (b - a > 2 * MC::W);
+  if (valid) {
+    fo.row_ptr[p] = baseS + ex2.x;
+    fo.row_ptr[np + p] = baseJ + ex2.y;
+    if (fo.K && far) {
+      fo.K[p] = 0.0;
+      fo.K[np + p] = 0.0;
+    }
+  }
+  soff[2 * threadIdx.x] = ex2.x;
+  soff[2 * threadIdx.x + 1] = ex2.y;
+  __syncwarp();
+  const Seg seg = {fo.col, fo.val, fo.cap};
+  // the warp's 32 pairs, one after the other (lane-parallel positions)
+  const unsigned farmask = __ballot_sync(FULL, far);
+  for (int j = 0; j < 32; ++j) {
+    if (!((farmask >> j) & 1u)) continue;  // warp-uniform
+    const int aj = __shfl_sync(FULL, a, j), bj = __shfl_sync(FULL, b, j);
+    const int i = wid * 32 + j;
+    far_warp_pair<WK, WL, PT, true>(pr, aj, bj, seg, baseS + soff[2 * i], seg, baseJ + soff[2 * i + 1]);
+  }
+}
+
+template <int WK, int WL, int PT>
+__global__ void __launch_bounds__(256) k_fill2(const MatFill mf) {
+  __shared__ int2 wtot[8];
+  __shared__ int soff[2 * TP0];
+  const Prob& p0 = mf.pr;
+  if (blockIdx.x == 0 && threadIdx.x == 0) mf.fo.row_ptr[p0.m] = *mf.fo.nnz;
+  Prob pr = p0;
+  pr.tau = *p0.tau_ptr;
+  const long long nn = (2 * (p0.n * 2LL * p0.W + p0.n - 1) + 7) / 8;  // near units (8 side rows)
+  const long long nt = p0.npt, U = nt + nn;
+  for (long long u = blockIdx.x; u < U; u += gridDim.x) {  // block-uniform
+    long long idx;
+    if (unit_decode(u, U, nn, idx)) {
+      fill_near_unit(pr, idx, mf.cnt, mf.fo, mf.side);
+    } else {
+      fill2_far_tile<WK, WL, PT>(pr, nt - 1 - idx, mf.cnt, mf.fo, wtot, soff);
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1666,6 +1775,41 @@ bool mode0_supported(int wK, int wL, int P) {
   return false;
 }
 
+// ---- mode-2 instantiations (compile-time warp-per-pair far path) ----
+bool mode2_supported(int wK, int wL, int P) { return wK == 4 && wL == 2 && P >= 1; }
+
+template <int WK, int WL, int PT>
+cudaError_t launch2_t(const Prob& pr, const MatCount* mc, const MatFill* mf, long long* grid_out, long long grid,
+                      cudaStream_t st) {
+  if (grid_out) {  // plan creation: persistent fill grid
+    int dev = 0, sms = 0, nb = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fill2<WK, WL, PT>, 256, 0);
+    if (e != cudaSuccess) return e;
+    const long long U = pr.npt + (2 * (pr.n * 2LL * pr.W + pr.n - 1) + 7) / 8;
+    *grid_out = (long long)(nb > 0 ? nb : 1) * sms;
+    if (*grid_out > U) *grid_out = U;
+    return cudaSuccess;
+  }
+  if (mc) {
+    const long long U = pr.nb_near + (pr.np + 31) / 32;
+    k_count2<WK, WL, PT><<<(unsigned)U, 32, 0, st>>>(*mc);
+  } else {
+    k_fill2<WK, WL, PT><<<(unsigned)grid, 256, 0, st>>>(*mf);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch2(const Prob& pr, const MatCount* mc, const MatFill* mf, long long* grid_out, long long grid,
+                    cudaStream_t st) {
+  if (pr.wK == 4 && pr.wL == 2) {
+    if (pr.P == 1) return launch2_t<4, 2, 1>(pr, mc, mf, grid_out, grid, st);
+    return launch2_t<4, 2, -1>(pr, mc, mf, grid_out, grid, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
 void setup_prob(sun_plan_s* pl, int which) {
   Prob& pr = pl->pr[which];
   const Layout& L = pl->lay;
@@ -1699,12 +1843,17 @@ void setup_prob(sun_plan_s* pl, int which) {
     pl->hfp[which].dc[i] = pl->pos_dc[which][i];
     pl->hfp[which].dd[i] = pl->pos_dd[which][i];
   }
-  pr.mode = mode0_supported(pr.wK, pr.wL, pr.P) ? 0 : 1;
+  pr.mode = mode0_supported(pr.wK, pr.wL, pr.P) ? 0 : (mode2_supported(pr.wK, pr.wL, pr.P) ? 2 : 1);
   pl->side[which] = NearSide{reinterpret_cast<int32_t*>(pl->ws + L.side_col[which]),
                              reinterpret_cast<double*>(pl->ws + L.side_val[which]),
                              reinterpret_cast<NearMeta*>(pl->ws + L.side_meta[which]), (4 * pr.W + 1) * (4 * pr.W + 1),
                              (4 * pr.W + 1) * (4 * pr.W) / 2};
-  if (pr.mode == 0) {
+  if (pr.mode == 2) {
+    pr.tp = TP0;
+    pr.npt = (pr.np + TP0 - 1) / TP0;
+    pr.ndt = pl->n - 1;
+    pr.nb_near = (long long)pl->n * 2 * pr.W + (pl->n - 1);
+  } else if (pr.mode == 0) {
     // scan slot = fill tile of Tiling<WK, WL>::TP pairs (staging-free W = 0: 8 pairs per thread)
     pr.tp = pr.wK == 0 ? 2048 : TP0;
     pr.npt = (pr.np + pr.tp - 1) / pr.tp;
@@ -1974,8 +2123,10 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
     if (pl->combined) {
       e1 = dispatch_attr0(pl->pr[0], pl->has_h1 ? &pl->pr[1] : nullptr, pl->has_h1 ? 0 : -1, pl->fill_grid[0]);
     } else {
-      for (int which = 0; which < nmat && e1 == cudaSuccess; ++which)
+      for (int which = 0; which < nmat && e1 == cudaSuccess; ++which) {
         if (pl->pr[which].mode == 0) e1 = dispatch_attr0(pl->pr[which], nullptr, -1, pl->fill_grid[which]);
+        if (pl->pr[which].mode == 2) e1 = launch2(pl->pr[which], nullptr, nullptr, &pl->fill_grid[which], 0, nullptr);
+      }
     }
     if (e1 != cudaSuccess) {
       delete pl;
@@ -2066,6 +2217,8 @@ static int enqueue_count(sun_plan pl, cudaStream_t st) {
       cudaStream_t s = which ? pl->aux[0] : st;
       if (pr.mode == 0) {
         CK(dispatch_count0(mc[which], mc[which], -1, s));
+      } else if (pr.mode == 2) {
+        CK(launch2(pr, &mc[which], nullptr, nullptr, 0, s));
       } else {
         const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
         CK(launch_mode1(pr, fp, pl->npos_far[which], mc[which].cnt, mc[which].tsum, nullptr, s));
@@ -2129,6 +2282,8 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
     cudaStream_t s = which ? pl->aux[0] : st;
     if (pr.mode == 0) {
       CK(dispatch_fill0(mf[which], mf[which], -1, pl->fill_grid[which], s));
+    } else if (pr.mode == 2) {
+      CK(launch2(pr, nullptr, &mf[which], nullptr, pl->fill_grid[which], s));
     } else {
       const FarPos* fp = (const FarPos*)(ws + (which ? L.fp1 : L.fp0));
       CK(launch_mode1(pr, fp, pl->npos_far[which], const_cast<int*>(mf[which].cnt), nullptr, &mf[which].fo, s));
