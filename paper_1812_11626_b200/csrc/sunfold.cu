@@ -34,8 +34,8 @@ namespace {
 constexpr int MAXOPS = 66;       // H0, H1 and up to 64 dissipators
 constexpr int WLMAX = WMAX / 2;  // wK >= 2 wL
 constexpr int F_MALFORMED = 1, F_PATTERN = 8;
-constexpr int TP0 = 256;          // mode 0: pairs per fill tile (scan slot) == threads per fill CTA
-constexpr int SLOTS_PER_TILE = 8;  // mode 0: count warps (single-warp CTAs) per fill tile
+constexpr int TP0 = 256;          // modes 0/2: pairs per fill tile == threads per fill CTA
+constexpr int SLOTS_PER_TILE = 8;  // modes 0/2: scan slots (one per count warp and per fill warp) per fill tile
 constexpr int WARP_TP = 64;       // mode 1: pairs per tile
 constexpr int WARP_THREADS = 256;
 constexpr int FAR_MAXPOS = 1024;
@@ -111,7 +111,7 @@ Layout make_layout(int n, int P) {
   long long m = (long long)n * n - 1;
   long long np = (long long)n * (n - 1) / 2;
   // slots: S tiles + J tiles + D slots
-  long long maxslots = 2 * (np / WARP_TP + 2) + n + 2;  // smallest slot: mode 1's 64-pair tile
+  long long maxslots = 2 * (np / 32 + 2) + n + 2;  // smallest slot: 32 pairs (modes 0 and 2)
   long long maxchunks = (maxslots + SCAN_TILE - 1) / SCAN_TILE + 1;
   long long nrb = (n + EXP_THREADS - 1) / EXP_THREADS;
   size_t off = 0;
@@ -631,9 +631,9 @@ __device__ __forceinline__ void count_far_slot(const FarCtx& pr, long long npt, 
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
-  if (lane == 0 && c) {  // into the scan slot (fill tile) of this count warp
-    atomicAdd(&tsum[s / SLOTS_PER_TILE], c);  // S rows and J rows of a far pair have the same length
-    atomicAdd(&tsum[npt + s / SLOTS_PER_TILE], c);
+  if (lane == 0 && c) {  // into this count warp's scan slot (near items of the slot add theirs)
+    atomicAdd(&tsum[s], c);  // S rows and J rows of a far pair have the same length
+    atomicAdd(&tsum[npt + s], c);
   }
 }
 
@@ -672,7 +672,7 @@ __global__ void __launch_bounds__(32) k_count0(const MatCount m0, const MatCount
     return;
   }
   u -= nn1;
-  const long long nw0 = (m0.pr.np + m0.pr.tp / SLOTS_PER_TILE - 1) / (m0.pr.tp / SLOTS_PER_TILE);
+  const long long nw0 = m0.pr.npt;  // one count warp per scan slot
   if (u < nw0) {
     const FarCtx prf{m0.pr.K.v, m0.pr.L, *m0.pr.tau_ptr, m0.pr.np, m0.pr.n, m0.pr.P};
     count_far_slot<WK, WL, PT>(prf, m0.pr.npt, u, m0.cnt, m0.tsum);
@@ -826,17 +826,18 @@ struct TileIn {
 __device__ __forceinline__ TileIn load_tile_in(long long np, long long npt, long long t, const int* __restrict__ cnt,
                                                const long long* __restrict__ toff) {
   const long long p = t * TP0 + threadIdx.x;
+  const long long slot = t * SLOTS_PER_TILE + (threadIdx.x >> 5);  // the warp's 32 pairs
   TileIn ti;
   ti.cS = p < np ? cnt[p] : 0;
   ti.cJ = p < np ? cnt[np + p] : 0;
-  ti.baseS = toff[t];
-  ti.baseJ = toff[npt + t];
+  ti.baseS = slot < npt ? toff[slot] : 0;
+  ti.baseJ = slot < npt ? toff[npt + slot] : 0;
   return ti;
 }
 
 template <int WK, int WL, int PT>
 __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, long long t, const TileIn& ti,
-                                              const FillOut& fo, int* scol, double* sval, int2* wtot) {
+                                              const FillOut& fo, int* scol, double* sval) {
   using MC = Mode0<WK, WL>;
   using FF = FillFar<WK, WL>;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -844,9 +845,8 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
   const long long p = t * TP0 + threadIdx.x;
   const bool valid = p < np;
   const int cS = ti.cS, cJ = ti.cJ;
-  int2 tot2;
-  const int2 ex2 = block_exclusive_scan2(cS, cJ, wtot, tot2);
-  const int exS = ex2.x, exJ = ex2.y;
+  int totS, totJ;  // warp-local offsets: every warp has a scan slot of its own (no CTA barrier)
+  const int exS = warp_excl_scan(cS, totS), exJ = warp_excl_scan(cJ, totJ);
   int a, b;
   warp_pairs(pr.n, t * TP0 + wid * 32, a, b);
   const bool far = valid && (b - a > 2 * MC::W);
@@ -964,7 +964,7 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
 // from warp scans with a running carry and a block scan of the warp totals.
 template <int WK, int WL, int PT>
 __device__ __forceinline__ void fill_direct_tile(const FarCtx& pr, long long npt, long long t,
-                                                 const int* __restrict__ cnt, const FillOut& fo, int2* wtot) {
+                                                 const int* __restrict__ cnt, const FillOut& fo) {
   using TL = Tiling<WK, WL>;
   static_assert(TL::DIRECT && WK == 0, "direct tile: W = 0");
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -980,11 +980,13 @@ __device__ __forceinline__ void fill_direct_tile(const FarCtx& pr, long long npt
     sS += cS[j];
     sJ += cJ[j];
   }
-  int2 tot2;
-  const int2 ex2 = block_exclusive_scan2(sS, sJ, wtot, tot2);  // per-thread totals, block order
-  // the warp's base = exclusive prefix of its lane 0 (threads ordered as warps x lanes)
-  const long long baseS = fo.toff[t] + __shfl_sync(FULL, ex2.x, 0);
-  const long long baseJ = fo.toff[npt + t] + __shfl_sync(FULL, ex2.y, 0);
+  (void)sS;
+  (void)sJ;
+  // warp w's 32 PPT pairs are scan slot t SLOTS_PER_TILE + w (no CTA barrier)
+  const long long slot = t * SLOTS_PER_TILE + wid;
+  if (slot >= npt) return;  // warp-uniform
+  const long long baseS = fo.toff[slot];
+  const long long baseJ = fo.toff[npt + slot];
   long long carryS = 0, carryJ = 0;
   int a, b;
   warp_pairs(pr.n, pw, a, b);
@@ -1037,7 +1039,6 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
   using FF = FillFar<WK, WL>;
   static_assert(Q1W <= 0, "combined fill: Q1 rows must be staging-free");
   extern __shared__ __align__(128) unsigned char dyn[];
-  __shared__ int2 wtot[8];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr bool HAS1 = Q1W >= 0;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1047,7 +1048,9 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
   // near units: 8 side rows each (2 per near item)
   const long long nn0 = (2 * (m0.pr.n * 2LL * m0.pr.W + m0.pr.n - 1) + 7) / 8;
   const long long nn1 = HAS1 ? (2 * (m1.pr.n * 2LL * m1.pr.W + m1.pr.n - 1) + 7) / 8 : 0;
-  const long long nt0 = m0.pr.npt, nt1 = HAS1 ? m1.pr.npt : 0;  // fill tiles = scan slots
+  // fill tiles: SLOTS_PER_TILE scan slots (one per warp) each
+  const long long nt0 = (m0.pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE;
+  const long long nt1 = HAS1 ? (m1.pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE : 0;
   const long long U0 = nt0 + nn0, U = U0 + nn1 + nt1;
   int* scol = reinterpret_cast<int*>(dyn + wid * FF::BYTES_PER_WARP);
   double* sval = reinterpret_cast<double*>(dyn + wid * FF::BYTES_PER_WARP + FF::COLW * 4);
@@ -1082,18 +1085,16 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
     long long idx;
     const int kind = decode(u, idx);
     if (kind == 0) {
-      __syncthreads();  // wtot of the previous unit consumed
       if constexpr (FF::DIRECT)
-        fill_direct_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, m0.cnt, m0.fo, wtot);
+        fill_direct_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, m0.cnt, m0.fo);
       else
-        fill_far_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, cur, m0.fo, scol, sval, wtot);
+        fill_far_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, cur, m0.fo, scol, sval);
     } else if (kind == 1) {
       fill_near_unit(m0.pr, idx, m0.cnt, m0.fo, m0.side);
     } else if (kind == 2) {
       if constexpr (HAS1) fill_near_unit(m1.pr, idx, m1.cnt, m1.fo, m1.side);
     } else {
-      __syncthreads();
-      if constexpr (HAS1) fill_direct_tile<0, 0, 0>(prf1, m1.pr.npt, idx, m1.cnt, m1.fo, wtot);
+      if constexpr (HAS1) fill_direct_tile<0, 0, 0>(prf1, m1.pr.npt, idx, m1.cnt, m1.fo);
     }
   }
   if (!FF::DIRECT && lane == 0) bulk_wait0();  // staging must outlive the bulk reads
@@ -1142,26 +1143,28 @@ __global__ void __launch_bounds__(32) k_count2(const MatCount mc) {
       tot += c;
     }
   }
-  if (lane == 0 && tot) {
-    atomicAdd(&mc.tsum[pw / TP0], tot);
-    atomicAdd(&mc.tsum[pr.npt + pw / TP0], tot);
+  if (lane == 0 && tot) {  // scan slot u = this warp's 32 pairs
+    atomicAdd(&mc.tsum[u], tot);
+    atomicAdd(&mc.tsum[pr.npt + u], tot);
   }
 }
 
 template <int WK, int WL, int PT>
 __device__ __forceinline__ void fill2_far_tile(const Prob& pr, long long t, const int* __restrict__ cnt,
-                                               const FillOut& fo, int2* wtot, int* soff) {
+                                               const FillOut& fo) {
   using MC = Mode0<WK, WL>;
   const int wid = threadIdx.x >> 5;
   const long long np = pr.np;
   const long long p = t * TP0 + threadIdx.x;
+  const long long slot = t * SLOTS_PER_TILE + wid;  // the warp's 32 pairs (no CTA barrier)
+  if (slot >= pr.npt) return;                       // warp-uniform
   const bool valid = p < np;
   const int w = valid ? cnt[p] : 0;
   const int cS = w & CNT_MASK, cJ = valid ? cnt[np + p] : 0;
-  __syncthreads();  // soff / wtot of the previous unit consumed
-  int2 tot2;
-  const int2 ex2 = block_exclusive_scan2(cS, cJ, wtot, tot2);
-  const long long baseS = fo.toff[t], baseJ = fo.toff[pr.npt + t];
+  int2 ex2, tot2;
+  ex2.x = warp_excl_scan(cS, tot2.x);
+  ex2.y = warp_excl_scan(cJ, tot2.y);
+  const long long baseS = fo.toff[slot], baseJ = fo.toff[pr.npt + slot];
   int a, b;
   warp_pairs(pr.n, t * TP0 + wid * 32, a, b);
   const bool far = valid && (b - a > 2 * MC::W);
@@ -1173,36 +1176,31 @@ __device__ __forceinline__ void fill2_far_tile(const Prob& pr, long long t, cons
       fo.K[np + p] = 0.0;
     }
   }
-  soff[2 * threadIdx.x] = ex2.x;
-  soff[2 * threadIdx.x + 1] = ex2.y;
-  __syncwarp();
   const Seg seg = {fo.col, fo.val, fo.cap};
   // the warp's 32 pairs, one after the other (lane-parallel positions)
   const unsigned farmask = __ballot_sync(FULL, far);
   for (int j = 0; j < 32; ++j) {
     if (!((farmask >> j) & 1u)) continue;  // warp-uniform
     const int aj = __shfl_sync(FULL, a, j), bj = __shfl_sync(FULL, b, j);
-    const int i = wid * 32 + j;
-    far_warp_pair<WK, WL, PT, true>(pr, aj, bj, seg, baseS + soff[2 * i], seg, baseJ + soff[2 * i + 1]);
+    const int oS = __shfl_sync(FULL, ex2.x, j), oJ = __shfl_sync(FULL, ex2.y, j);
+    far_warp_pair<WK, WL, PT, true>(pr, aj, bj, seg, baseS + oS, seg, baseJ + oJ);
   }
 }
 
 template <int WK, int WL, int PT>
 __global__ void __launch_bounds__(256) k_fill2(const MatFill mf) {
-  __shared__ int2 wtot[8];
-  __shared__ int soff[2 * TP0];
   const Prob& p0 = mf.pr;
   if (blockIdx.x == 0 && threadIdx.x == 0) mf.fo.row_ptr[p0.m] = *mf.fo.nnz;
   Prob pr = p0;
   pr.tau = *p0.tau_ptr;
   const long long nn = (2 * (p0.n * 2LL * p0.W + p0.n - 1) + 7) / 8;  // near units (8 side rows)
-  const long long nt = p0.npt, U = nt + nn;
+  const long long nt = (p0.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE, U = nt + nn;
   for (long long u = blockIdx.x; u < U; u += gridDim.x) {  // block-uniform
     long long idx;
     if (unit_decode(u, U, nn, idx)) {
       fill_near_unit(pr, idx, mf.cnt, mf.fo, mf.side);
     } else {
-      fill2_far_tile<WK, WL, PT>(pr, nt - 1 - idx, mf.cnt, mf.fo, wtot, soff);
+      fill2_far_tile<WK, WL, PT>(pr, nt - 1 - idx, mf.cnt, mf.fo);
     }
   }
 }
@@ -1787,7 +1785,7 @@ cudaError_t launch2_t(const Prob& pr, const MatCount* mc, const MatFill* mf, lon
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fill2<WK, WL, PT>, 256, 0);
     if (e != cudaSuccess) return e;
-    const long long U = pr.npt + (2 * (pr.n * 2LL * pr.W + pr.n - 1) + 7) / 8;
+    const long long U = (pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE + (2 * (pr.n * 2LL * pr.W + pr.n - 1) + 7) / 8;
     *grid_out = (long long)(nb > 0 ? nb : 1) * sms;
     if (*grid_out > U) *grid_out = U;
     return cudaSuccess;
@@ -1849,13 +1847,14 @@ void setup_prob(sun_plan_s* pl, int which) {
                              reinterpret_cast<NearMeta*>(pl->ws + L.side_meta[which]), (4 * pr.W + 1) * (4 * pr.W + 1),
                              (4 * pr.W + 1) * (4 * pr.W) / 2};
   if (pr.mode == 2) {
-    pr.tp = TP0;
-    pr.npt = (pr.np + TP0 - 1) / TP0;
+    pr.tp = TP0 / SLOTS_PER_TILE;  // scan slot = one count warp's 32 pairs
+    pr.npt = (pr.np + pr.tp - 1) / pr.tp;
     pr.ndt = pl->n - 1;
     pr.nb_near = (long long)pl->n * 2 * pr.W + (pl->n - 1);
   } else if (pr.mode == 0) {
-    // scan slot = fill tile of Tiling<WK, WL>::TP pairs (staging-free W = 0: 8 pairs per thread)
-    pr.tp = pr.wK == 0 ? 2048 : TP0;
+    // scan slot = one count warp's pairs = one fill warp's pairs (Tiling<WK, WL>::TP / 8:
+    // 32, or 256 for the staging-free W = 0 tiles of 8 pairs per thread)
+    pr.tp = (pr.wK == 0 ? 2048 : TP0) / SLOTS_PER_TILE;
     pr.npt = (pr.np + pr.tp - 1) / pr.tp;
     pr.ndt = pl->n - 1;
     const long long items = (long long)pl->n * 2 * pr.W + (pl->n - 1);
@@ -1871,7 +1870,7 @@ void setup_prob(sun_plan_s* pl, int which) {
 // ---- mode-0 launchers.  Q1W = -1: one matrix per launch; Q1W = 0: Q0 + Q1 (Q1 = (0, 0, 0)).
 template <int WK, int WL, int PT, int Q1W>
 cudaError_t launch_count0(const MatCount& m0, const MatCount& m1, cudaStream_t st) {
-  auto warps = [](const Prob& p) { return (p.np + p.tp / SLOTS_PER_TILE - 1) / (p.tp / SLOTS_PER_TILE); };
+  auto warps = [](const Prob& p) { return p.npt; };  // one count warp per scan slot
   const long long U = warps(m0.pr) + m0.pr.nb_near + (Q1W >= 0 ? warps(m1.pr) + m1.pr.nb_near : 0);
   if (U > 0) k_count0<WK, WL, PT, Q1W><<<(unsigned)U, 32, 0, st>>>(m0, m1);
   return cudaGetLastError();
@@ -1888,8 +1887,9 @@ cudaError_t attr_fill0(const Prob& p0, const Prob* p1, long long& grid) {
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fill0<WK, WL, PT, Q1W>, 256, smem);
   if (e != cudaSuccess) return e;
-  long long U = p0.npt + (2 * (p0.n * 2LL * p0.W + p0.n - 1) + 7) / 8;
-  if (Q1W >= 0 && p1) U += p1->npt + (2 * (p1->n * 2LL * p1->W + p1->n - 1) + 7) / 8;
+  auto tiles = [](const Prob& p) { return (p.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE; };
+  long long U = tiles(p0) + (2 * (p0.n * 2LL * p0.W + p0.n - 1) + 7) / 8;
+  if (Q1W >= 0 && p1) U += tiles(*p1) + (2 * (p1->n * 2LL * p1->W + p1->n - 1) + 7) / 8;
   grid = (long long)(nb > 0 ? nb : 1) * sms;
   if (grid > U) grid = U;
   return cudaSuccess;
