@@ -545,18 +545,39 @@ __device__ __forceinline__ int near_item(const Prob& pr, long long item, int& a,
   return 0;
 }
 
-// unit u of U: near units at evenly spread positions (Bresenham).  floor(u nn / U) in double
-// precision is exact here: u nn < 2^53 is exact, the quotient is < 2^31, and a non-integer
-// quotient is at least 1/U < 2^-20 away from the next integer, far above the rounding error.
-__device__ __forceinline__ bool unit_decode(long long u, long long U, long long nnear_units, long long& idx) {
-  const double r = (double)nnear_units / (double)U;
-  const long long k0 = (long long)floor((double)u * (double)nnear_units / (double)U);
-  const long long k1 = (long long)floor((double)(u + 1) * (double)nnear_units / (double)U);
-  (void)r;
-  const bool is_near = k1 > k0;
-  idx = is_near ? k0 : u - k0;
-  return is_near;
-}
+// Units u = blockIdx.x + k gridDim.x of a persistent loop over U units, nn of them near units
+// spread evenly (Bresenham): unit u is near iff floor((u + 1) nn / U) > floor(u nn / U) =: k0,
+// near index k0, else far index u - k0.  Kept incrementally (k0 and r = u nn mod U advance by
+// the constants of G nn = qG U + rG), so the loop needs no division (nn <= U).
+struct UnitIter {
+  long long u, k0, r;  // current unit, floor(u nn / U), u nn mod U
+  long long U, nn, qG, rG, G;
+  __device__ __forceinline__ void init(long long u0, long long G_, long long U_, long long nn_) {
+    U = U_ > 0 ? U_ : 1;
+    nn = nn_;
+    G = G_;
+    u = u0;
+    k0 = u0 * nn / U;
+    r = u0 * nn % U;
+    qG = G * nn / U;
+    rG = G * nn % U;
+  }
+  __device__ __forceinline__ void advance() {
+    u += G;
+    k0 += qG;
+    r += rG;
+    if (r >= U) {
+      r -= U;
+      ++k0;
+    }
+  }
+  // near unit (idx = near index) or far unit (idx = far index)
+  __device__ __forceinline__ bool decode(long long& idx) const {
+    const bool is_near = r + nn >= U;
+    idx = is_near ? k0 : u - k0;
+    return is_near;
+  }
+};
 
 // ---- count pass ------------------------------------------------------------------------
 // Every count CTA is a single warp, so no unit waits on a slow sibling warp:
@@ -1058,9 +1079,10 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
   FarCtx prf1{};
   if (HAS1) prf1 = FarCtx{m1.pr.K.v, m1.pr.L, *m1.pr.tau_ptr, m1.pr.np, m1.pr.n, m1.pr.P};
   // unit -> kind: 0 Q0 far tile, 1 Q0 near unit, 2 Q1 near unit, 3 Q1 tile; idx
-  auto decode = [&](long long v, long long& idx) -> int {
+  auto decode = [&](const UnitIter& it, long long& idx) -> int {
+    long long v = it.u;
     if (v < U0) {
-      if (unit_decode(v, U0, nn0, idx)) return 1;
+      if (it.decode(idx)) return 1;
       idx = nt0 - 1 - idx;  // far tiles, last first
       return 0;
     }
@@ -1072,18 +1094,22 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
     idx = v - nn1;
     return 3;
   };
-  long long u = blockIdx.x;
+  UnitIter it, nit;  // this unit, the next one (prefetched)
+  it.init(blockIdx.x, gridDim.x, U0, nn0);
+  nit = it;
   TileIn nxt{0, 0, 0, 0};
-  auto prefetch = [&](long long v) {
+  auto prefetch = [&](const UnitIter& v) {
     long long idx;
-    if (v < U && decode(v, idx) == 0 && !FF::DIRECT) nxt = load_tile_in(m0.pr.np, m0.pr.npt, idx, m0.cnt, m0.fo.toff);
+    if (v.u < U && decode(v, idx) == 0 && !FF::DIRECT)
+      nxt = load_tile_in(m0.pr.np, m0.pr.npt, idx, m0.cnt, m0.fo.toff);
   };
-  prefetch(u);
-  for (; u < U; u += gridDim.x) {  // block-uniform
+  prefetch(nit);
+  for (; it.u < U; it.advance()) {  // block-uniform
     const TileIn cur = nxt;
-    prefetch(u + gridDim.x);
+    nit.advance();
+    prefetch(nit);
     long long idx;
-    const int kind = decode(u, idx);
+    const int kind = decode(it, idx);
     if (kind == 0) {
       if constexpr (FF::DIRECT)
         fill_direct_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, m0.cnt, m0.fo);
@@ -1195,9 +1221,11 @@ __global__ void __launch_bounds__(256) k_fill2(const MatFill mf) {
   pr.tau = *p0.tau_ptr;
   const long long nn = (2 * (p0.n * 2LL * p0.W + p0.n - 1) + 7) / 8;  // near units (8 side rows)
   const long long nt = (p0.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE, U = nt + nn;
-  for (long long u = blockIdx.x; u < U; u += gridDim.x) {  // block-uniform
+  UnitIter it;
+  it.init(blockIdx.x, gridDim.x, U, nn);
+  for (; it.u < U; it.advance()) {  // block-uniform
     long long idx;
-    if (unit_decode(u, U, nn, idx)) {
+    if (it.decode(idx)) {
       fill_near_unit(pr, idx, mf.cnt, mf.fo, mf.side);
     } else {
       fill2_far_tile<WK, WL, PT>(pr, nt - 1 - idx, mf.cnt, mf.fo);
