@@ -21,6 +21,10 @@ Modules
   paper_eqs  the paper's own component formulas Eq. 6 (q_sn), Eq. 10 (r_sm,
              with the R1 reading) and Eq. 11 (k_s, with the R2 reading) from
              brute-force f, d -- used only to pin O1 to the paper's equations.
+  gks        O3: the same trace definition for a generator given by a dense rate
+             matrix A over the basis (Eq. 7), L_D(X) = sum_jk a_jk
+             (F_j X F_k - 1/2 {F_k F_j, X}); the oracle of the batched dense unfold
+             (SURVEY §8(f) F3).
   sparse     O2: the same trace definition with CSR operators, column by
              column (L(F_m) touches only the <= 2 matrix units of F_m, or the
              l+1 diagonal units of D^l), in plain C with OpenMP (sparse_o2.c).
