@@ -193,6 +193,34 @@ size_t sun_rk4_work_bytes(int64_t m);
  * sets the default to 0.  Errors: SUN_ERR_ARG. */
 int sun_plan_set_graphs(sun_plan plan, int32_t enable);
 
+/* ---- Dense unfold of a generator given by a rate matrix A -----------
+ * PAPER.md Eq. 7 writes the dissipator with a positive semidefinite M x M rate
+ * matrix A over the basis; P:568-570 samples "a 'dense', randomly generated, rate matrix A"
+ * at N = 100 over > 10^3 realisations.  For each realisation r of a batch:
+ *   L(X) = -i[H, X] + sum_jk a_jk (F_j X F_k - 1/2 {F_k F_j, X})      (F_k^+ = F_k)
+ *   Q_sm = Tr(F_s L(F_m)),  K_s = Tr(F_s L(I/N))       (dense; generator order R5)
+ * n: N, 2 <= N <= 1024.  batch: number of realisations (>= 0; 0 is a no-op).
+ * H: device double[batch][N][N][2]: complex Hermitian H (row-major, interleaved re, im; the
+ *    Hermiticity is not checked here).
+ * A: device double[batch][M][M][2]: complex Hermitian rate matrix in the F basis (row-major),
+ *    or NULL: no dissipator (Q = Q_H, K = 0).
+ * Q: device double[batch][M][M] (row-major, all M^2 entries written; real because L
+ *    preserves Hermiticity).  K: device double[batch][M], or NULL: not written.
+ * work: device scratch owned by the caller, >= sun_dense_work_bytes(n, 1) bytes (256-byte
+ *    aligned); realisations are processed floor(work_bytes / sun_dense_work_bytes(n, 1)) at a
+ *    time.  Asynchronous on `stream`; deterministic.
+ * Errors: SUN_ERR_DIM (N out of range), SUN_ERR_ARG (batch < 0; null H, Q or work),
+ *    SUN_ERR_CAPACITY (work too small), SUN_ERR_CUDA. */
+int sun_unfold_dense(int32_t n, int32_t batch, const double* H, const double* A, double* Q, double* K, void* work,
+                     size_t work_bytes, void* stream);
+
+/* Scratch bytes for `chunk` realisations at once (16 N^4 + 16 (N-1) N^2 + 16 N^2 each, each
+ * part 256-byte aligned); 0 if N is out of range or chunk < 1. */
+size_t sun_dense_work_bytes(int32_t n, int32_t chunk);
+
+/* Kernel launches sun_unfold_dense makes for these arguments (0 if it would fail). */
+int sun_dense_launches(int32_t n, int32_t batch, int32_t has_a, size_t work_bytes);
+
 /* Fill a diagnostics struct for the plan. */
 int sun_plan_info(sun_plan plan, sun_plan_info_t* info);
 

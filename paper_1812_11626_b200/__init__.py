@@ -162,6 +162,8 @@ class Plan:
     @staticmethod
     def _trim(bufs, nnz0, nnz1):
         Q0, Q1, K = bufs
+        if Q0.col.numel() == nnz0 and (Q1 is None or Q1.col.numel() == nnz1):
+            return bufs  # exact capacities: no views to make
         Q0 = CSR(Q0.row_ptr, Q0.col[:nnz0], Q0.val[:nnz0])
         if Q1 is not None:
             Q1 = CSR(Q1.row_ptr, Q1.col[:nnz1], Q1.val[:nnz1])
@@ -306,6 +308,53 @@ def rk4(Q0: CSR, Q1: Optional[CSR], K: Optional[torch.Tensor], v: torch.Tensor, 
                          ctypes.c_int64(nsteps), ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(w.data_ptr()),
                          ctypes.c_void_p(_stream_handle(stream))), "sun_rk4")
     return v
+
+
+def dense_work_bytes(n: int, chunk: int = 1) -> int:
+    """Scratch bytes of unfold_dense for `chunk` realisations at once (sun_dense_work_bytes)."""
+    return int(lib().sun_dense_work_bytes(n, chunk))
+
+
+def unfold_dense(H: torch.Tensor, A: Optional[torch.Tensor] = None, Q: Optional[torch.Tensor] = None,
+                 K: Optional[torch.Tensor] = None, work: Optional[torch.Tensor] = None, chunk: int = 1,
+                 stream=None):
+    """Dense unfold of L = -i[H, .] + L_D[A] (Eq. 7) for a batch of realisations
+    (sun_unfold_dense).
+
+    H: complex128 (B, N, N) or (N, N) on the GPU; A: complex128 (B, M, M) / (M, M) rate
+    matrix over the basis (generator order R5), or None.  Returns (Q (B, M, M) float64,
+    K (B, M) float64), squeezed like H.  `work` (any dtype, >= dense_work_bytes(N, 1)
+    bytes) may be passed to reuse scratch; else `chunk` realisations' worth is allocated.
+    """
+    squeeze = H.dim() == 2
+    Hb = H.unsqueeze(0) if squeeze else H
+    assert Hb.is_cuda and Hb.dtype == torch.complex128 and Hb.dim() == 3 and Hb.shape[1] == Hb.shape[2]
+    B, n = int(Hb.shape[0]), int(Hb.shape[1])
+    m = n * n - 1
+    Hb = Hb.contiguous()
+    Ab = None
+    if A is not None:
+        Ab = (A.unsqueeze(0) if A.dim() == 2 else A).contiguous()
+        assert Ab.dtype == torch.complex128 and tuple(Ab.shape) == (B, m, m) and Ab.device == Hb.device
+    if Q is None:
+        Q = torch.empty((B, m, m), dtype=torch.float64, device=Hb.device)
+    if K is None:
+        K = torch.empty((B, m), dtype=torch.float64, device=Hb.device)
+    assert Q.is_contiguous() and Q.numel() == B * m * m and K.is_contiguous() and K.numel() == B * m
+    if work is None:
+        nb = dense_work_bytes(n, max(1, min(chunk, B)))
+        if nb == 0:
+            raise SunError(f"sun_dense_work_bytes: N = {n} out of range")
+        work = torch.empty((nb + 15) // 16, dtype=torch.complex128, device=Hb.device)
+    wb = work.numel() * work.element_size()
+    _check(lib().sun_unfold_dense(n, B, ctypes.c_void_p(Hb.data_ptr()),
+                                  ctypes.c_void_p(Ab.data_ptr()) if Ab is not None else None,
+                                  ctypes.c_void_p(Q.data_ptr()), ctypes.c_void_p(K.data_ptr()),
+                                  ctypes.c_void_p(work.data_ptr()), ctypes.c_size_t(wb),
+                                  ctypes.c_void_p(_stream_handle(stream))), "sun_unfold_dense")
+    if squeeze:
+        return Q.view(m, m), K.view(m)
+    return Q.view(B, m, m), K.view(B, m)
 
 
 def apply(Q0: CSR, Q1: Optional[CSR], eps: float, K: Optional[torch.Tensor], v: torch.Tensor,

@@ -50,6 +50,11 @@ SIGNATURES = {
     "sun_rk4": (ctypes.c_int, [P, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                ctypes.c_double, ctypes.c_int64, P, P, P]),
     "sun_rk4_work_bytes": (ctypes.c_size_t, [ctypes.c_int64]),
+    "sun_unfold_dense": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p,
+                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t,
+                                        ctypes.c_void_p]),
+    "sun_dense_work_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32]),
+    "sun_dense_launches": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_size_t]),
     "sun_plan_destroy": (None, [P]),
     "sun_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "sun_gen_index": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),

@@ -192,7 +192,9 @@ struct sun_plan_s {
   std::vector<GraphEntry> graphs;
   unsigned long long graph_clock = 0;
   bool use_graphs = true;
+  HeaderPrefix* hpin = nullptr;  // pinned host copy of the header prefix (nnz readback)
   ~sun_plan_s() {
+    if (hpin) cudaFreeHost(hpin);
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
     for (int i = 0; i < 2; ++i) {
       if (aux[i]) cudaStreamDestroy(aux[i]);
@@ -1757,6 +1759,10 @@ int cuda_fail(cudaError_t e) {
   snprintf(g_errbuf, sizeof(g_errbuf), "CUDA error: %s", cudaGetErrorString(e));
   return SUN_ERR_CUDA;
 }
+}  // namespace
+// shared with sunfold_dense.cu (same library)
+int sunfold_cuda_fail(cudaError_t e) { return cuda_fail(e); }
+namespace {
 #define CK(x)                                    \
   do {                                           \
     cudaError_t e_ = (x);                        \
@@ -2263,9 +2269,15 @@ static int enqueue_count(sun_plan pl, cudaStream_t st) {
 int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
   if (!pl) return SUN_ERR_ARG;
   if (!pl->counted) return SUN_ERR_STATE;
-  HeaderPrefix h;
-  CK(cudaMemcpyAsync(&h, pl->ws + pl->lay.hdr, sizeof(h), cudaMemcpyDeviceToHost, pl->count_stream));
+  if (!pl->hpin && cudaMallocHost(&pl->hpin, sizeof(HeaderPrefix)) != cudaSuccess) {
+    pl->hpin = nullptr;  // pageable fallback
+    (void)cudaGetLastError();
+  }
+  HeaderPrefix hloc;
+  HeaderPrefix* hp = pl->hpin ? pl->hpin : &hloc;
+  CK(cudaMemcpyAsync(hp, pl->ws + pl->lay.hdr, sizeof(HeaderPrefix), cudaMemcpyDeviceToHost, pl->count_stream));
   CK(cudaStreamSynchronize(pl->count_stream));
+  const HeaderPrefix h = *hp;
   if (h.flags & F_MALFORMED) return SUN_ERR_ARG;
   for (int k = 0; k < 1 + pl->has_h1; ++k) {
     double dev;

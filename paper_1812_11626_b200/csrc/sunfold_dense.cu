@@ -1,0 +1,389 @@
+// sunfold_dense.cu — dense unfold of a GKSL generator given by a rate matrix A (include/sunfold.h,
+// sun_unfold_dense).  SURVEY §8(f) F3 ("a 'dense', randomly generated, rate matrix A
+// ... N = 100 ... more than 10^3 realizations") and the general-A half of F4 (Eq. 7).
+//
+//   L(X) = -i[H, X] + sum_jk a_jk (F_j X F_k - 1/2 {F_k F_j, X})      (Eq. 7 with F_k^+ = F_k)
+//   Q_sm = Tr(F_s L(F_m)),  K_s = Tr(F_s L(I/N))
+//
+// No structure constants and no contraction: in the matrix-unit basis the superoperator is
+//   S[(ab),(cd)] = [L(E_cd)]_ab = Y[(a,c),(d,b)] + (-i Kh)_ac d_db + d_ac (i Kh^+)_db,
+//   Y = Fm A Fm^T  (Fm[(a,c), j] = (F_j)_ac),  G = sum_jk a_jk F_k F_j,  Kh = H - (i/2) G,
+// and Q = (basis change of S on both sides).  Every basis change is a 2 x 2 combination
+// (S_ab, J_ab have two entries) or a prefix / suffix sum over the diagonal (D^l), so the whole
+// unfold is O(M^2) = O(N^4) and HBM-bound.  Two streaming passes carry the bulk:
+//   k_dense_expand   A rows S(p), J(p) -> Z[b][a][c][d] = Y[(a,c),(d,b)] for (a,c) = p, (c,a)
+//                    (Z is Y realigned so that each pass reads and writes contiguous runs)
+//   k_dense_project  Z rows (x,y), (y,x) (+ the Kh terms) -> Q rows S(p), J(p) and K
+// plus O(N^3) kernels for the D^l rows/columns (k_dense_dexp, k_dense_zdiag, k_dense_kh,
+// k_dense_vdiag, k_dense_drows).  Shares no code with the oracle (oracle/gks.py).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "sunfold.h"
+
+int sunfold_cuda_fail(cudaError_t e);  // sunfold.cu: records the message for sun_status_string
+
+namespace {
+
+constexpr int DT = 256;  // threads per CTA
+constexpr unsigned FULLM = 0xffffffffu;
+constexpr double RS2 = 0.70710678118654752440;  // 1/sqrt(2)
+
+struct DenseArgs {
+  int n, batch;
+  long long m, np;          // M = N^2 - 1, N(N-1)/2
+  const double2* H;         // [batch][N][N]
+  const double2* A;         // [batch][M][M] or null
+  double* Q;                // [batch][M][M]
+  double* K;                // [batch][M] or null
+  double2* Z;               // [chunk][N^4]
+  double2* UD;              // [chunk][N-1][N^2]  (U = A Fm^T on the D rows of A; reused for VD)
+  double2* Kh;              // [chunk][N^2]
+  int r0;                   // first realisation of this chunk
+};
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cmuli(double2 a) { return make_double2(-a.y, a.x); }   // i a
+__device__ __forceinline__ double2 cmulmi(double2 a) { return make_double2(a.y, -a.x); }  // -i a
+__device__ __forceinline__ double inv_ll1(int l) { return 1.0 / sqrt((double)l * (double)(l + 1)); }
+
+__device__ __forceinline__ long long pair_idx(long long n, long long u, long long w) {  // u < w
+  return u * (2 * n - u - 1) / 2 + (w - u - 1);
+}
+// pair q -> (u, w), u < w (lexicographic)
+__device__ __forceinline__ void pair_of(long long n, long long q, int& u, int& w) {
+  const double t = 2.0 * (double)n - 1.0;
+  const double disc = t * t - 8.0 * (double)q;
+  long long a = (long long)floor((t - sqrt(disc > 0.0 ? disc : 0.0)) * 0.5);
+  if (a < 0) a = 0;
+  while (a > 0 && a * (2 * n - a - 1) / 2 > q) --a;
+  while (a + 1 <= n - 2 && (a + 1) * (2 * n - a - 2) / 2 <= q) ++a;
+  u = (int)a;
+  w = (int)(a + 1 + (q - a * (2 * n - a - 1) / 2));
+}
+
+// Warp 0: diag[d] = sum_l delta_l(d) c_l for d in [0, n) from the D coefficients c_l = dv[l-1]
+// (delta_l(d) = 1/sqrt(l(l+1)) for d < l, -l/sqrt(l(l+1)) for d = l, else 0; A.1).
+// Suffix sums S(l) = sum_{l' >= l} w_l', w_l = c_l inv(l):  diag[l] = S(l) - (l+1) w_l,
+// diag[0] = S(1).
+__device__ void warp_diag_from_d(const double2* __restrict__ dv, double2* diag, int n) {
+  const int lane = threadIdx.x & 31;
+  double2 carry = make_double2(0.0, 0.0);
+  for (int top = n - 1; top >= 1; top -= 32) {
+    const int l = top - lane;
+    const double2 w = l >= 1 ? cscale(dv[l - 1], inv_ll1(l)) : make_double2(0.0, 0.0);
+    double2 s = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double x = __shfl_up_sync(FULLM, s.x, o), y = __shfl_up_sync(FULLM, s.y, o);
+      if (lane >= o) {
+        s.x += x;
+        s.y += y;
+      }
+    }
+    const double2 S = cadd(carry, s);
+    if (l >= 1) diag[l] = csub(S, cscale(w, (double)(l + 1)));
+    carry = make_double2(__shfl_sync(FULLM, S.x, 31), __shfl_sync(FULLM, S.y, 31));
+  }
+  if (lane == 0) diag[0] = carry;
+}
+
+// Warp 0: out[l-1] = (sum_{c<l} v_c - l v_l) / sqrt(l(l+1)) for l in [1, n) (Tr(D^l X) from the
+// diagonal v of X; A.1), and *tot = sum_c v_c.  Only real parts are needed.
+__device__ void warp_d_from_diag(const double* v, double* out, double* tot, int n) {
+  const int lane = threadIdx.x & 31;
+  double carry = 0.0;
+  for (int base = 0; base < n; base += 32) {
+    const int c = base + lane;
+    const double x = c < n ? v[c] : 0.0;
+    double s = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(FULLM, s, o);
+      if (lane >= o) s += y;
+    }
+    const double excl = carry + s - x;  // sum_{c' < c}
+    if (c >= 1 && c < n) out[c - 1] = (excl - (double)c * x) * inv_ll1(c);
+    carry += __shfl_sync(FULLM, s, 31);
+  }
+  if (lane == 0) *tot = carry;
+}
+
+// U = A Fm^T on one row of A (length M): U[(d,b)] = sum_k a_k (F_k)_db, for d != b the 2-term
+// combination over S(min,max), J(min,max); for d == b the suffix table `diag`.
+__device__ __forceinline__ double2 expand_entry(const double2* __restrict__ arow, const double2* diag, long long n,
+                                                long long np, int d, int b) {
+  if (d == b) return diag[d];
+  const bool lo = d < b;
+  const long long q = lo ? pair_idx(n, d, b) : pair_idx(n, b, d);
+  const double2 s = __ldg(arow + q), j = __ldg(arow + np + q);
+  // (S_q)_db = 1/sqrt2;  (J_q)_db = -i/sqrt2 if d < b, +i/sqrt2 if d > b
+  return cscale(cadd(s, lo ? cmulmi(j) : cmuli(j)), RS2);
+}
+
+// (1) U rows of the D^l rows of A: UD[l-1][b][d] = sum_k A[D^l][k] (F_k)_db.  grid (N-1, chunk)
+__global__ void __launch_bounds__(DT) k_dense_dexp(const DenseArgs g) {
+  extern __shared__ double2 sdiag[];  // [N]
+  const int n = g.n, r = blockIdx.y, l = blockIdx.x + 1;
+  const long long m = g.m, np = g.np, n2 = (long long)n * n;
+  const double2* arow = g.A + (long long)(g.r0 + r) * m * m + (2 * np + l - 1) * m;
+  if (threadIdx.x < 32) warp_diag_from_d(arow + 2 * np, sdiag, n);
+  __syncthreads();
+  double2* out = g.UD + ((long long)r * (n - 1) + (l - 1)) * n2;
+  for (long long t = threadIdx.x; t < n2; t += DT) {
+    const int b = (int)(t / n), d = (int)(t % n);
+    out[t] = expand_entry(arow, sdiag, n, np, d, b);
+  }
+}
+
+// (2) the pair rows: CTA per pair p = (x, y), x < y.  U rows S(p), J(p) on the fly, then
+//   Y[(x,y),(d,b)] = (U_S - i U_J)/sqrt2,  Y[(y,x),(d,b)] = (U_S + i U_J)/sqrt2
+// written to Z[b][x][y][d] and Z[b][y][x][d] (contiguous in d).  grid (np, chunk)
+__global__ void __launch_bounds__(DT) k_dense_expand(const DenseArgs g) {
+  extern __shared__ double2 sdiag[];  // [2][N]
+  const int n = g.n, r = blockIdx.y;
+  const long long m = g.m, np = g.np, n2 = (long long)n * n;
+  const long long p = blockIdx.x;
+  int x, y;
+  pair_of(n, p, x, y);
+  const double2* A = g.A + (long long)(g.r0 + r) * m * m;
+  const double2 *aS = A + p * m, *aJ = A + (np + p) * m;
+  if (threadIdx.x < 32)
+    warp_diag_from_d(aS + 2 * np, sdiag, n);
+  else if (threadIdx.x < 64)
+    warp_diag_from_d(aJ + 2 * np, sdiag + n, n);
+  __syncthreads();
+  double2* Z = g.Z + (long long)r * n2 * n2;
+  double2* zxy = Z + ((long long)x * n + y) * n;  // + b N^3 + d
+  double2* zyx = Z + ((long long)y * n + x) * n;
+  const long long n3 = n2 * n;
+  for (long long t = threadIdx.x; t < n2; t += DT) {
+    const int b = (int)(t / n), d = (int)(t % n);
+    const double2 uS = expand_entry(aS, sdiag, n, np, d, b);
+    const double2 uJ = expand_entry(aJ, sdiag + n, n, np, d, b);
+    zxy[b * n3 + d] = cscale(cadd(uS, cmulmi(uJ)), RS2);
+    zyx[b * n3 + d] = cscale(cadd(uS, cmuli(uJ)), RS2);
+  }
+}
+
+// (3) the diagonal rows a = c = x:  Z[b][x][x][d] = sum_l delta_l(x) UD[l-1][b][d] (suffix sums
+// over l).  grid (ceil(N^2 / DT), chunk), thread per (b, d)
+__global__ void __launch_bounds__(DT) k_dense_zdiag(const DenseArgs g) {
+  const int n = g.n, r = blockIdx.y;
+  const long long n2 = (long long)n * n;
+  const long long t = (long long)blockIdx.x * DT + threadIdx.x;
+  if (t >= n2) return;
+  const int b = (int)(t / n), d = (int)(t % n);
+  const double2* ud = g.UD + (long long)r * (n - 1) * n2 + t;
+  double2* Z = g.Z + (long long)r * n2 * n2 + (long long)b * n2 * n + d;  // + (x N + x) N
+  double2 S = make_double2(0.0, 0.0);
+  for (int l = n - 1; l >= 1; --l) {
+    const double2 w = cscale(ud[(long long)(l - 1) * n2], inv_ll1(l));
+    Z[((long long)l * n + l) * n] = csub(S, cscale(w, (double)l));
+    S = cadd(S, w);
+  }
+  Z[0] = S;
+}
+
+// (4) G_ce = sum_x Z[x][x][e][c] (= sum_jk a_jk (F_k F_j)_ce) and Kh = H - (i/2) G.
+// grid (ceil(N^2 / DT), chunk), thread per (e, c)
+__global__ void __launch_bounds__(DT) k_dense_kh(const DenseArgs g) {
+  const int n = g.n, r = blockIdx.y;
+  const long long n2 = (long long)n * n;
+  const long long t = (long long)blockIdx.x * DT + threadIdx.x;
+  if (t >= n2) return;
+  const int e = (int)(t / n), c = (int)(t % n);
+  double2 G = make_double2(0.0, 0.0);
+  if (g.A) {
+    const double2* Z = g.Z + (long long)r * n2 * n2 + t;
+    for (int x = 0; x < n; ++x) G = cadd(G, Z[((long long)x * n + x) * n2]);
+  }
+  const double2 h = g.H[(long long)(g.r0 + r) * n2 + (long long)c * n + e];
+  g.Kh[(long long)r * n2 + (long long)c * n + e] = make_double2(h.x + 0.5 * G.y, h.y - 0.5 * G.x);
+}
+
+// S in Z coordinates: Z'[b][a][c][d] = Z[b][a][c][d] + (-i Kh_ac) [d == b] + (i conj(Kh_bd)) [a == c]
+__device__ __forceinline__ double2 zprime(const double2* __restrict__ zrow, const double2* __restrict__ kh, int n,
+                                          bool has_a, int b, int a, int c, int d) {
+  double2 z = has_a ? __ldg(zrow + (long long)c * n + d) : make_double2(0.0, 0.0);
+  if (d == b) z = cadd(z, cmulmi(__ldg(kh + (long long)a * n + c)));
+  if (a == c) {
+    const double2 k = __ldg(kh + (long long)b * n + d);
+    z = cadd(z, cmuli(make_double2(k.x, -k.y)));
+  }
+  return z;
+}
+
+// (5) the pair rows of Q: CTA per pair p = (x, y).  Rows (b,a) = (x,y), (y,x) of Z':
+//   V_S = (Z'_xy + Z'_yx)/sqrt2,  V_J = (-i Z'_xy + i Z'_yx)/sqrt2     [(F_s)_ba weights]
+//   Q[s][S(u,w)] = Re(V_s[u,w] + V_s[w,u])/sqrt2,  Q[s][J(u,w)] = Re(-i V_s[u,w] + i V_s[w,u])/sqrt2
+//   Q[s][D^l] from the diagonal V_s[c,c] (prefix sums), K_s = sum_c Re V_s[c,c] / N.
+// grid (np, chunk)
+__global__ void __launch_bounds__(DT) k_dense_project(const DenseArgs g) {
+  extern __shared__ double sv[];  // [2][N] diagonal of V_S, V_J
+  const int n = g.n, r = blockIdx.y;
+  const long long m = g.m, np = g.np, n2 = (long long)n * n;
+  const long long p = blockIdx.x;
+  int x, y;
+  pair_of(n, p, x, y);
+  const bool has_a = g.A != nullptr;
+  const double2* Z = g.Z + (long long)r * n2 * n2;
+  const double2* zxy = Z + ((long long)x * n + y) * n2;  // row (b,a) = (x,y)
+  const double2* zyx = Z + ((long long)y * n + x) * n2;  // row (b,a) = (y,x)
+  const double2* kh = g.Kh + (long long)r * n2;
+  double* qS = g.Q + (long long)(g.r0 + r) * m * m + p * m;
+  double* qJ = qS + np * m;
+  for (long long q = threadIdx.x; q < np; q += DT) {
+    int u, w;
+    pair_of(n, q, u, w);
+    const double2 a1 = zprime(zxy, kh, n, has_a, x, y, u, w), a2 = zprime(zxy, kh, n, has_a, x, y, w, u);
+    const double2 b1 = zprime(zyx, kh, n, has_a, y, x, u, w), b2 = zprime(zyx, kh, n, has_a, y, x, w, u);
+    // V_S at (u,w), (w,u) and V_J at (u,w), (w,u)
+    const double2 s1 = cscale(cadd(a1, b1), RS2), s2 = cscale(cadd(a2, b2), RS2);
+    const double2 j1 = cscale(cadd(cmulmi(a1), cmuli(b1)), RS2), j2 = cscale(cadd(cmulmi(a2), cmuli(b2)), RS2);
+    // Re(V1 + V2)/sqrt2 and Re(-i V1 + i V2)/sqrt2 = (Im V1 - Im V2)/sqrt2
+    qS[q] = (s1.x + s2.x) * RS2;
+    qS[np + q] = (s1.y - s2.y) * RS2;
+    qJ[q] = (j1.x + j2.x) * RS2;
+    qJ[np + q] = (j1.y - j2.y) * RS2;
+  }
+  for (int c = threadIdx.x; c < n; c += DT) {
+    const double2 a = zprime(zxy, kh, n, has_a, x, y, c, c), b = zprime(zyx, kh, n, has_a, y, x, c, c);
+    sv[c] = (a.x + b.x) * RS2;            // Re V_S[c,c]
+    sv[n + c] = (a.y - b.y) * RS2;        // Re V_J[c,c] = Re((-i a + i b)/sqrt2)
+  }
+  __syncthreads();
+  __shared__ double tot[2];
+  if (threadIdx.x < 32)
+    warp_d_from_diag(sv, qS + 2 * np, &tot[0], n);
+  else if (threadIdx.x < 64)
+    warp_d_from_diag(sv + n, qJ + 2 * np, &tot[1], n);
+  __syncthreads();
+  if (g.K && threadIdx.x == 0) {
+    double* K = g.K + (long long)(g.r0 + r) * m;
+    K[p] = tot[0] / n;
+    K[np + p] = tot[1] / n;
+  }
+}
+
+// (6) V rows of the D^l rows of Q: VD[l-1][(c,d)] = sum_x delta_l(x) Z'[x][x][c][d] (prefix sums
+// over x).  grid (ceil(N^2 / DT), chunk), thread per (c, d).  VD reuses the UD buffer.
+__global__ void __launch_bounds__(DT) k_dense_vdiag(const DenseArgs g) {
+  const int n = g.n, r = blockIdx.y;
+  const long long n2 = (long long)n * n;
+  const long long t = (long long)blockIdx.x * DT + threadIdx.x;
+  if (t >= n2) return;
+  const int c = (int)(t / n), d = (int)(t % n);
+  const bool has_a = g.A != nullptr;
+  const double2* Z = g.Z + (long long)r * n2 * n2;
+  const double2* kh = g.Kh + (long long)r * n2;
+  double2* vd = g.UD + (long long)r * (n - 1) * n2 + t;
+  double2 P = make_double2(0.0, 0.0);
+  for (int xx = 0; xx < n; ++xx) {
+    const double2 z = zprime(Z + ((long long)xx * n + xx) * n2, kh, n, has_a, xx, xx, c, d);
+    if (xx >= 1) vd[(long long)(xx - 1) * n2] = cscale(csub(P, cscale(z, (double)xx)), inv_ll1(xx));
+    P = cadd(P, z);
+  }
+}
+
+// (7) Q rows D^l from VD: CTA per l.  grid (N-1, chunk)
+__global__ void __launch_bounds__(DT) k_dense_drows(const DenseArgs g) {
+  extern __shared__ double sv[];  // [N]
+  const int n = g.n, r = blockIdx.y, l = blockIdx.x + 1;
+  const long long m = g.m, np = g.np, n2 = (long long)n * n;
+  const double2* V = g.UD + ((long long)r * (n - 1) + (l - 1)) * n2;
+  const long long s = 2 * np + l - 1;
+  double* qrow = g.Q + (long long)(g.r0 + r) * m * m + s * m;
+  for (long long q = threadIdx.x; q < np; q += DT) {
+    int u, w;
+    pair_of(n, q, u, w);
+    const double2 v1 = __ldg(V + (long long)u * n + w), v2 = __ldg(V + (long long)w * n + u);
+    qrow[q] = (v1.x + v2.x) * RS2;
+    qrow[np + q] = (v1.y - v2.y) * RS2;
+  }
+  for (int c = threadIdx.x; c < n; c += DT) sv[c] = V[(long long)c * n + c].x;
+  __syncthreads();
+  __shared__ double tot;
+  if (threadIdx.x < 32) warp_d_from_diag(sv, qrow + 2 * np, &tot, n);
+  __syncthreads();
+  if (g.K && threadIdx.x == 0) g.K[(long long)(g.r0 + r) * m + s] = tot / n;
+}
+
+constexpr int DENSE_NMAX = 1024;  // shared-memory tables of 2N complex per CTA (<= 32 KB)
+
+size_t per_realisation_bytes(long long n) {
+  const long long n2 = n * n;
+  auto al = [](long long b) { return (size_t)((b + 255) & ~255LL); };
+  return al(16 * n2 * n2) + al(16 * (n - 1) * n2) + al(16 * n2);
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t sun_dense_work_bytes(int32_t n, int32_t chunk) {
+  if (n < 2 || n > DENSE_NMAX || chunk < 1) return 0;
+  return per_realisation_bytes(n) * (size_t)chunk;
+}
+
+int sun_unfold_dense(int32_t n, int32_t batch, const double* H, const double* A, double* Q, double* K, void* work,
+                     size_t work_bytes, void* stream) {
+  if (n < 2 || n > DENSE_NMAX) return SUN_ERR_DIM;
+  if (batch < 0) return SUN_ERR_ARG;
+  if (batch == 0) return SUN_OK;
+  if (!H || !Q || !work) return SUN_ERR_ARG;
+  const size_t per = per_realisation_bytes(n);
+  if (work_bytes < per) return SUN_ERR_CAPACITY;
+  long long chunk = (long long)(work_bytes / per);
+  if (chunk > batch) chunk = batch;
+  if (chunk > 65535) chunk = 65535;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long nn = n, n2 = nn * nn;
+  DenseArgs g;
+  g.n = n;
+  g.batch = batch;
+  g.m = n2 - 1;
+  g.np = nn * (nn - 1) / 2;
+  g.H = reinterpret_cast<const double2*>(H);
+  g.A = reinterpret_cast<const double2*>(A);
+  g.Q = Q;
+  g.K = K;
+  char* ws = (char*)work;
+  auto al = [](long long b) { return (size_t)((b + 255) & ~255LL); };
+  g.Z = reinterpret_cast<double2*>(ws);
+  g.UD = reinterpret_cast<double2*>(ws + chunk * al(16 * n2 * n2));
+  g.Kh = reinterpret_cast<double2*>(ws + chunk * (al(16 * n2 * n2) + al(16 * (nn - 1) * n2)));
+  const unsigned gsq = (unsigned)((n2 + DT - 1) / DT);
+  for (long long r0 = 0; r0 < batch; r0 += chunk) {
+    const unsigned cb = (unsigned)(batch - r0 < chunk ? batch - r0 : chunk);
+    g.r0 = (int)r0;
+    if (A) {
+      k_dense_dexp<<<dim3((unsigned)(n - 1), cb), DT, n * sizeof(double2), st>>>(g);
+      k_dense_expand<<<dim3((unsigned)g.np, cb), DT, 2 * n * sizeof(double2), st>>>(g);
+      k_dense_zdiag<<<dim3(gsq, cb), DT, 0, st>>>(g);
+    }
+    k_dense_kh<<<dim3(gsq, cb), DT, 0, st>>>(g);
+    k_dense_project<<<dim3((unsigned)g.np, cb), DT, 2 * n * sizeof(double), st>>>(g);
+    k_dense_vdiag<<<dim3(gsq, cb), DT, 0, st>>>(g);
+    k_dense_drows<<<dim3((unsigned)(n - 1), cb), DT, n * sizeof(double), st>>>(g);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return sunfold_cuda_fail(e);
+  }
+  return SUN_OK;
+}
+
+int sun_dense_launches(int32_t n, int32_t batch, int32_t has_a, size_t work_bytes) {
+  if (n < 2 || n > DENSE_NMAX || batch <= 0) return 0;
+  const size_t per = per_realisation_bytes(n);
+  if (work_bytes < per) return 0;
+  long long chunk = (long long)(work_bytes / per);
+  if (chunk > batch) chunk = batch;
+  if (chunk > 65535) chunk = 65535;
+  const long long chunks = (batch + chunk - 1) / chunk;
+  return (int)(chunks * (has_a ? 7 : 4));
+}
+
+}  // extern "C"

@@ -244,3 +244,53 @@ CONFIG_NAMES = {
     3: "c3_banded_N512_P4",
     4: "c4_dimer_N1000_drive",
 }
+
+
+# ---- F3: ensembles of random dense generators ------------------------------
+# The ensemble of ref. [Karol] is not in the container; the reading used here (F3):
+# H from the GUE (H = (X + X^+)/2, X complex Ginibre), rate matrix A = G G^+ with G a complex
+# Ginibre M x r matrix (a Wishart GKS matrix, positive semidefinite), normalised to Tr A = N.
+def gks_ensemble(n: int, batch: int, seed: int = 0, rank: int = 0):
+    """(H (batch, N, N) complex128, A (batch, M, M) complex128) host arrays, seeded."""
+    rng = np.random.default_rng(seed)
+    m = n * n - 1
+    r = rank or m
+    H = np.empty((batch, n, n), dtype=np.complex128)
+    A = np.empty((batch, m, m), dtype=np.complex128)
+    for b in range(batch):
+        X = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        H[b] = (X + X.conj().T) / 2
+        G = rng.standard_normal((m, r)) + 1j * rng.standard_normal((m, r))
+        Ab = G @ G.conj().T
+        A[b] = Ab * (n / np.trace(Ab).real)
+    return H, A
+
+
+def gks_ensemble_torch(n: int, batch: int, seed: int = 0, device="cuda"):
+    """The same recipe drawn on the device with torch (large N: the Wishart product is an
+    M x M x M complex GEMM); not bitwise equal to gks_ensemble."""
+    import torch
+
+    gen = torch.Generator(device=device)
+    gen.manual_seed(seed)
+    m = n * n - 1
+    H = torch.empty((batch, n, n), dtype=torch.complex128, device=device)
+    A = torch.empty((batch, m, m), dtype=torch.complex128, device=device)
+    for b in range(batch):
+        X = torch.randn((n, n), dtype=torch.complex128, device=device, generator=gen) * np.sqrt(2.0)
+        H[b] = (X + X.conj().T) / 2
+        G = torch.randn((m, m), dtype=torch.complex128, device=device, generator=gen) * np.sqrt(2.0)
+        torch.matmul(G, G.conj().T, out=A[b])
+        A[b] *= n / torch.diagonal(A[b]).real.sum()
+        del G
+    return H, A
+
+
+def rank_p_coefficients(n: int, P: int, seed: int = 0):
+    """Random complex coefficient vectors l_p (P, M) and rates gamma_p (P,) for A = sum_p
+    gamma_p l_p l_p^+ (the spectral form)."""
+    rng = np.random.default_rng(seed)
+    m = n * n - 1
+    l = rng.standard_normal((P, m)) + 1j * rng.standard_normal((P, m))
+    g = rng.uniform(0.05, 0.5, size=P)
+    return l, g
