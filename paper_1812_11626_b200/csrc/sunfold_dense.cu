@@ -141,9 +141,24 @@ __global__ void __launch_bounds__(DT) k_dense_dexp(const DenseArgs g) {
 
 // (2) the pair rows: CTA per pair p = (x, y), x < y.  U rows S(p), J(p) on the fly, then
 //   Y[(x,y),(d,b)] = (U_S - i U_J)/sqrt2,  Y[(y,x),(d,b)] = (U_S + i U_J)/sqrt2
-// written to Z[b][x][y][d] and Z[b][y][x][d] (contiguous in d).  grid (np, chunk)
-__global__ void __launch_bounds__(DT) k_dense_expand(const DenseArgs g) {
-  extern __shared__ double2 sdiag[];  // [2][N]
+// written to Z[b][x][y][d] and Z[b][y][x][d] (contiguous in d).  The (b, d) plane is walked in
+// 16 x 16 tiles on and above the diagonal (d >= b), one tile per warp at a time (warp-private
+// staging, no CTA barrier): each A entry pair(b, d) is read once (contiguous in d) and gives
+// both (d, b) -- written directly, d fastest -- and the mirrored (b, d) position, staged in
+// shared memory and written out transposed.  grid (np, chunk)
+constexpr int TW = 16;           // warp tile edge
+constexpr int WPC = DT / 32;     // warps per CTA
+struct WarpTile {
+  double2 a[TW][TW + 1], b[TW][TW + 1];
+};
+__device__ __forceinline__ double2 jcomb(double2 s, double2 j, bool minus) {  // (s -+ i j)/sqrt2
+  return cscale(cadd(s, minus ? cmulmi(j) : cmuli(j)), RS2);
+}
+__global__ void __launch_bounds__(DT, 2) k_dense_expand(const DenseArgs g) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpTile& T = reinterpret_cast<WarpTile*>(dsm)[wid];
+  double2* sdiag = reinterpret_cast<double2*>(dsm + WPC * sizeof(WarpTile));  // [2][N]
   const int n = g.n, r = blockIdx.y;
   const long long m = g.m, np = g.np, n2 = (long long)n * n;
   const long long p = blockIdx.x;
@@ -151,21 +166,69 @@ __global__ void __launch_bounds__(DT) k_dense_expand(const DenseArgs g) {
   pair_of(n, p, x, y);
   const double2* A = g.A + (long long)(g.r0 + r) * m * m;
   const double2 *aS = A + p * m, *aJ = A + (np + p) * m;
-  if (threadIdx.x < 32)
+  if (wid == 0)
     warp_diag_from_d(aS + 2 * np, sdiag, n);
-  else if (threadIdx.x < 64)
+  else if (wid == 1)
     warp_diag_from_d(aJ + 2 * np, sdiag + n, n);
   __syncthreads();
   double2* Z = g.Z + (long long)r * n2 * n2;
   double2* zxy = Z + ((long long)x * n + y) * n;  // + b N^3 + d
   double2* zyx = Z + ((long long)y * n + x) * n;
   const long long n3 = n2 * n;
-  for (long long t = threadIdx.x; t < n2; t += DT) {
-    const int b = (int)(t / n), d = (int)(t % n);
-    const double2 uS = expand_entry(aS, sdiag, n, np, d, b);
-    const double2 uJ = expand_entry(aJ, sdiag + n, n, np, d, b);
-    zxy[b * n3 + d] = cscale(cadd(uS, cmulmi(uJ)), RS2);
-    zyx[b * n3 + d] = cscale(cadd(uS, cmuli(uJ)), RS2);
+  const int nt = (n + TW - 1) / TW;
+  const int hi = lane >> 4, lo = lane & 15;
+  int cnt = 0;
+  for (int tb = 0; tb < nt; ++tb) {
+    for (int td = tb; td < nt; ++td) {
+      if (cnt++ % WPC != wid) continue;  // warp-uniform
+      const int b0 = tb * TW, d0 = td * TW;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // two batches of 4 rows: all loads first, then the math
+        double2 sS[4], sJ[4], jS[4], jJ[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int b = b0 + 8 * h + 2 * k + hi, d = d0 + lo;
+          const bool ok = b < n && d < n && d > b;
+          const long long q = ok ? pair_idx(n, b, d) : 0;  // a valid address either way
+          sS[k] = __ldg(aS + q);
+          sJ[k] = __ldg(aS + np + q);
+          jS[k] = __ldg(aJ + q);
+          jJ[k] = __ldg(aJ + np + q);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int i = 8 * h + 2 * k + hi, j = lo;
+          const int b = b0 + i, d = d0 + j;
+          if (b < n && d < n && d >= b) {
+            double2 uS, uJ;  // U at (d, b)
+            if (d == b) {
+              uS = sdiag[d];
+              uJ = sdiag[n + d];
+            } else {
+              // (S_q)_db = (S_q)_bd = 1/sqrt2; (J_q)_db = +i/sqrt2 (d > b), (J_q)_bd = -i/sqrt2
+              uS = jcomb(sS[k], sJ[k], false);
+              uJ = jcomb(jS[k], jJ[k], false);
+              const double2 vS = jcomb(sS[k], sJ[k], true), vJ = jcomb(jS[k], jJ[k], true);  // U at (b, d)
+              T.a[i][j] = jcomb(vS, vJ, true);   // Y[(x,y),(b,d)] -> Z[d][x][y][b]
+              T.b[i][j] = jcomb(vS, vJ, false);  // Y[(y,x),(b,d)] -> Z[d][y][x][b]
+            }
+            zxy[b * n3 + d] = jcomb(uS, uJ, true);
+            zyx[b * n3 + d] = jcomb(uS, uJ, false);
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll 4
+      for (int k = 0; k < TW / 2; ++k) {
+        const int i = 2 * k + hi, j = lo;  // row d = d0 + i, column b = b0 + j
+        const int d = d0 + i, b = b0 + j;
+        if (b < n && d < n && d > b) {
+          zxy[(long long)d * n3 + b] = T.a[j][i];
+          zyx[(long long)d * n3 + b] = T.b[j][i];
+        }
+      }
+      __syncwarp();
+    }
   }
 }
 
@@ -205,6 +268,15 @@ __global__ void __launch_bounds__(DT) k_dense_kh(const DenseArgs g) {
   g.Kh[(long long)r * n2 + (long long)c * n + e] = make_double2(h.x + 0.5 * G.y, h.y - 0.5 * G.x);
 }
 
+// the Kh terms of S in Z coordinates (added to a raw Z value)
+__device__ __forceinline__ double2 zdelta(double2 z, const double2* __restrict__ kh, int n, int b, int a, int c, int d) {
+  if (d == b) z = cadd(z, cmulmi(__ldg(kh + (long long)a * n + c)));
+  if (a == c) {
+    const double2 k = __ldg(kh + (long long)b * n + d);
+    z = cadd(z, cmuli(make_double2(k.x, -k.y)));
+  }
+  return z;
+}
 // S in Z coordinates: Z'[b][a][c][d] = Z[b][a][c][d] + (-i Kh_ac) [d == b] + (i conj(Kh_bd)) [a == c]
 __device__ __forceinline__ double2 zprime(const double2* __restrict__ zrow, const double2* __restrict__ kh, int n,
                                           bool has_a, int b, int a, int c, int d) {
@@ -221,9 +293,15 @@ __device__ __forceinline__ double2 zprime(const double2* __restrict__ zrow, cons
 //   V_S = (Z'_xy + Z'_yx)/sqrt2,  V_J = (-i Z'_xy + i Z'_yx)/sqrt2     [(F_s)_ba weights]
 //   Q[s][S(u,w)] = Re(V_s[u,w] + V_s[w,u])/sqrt2,  Q[s][J(u,w)] = Re(-i V_s[u,w] + i V_s[w,u])/sqrt2
 //   Q[s][D^l] from the diagonal V_s[c,c] (prefix sums), K_s = sum_c Re V_s[c,c] / N.
-// grid (np, chunk)
-__global__ void __launch_bounds__(DT) k_dense_project(const DenseArgs g) {
-  extern __shared__ double sv[];  // [2][N] diagonal of V_S, V_J
+// The (u, w) plane (u < w) is walked in 16 x 16 tiles, one per warp at a time: the transposed
+// blocks Z'[w][u] of both rows are staged in warp-private shared memory (contiguous loads),
+// the direct blocks Z'[u][w] are read in the compute phase (contiguous); outputs pair(u, w)
+// go out in runs of consecutive pairs.  grid (np, chunk)
+__global__ void __launch_bounds__(DT, 2) k_dense_project(const DenseArgs g) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  WarpTile& T = reinterpret_cast<WarpTile*>(dsm)[wid];
+  double* sv = reinterpret_cast<double*>(dsm + WPC * sizeof(WarpTile));  // [2][N] diagonal of V_S, V_J
   const int n = g.n, r = blockIdx.y;
   const long long m = g.m, np = g.np, n2 = (long long)n * n;
   const long long p = blockIdx.x;
@@ -236,19 +314,62 @@ __global__ void __launch_bounds__(DT) k_dense_project(const DenseArgs g) {
   const double2* kh = g.Kh + (long long)r * n2;
   double* qS = g.Q + (long long)(g.r0 + r) * m * m + p * m;
   double* qJ = qS + np * m;
-  for (long long q = threadIdx.x; q < np; q += DT) {
-    int u, w;
-    pair_of(n, q, u, w);
-    const double2 a1 = zprime(zxy, kh, n, has_a, x, y, u, w), a2 = zprime(zxy, kh, n, has_a, x, y, w, u);
-    const double2 b1 = zprime(zyx, kh, n, has_a, y, x, u, w), b2 = zprime(zyx, kh, n, has_a, y, x, w, u);
-    // V_S at (u,w), (w,u) and V_J at (u,w), (w,u)
-    const double2 s1 = cscale(cadd(a1, b1), RS2), s2 = cscale(cadd(a2, b2), RS2);
-    const double2 j1 = cscale(cadd(cmulmi(a1), cmuli(b1)), RS2), j2 = cscale(cadd(cmulmi(a2), cmuli(b2)), RS2);
-    // Re(V1 + V2)/sqrt2 and Re(-i V1 + i V2)/sqrt2 = (Im V1 - Im V2)/sqrt2
-    qS[q] = (s1.x + s2.x) * RS2;
-    qS[np + q] = (s1.y - s2.y) * RS2;
-    qJ[q] = (j1.x + j2.x) * RS2;
-    qJ[np + q] = (j1.y - j2.y) * RS2;
+  const int nt = (n + TW - 1) / TW;
+  const int hi = lane >> 4, lo = lane & 15;
+  int cnt = 0;
+  for (int tu = 0; tu < nt; ++tu) {
+    for (int tw = tu; tw < nt; ++tw) {
+      if (cnt++ % WPC != wid) continue;  // warp-uniform
+      const int u0 = tu * TW, w0 = tw * TW;
+      {  // stage the transposed blocks: all loads first
+        double2 za[8], zb[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = 2 * k + hi, j = lo;  // row w = w0 + i, column u = u0 + j
+          const bool ok = has_a && w0 + i < n && u0 + j < n;
+          const long long o = ok ? (long long)(w0 + i) * n + (u0 + j) : 0;
+          za[k] = ok ? __ldg(zxy + o) : make_double2(0.0, 0.0);
+          zb[k] = ok ? __ldg(zyx + o) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int i = 2 * k + hi, j = lo;
+          if (w0 + i < n && u0 + j < n) {
+            T.a[i][j] = zdelta(za[k], kh, n, x, y, w0 + i, u0 + j);
+            T.b[i][j] = zdelta(zb[k], kh, n, y, x, w0 + i, u0 + j);
+          }
+        }
+      }
+      __syncwarp();
+      double2 za[8], zb[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {  // direct blocks: all loads first
+        const int u = u0 + 2 * k + hi, w = w0 + lo;
+        const bool ok = has_a && u < w && w < n;
+        const long long o = ok ? (long long)u * n + w : 0;
+        za[k] = ok ? __ldg(zxy + o) : make_double2(0.0, 0.0);
+        zb[k] = ok ? __ldg(zyx + o) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int k = 0; k < TW / 2; ++k) {
+        const int i = 2 * k + hi, j = lo;  // u = u0 + i, w = w0 + j
+        const int u = u0 + i, w = w0 + j;
+        if (u < w && w < n) {
+          const double2 a1 = zdelta(za[k], kh, n, x, y, u, w), b1 = zdelta(zb[k], kh, n, y, x, u, w);
+          const double2 a2 = T.a[j][i], b2 = T.b[j][i];
+          // V_S at (u,w), (w,u) and V_J at (u,w), (w,u)
+          const double2 s1 = cscale(cadd(a1, b1), RS2), s2 = cscale(cadd(a2, b2), RS2);
+          const double2 j1 = cscale(cadd(cmulmi(a1), cmuli(b1)), RS2), j2 = cscale(cadd(cmulmi(a2), cmuli(b2)), RS2);
+          const long long q = pair_idx(n, u, w);
+          // Re(V1 + V2)/sqrt2 and Re(-i V1 + i V2)/sqrt2 = (Im V1 - Im V2)/sqrt2
+          qS[q] = (s1.x + s2.x) * RS2;
+          qS[np + q] = (s1.y - s2.y) * RS2;
+          qJ[q] = (j1.x + j2.x) * RS2;
+          qJ[np + q] = (j1.y - j2.y) * RS2;
+        }
+      }
+      __syncwarp();
+    }
   }
   for (int c = threadIdx.x; c < n; c += DT) {
     const double2 a = zprime(zxy, kh, n, has_a, x, y, c, c), b = zprime(zyx, kh, n, has_a, y, x, c, c);
@@ -257,9 +378,9 @@ __global__ void __launch_bounds__(DT) k_dense_project(const DenseArgs g) {
   }
   __syncthreads();
   __shared__ double tot[2];
-  if (threadIdx.x < 32)
+  if (wid == 0)
     warp_d_from_diag(sv, qS + 2 * np, &tot[0], n);
-  else if (threadIdx.x < 64)
+  else if (wid == 1)
     warp_d_from_diag(sv + n, qJ + 2 * np, &tot[1], n);
   __syncthreads();
   if (g.K && threadIdx.x == 0) {
@@ -357,16 +478,24 @@ int sun_unfold_dense(int32_t n, int32_t batch, const double* H, const double* A,
   g.UD = reinterpret_cast<double2*>(ws + chunk * al(16 * n2 * n2));
   g.Kh = reinterpret_cast<double2*>(ws + chunk * (al(16 * n2 * n2) + al(16 * (nn - 1) * n2)));
   const unsigned gsq = (unsigned)((n2 + DT - 1) / DT);
+  const size_t sm_exp = WPC * sizeof(WarpTile) + 2 * n * sizeof(double2);
+  const size_t sm_prj = WPC * sizeof(WarpTile) + 2 * n * sizeof(double);
+  {
+    cudaError_t e = cudaFuncSetAttribute(k_dense_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_exp);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(k_dense_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_prj);
+    if (e != cudaSuccess) return sunfold_cuda_fail(e);
+  }
   for (long long r0 = 0; r0 < batch; r0 += chunk) {
     const unsigned cb = (unsigned)(batch - r0 < chunk ? batch - r0 : chunk);
     g.r0 = (int)r0;
     if (A) {
       k_dense_dexp<<<dim3((unsigned)(n - 1), cb), DT, n * sizeof(double2), st>>>(g);
-      k_dense_expand<<<dim3((unsigned)g.np, cb), DT, 2 * n * sizeof(double2), st>>>(g);
+      k_dense_expand<<<dim3((unsigned)g.np, cb), DT, sm_exp, st>>>(g);
       k_dense_zdiag<<<dim3(gsq, cb), DT, 0, st>>>(g);
     }
     k_dense_kh<<<dim3(gsq, cb), DT, 0, st>>>(g);
-    k_dense_project<<<dim3((unsigned)g.np, cb), DT, 2 * n * sizeof(double), st>>>(g);
+    k_dense_project<<<dim3((unsigned)g.np, cb), DT, sm_prj, st>>>(g);
     k_dense_vdiag<<<dim3(gsq, cb), DT, 0, st>>>(g);
     k_dense_drows<<<dim3((unsigned)(n - 1), cb), DT, n * sizeof(double), st>>>(g);
     const cudaError_t e = cudaGetLastError();
