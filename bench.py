@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-rk4", action="store_true")
+    ap.add_argument("--no-f3", action="store_true")
     return ap.parse_args()
 
 
@@ -400,6 +401,40 @@ def main():
         rk4 = {"ms_per_step": rk_ms, "steps": nst, "h": h, "bytes_per_step": step_bytes,
                "roofline": {"bound": "hbm", "achieved": rk_gbs, "peak": peak, "unit": "GB/s", "frac": rk_gbs / peak},
                "kernel": "k_rk4_stage (4 fused SpMV stages per RK4 step)"}
+    # F3: batched dense unfold from random rate matrices A (Eq. 7) at
+    # N = 100; inputs drawn on the device (Wishart GKS matrices, workloads.gks_ensemble_torch).
+    f3 = None
+    if not args.no_f3:
+        from workloads import gks_ensemble_torch
+
+        n3, b3 = 100, 4
+        m3 = n3 * n3 - 1
+        H3, A3 = gks_ensemble_torch(n3, b3, seed=11 + rank)
+        Q3 = torch.empty((b3, m3, m3), dtype=torch.float64, device="cuda")
+        K3 = torch.empty((b3, m3), dtype=torch.float64, device="cuda")
+        nb3 = sun.dense_work_bytes(n3, 2)
+        w3 = torch.empty((nb3 + 15) // 16, dtype=torch.complex128, device="cuda")
+        sun.unfold_dense(H3, A3, Q3, K3, w3)  # warm-up
+        f3_ms = []
+        for _ in range(3):  # every call streams > 10 GB: no L2 reuse between calls
+            a, b = ev(), ev()
+            a.record(stream)
+            sun.unfold_dense(H3, A3, Q3, K3, w3)
+            b.record(stream)
+            torch.cuda.synchronize()
+            f3_ms.append(a.elapsed_time(b))
+        t3 = min(f3_ms) * 1e-3
+        alg3 = b3 * (16 * m3 * m3 + 16 * n3 * n3 + 8 * m3 * m3 + 8 * m3)
+        f3 = {"workload": f"Wishart GKS ensemble N={n3} (M={m3}), batch {b3}, dense Q and K",
+              "ms_per_realisation": t3 * 1e3 / b3, "realisations_per_s": b3 / t3,
+              "roofline": {"bound": "hbm", "achieved": alg3 / t3 / 1e9, "peak": peak, "unit": "GB/s",
+                           "frac": alg3 / t3 / 1e9 / peak, "algorithmic_bytes_per_realisation": alg3 // b3,
+                           "note": "algorithmic = A, H read + Q, K written; the two-pass design also writes "
+                                   "and reads the realigned superoperator Z (16 N^4 B each way)"},
+              "gpu_launches": int(sun.lib().sun_dense_launches(n3, b3, 1, nb3)),
+              "kernels": "k_dense_expand, k_dense_project (+ 5 O(N^3) D-row kernels)"}
+        del H3, A3, Q3, K3, w3
+        torch.cuda.empty_cache()
     info = plan.info()
     launches_per_step = plan.launches_per_run()
     plan.close()
@@ -480,6 +515,7 @@ def main():
         "roofline": roofline,
         "cpu_baseline": cpu,
         "rk4": rk4,
+        "f3_dense": f3,
         "plan": {k: info[k] for k in ("w_h0", "w_l", "w_k", "mode_q0", "npos_far_q0", "tiles_q0")},
         "wall_s_timed_region": t_wall,
     }

@@ -29,6 +29,12 @@ def _dev(x):
     return torch.tensor(x, dtype=torch.complex128, device="cuda")
 
 
+def _operator(l, n):
+    """L = sum_j l_j F_j for complex coefficients (oracle.basis.reconstruct_fast, real parts)."""
+    e = np.eye(n) / n
+    return (basis.reconstruct_fast(l.real, n) - e) + 1j * (basis.reconstruct_fast(l.imag, n) - e)
+
+
 def _csr_dense(r, m):
     Q = np.zeros((m, m))
     rp, c, v = r["row_ptr"], r["col"], r["val"]
@@ -89,8 +95,7 @@ def test_dense_spectral_form_vs_o2(n, P):
     Q, K = sun.unfold_dense(_dev(H), _dev(A))
     Q, K = Q.cpu().numpy(), K.cpu().numpy()
     # oracle side: the operators L_p = sum_j l_pj F_j (traceless), through O2's trace definition
-    F = basis.generators(n)
-    Ls = [ZCSR.from_dense(np.einsum("j,jab->ab", l[p], F)) for p in range(P)]
+    Ls = [ZCSR.from_dense(_operator(l[p], n)) for p in range(P)]
     r = sparse.unfold_csr(ZCSR.from_dense(H), Ls, list(g), tau=0.0)
     Qo = _csr_dense(r, m)
     sc = np.abs(Qo).max()
@@ -98,7 +103,31 @@ def test_dense_spectral_form_vs_o2(n, P):
     assert np.abs(K - r["K"]).max() <= 1e-12 * sc
 
 
-@pytest.mark.parametrize("n", [40, 64])
+def test_dense_banded_spectral_form_vs_o2_full_size():
+    """N = 100 (the F3 size): A = sum_p gamma_p l_p l_p^+ with l_p supported on a band
+    of generators (so L_p = sum_j l_pj F_j is banded and O2 is fast) against O2."""
+    sun = _sun()
+    n, P = 100, 2
+    m = n * n - 1
+    l, g = rank_p_coefficients(n, P, seed=7, band=2)
+    Ad = torch.zeros((m, m), dtype=torch.complex128, device="cuda")
+    for p in range(P):
+        lp = _dev(l[p])
+        Ad += g[p] * torch.outer(lp, lp.conj())
+    rng = np.random.default_rng(900)
+    X = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    H = (X + X.conj().T) / 2
+    Q, K = sun.unfold_dense(_dev(H), Ad)
+    Q, K = Q.cpu().numpy(), K.cpu().numpy()
+    Ls = [ZCSR.from_dense(_operator(l[p], n)) for p in range(P)]
+    r = sparse.unfold_csr(ZCSR.from_dense(H), Ls, list(g), tau=0.0)
+    Qo = _csr_dense(r, m)
+    sc = np.abs(Qo).max()
+    assert np.abs(Q - Qo).max() <= 1e-12 * sc
+    assert np.abs(K - r["K"]).max() <= 1e-12 * sc
+
+
+@pytest.mark.parametrize("n", [40, 64, 100])
 def test_dense_depolarising_closed_form(n):
     """A = gamma I: L_D(X) = gamma (Tr(X) I - N X) (Fierz), so Q = Q_H - gamma N I and K = 0."""
     sun = _sun()

@@ -286,11 +286,23 @@ def gks_ensemble_torch(n: int, batch: int, seed: int = 0, device="cuda"):
     return H, A
 
 
-def rank_p_coefficients(n: int, P: int, seed: int = 0):
+def rank_p_coefficients(n: int, P: int, seed: int = 0, band: int = 0):
     """Random complex coefficient vectors l_p (P, M) and rates gamma_p (P,) for A = sum_p
-    gamma_p l_p l_p^+ (the spectral form)."""
+    gamma_p l_p l_p^+ (the spectral form).  band > 0: only the S_ab / J_ab with
+    b - a <= band (and every D^l) get a coefficient (generator order R5), so that
+    L_p = sum_j l_pj F_j is banded."""
     rng = np.random.default_rng(seed)
     m = n * n - 1
     l = rng.standard_normal((P, m)) + 1j * rng.standard_normal((P, m))
+    if band > 0:
+        npairs = n * (n - 1) // 2
+        keep = np.ones(m, dtype=bool)
+        q = 0
+        for a in range(n):
+            for b in range(a + 1, n):
+                if b - a > band:
+                    keep[q] = keep[npairs + q] = False
+                q += 1
+        l[:, ~keep] = 0.0
     g = rng.uniform(0.05, 0.5, size=P)
     return l, g
