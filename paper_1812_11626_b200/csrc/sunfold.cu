@@ -759,7 +759,8 @@ __device__ __forceinline__ void warp_near_row_write(const NearSide& side, long l
   }
 }
 
-// near unit j: side rows 8j .. 8j + 7 (row 2i = S row / D row of near item i, 2i + 1 = J row)
+// near unit j (modes 0, 1-row-per-warp): side rows 8j .. 8j + 7 (row 2i = S row / D row of near
+// item i, 2i + 1 = J row)
 __device__ __forceinline__ void fill_near_unit(const Prob& pr, long long j, const int* __restrict__ cnt,
                                                const FillOut& fo, const NearSide& side) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -791,6 +792,131 @@ __device__ __forceinline__ void fill_near_unit(const Prob& pr, long long j, cons
     }
     warp_near_row_write(side, srow, m, pr.inv, (int)(2 * np - 1), fo, o);
   }
+}
+
+__host__ __device__ inline long long near_units1(long long n, long long W) {  // units of 8 side rows
+  return (2 * (n * 2 * W + n - 1) + 7) / 8;
+}
+
+// Mode 2 (long window rows, N^2 tails): near units of NEAR_UNIT_ROWS side rows (batched).
+// Near rows written by near units of
+// NEAR_UNIT_ROWS side rows (8 per warp) from the count pass's side buffer: window entries
+// copied, chain-tail entries tr * inv[l], l in (hi, lend], generated with the count pass's
+// expression (bitwise identical).  Row offset = slot offset + the slot's earlier counts; D
+// rows have a scan slot of their own.  Each warp first resolves its 8 rows' offsets and
+// metadata together (lane r: row r; the slot prefix sums by warp-wide loads, all issued
+// before any is consumed), then writes the 8 rows as one flattened, lane-strided stream, so
+// no row waits on another's lookups.
+#ifndef SUN_NEAR_WARP_ROWS
+#define SUN_NEAR_WARP_ROWS 8
+#endif
+constexpr int NEAR_WARP_ROWS = SUN_NEAR_WARP_ROWS;
+constexpr int NEAR_UNIT_ROWS = 8 * NEAR_WARP_ROWS;
+__host__ __device__ inline long long near_units(long long n, long long W) {
+  return (2 * (n * 2 * W + n - 1) + NEAR_UNIT_ROWS - 1) / NEAR_UNIT_ROWS;
+}
+struct NearRowP {
+  long long o, sbase;  // output offset of the row, side-buffer offset of its slot
+  double tr;           // chain-tail trace
+  int pref, len;       // exclusive prefix of len over the warp's rows; entries to write
+  int n1, b2, nwin, hi;
+};
+
+__device__ __forceinline__ void fill_near_unit_b(const Prob& pr, long long j, const int* __restrict__ cnt,
+                                                 const FillOut& fo, const NearSide& side, NearRowP* rows) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long np = pr.np;
+  const long long nside = 2 * ((long long)pr.n * 2 * pr.W + pr.n - 1);
+  const long long srow = j * NEAR_UNIT_ROWS + wid * NEAR_WARP_ROWS + lane;  // lanes 0..7: the warp's rows
+  int kind = 0, half = 0, lam = 0;
+  long long p = 0;
+  if (lane < NEAR_WARP_ROWS && srow < nside) {
+    int a, b;
+    half = (int)(srow & 1);
+    kind = near_item(pr, srow >> 1, a, b, lam);
+    if (kind == 2 && half) kind = 0;  // D items use one side row
+    if (kind == 1) p = (long long)pidx32(pr.n, a, b);
+  }
+  // slot prefix sums of the near-pair rows (mode 2 packs nR above CNT_BITS)
+  int s1 = 0;
+#pragma unroll
+  for (int r = 0; r < NEAR_WARP_ROWS; ++r) {
+    const int kr = __shfl_sync(FULL, kind, r);
+    const long long pr_ = __shfl_sync(FULL, p, r);
+    const int hr = __shfl_sync(FULL, half, r);
+    int sum = 0;
+    if (kr == 1) {  // warp-uniform
+      const long long ts = (pr_ / pr.tp) * pr.tp;
+      const int* c = cnt + (hr ? np : 0);
+      for (long long q = ts + lane; q < pr_; q += 32) sum += __ldg(&c[q]) & CNT_MASK;
+    }
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) sum += __shfl_xor_sync(FULL, sum, sh);
+    if (lane == r) s1 = sum;
+  }
+  int len = 0;
+  NearRowP rp{};
+  if (kind != 0) {
+    const NearMeta m = side.meta[srow];
+    long long o;
+    if (kind == 1) {
+      o = fo.toff[(half ? pr.npt : 0) + p / pr.tp] + s1;
+      if (fo.K) fo.K[(half ? np : 0) + p] = m.k;
+    } else {
+      o = fo.toff[2 * pr.npt + lam - 1];
+      fo.row_ptr[2 * np + lam - 1] = o;
+      if (fo.K) fo.K[2 * np + lam - 1] = m.k;
+    }
+    const int nwin = m.n1 + m.n2 + m.nd;
+    const long long want = nwin + (m.lend > m.hi ? m.lend - m.hi : 0);
+    const long long room = fo.cap - o;  // writes at or beyond the capacity are dropped
+    len = (int)(want < room ? want : (room > 0 ? room : 0));
+    rp = NearRowP{o, srow * side.nc, m.tr, 0, len, m.n1, m.n1 + m.n2, nwin, m.hi};
+  }
+  int ex = len;  // exclusive prefix over lanes 0..7
+#pragma unroll
+  for (int o = 1; o < NEAR_WARP_ROWS; o <<= 1) {
+    const int y = __shfl_up_sync(FULL, ex, o);
+    if (lane >= o) ex += y;
+  }
+  const int total = __shfl_sync(FULL, ex, NEAR_WARP_ROWS - 1);
+  ex -= len;
+  if (lane < NEAR_WARP_ROWS) {
+    rp.pref = ex;
+    rp.len = len;
+    rows[lane] = rp;
+  }
+  __syncwarp();
+  const int dbase = (int)(2 * np - 1);
+  int pf[NEAR_WARP_ROWS], pe[NEAR_WARP_ROWS];  // row t owns [pf[t], pe[t])
+#pragma unroll
+  for (int t = 0; t < NEAR_WARP_ROWS; ++t) {
+    pf[t] = __shfl_sync(FULL, ex, t);
+    pe[t] = pf[t] + __shfl_sync(FULL, len, t);
+  }
+#pragma unroll 4
+  for (int k = lane; k < total; k += 32) {
+    int r = 0;
+#pragma unroll
+    for (int t = 1; t < NEAR_WARP_ROWS; ++t)
+      if (pf[t] <= k && k < pe[t]) r = t;
+    const NearRowP& R = rows[r];
+    const int idx = k - R.pref;
+    int c;
+    double v;
+    if (idx < R.nwin) {
+      const int sidx = idx < R.n1 ? idx : (idx < R.b2 ? side.seg + (idx - R.n1) : 2 * side.seg + (idx - R.b2));
+      c = __ldg(&side.col[R.sbase + sidx]);
+      v = __ldg(&side.val[R.sbase + sidx]);
+    } else {
+      const int l = R.hi + 1 + (idx - R.nwin);
+      c = dbase + l;
+      v = R.tr * __ldg(&pr.inv[l]);
+    }
+    fo.col[R.o + idx] = c;
+    fo.val[R.o + idx] = v;
+  }
+  __syncwarp();  // rows[] reused by the warp's next unit
 }
 
 // Copy a warp's staged segment [g0, g1) (tile-local offsets) to global memory, skipping the
@@ -1068,9 +1194,9 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
     m0.fo.row_ptr[m0.pr.m] = *m0.fo.nnz;
     if (HAS1) m1.fo.row_ptr[m1.pr.m] = *m1.fo.nnz;
   }
-  // near units: 8 side rows each (2 per near item)
-  const long long nn0 = (2 * (m0.pr.n * 2LL * m0.pr.W + m0.pr.n - 1) + 7) / 8;
-  const long long nn1 = HAS1 ? (2 * (m1.pr.n * 2LL * m1.pr.W + m1.pr.n - 1) + 7) / 8 : 0;
+  // near units: NEAR_UNIT_ROWS side rows each (2 per near item)
+  const long long nn0 = near_units1(m0.pr.n, m0.pr.W);
+  const long long nn1 = HAS1 ? near_units1(m1.pr.n, m1.pr.W) : 0;
   // fill tiles: SLOTS_PER_TILE scan slots (one per warp) each
   const long long nt0 = (m0.pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE;
   const long long nt1 = HAS1 ? (m1.pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE : 0;
@@ -1118,7 +1244,9 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
       else
         fill_far_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, cur, m0.fo, scol, sval);
     } else if (kind == 1) {
+#ifndef SUN_EXP_NO_NEAR
       fill_near_unit(m0.pr, idx, m0.cnt, m0.fo, m0.side);
+#endif
     } else if (kind == 2) {
       if constexpr (HAS1) fill_near_unit(m1.pr, idx, m1.cnt, m1.fo, m1.side);
     } else {
@@ -1217,18 +1345,19 @@ __device__ __forceinline__ void fill2_far_tile(const Prob& pr, long long t, cons
 
 template <int WK, int WL, int PT>
 __global__ void __launch_bounds__(256) k_fill2(const MatFill mf) {
+  __shared__ NearRowP nrows[8][NEAR_WARP_ROWS];
   const Prob& p0 = mf.pr;
   if (blockIdx.x == 0 && threadIdx.x == 0) mf.fo.row_ptr[p0.m] = *mf.fo.nnz;
   Prob pr = p0;
   pr.tau = *p0.tau_ptr;
-  const long long nn = (2 * (p0.n * 2LL * p0.W + p0.n - 1) + 7) / 8;  // near units (8 side rows)
+  const long long nn = near_units(p0.n, p0.W);
   const long long nt = (p0.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE, U = nt + nn;
   UnitIter it;
   it.init(blockIdx.x, gridDim.x, U, nn);
   for (; it.u < U; it.advance()) {  // block-uniform
     long long idx;
     if (it.decode(idx)) {
-      fill_near_unit(pr, idx, mf.cnt, mf.fo, mf.side);
+      fill_near_unit_b(pr, idx, mf.cnt, mf.fo, mf.side, nrows[threadIdx.x >> 5]);
     } else {
       fill2_far_tile<WK, WL, PT>(pr, nt - 1 - idx, mf.cnt, mf.fo);
     }
@@ -1819,7 +1948,7 @@ cudaError_t launch2_t(const Prob& pr, const MatCount* mc, const MatFill* mf, lon
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fill2<WK, WL, PT>, 256, 0);
     if (e != cudaSuccess) return e;
-    const long long U = (pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE + (2 * (pr.n * 2LL * pr.W + pr.n - 1) + 7) / 8;
+    const long long U = (pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE + near_units(pr.n, pr.W);
     *grid_out = (long long)(nb > 0 ? nb : 1) * sms;
     if (*grid_out > U) *grid_out = U;
     return cudaSuccess;
@@ -1922,8 +2051,8 @@ cudaError_t attr_fill0(const Prob& p0, const Prob* p1, long long& grid) {
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fill0<WK, WL, PT, Q1W>, 256, smem);
   if (e != cudaSuccess) return e;
   auto tiles = [](const Prob& p) { return (p.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE; };
-  long long U = tiles(p0) + (2 * (p0.n * 2LL * p0.W + p0.n - 1) + 7) / 8;
-  if (Q1W >= 0 && p1) U += tiles(*p1) + (2 * (p1->n * 2LL * p1->W + p1->n - 1) + 7) / 8;
+  long long U = tiles(p0) + near_units1(p0.n, p0.W);
+  if (Q1W >= 0 && p1) U += tiles(*p1) + near_units1(p1->n, p1->W);
   grid = (long long)(nb > 0 ? nb : 1) * sms;
   if (grid > U) grid = U;
   return cudaSuccess;
