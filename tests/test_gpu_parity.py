@@ -89,6 +89,9 @@ SMALL = [
     banded_random_problem(97, seed=7, wH=1, wL=3, P=2),
     banded_random_problem(150, seed=8, wH=5, wL=0, P=1, drive_w=2),
     banded_random_problem(70, seed=9, wH=15, wL=7, P=1),
+    banded_random_problem(50, seed=11, wH=4, wL=2, P=1),   # mode 2, one dissipator
+    banded_random_problem(45, seed=12, wH=3, wL=0, P=1),   # mode 0 widths (3, 0)
+    banded_random_problem(77, seed=13, wH=1, wL=1, P=2),   # mode 0 widths (2, 1), runtime P
 ]
 
 
