@@ -115,9 +115,11 @@ class ClockSampler:
 
     def __init__(self, index: int):
         self.index = index
-        self.rows = []  # (sm_mhz, sm_max_mhz, reasons bitmask)
+        self.rows = []  # (t, sm_mhz, sm_max_mhz, reasons bitmask)
         self._stop = threading.Event()
+        self._ready = threading.Event()
         self._thr = None
+        self.t0 = self.t1 = None
 
     def _run_nvml(self):
         import pynvml
@@ -129,7 +131,8 @@ class ClockSampler:
             while not self._stop.is_set():
                 sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
                 rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.rows.append((float(sm), float(smax), int(rs)))
+                self.rows.append((time.perf_counter(), float(sm), float(smax), int(rs)))
+                self._ready.set()
                 self._stop.wait(0.005)
         finally:
             pynvml.nvmlShutdown()
@@ -142,7 +145,8 @@ class ClockSampler:
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 if out.returncode == 0 and out.stdout.strip():
                     r = [x.strip() for x in out.stdout.strip().split(",")]
-                    self.rows.append((float(r[0]), float(r[1]), int(r[2], 16)))
+                    self.rows.append((time.perf_counter(), float(r[0]), float(r[1]), int(r[2], 16)))
+                    self._ready.set()
             except Exception:
                 pass
             self._stop.wait(0.02)
@@ -156,24 +160,32 @@ class ClockSampler:
     def __enter__(self):
         self._thr = threading.Thread(target=self._run, daemon=True)
         self._thr.start()
-        time.sleep(0.02)  # the first samples precede the timed region's first step
+        self._ready.wait(5.0)  # NVML initialised and sampling before the timed region starts
+        self.t0 = time.perf_counter()
         return self
 
     def __exit__(self, *exc):
+        self.t1 = time.perf_counter()
         self._stop.set()
         if self._thr:
             self._thr.join(timeout=10)
 
     def summary(self):
-        if not self.rows:
+        inside = [r for r in self.rows if self.t0 is not None and self.t0 <= r[0] <= self.t1]
+        window = "timed region"
+        if not inside and self.rows:  # region shorter than the sampling period: nearest sample before it
+            before = [r for r in self.rows if self.t0 is None or r[0] < self.t0]
+            inside = before[-1:] if before else self.rows[:1]
+            window = "last sample before the timed region (region shorter than the 5 ms period)"
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         reasons = set()
-        for _, _, rs in self.rows:
+        for _, _, _, rs in inside:
             for bit, nm in self.REASONS.items():
                 if rs & bit:
                     reasons.add(nm)
-        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
-                "reasons": sorted(reasons), "samples": len(self.rows), "source": "nvml"}
+        return {"sm_mhz": statistics.median(r[1] for r in inside), "sm_max_mhz": max(r[2] for r in inside),
+                "reasons": sorted(reasons), "samples": len(inside), "window": window, "source": "nvml"}
 
 
 # ---------------------------------------------------------------------------------------

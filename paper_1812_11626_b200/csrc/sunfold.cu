@@ -1601,27 +1601,44 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_chain(ScanArgs A) {
   long long total;
   const long long ex = block_scan_ll(local, wsum, total);
   unsigned long long* st = A.status[y];
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {  // warp 0: publish the aggregate, then a warp-parallel look-back
+    const int lane = threadIdx.x;
     long long prefix = 0;
     if (chunk == 0) {
-      __threadfence();
-      atomicExch(&st[0], SCAN_P | (unsigned long long)total);
-    } else {
-      __threadfence();
-      atomicExch(&st[chunk], SCAN_A | (unsigned long long)total);
-      for (long long k = chunk - 1; k >= 0; --k) {
-        unsigned long long s;
-        do {
-          s = atomicAdd(&st[k], 0ull);
-        } while ((s & ~SCAN_V) == 0ull);
-        prefix += (long long)(s & SCAN_V);
-        if ((s & ~SCAN_V) == SCAN_P) break;
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(&st[0], SCAN_P | (unsigned long long)total);
       }
-      __threadfence();
-      atomicExch(&st[chunk], SCAN_P | (unsigned long long)(prefix + total));
+    } else {
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(&st[chunk], SCAN_A | (unsigned long long)total);
+      }
+      // lanes read 32 predecessors at once (lane 0 = the closest); the window ends at the
+      // closest inclusive prefix (P), aggregates (A) before it are summed
+      for (long long khi = chunk - 1;; khi -= 32) {
+        const long long k = khi - lane;
+        const volatile unsigned long long* vst = st;
+        unsigned long long s = k >= 0 ? vst[k] : SCAN_P;  // beyond chunk 0: an empty P
+        while (__any_sync(FULL, (s & ~SCAN_V) == 0ull))
+          if ((s & ~SCAN_V) == 0ull) s = vst[k];
+        const unsigned pmask = __ballot_sync(FULL, (s & ~SCAN_V) == SCAN_P);
+        const int lim = pmask ? __ffs(pmask) - 1 : 31;
+        long long part = lane <= lim ? (long long)(s & SCAN_V) : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+        prefix += part;
+        if (pmask) break;
+      }
+      if (lane == 0) {
+        __threadfence();
+        atomicExch(&st[chunk], SCAN_P | (unsigned long long)(prefix + total));
+      }
     }
-    prefix_s = prefix;
-    if (chunk == nchunks - 1 || nchunks == 0) *A.nnz[y] = prefix + total;
+    if (lane == 0) {
+      prefix_s = prefix;
+      if (chunk == nchunks - 1 || nchunks == 0) *A.nnz[y] = prefix + total;
+    }
   }
   __syncthreads();
   long long run = prefix_s + ex;
