@@ -204,12 +204,29 @@ def cpu_oracle_run(prob, reps: int = 1):
     return nnz, times, sparse.max_threads()
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(prob, reps: int = 2):
     nnz, times, cores = cpu_oracle_run(prob, reps)
     t = statistics.mean(times)
-    return {"value": nnz / t, "unit": UNIT, "cores": cores, "kind": "oracle",
+    # one single-threaded unfold as well
+    from oracle import sparse
+
+    t1 = time.perf_counter()
+    sparse.unfold_problem(prob, nthreads=1)
+    t1 = time.perf_counter() - t1
+    return {"value": nnz / t, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+            "single_thread": {"value": nnz / t1, "unit": UNIT, "seconds_per_unfold": t1},
             "sample": f"{reps} full unfolds (Q0+K+Q1) of {prob.name} by oracle O2 (oracle/sparse_o2.c, "
-                      f"OpenMP, column-wise trace definition); mean {t:.3f} s each",
+                      f"OpenMP, column-wise trace definition); mean {t:.3f} s each; plus one on 1 thread",
             "seconds_per_unfold": t}
 
 

@@ -193,6 +193,7 @@ struct sun_plan_s {
   unsigned long long graph_clock = 0;
   bool use_graphs = true;
   HeaderPrefix* hpin = nullptr;  // pinned host copy of the header prefix (nnz readback)
+  int hdr_enqueued = 0;          // the last count/run sequence already copies the header to hpin
   ~sun_plan_s() {
     if (hpin) cudaFreeHost(hpin);
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
@@ -2421,7 +2422,8 @@ int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
   }
   HeaderPrefix hloc;
   HeaderPrefix* hp = pl->hpin ? pl->hpin : &hloc;
-  CK(cudaMemcpyAsync(hp, pl->ws + pl->lay.hdr, sizeof(HeaderPrefix), cudaMemcpyDeviceToHost, pl->count_stream));
+  if (!pl->hdr_enqueued)
+    CK(cudaMemcpyAsync(hp, pl->ws + pl->lay.hdr, sizeof(HeaderPrefix), cudaMemcpyDeviceToHost, pl->count_stream));
   CK(cudaStreamSynchronize(pl->count_stream));
   const HeaderPrefix h = *hp;
   if (h.flags & F_MALFORMED) return SUN_ERR_ARG;
@@ -2483,13 +2485,30 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
 // the sequence (captured on the plan's capture stream; kernel arguments, including the output
 // pointers and capacities, are part of the key), or enqueue directly if graphs are disabled.
 static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st) {
+  // the nnz / flags readback of sun_plan_nnz rides in the same sequence (a memcpy node of the
+  // graph into pinned host memory), so sun_plan_nnz only waits for the stream
+  if (kind != 1 && !pl->hpin && cudaMallocHost(&pl->hpin, sizeof(HeaderPrefix)) != cudaSuccess) {
+    pl->hpin = nullptr;  // pageable fallback in sun_plan_nnz
+    (void)cudaGetLastError();
+  }
+  const bool readback = kind != 1 && pl->hpin;
   auto direct = [&](cudaStream_t s) -> int {
     int rc = SUN_OK;
     if (kind != 1) rc = enqueue_count(pl, s);
     if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s);
+    if (rc == SUN_OK && readback) {
+      const cudaError_t e =
+          cudaMemcpyAsync(pl->hpin, pl->ws + pl->lay.hdr, sizeof(HeaderPrefix), cudaMemcpyDeviceToHost, s);
+      if (e != cudaSuccess) rc = cuda_fail(e);
+    }
     return rc;
   };
-  if (!pl->use_graphs) return direct(st);
+  pl->hdr_enqueued = 0;
+  if (!pl->use_graphs) {
+    const int rc = direct(st);
+    pl->hdr_enqueued = rc == SUN_OK && readback ? 1 : 0;
+    return rc;
+  }
   uintptr_t key[12] = {(uintptr_t)kind, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   if (kind != 0) {
     key[1] = (uintptr_t)Q0->row_ptr; key[2] = (uintptr_t)Q0->col; key[3] = (uintptr_t)Q0->val;
@@ -2534,6 +2553,7 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
     pl->graphs.push_back(ge);
   }
   CK(cudaGraphLaunch(exec, st));
+  pl->hdr_enqueued = readback ? 1 : 0;
   return SUN_OK;
 }
 
