@@ -168,6 +168,13 @@ int sun_expand_state(const sun_zcsr* rho, double* v, void* stream);
  * diag: device float64[N].  Asynchronous.  Errors: SUN_ERR_ARG, SUN_ERR_DIM, _CUDA. */
 int sun_state_diag(const double* v, int32_t n, double* diag, void* stream);
 
+/* rho(T) from its coherence vector (Step 3.2; Eq. 5): rho = I/N + sum_j v_j F_j,
+ * written as a dense complex N x N array (row-major, interleaved re, im; all 2 N^2 doubles
+ * written).  Off-diagonal entries from the S_ab / J_ab coefficients, the diagonal as in
+ * sun_state_diag.  v: device float64[N^2 - 1]; rho: device float64[2 N^2].  Asynchronous.
+ * Errors: SUN_ERR_ARG, SUN_ERR_DIM, SUN_ERR_CUDA. */
+int sun_state_reconstruct(const double* v, int32_t n, double* rho, void* stream);
+
 /* Fixed-step classic fourth-order Runge-Kutta (the paper's integrator, Step 3.1 P:464-470) of
  *   dv/dt = (Q0 + eps(t) Q1) v + K,   eps(t) = eps0 + eps1 sin(omega t)   (Eq. 9, reading R10)
  * from t0 over nsteps steps of size h:

@@ -310,6 +310,16 @@ def rk4(Q0: CSR, Q1: Optional[CSR], K: Optional[torch.Tensor], v: torch.Tensor, 
     return v
 
 
+def state_reconstruct(v: torch.Tensor, n: int, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """rho = I/N + sum_j v_j F_j as a dense complex128 N x N tensor (Step 3.2; sun_state_reconstruct)."""
+    assert v.is_cuda and v.dtype == torch.float64 and v.numel() == n * n - 1
+    rho = out if out is not None else torch.empty((n, n), dtype=torch.complex128, device=v.device)
+    assert rho.dtype == torch.complex128 and rho.is_contiguous() and rho.numel() == n * n
+    _check(lib().sun_state_reconstruct(ctypes.c_void_p(v.data_ptr()), n, ctypes.c_void_p(rho.data_ptr()),
+                                       ctypes.c_void_p(_stream_handle(stream))), "sun_state_reconstruct")
+    return rho
+
+
 def dense_work_bytes(n: int, chunk: int = 1) -> int:
     """Scratch bytes of unfold_dense for `chunk` realisations at once (sun_dense_work_bytes)."""
     return int(lib().sun_dense_work_bytes(n, chunk))

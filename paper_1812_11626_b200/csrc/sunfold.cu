@@ -1854,9 +1854,31 @@ __global__ void __launch_bounds__(1024) k_state_diag(int n, const int64_t* __res
   }
 }
 
+// rho(T) (Step 3.2; Eq. 5): rho = I/N + sum_j v_j F_j as a dense complex N x N array.
+// Off-diagonal entries from the S/J pair (thread per pair): rho_ab = (v_S - i v_J)/sqrt2,
+// rho_ba = (v_S + i v_J)/sqrt2; the diagonal comes from k_state_pop writing with a stride.
+__global__ void k_state_rho_offdiag(int n, const double* __restrict__ v, double2* __restrict__ rho) {
+  const long long np = (long long)n * (n - 1) / 2;
+  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (p >= np) return;
+  const double t = 2.0 * n - 1.0;
+  long long a = (long long)floor((t - sqrt(fmax(t * t - 8.0 * (double)p, 0.0))) * 0.5);
+  if (a < 0) a = 0;
+  while (a > 0 && a * (2LL * n - a - 1) / 2 > p) --a;
+  while (a + 1 <= n - 2 && (a + 1) * (2LL * n - a - 2) / 2 <= p) ++a;
+  const long long b = a + 1 + (p - a * (2LL * n - a - 1) / 2);
+  const double s = v[p], j = v[np + p];
+  const double r = 0.70710678118654752440;
+  rho[a * n + b] = make_double2(s * r, -j * r);
+  rho[b * n + a] = make_double2(s * r, j * r);
+}
+
 // diag[a] = 1/N + sum_{l >= max(a,1)} v_{D^l} delta_l(a): delta_l(a) = 1/sqrt(l(l+1)) for
 // l > a, -a/sqrt(a(a+1)) for l = a.  Suffix sums by one CTA (fixed order).
-__global__ void __launch_bounds__(1024) k_state_pop(int n, const double* __restrict__ v, double* diag) {
+// dstride: element stride of the output (1: diag[a]; 2(N+1): the real parts of the diagonal of
+// an interleaved complex N x N array, whose imaginary parts are then set to 0)
+__global__ void __launch_bounds__(1024) k_state_pop(int n, const double* __restrict__ v, double* diag,
+                                                    long long dstride = 1) {
   __shared__ double carry_s;
   __shared__ double wsum[32];
   const long long dbase = (long long)n * (n - 1) - 1;
@@ -1889,7 +1911,8 @@ __global__ void __launch_bounds__(1024) k_state_pop(int n, const double* __restr
     const double suf = carry_s + (wid > 0 ? wsum[wid - 1] : 0.0) + x;  // sum_{l > a}
     if (a >= 0) {
       const double self = a >= 1 ? -(double)a * v[dbase + a] / sqrt((double)a * (double)(a + 1)) : 0.0;
-      diag[a] = 1.0 / (double)n + suf + self;
+      diag[(long long)a * dstride] = 1.0 / (double)n + suf + self;
+      if (dstride > 1) diag[(long long)a * dstride + 1] = 0.0;
     }
     __syncthreads();
     if (threadIdx.x == blockDim.x - 1) carry_s = suf;
@@ -2681,6 +2704,18 @@ int sun_state_diag(const double* v, int32_t n, double* diag, void* stream) {
   if (!v || !diag) return SUN_ERR_ARG;
   if (n < 2 || n > 46340) return SUN_ERR_DIM;
   k_state_pop<<<1, 1024, 0, (cudaStream_t)stream>>>(n, v, diag);
+  CK(cudaGetLastError());
+  return SUN_OK;
+}
+
+int sun_state_reconstruct(const double* v, int32_t n, double* rho, void* stream) {
+  if (!v || !rho) return SUN_ERR_ARG;
+  if (n < 2 || n > 46340) return SUN_ERR_DIM;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long np = (long long)n * (n - 1) / 2;
+  double2* r = reinterpret_cast<double2*>(rho);
+  k_state_rho_offdiag<<<(unsigned)((np + 255) / 256), 256, 0, st>>>(n, v, r);
+  k_state_pop<<<1, 1024, 0, st>>>(n, v, rho, 2LL * (n + 1));
   CK(cudaGetLastError());
   return SUN_OK;
 }

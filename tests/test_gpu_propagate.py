@@ -30,6 +30,19 @@ def _dense_random_rho(n, seed):
     return rho / np.trace(rho)
 
 
+@pytest.mark.parametrize("n", [2, 6, 33, 100])
+def test_state_reconstruct(n):
+    """rho(T) (Step 3.2): sun_state_reconstruct(v) against oracle basis.reconstruct(v) and
+    against the density matrix v was projected from (Eq. 5 is an isometry for Tr rho = 1)."""
+    sun = _sun()
+    rho = _dense_random_rho(n, 40 + n)
+    v = basis.project(rho).real
+    got = sun.state_reconstruct(torch.tensor(v, device="cuda"), n).cpu().numpy()
+    ref = basis.reconstruct_fast(v, n)
+    assert np.abs(got - ref).max() <= 1e-14 * max(1.0, np.abs(ref).max())
+    assert np.abs(got - rho).max() <= 1e-13 * max(1.0, np.abs(rho).max())
+
+
 def test_expand_state_and_populations():
     sun = _sun()
     for n, seed in ((2, 0), (6, 1), (33, 2)):
