@@ -154,23 +154,32 @@ struct WarpTile {
 __device__ __forceinline__ double2 jcomb(double2 s, double2 j, bool minus) {  // (s -+ i j)/sqrt2
   return cscale(cadd(s, minus ? cmulmi(j) : cmuli(j)), RS2);
 }
+// WP (small N, a single tile per row): warp per pair instead of CTA per pair, WPC pairs per CTA.
+template <bool WP>
 __global__ void __launch_bounds__(DT, 2) k_dense_expand(const DenseArgs g) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpTile& T = reinterpret_cast<WarpTile*>(dsm)[wid];
-  double2* sdiag = reinterpret_cast<double2*>(dsm + WPC * sizeof(WarpTile));  // [2][N]
   const int n = g.n, r = blockIdx.y;
   const long long m = g.m, np = g.np, n2 = (long long)n * n;
-  const long long p = blockIdx.x;
+  const long long p = WP ? (long long)blockIdx.x * WPC + wid : blockIdx.x;
+  if (WP && p >= np) return;  // warp-uniform; no CTA barrier in WP mode
+  double2* sdiag = reinterpret_cast<double2*>(dsm + WPC * sizeof(WarpTile)) + (WP ? wid * 2 * n : 0);  // [2][N]
   int x, y;
   pair_of(n, p, x, y);
   const double2* A = g.A + (long long)(g.r0 + r) * m * m;
   const double2 *aS = A + p * m, *aJ = A + (np + p) * m;
-  if (wid == 0)
+  if constexpr (WP) {
     warp_diag_from_d(aS + 2 * np, sdiag, n);
-  else if (wid == 1)
     warp_diag_from_d(aJ + 2 * np, sdiag + n, n);
-  __syncthreads();
+    __syncwarp();
+  } else {
+    if (wid == 0)
+      warp_diag_from_d(aS + 2 * np, sdiag, n);
+    else if (wid == 1)
+      warp_diag_from_d(aJ + 2 * np, sdiag + n, n);
+    __syncthreads();
+  }
   double2* Z = g.Z + (long long)r * n2 * n2;
   double2* zxy = Z + ((long long)x * n + y) * n;  // + b N^3 + d
   double2* zyx = Z + ((long long)y * n + x) * n;
@@ -180,7 +189,7 @@ __global__ void __launch_bounds__(DT, 2) k_dense_expand(const DenseArgs g) {
   int cnt = 0;
   for (int tb = 0; tb < nt; ++tb) {
     for (int td = tb; td < nt; ++td) {
-      if (cnt++ % WPC != wid) continue;  // warp-uniform
+      if (!WP && cnt++ % WPC != wid) continue;  // warp-uniform
       const int b0 = tb * TW, d0 = td * TW;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {  // two batches of 4 rows: all loads first, then the math
@@ -297,14 +306,17 @@ __device__ __forceinline__ double2 zprime(const double2* __restrict__ zrow, cons
 // blocks Z'[w][u] of both rows are staged in warp-private shared memory (contiguous loads),
 // the direct blocks Z'[u][w] are read in the compute phase (contiguous); outputs pair(u, w)
 // go out in runs of consecutive pairs.  grid (np, chunk)
+template <bool WP>
 __global__ void __launch_bounds__(DT, 2) k_dense_project(const DenseArgs g) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   WarpTile& T = reinterpret_cast<WarpTile*>(dsm)[wid];
-  double* sv = reinterpret_cast<double*>(dsm + WPC * sizeof(WarpTile));  // [2][N] diagonal of V_S, V_J
   const int n = g.n, r = blockIdx.y;
   const long long m = g.m, np = g.np, n2 = (long long)n * n;
-  const long long p = blockIdx.x;
+  const long long p = WP ? (long long)blockIdx.x * WPC + wid : blockIdx.x;
+  if (WP && p >= np) return;  // warp-uniform; no CTA barrier in WP mode
+  // [2][N] diagonal of V_S, V_J
+  double* sv = reinterpret_cast<double*>(dsm + WPC * sizeof(WarpTile)) + (WP ? wid * 2 * n : 0);
   int x, y;
   pair_of(n, p, x, y);
   const bool has_a = g.A != nullptr;
@@ -319,7 +331,7 @@ __global__ void __launch_bounds__(DT, 2) k_dense_project(const DenseArgs g) {
   int cnt = 0;
   for (int tu = 0; tu < nt; ++tu) {
     for (int tw = tu; tw < nt; ++tw) {
-      if (cnt++ % WPC != wid) continue;  // warp-uniform
+      if (!WP && cnt++ % WPC != wid) continue;  // warp-uniform
       const int u0 = tu * TW, w0 = tw * TW;
       {  // stage the transposed blocks: all loads first
         double2 za[8], zb[8];
@@ -371,19 +383,27 @@ __global__ void __launch_bounds__(DT, 2) k_dense_project(const DenseArgs g) {
       __syncwarp();
     }
   }
-  for (int c = threadIdx.x; c < n; c += DT) {
+  for (int c = WP ? lane : (int)threadIdx.x; c < n; c += WP ? 32 : DT) {
     const double2 a = zprime(zxy, kh, n, has_a, x, y, c, c), b = zprime(zyx, kh, n, has_a, y, x, c, c);
     sv[c] = (a.x + b.x) * RS2;            // Re V_S[c,c]
     sv[n + c] = (a.y - b.y) * RS2;        // Re V_J[c,c] = Re((-i a + i b)/sqrt2)
   }
-  __syncthreads();
-  __shared__ double tot[2];
-  if (wid == 0)
+  __shared__ double tot_all[WPC][2];
+  double* tot = tot_all[WP ? wid : 0];
+  if constexpr (WP) {
+    __syncwarp();
     warp_d_from_diag(sv, qS + 2 * np, &tot[0], n);
-  else if (wid == 1)
     warp_d_from_diag(sv + n, qJ + 2 * np, &tot[1], n);
-  __syncthreads();
-  if (g.K && threadIdx.x == 0) {
+    __syncwarp();
+  } else {
+    __syncthreads();
+    if (wid == 0)
+      warp_d_from_diag(sv, qS + 2 * np, &tot[0], n);
+    else if (wid == 1)
+      warp_d_from_diag(sv + n, qJ + 2 * np, &tot[1], n);
+    __syncthreads();
+  }
+  if (g.K && (WP ? lane == 0 : threadIdx.x == 0)) {
     double* K = g.K + (long long)(g.r0 + r) * m;
     K[p] = tot[0] / n;
     K[np + p] = tot[1] / n;
@@ -478,12 +498,20 @@ int sun_unfold_dense(int32_t n, int32_t batch, const double* H, const double* A,
   g.UD = reinterpret_cast<double2*>(ws + chunk * al(16 * n2 * n2));
   g.Kh = reinterpret_cast<double2*>(ws + chunk * (al(16 * n2 * n2) + al(16 * (nn - 1) * n2)));
   const unsigned gsq = (unsigned)((n2 + DT - 1) / DT);
-  const size_t sm_exp = WPC * sizeof(WarpTile) + 2 * n * sizeof(double2);
-  const size_t sm_prj = WPC * sizeof(WarpTile) + 2 * n * sizeof(double);
+  // N <= 2 TW: at most 3 tiles of 16 x 16 per pair row, so one warp per pair (WPC pairs per CTA)
+#ifndef SUN_DENSE_WP_MAXN
+#define SUN_DENSE_WP_MAXN 32
+#endif
+  const bool wp = n <= SUN_DENSE_WP_MAXN;
+  const size_t sm_exp = WPC * sizeof(WarpTile) + (wp ? WPC : 1) * 2 * n * sizeof(double2);
+  const size_t sm_prj = WPC * sizeof(WarpTile) + (wp ? WPC : 1) * 2 * n * sizeof(double);
+  const unsigned gpair = (unsigned)(wp ? (g.np + WPC - 1) / WPC : g.np);
   {
-    cudaError_t e = cudaFuncSetAttribute(k_dense_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_exp);
+    cudaError_t e = cudaFuncSetAttribute(wp ? k_dense_expand<true> : k_dense_expand<false>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_exp);
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(k_dense_project, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_prj);
+      e = cudaFuncSetAttribute(wp ? k_dense_project<true> : k_dense_project<false>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_prj);
     if (e != cudaSuccess) return sunfold_cuda_fail(e);
   }
   for (long long r0 = 0; r0 < batch; r0 += chunk) {
@@ -491,11 +519,17 @@ int sun_unfold_dense(int32_t n, int32_t batch, const double* H, const double* A,
     g.r0 = (int)r0;
     if (A) {
       k_dense_dexp<<<dim3((unsigned)(n - 1), cb), DT, n * sizeof(double2), st>>>(g);
-      k_dense_expand<<<dim3((unsigned)g.np, cb), DT, sm_exp, st>>>(g);
+      if (wp)
+        k_dense_expand<true><<<dim3(gpair, cb), DT, sm_exp, st>>>(g);
+      else
+        k_dense_expand<false><<<dim3(gpair, cb), DT, sm_exp, st>>>(g);
       k_dense_zdiag<<<dim3(gsq, cb), DT, 0, st>>>(g);
     }
     k_dense_kh<<<dim3(gsq, cb), DT, 0, st>>>(g);
-    k_dense_project<<<dim3((unsigned)g.np, cb), DT, sm_prj, st>>>(g);
+    if (wp)
+      k_dense_project<true><<<dim3(gpair, cb), DT, sm_prj, st>>>(g);
+    else
+      k_dense_project<false><<<dim3(gpair, cb), DT, sm_prj, st>>>(g);
     k_dense_vdiag<<<dim3(gsq, cb), DT, 0, st>>>(g);
     k_dense_drows<<<dim3((unsigned)(n - 1), cb), DT, n * sizeof(double), st>>>(g);
     const cudaError_t e = cudaGetLastError();

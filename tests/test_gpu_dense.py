@@ -80,7 +80,7 @@ def test_dense_chunking_is_bitwise_stable():
     assert torch.equal(Qs, Q4[2]) and torch.equal(Ks, K4[2])
 
 
-@pytest.mark.parametrize("n,P", [(33, 2), (40, 3)])
+@pytest.mark.parametrize("n,P", [(17, 3), (32, 2), (33, 2), (40, 3)])
 def test_dense_spectral_form_vs_o2(n, P):
     """A = sum_p gamma_p l_p l_p^+ (rank P, dense in the F basis) against O2 on L_p = sum_j l_pj F_j."""
     sun = _sun()
@@ -127,7 +127,7 @@ def test_dense_banded_spectral_form_vs_o2_full_size():
     assert np.abs(K - r["K"]).max() <= 1e-12 * sc
 
 
-@pytest.mark.parametrize("n", [40, 64, 100])
+@pytest.mark.parametrize("n", [16, 32, 40, 64, 100])
 def test_dense_depolarising_closed_form(n):
     """A = gamma I: L_D(X) = gamma (Tr(X) I - N X) (Fierz), so Q = Q_H - gamma N I and K = 0."""
     sun = _sun()
