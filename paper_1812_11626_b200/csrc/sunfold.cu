@@ -548,39 +548,6 @@ __device__ __forceinline__ int near_item(const Prob& pr, long long item, int& a,
   return 0;
 }
 
-// Units u = blockIdx.x + k gridDim.x of a persistent loop over U units, nn of them near units
-// spread evenly (Bresenham): unit u is near iff floor((u + 1) nn / U) > floor(u nn / U) =: k0,
-// near index k0, else far index u - k0.  Kept incrementally (k0 and r = u nn mod U advance by
-// the constants of G nn = qG U + rG), so the loop needs no division (nn <= U).
-struct UnitIter {
-  long long u, k0, r;  // current unit, floor(u nn / U), u nn mod U
-  long long U, nn, qG, rG, G;
-  __device__ __forceinline__ void init(long long u0, long long G_, long long U_, long long nn_) {
-    U = U_ > 0 ? U_ : 1;
-    nn = nn_;
-    G = G_;
-    u = u0;
-    k0 = u0 * nn / U;
-    r = u0 * nn % U;
-    qG = G * nn / U;
-    rG = G * nn % U;
-  }
-  __device__ __forceinline__ void advance() {
-    u += G;
-    k0 += qG;
-    r += rG;
-    if (r >= U) {
-      r -= U;
-      ++k0;
-    }
-  }
-  // near unit (idx = near index) or far unit (idx = far index)
-  __device__ __forceinline__ bool decode(long long& idx) const {
-    const bool is_near = r + nn >= U;
-    idx = is_near ? k0 : u - k0;
-    return is_near;
-  }
-};
 
 // ---- count pass ------------------------------------------------------------------------
 // Every count CTA is a single warp, so no unit waits on a slow sibling warp:
@@ -1182,7 +1149,7 @@ struct MatFill {
 
 // Fill pass of Q0 and, with Q1W >= 0, of Q1 (widths Q1W, 0, no dissipators; staging-free
 // rows only, i.e. Q1W = 0) in one persistent launch: units u = blockIdx.x + k gridDim.x over
-//   [Q0 far tiles, last first, with Q0 near units spread evenly among them][Q1 near][Q1 tiles]
+//   [Q0 near units][Q0 far tiles, last first][Q1 near][Q1 tiles]
 // The next far tile's counts and offsets are loaded before the current unit runs.
 template <int WK, int WL, int PT, int Q1W>
 __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFill m1) {
@@ -1208,11 +1175,13 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
   FarCtx prf1{};
   if (HAS1) prf1 = FarCtx{m1.pr.K.v, m1.pr.L, *m1.pr.tau_ptr, m1.pr.np, m1.pr.n, m1.pr.P};
   // unit -> kind: 0 Q0 far tile, 1 Q0 near unit, 2 Q1 near unit, 3 Q1 tile; idx
-  auto decode = [&](const UnitIter& it, long long& idx) -> int {
-    long long v = it.u;
+  auto decode = [&](long long v, long long& idx) -> int {
+    if (v < nn0) {  // the latency-bound near units first (measured: equal at c4, faster at c2)
+      idx = v;
+      return 1;
+    }
     if (v < U0) {
-      if (it.decode(idx)) return 1;
-      idx = nt0 - 1 - idx;  // far tiles, last first
+      idx = nt0 - 1 - (v - nn0);  // far tiles, last first
       return 0;
     }
     v -= U0;
@@ -1223,22 +1192,18 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
     idx = v - nn1;
     return 3;
   };
-  UnitIter it, nit;  // this unit, the next one (prefetched)
-  it.init(blockIdx.x, gridDim.x, U0, nn0);
-  nit = it;
   TileIn nxt{0, 0, 0, 0};
-  auto prefetch = [&](const UnitIter& v) {
+  auto prefetch = [&](long long v) {
     long long idx;
-    if (v.u < U && decode(v, idx) == 0 && !FF::DIRECT)
+    if (v < U && decode(v, idx) == 0 && !FF::DIRECT)
       nxt = load_tile_in(m0.pr.np, m0.pr.npt, idx, m0.cnt, m0.fo.toff);
   };
-  prefetch(nit);
-  for (; it.u < U; it.advance()) {  // block-uniform
+  prefetch(blockIdx.x);
+  for (long long u = blockIdx.x; u < U; u += gridDim.x) {  // block-uniform
     const TileIn cur = nxt;
-    nit.advance();
-    prefetch(nit);
+    prefetch(u + gridDim.x);
     long long idx;
-    const int kind = decode(it, idx);
+    const int kind = decode(u, idx);
     if (kind == 0) {
       if constexpr (FF::DIRECT)
         fill_direct_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, m0.cnt, m0.fo);
@@ -1353,11 +1318,10 @@ __global__ void __launch_bounds__(256) k_fill2(const MatFill mf) {
   pr.tau = *p0.tau_ptr;
   const long long nn = near_units(p0.n, p0.W);
   const long long nt = (p0.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE, U = nt + nn;
-  UnitIter it;
-  it.init(blockIdx.x, gridDim.x, U, nn);
-  for (; it.u < U; it.advance()) {  // block-uniform
-    long long idx;
-    if (it.decode(idx)) {
+  for (long long u = blockIdx.x; u < U; u += gridDim.x) {  // block-uniform: near units first
+    const bool nearu = u < nn;
+    const long long idx = nearu ? u : u - nn;
+    if (nearu) {
       fill_near_unit_b(pr, idx, mf.cnt, mf.fo, mf.side, nrows[threadIdx.x >> 5]);
     } else {
       fill2_far_tile<WK, WL, PT>(pr, nt - 1 - idx, mf.cnt, mf.fo);
