@@ -228,6 +228,21 @@ size_t sun_dense_work_bytes(int32_t n, int32_t chunk);
 /* Kernel launches sun_unfold_dense makes for these arguments (0 if it would fail). */
 int sun_dense_launches(int32_t n, int32_t batch, int32_t has_a, size_t work_bytes);
 
+/* ---- Structure constants (Step 2.2; Eqs. 2-4) ----
+ * The nonzero f_mns (which = 0) or d_mns (which = 1) of SU(N) over the basis F (generator order
+ * R5), every ordered triple (f totally antisymmetric, d totally symmetric), generated on
+ * the device from the closed-form classes (triangle, pair, DDD).  Counts:
+ * NZ_F = 5N^3 - 9N^2 - 2N + 6, NZ_D = 6N^3 - N(21N+7)/2 + 1.  The unfold itself never
+ * stores them.  Deterministic order (by index pair, then class).
+ * n: 2 <= N <= 1024.  idx: device int32[cap][3] (m, n, s) and val: device double[cap], or both
+ * NULL with cap = 0 (count only).  nnz: host int64*, the total (written; the call synchronises
+ * `stream`).  work: device scratch of sun_sc_work_bytes(n) bytes.
+ * Errors: SUN_ERR_DIM, SUN_ERR_ARG, SUN_ERR_CAPACITY (work too small, or cap < nnz: entries
+ * beyond cap are not written), SUN_ERR_CUDA. */
+int sun_structure_constants(int32_t n, int32_t which, int32_t* idx, double* val, int64_t cap, int64_t* nnz,
+                            void* work, size_t work_bytes, void* stream);
+size_t sun_sc_work_bytes(int32_t n);
+
 /* Fill a diagnostics struct for the plan. */
 int sun_plan_info(sun_plan plan, sun_plan_info_t* info);
 

@@ -320,6 +320,31 @@ def state_reconstruct(v: torch.Tensor, n: int, out: Optional[torch.Tensor] = Non
     return rho
 
 
+def structure_constants(n: int, which: str = "f", count_only: bool = False, stream=None):
+    """Nonzero f_mns ('f') or d_mns ('d') of SU(N), every ordered triple, generated on the GPU from
+    index arithmetic (sun_structure_constants; Step 2.2).  Returns (idx int32 (nnz, 3),
+    val float64 (nnz,)) on the device, or the count only."""
+    w = {"f": 0, "d": 1}[which]
+    dev = torch.device("cuda")
+    nb = int(lib().sun_sc_work_bytes(n))
+    if nb == 0:
+        raise SunError(f"sun_sc_work_bytes: N = {n} out of range")
+    work = torch.empty((nb + 7) // 8, dtype=torch.int64, device=dev)
+    cnt = ctypes.c_int64()
+    h = ctypes.c_void_p(_stream_handle(stream))
+    _check(lib().sun_structure_constants(n, w, None, None, 0, ctypes.addressof(cnt), ctypes.c_void_p(work.data_ptr()),
+                                         nb, h), "sun_structure_constants")
+    if count_only:
+        return int(cnt.value)
+    nnz = int(cnt.value)
+    idx = torch.empty((max(nnz, 1), 3), dtype=torch.int32, device=dev)
+    val = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
+    _check(lib().sun_structure_constants(n, w, ctypes.c_void_p(idx.data_ptr()), ctypes.c_void_p(val.data_ptr()), nnz,
+                                         ctypes.addressof(cnt), ctypes.c_void_p(work.data_ptr()), nb, h),
+           "sun_structure_constants")
+    return idx[:nnz], val[:nnz]
+
+
 def dense_work_bytes(n: int, chunk: int = 1) -> int:
     """Scratch bytes of unfold_dense for `chunk` realisations at once (sun_dense_work_bytes)."""
     return int(lib().sun_dense_work_bytes(n, chunk))

@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsunfold.so")
-SOURCES = [os.path.join(CSRC, "sunfold.cu"), os.path.join(CSRC, "sunfold_dense.cu")]
+SOURCES = [os.path.join(CSRC, "sunfold.cu"), os.path.join(CSRC, "sunfold_dense.cu"), os.path.join(CSRC, "sunfold_sc.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, "sunfold_kernels.cuh"), os.path.join(ROOT, "include", "sunfold.h")]
 
 NVCC_FLAGS = [
