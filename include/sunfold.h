@@ -193,6 +193,20 @@ int sun_rk4(const sun_dcsr* Q0, const sun_dcsr* Q1, const double* K, double eps0
 /* Bytes of scratch sun_rk4 needs for an M-row system (4 M doubles + M + 2 ints); 0 if M <= 0. */
 size_t sun_rk4_work_bytes(int64_t m);
 
+/* F1, matrix-free: the same fixed-step RK4 as sun_rk4 on the system of a counted plan (after
+ * sun_count or sun_run on the current operator values), without reading Q0 / Q1: every stage
+ * regenerates the far-pair entries from the plan's band storage with the count/fill
+ * expressions and tau masks, takes the near and D rows from the count pass's side buffer
+ * (chain tails in O(1) from a per-stage prefix over the D coefficients), K from the same data.
+ * Supported: mode-0 plans (sun_plan_info mode_q0 = 0) without a drive or with a diagonal H1;
+ * else SUN_ERR_BANDWIDTH.  v: device float64[M], in/out.  work: device scratch of
+ * sun_rk4_plan_work_bytes(plan) bytes (4 M + N doubles).  Asynchronous on `stream`.
+ * Errors: SUN_ERR_ARG, SUN_ERR_STATE (plan not counted), SUN_ERR_BANDWIDTH, SUN_ERR_CAPACITY,
+ * SUN_ERR_CUDA. */
+int sun_rk4_plan(sun_plan plan, double eps0, double eps1, double omega, double t0, double h, int64_t nsteps,
+                 double* v, void* work, size_t work_bytes, void* stream);
+size_t sun_rk4_plan_work_bytes(sun_plan plan);
+
 /* Enable (1, the default) or disable (0) CUDA-graph replay of this plan's enqueue sequences.
  * With graphs, sun_count / sun_unfold / sun_run capture their launches once per distinct
  * output buffer set and replay the graph (one launch); without, every kernel is launched

@@ -221,6 +221,20 @@ class Plan:
         nnz0, nnz1 = self.nnz()
         return self.fill(nnz0, nnz1, out)
 
+    def rk4(self, v: torch.Tensor, h: float, nsteps: int, t0: float = 0.0, eps0: float = 0.0, eps1: float = 0.0,
+            omega: float = 1.0, work=None) -> torch.Tensor:
+        """Matrix-free RK4 of this plan's system in place on v (sun_rk4_plan; F1): Q0 / Q1 are
+        regenerated in every stage instead of read.  Needs a counted plan (after run())."""
+        L = lib()
+        nb = int(L.sun_rk4_plan_work_bytes(self._plan))
+        w = work if work is not None else torch.empty((nb + 7) // 8, dtype=torch.float64, device=v.device)
+        wb = w.numel() * w.element_size()
+        _check(L.sun_rk4_plan(self._plan, ctypes.c_double(eps0), ctypes.c_double(eps1), ctypes.c_double(omega),
+                              ctypes.c_double(t0), ctypes.c_double(h), ctypes.c_int64(nsteps),
+                              ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(w.data_ptr()), ctypes.c_size_t(wb),
+                              ctypes.c_void_p(_stream_handle(self.stream))), "sun_rk4_plan")
+        return v
+
     def launches_per_run(self) -> int:
         """Kernels of this library launched by one run() (sun_run: count + fill)."""
         inf = self.info()

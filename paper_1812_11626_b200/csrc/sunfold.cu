@@ -1733,6 +1733,173 @@ __global__ void __launch_bounds__(256) k_rk4_stage(const Rk4Stage S) {
   if (lane == 0) rk4_epilogue(S, row, s0 + S.eps * s1 + (S.K ? S.K[row] : 0.0));
 }
 
+// ---------------------------------------------------------------------------------------
+// F1, matrix-free (sun_rk4_plan): one RK4 stage y = (Q0 + eps Q1) x + K with x = v + c k_prev,
+// Q0 and Q1 never read from memory.  Far pairs: thread per pair, the U values regenerated from
+// the band storage exactly as the count / fill passes do (same expressions, same tau masks), so
+// each stored entry of Q0 is reproduced bit for bit.  Near-pair and D rows: warp per side row,
+// window entries from the count pass's side buffer, the chain tail sum_l tr inv[l] x_{D^l} in
+// O(1) from the prefix P[l] = sum_{l' <= l} inv[l'] x_{D^l'} (k_mf_prefix, one CTA per stage).
+// Q1: a diagonal drive only (Q1 = Q_H[H1] couples S_ab and J_ab), from the H1 band.  Mode 0.
+// ---------------------------------------------------------------------------------------
+struct MfStage {
+  Prob p0, p1;        // Q0 and (has1) Q1 problems of the plan
+  NearSide side;      // Q0 side buffer (count pass)
+  int has1;
+  const double* pref; // [n]
+  double* pref_out;
+  const double* x;    // this stage's input (v, v + h/2 k1, v + h/2 k2, v + h k3)
+  double* xn;         // the next stage's input, written by the epilogue (stages 1-3)
+  const double* v;
+  double* acc;
+  double* vout;
+  double eps, cn, h6; // cn: the next stage's step (h/2, h/2, h)
+  long long m;
+  int mode, nfar_blocks;
+};
+
+__device__ __forceinline__ double mf_x(const MfStage& S, long long j) { return __ldg(&S.x[j]); }
+// stage k_i = y: acc = k1 / acc += 2 k_i, and the next input v + cn k_i; or the RK4 update
+__device__ __forceinline__ void mf_epilogue(const MfStage& S, long long row, double y) {
+  if (S.mode == 0) {
+    S.acc[row] = y;
+    S.xn[row] = S.v[row] + S.cn * y;
+  } else if (S.mode == 1) {
+    S.acc[row] += 2.0 * y;
+    S.xn[row] = S.v[row] + S.cn * y;
+  } else {
+    S.vout[row] = S.v[row] + S.h6 * (S.acc[row] + y);
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_mf_prefix(const MfStage S) {
+  __shared__ double wsum[32];
+  __shared__ double carry_s;
+  const int n = S.p0.n;
+  const long long dcol = 2 * S.p0.np - 1;  // column of D^l = dcol + l
+  if (threadIdx.x == 0) carry_s = 0.0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int l = base + threadIdx.x;
+    const double w = (l >= 1 && l < n) ? S.p0.inv[l] * mf_x(S, dcol + l) : 0.0;
+    double x = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      double t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(FULL, t, o);
+        if (lane >= o) t += y;
+      }
+      wsum[lane] = t;
+    }
+    __syncthreads();
+    const double incl = carry_s + (wid > 0 ? wsum[wid - 1] : 0.0) + x;
+    if (l < n) S.pref_out[l] = incl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry_s = incl;
+    __syncthreads();
+  }
+}
+
+// Q1 = Q_H[diagonal H1] on the rows S_ab (half 0) / J_ab (half 1): U1 at (a, b) only
+__device__ __forceinline__ double mf_q1(const MfStage& S, const FarCtx& f1, int a, int b, long long p, int half) {
+  double ux[1], uy[1];
+  far_values<0, 0, 0>(f1, a, b, ux, uy);
+  unsigned mr, mi;
+  far_masks<0, 0>(f1.n, f1.tau, a, b, ux, uy, mr, mi);
+  const long long np = f1.np;
+  const double xs = mf_x(S, p), xj = mf_x(S, np + p);
+  // S row: [Re U at p] [-Im U at NP + p];  J row: [Im U at p] [Re U at NP + p]
+  if (half == 0) return ((mr & 1u) ? ux[0] * xs : 0.0) + ((mi & 1u) ? -uy[0] * xj : 0.0);
+  return ((mi & 1u) ? uy[0] * xs : 0.0) + ((mr & 1u) ? ux[0] * xj : 0.0);
+}
+
+template <int WK, int WL, int PT>
+__global__ void __launch_bounds__(256) k_mf_stage(const MfStage S) {
+  using MC = Mode0<WK, WL>;
+  constexpr int NPOS = FarT<WK, WL>::NPOS;
+  const int lane = threadIdx.x & 31;
+  const long long np = S.p0.np;
+  const FarCtx f0{S.p0.K.v, S.p0.L, *S.p0.tau_ptr, np, S.p0.n, S.p0.P};
+  FarCtx f1{};
+  if (S.has1) f1 = FarCtx{S.p1.K.v, S.p1.L, *S.p1.tau_ptr, np, S.p1.n, 0};
+  if ((int)blockIdx.x < S.nfar_blocks) {  // far pairs, thread per pair
+    const long long p0w = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31);
+    if (p0w >= np) return;  // warp-uniform
+    int a, b;
+    warp_pairs(S.p0.n, p0w, a, b);
+    const long long p = p0w + lane;
+    if (p >= np || b - a <= 2 * MC::W) return;  // near pairs: the side-row part
+    double ux[NPOS], uy[NPOS];
+    far_values<WK, WL, PT>(f0, a, b, ux, uy);
+    unsigned mr, mi;
+    far_masks<WK, WL>(f0.n, f0.tau, a, b, ux, uy, mr, mi);
+    int q[NPOS];
+    far_cols<WK, WL>(f0.n, a, b, q);
+    double yS = 0.0, yJ = 0.0;
+#pragma unroll
+    for (int k = 0; k < NPOS; ++k) {
+      const double xs = ((mr | mi) >> k) & 1u ? mf_x(S, q[k]) : 0.0;
+      const double xj = ((mr | mi) >> k) & 1u ? mf_x(S, np + q[k]) : 0.0;
+      if ((mr >> k) & 1u) {
+        yS += ux[k] * xs;
+        yJ += ux[k] * xj;
+      }
+      if ((mi >> k) & 1u) {
+        yS -= uy[k] * xj;
+        yJ += uy[k] * xs;
+      }
+    }
+    if (S.has1) {
+      yS += S.eps * mf_q1(S, f1, a, b, p, 0);
+      yJ += S.eps * mf_q1(S, f1, a, b, p, 1);
+    }
+    mf_epilogue(S, p, yS);  // K = 0 on far rows
+    mf_epilogue(S, np + p, yJ);
+    return;
+  }
+  // side rows (near pairs' S / J rows, D rows), warp per row
+  const long long srow = (long long)(blockIdx.x - S.nfar_blocks) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const long long nside = 2 * ((long long)S.p0.n * 2 * S.p0.W + S.p0.n - 1);
+  if (srow >= nside) return;  // warp-uniform
+  int a, b, lam;
+  const int half = (int)(srow & 1);
+  const int kind = near_item(S.p0, srow >> 1, a, b, lam);
+  if (kind == 0 || (kind == 2 && half)) return;
+  const NearMeta mt = S.side.meta[srow];
+  const int32_t* sc = S.side.col + srow * S.side.nc;
+  const double* sv = S.side.val + srow * S.side.nc;
+  const int nwin = mt.n1 + mt.n2 + mt.nd, b2 = mt.n1 + mt.n2;
+  double y = 0.0;
+  for (int k = lane; k < nwin; k += 32) {
+    const int sidx = k < mt.n1 ? k : (k < b2 ? S.side.seg + (k - mt.n1) : 2 * S.side.seg + (k - b2));
+    y += __ldg(&sv[sidx]) * mf_x(S, __ldg(&sc[sidx]));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(FULL, y, o);
+  if (lane == 0) {
+    if (mt.lend > mt.hi) y += mt.tr * (S.pref[mt.lend] - S.pref[mt.hi]);  // chain tail l in (hi, lend]
+    y += mt.k;
+    long long row;
+    if (kind == 1) {
+      const long long p = (long long)pidx32(S.p0.n, a, b);
+      row = (half ? np : 0) + p;
+      if (S.has1) y += S.eps * mf_q1(S, f1, a, b, p, half);
+    } else {
+      row = 2 * np + lam - 1;  // Q1 D rows are empty for a diagonal drive
+    }
+    mf_epilogue(S, row, y);
+  }
+}
+
 // rows of Q0 longer than RK4_LONG, listed in ascending order (ballot compaction per warp and
 // an atomic per warp: the list order is fixed by the row order within each warp, the warps'
 // slots may vary, which does not change any row's result)
@@ -2108,6 +2275,20 @@ cudaError_t dispatch_fill0(const MatFill& m0, const MatFill& m1, int q1w, long l
   SUN_DISPATCH0(m0.pr, q1w, 0);
 #undef SUN_X0
 #undef SUN_X1
+}
+
+template <int WK, int WL, int PT>
+cudaError_t launch_mf_t(const MfStage& S, unsigned grid, cudaStream_t st) {
+  k_mf_stage<WK, WL, PT><<<grid, 256, 0, st>>>(S);
+  return cudaGetLastError();
+}
+cudaError_t dispatch_mf(const MfStage& S, unsigned grid, cudaStream_t st) {
+  const int pt_ = mode0_pt(S.p0.P);
+#define SUN_XM(WK, WL, PT) \
+  if (S.p0.wK == WK && S.p0.wL == WL && pt_ == PT) return launch_mf_t<WK, WL, PT>(S, grid, st);
+  SUN_MODE0_LIST(SUN_XM)
+#undef SUN_XM
+  return cudaErrorInvalidValue;
 }
 
 long long nslots_of(const Prob& pr) { return 2 * pr.npt + pr.ndt; }
@@ -2736,6 +2917,69 @@ int sun_rk4(const sun_dcsr* Q0, const sun_dcsr* Q1, const double* K, double eps0
     S.kp = kA; S.kout = nullptr; S.c = h; S.eps = eps(t + h); S.mode = 2;     // k4 = f(t + h, v + h k3); v'
     k_rk4_stage<<<grid, 256, 0, st>>>(S);
     CK(cudaGetLastError());
+    double* tmp = cur;
+    cur = nxt;
+    nxt = tmp;
+  }
+  if (cur != v) CK(cudaMemcpyAsync(v, cur, (size_t)m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  return SUN_OK;
+}
+
+size_t sun_rk4_plan_work_bytes(sun_plan pl) {
+  if (!pl) return 0;
+  const long long m = (long long)pl->n * pl->n - 1;
+  return (size_t)(4 * m + pl->n) * sizeof(double);
+}
+
+int sun_rk4_plan(sun_plan pl, double eps0, double eps1, double omega, double t0, double h, int64_t nsteps,
+                 double* v, void* work, size_t work_bytes, void* stream) {
+  if (!pl || !v || !work || nsteps < 0) return SUN_ERR_ARG;
+  if (!pl->counted) return SUN_ERR_STATE;
+  if (pl->pr[0].mode != 0 || (pl->has_h1 && pl->wH1 != 0)) return SUN_ERR_BANDWIDTH;
+  if (work_bytes < sun_rk4_plan_work_bytes(pl)) return SUN_ERR_CAPACITY;
+  if (nsteps == 0) return SUN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const long long m = pl->pr[0].m, np = pl->pr[0].np;
+  double* kA = (double*)work;
+  double* kB = kA + m;
+  double* acc = kA + 2 * m;
+  double* vb = kA + 3 * m;
+  double* pref = kA + 4 * m;
+  MfStage S{};
+  S.p0 = pl->pr[0];
+  S.p1 = pl->has_h1 ? pl->pr[1] : pl->pr[0];
+  S.has1 = pl->has_h1;
+  S.side = pl->side[0];
+  S.pref = pref;
+  S.pref_out = pref;
+  S.acc = acc;
+  S.h6 = h / 6.0;
+  S.m = m;
+  S.nfar_blocks = (int)((np + 255) / 256);
+  const long long nside = 2 * ((long long)pl->n * 2 * S.p0.W + pl->n - 1);
+  const unsigned grid = (unsigned)(S.nfar_blocks + (nside + 7) / 8);
+  auto eps = [&](double t) { return eps0 + eps1 * sin(omega * t); };
+  double* cur = v;
+  double* nxt = vb;
+  auto stage = [&]() -> cudaError_t {
+    k_mf_prefix<<<1, 1024, 0, st>>>(S);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = dispatch_mf(S, grid, st);
+    return e;
+  };
+  // stage inputs x are double-buffered in kA / kB (each stage writes the next one's input)
+  for (int64_t i = 0; i < nsteps; ++i) {
+    const double t = t0 + (double)i * h;
+    S.v = cur;
+    S.vout = nxt;
+    S.x = cur; S.xn = kA; S.cn = 0.5 * h; S.eps = eps(t); S.mode = 0;               // k1 = f(t, v)
+    CK(stage());
+    S.x = kA; S.xn = kB; S.cn = 0.5 * h; S.eps = eps(t + 0.5 * h); S.mode = 1;      // k2 at v + h/2 k1
+    CK(stage());
+    S.x = kB; S.xn = kA; S.cn = h; S.mode = 1;                                      // k3 at v + h/2 k2
+    CK(stage());
+    S.x = kA; S.xn = nullptr; S.eps = eps(t + h); S.mode = 2;                       // k4 at v + h k3; v'
+    CK(stage());
     double* tmp = cur;
     cur = nxt;
     nxt = tmp;

@@ -143,3 +143,57 @@ def test_unfold_split_sums_to_q0(idx):
     # Q_H is skew-symmetric
     A = tocsr(QH)
     assert abs(A + A.T).max() <= 1e-12 * max(1.0, abs(A).max())
+
+
+@pytest.mark.parametrize("n,drive", [(3, True), (16, True), (33, False), (130, True)])
+def test_rk4_matrix_free_matches_csr_rk4(n, drive):
+    """sun_rk4_plan (Q regenerated per stage) against sun_rk4 on the assembled CSR (pinned above
+    to the oracle) and, at n = 3, against RK4 on rho itself (Eq. 1)."""
+    sun = _sun()
+    prob = dimer_problem(n, drive)
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    Q0, Q1, K = plan.run()
+    assert plan.info()["mode_q0"] == 0
+    v0 = sun.expand_state(ZCSR.from_triplets(n, [0], [0], [1.0]))
+    h, steps, t0 = (0.05 if n <= 16 else 1e-3), 12, 0.3
+    kw = dict(t0=t0, eps0=1.0, eps1=1.5, omega=1.0) if drive else dict(t0=t0)
+    va = v0.clone()
+    sun.rk4(Q0, Q1, K, va, h, steps, **kw)
+    vb = v0.clone()
+    plan.rk4(vb, h, steps, **kw)
+    torch.cuda.synchronize()
+    a, b = va.cpu().numpy(), vb.cpu().numpy()
+    assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
+    if n == 3:
+        rho0 = np.zeros((n, n), complex)
+        rho0[0, 0] = 1.0
+        rho = propagate.rk4_rho(prob.H0.to_dense(), prob.H1.to_dense(), [L.to_dense() for L in prob.Ls], prob.gammas,
+                                rho0, t0, h, steps, eps0=1.0, eps1=1.5, omega=1.0)
+        ref = basis.project(rho).real
+        assert np.abs(b - ref).max() <= 1e-12 * np.abs(ref).max()
+    plan.close()
+
+
+def test_rk4_matrix_free_full_size_and_errors():
+    sun = _sun()
+    prob = config(4)
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    Q0, Q1, K = plan.run()
+    v0 = sun.expand_state(ZCSR.from_triplets(prob.n, [0], [0], [1.0]))
+    va, vb = v0.clone(), v0.clone()
+    sun.rk4(Q0, Q1, K, va, 1e-5, 3, eps0=1.0, eps1=1.5, omega=1.0)
+    plan.rk4(vb, 1e-5, 3, eps0=1.0, eps1=1.5, omega=1.0)
+    a, b = va.cpu().numpy(), vb.cpu().numpy()
+    assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
+    plan.close()
+    # not counted yet -> state error; a mode-2 plan (c3 widths) -> unsupported
+    p2 = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    with pytest.raises(sun.SunError):
+        p2.rk4(v0.clone(), 1e-5, 1)
+    p2.close()
+    c3 = config(3)
+    p3 = sun.Plan(c3.H0, c3.H1, c3.Ls, c3.gammas)
+    p3.run()
+    with pytest.raises(sun.SunError, match="bandwidth"):
+        p3.rk4(sun.expand_state(ZCSR.from_triplets(c3.n, [0], [0], [1.0])), 1e-5, 1)
+    p3.close()
