@@ -430,6 +430,25 @@ def main():
         rk4 = {"ms_per_step": rk_ms, "steps": nst, "h": h, "bytes_per_step": step_bytes,
                "roofline": {"bound": "hbm", "achieved": rk_gbs, "peak": peak, "unit": "GB/s", "frac": rk_gbs / peak},
                "kernel": "k_rk4_stage (4 fused SpMV stages per RK4 step)"}
+        # the matrix-free variant (sun_rk4_plan): Q0 / Q1 regenerated per stage, not read
+        v0 = sun.expand_state(_Z.from_triplets(prob.n, [0], [0], [1.0]))
+        va, vb = v0.clone(), v0.clone()
+        sun.rk4(Q0, Q1, K, va, h, nst, eps0=1.0, eps1=1.5, omega=1.0, work=work)
+        plan.rk4(vb, h, nst, eps0=1.0, eps1=1.5, omega=1.0)  # also the warm-up
+        torch.cuda.synchronize()
+        diff = float((va - vb).abs().max() / va.abs().max())
+        flush.fill_(1.0)
+        torch.cuda._sleep(200_000)
+        a, b = ev(), ev()
+        a.record(stream)
+        plan.rk4(vb, h, nst, eps0=1.0, eps1=1.5, omega=1.0)
+        b.record(stream)
+        torch.cuda.synchronize()
+        mf_ms = a.elapsed_time(b) / nst
+        rk4["matrix_free"] = {"ms_per_step": mf_ms, "speedup_vs_csr": rk_ms / mf_ms, "max_rel_diff_vs_csr": diff,
+                              "kernels": "k_mf_prefix + k_mf_stage per stage (8 launches per step)",
+                              "note": "no matrix traffic: x gathered (L2), v/acc/next-x streamed, the U values "
+                                      "recomputed in fp64 (latency / fp64-issue bound)"}
     # F3: batched dense unfold from random rate matrices A (Eq. 7) at
     # N = 100; inputs drawn on the device (Wishart GKS matrices, workloads.gks_ensemble_torch).
     f3 = None
