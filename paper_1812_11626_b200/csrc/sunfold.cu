@@ -655,7 +655,17 @@ __global__ void __launch_bounds__(32) k_count0(const MatCount m0, const MatCount
   }
   u -= nn0;
   if (u < nn1) {
-    if constexpr (HAS1) {
+    if constexpr (HAS1 && Q1W == 0) {
+      // Q1 = Q_H[H1] with H1 diagonal (this instantiation): its near items are the D rows, and
+      // L^+(D^l) = i[H1, D^l] is exactly zero (diagonal matrices: h_a d_a - d_a h_a = 0 in
+      // floating point too), so every D row is empty; record that without evaluating it
+      if ((threadIdx.x & 31) == 0) {
+        const long long lam = u + 1;  // Q1 has W = 0: near item u is the D row l = u + 1
+        m1.cnt[2 * m1.pr.np + lam - 1] = 0;
+        m1.tsum[2 * m1.pr.npt + lam - 1] = 0;
+        m1.side.meta[2 * u] = NearMeta{0.0, 0.0, 0, 0, 0, 0, 0, 0};
+      }
+    } else if constexpr (HAS1) {
       Prob prn = m1.pr;
       prn.tau = *m1.pr.tau_ptr;
       count_near_item<Q1K, 0>(prn, u, scr, m1.cnt, m1.tsum, m1.side);
