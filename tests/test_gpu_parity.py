@@ -219,3 +219,31 @@ def test_run_single_pass_matches_two_pass_and_capacity_fallback():
     torch.cuda.synchronize()
     assert torch.equal(C[0].col, B[0].col) and torch.equal(C[0].val, B[0].val)
     plan.close()
+
+
+def test_plan_rerun_uses_current_operator_values():
+    """A plan re-runs the whole path on the operators' current values (bench.py's step): the
+    device values of H0 and L are changed in place between run() calls (same pattern, new
+    values, also a different tau), and each result equals the oracle for those values."""
+    sun = _gpu()
+    from workloads import Problem
+
+    prob = dimer_problem(40, True)
+    H0 = sun.DeviceZCSR.from_host(prob.H0)
+    H1 = sun.DeviceZCSR.from_host(prob.H1)
+    Ls = [sun.DeviceZCSR.from_host(x) for x in prob.Ls]
+    plan = sun.Plan(H0, H1, Ls, prob.gammas)
+    for scale_h, scale_l in ((1.0, 1.0), (1.7, 0.6), (0.3, 2.5)):
+        if (scale_h, scale_l) != (1.0, 1.0):
+            H0.val.mul_(scale_h)
+            Ls[0].val.mul_(scale_l)
+        Q0, Q1, K = plan.run()
+        torch.cuda.synchronize()
+        h0 = ZCSR(prob.H0.n, prob.H0.row_ptr, prob.H0.col, H0.val.cpu().numpy())
+        l0 = ZCSR(prob.Ls[0].n, prob.Ls[0].row_ptr, prob.Ls[0].col, Ls[0].val.cpu().numpy())
+        cur = Problem("rerun", prob.n, h0, prob.H1, [l0], prob.gammas)
+        ref = sparse.unfold_problem(cur)
+        _compare_csr(Q0, ref["Q0"], "rerun:Q0")
+        _compare_csr(Q1, ref["Q1"], "rerun:Q1")
+        assert np.abs(_np(K) - ref["Q0"]["K"]).max() <= 1e-12 * max(1.0, np.abs(ref["Q0"]["K"]).max())
+    plan.close()
