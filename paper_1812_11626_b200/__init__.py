@@ -46,6 +46,11 @@ class CSR(NamedTuple):
     def nnz(self) -> int:
         return int(self.col.shape[0])
 
+    def to_torch(self) -> torch.Tensor:
+        """A torch.sparse_csr_tensor of this matrix (column indices widened to int64: a copy)."""
+        return torch.sparse_csr_tensor(self.row_ptr, self.col.to(torch.int64), self.val, size=(self.m, self.m),
+                                       check_invariants=False)
+
 
 class DeviceZCSR(NamedTuple):
     n: int
@@ -79,8 +84,24 @@ def _stream_handle(stream) -> int:
 
 
 def _to_device(A) -> DeviceZCSR:
+    """Operator marshalling: DeviceZCSR as is; host ZCSR (workloads); a torch sparse-CSR tensor;
+    a dense N x N torch tensor or numpy array (its nonzero entries, row-major)."""
     if isinstance(A, DeviceZCSR):
         return A
+    if isinstance(A, np.ndarray):
+        A = torch.as_tensor(A)
+    if isinstance(A, torch.Tensor):
+        dev = A.device if A.is_cuda else torch.device("cuda")
+        if A.layout == torch.sparse_csr:
+            return DeviceZCSR(int(A.shape[0]), A.crow_indices().to(dev, torch.int64),
+                              A.col_indices().to(dev, torch.int32), A.values().to(dev, torch.complex128))
+        assert A.dim() == 2 and A.shape[0] == A.shape[1], "operators are N x N"
+        D = A.to(dev, torch.complex128)
+        nzr, nzc = torch.nonzero(D, as_tuple=True)  # row-major order, columns ascending
+        counts = torch.bincount(nzr, minlength=D.shape[0])
+        rp = torch.zeros(D.shape[0] + 1, dtype=torch.int64, device=dev)
+        rp[1:] = torch.cumsum(counts, 0)
+        return DeviceZCSR(int(D.shape[0]), rp, nzc.to(torch.int32), D[nzr, nzc].contiguous())
     return DeviceZCSR.from_host(A)
 
 

@@ -247,3 +247,23 @@ def test_plan_rerun_uses_current_operator_values():
         _compare_csr(Q1, ref["Q1"], "rerun:Q1")
         assert np.abs(_np(K) - ref["Q0"]["K"]).max() <= 1e-12 * max(1.0, np.abs(ref["Q0"]["K"]).max())
     plan.close()
+
+
+def test_wrapper_accepts_dense_and_sparse_torch_inputs():
+    """The Python wrapper's operator marshalling: dense torch / numpy and torch
+    sparse-CSR inputs give the same unfold as host CSR; outputs convert to torch sparse CSR."""
+    sun = _gpu()
+    prob = dimer_problem(20, True)
+    ref = sun.unfold(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    dense = [torch.tensor(x.to_dense(), device="cuda") for x in (prob.H0, prob.H1, prob.Ls[0])]
+    got = sun.unfold(dense[0], dense[1].to_sparse_csr(), [prob.Ls[0].to_dense()], prob.gammas)
+    torch.cuda.synchronize()
+    for a, b in ((ref[0], got[0]), (ref[1], got[1])):
+        assert torch.equal(a.row_ptr, b.row_ptr) and torch.equal(a.col, b.col) and torch.equal(a.val, b.val)
+    assert torch.equal(ref[2], got[2])
+    T = ref[0].to_torch()
+    D = T.to_dense().cpu().numpy()
+    rp, c, v = _np(ref[0].row_ptr), _np(ref[0].col), _np(ref[0].val)
+    for s in (0, 5, ref[0].m - 1):
+        assert np.array_equal(np.nonzero(D[s])[0], c[rp[s]:rp[s + 1]])
+        assert np.array_equal(D[s, c[rp[s]:rp[s + 1]]], v[rp[s]:rp[s + 1]])
