@@ -1149,6 +1149,45 @@ __device__ __forceinline__ void fill_direct_tile(const FarCtx& pr, long long npt
   }
 }
 
+// Q1 rows of the warp's 32 pairs of Q0 far tile t (combined fill, Q1 = Q_H[diagonal H1], all
+// pairs "far" at width 0, rows of <= 2 entries): Q1's scan slot t covers the same 256 pairs,
+// so the warp's offset is the slot offset plus the counts of the tile's earlier warps.
+__device__ __forceinline__ void fill_q1_chunk(const FarCtx& f1, long long npt1, long long t, const int* __restrict__ cnt1,
+                                              const FillOut& fo) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long np = f1.np;
+  const long long p = t * TP0 + threadIdx.x;
+  const bool valid = p < np;
+  const int c = valid ? cnt1[p] : 0;  // S and J rows of a pair have the same length
+  int before = 0;
+  for (int i = 0; i < wid; ++i) {     // the tile's earlier warps
+    const long long q = t * TP0 + i * 32 + lane;
+    before += q < np ? __ldg(&cnt1[q]) : 0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(FULL, before, o);
+  int tot;
+  const int ex = warp_excl_scan(c, tot);
+  int a, b;
+  warp_pairs(f1.n, t * TP0 + wid * 32, a, b);
+  if (!valid) return;
+  const long long rS = fo.toff[t] + before + ex, rJ = fo.toff[npt1 + t] + before + ex;
+  fo.row_ptr[p] = rS;
+  fo.row_ptr[np + p] = rJ;
+  double ux[1], uy[1];
+  far_values<0, 0, 0>(f1, a, b, ux, uy);
+  unsigned mr, mi;
+  far_masks<0, 0>(f1.n, f1.tau, a, b, ux, uy, mr, mi);
+  const Seg seg = {fo.col, fo.val, fo.cap};
+  // S row: [Re U at p] [-Im U at NP + p];  J row: [Im U at p] [Re U at NP + p]
+  int o = 0;
+  if (mr & 1u) seg.emit(rS + o++, (int)p, ux[0]);
+  if (mi & 1u) seg.emit(rS + o, (int)(np + p), -uy[0]);
+  o = 0;
+  if (mi & 1u) seg.emit(rJ + o++, (int)p, uy[0]);
+  if (mr & 1u) seg.emit(rJ + o, (int)(np + p), ux[0]);
+}
+
 // One output matrix's arguments of the fill pass.
 struct MatFill {
   Prob pr;
@@ -1177,7 +1216,9 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
   const long long nn1 = HAS1 ? near_units1(m1.pr.n, m1.pr.W) : 0;
   // fill tiles: SLOTS_PER_TILE scan slots (one per warp) each
   const long long nt0 = (m0.pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE;
-  const long long nt1 = HAS1 ? (m1.pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE : 0;
+  // Q1 tiles: none when the Q0 far tiles write Q1's rows (staged Q0 tiles of 256 pairs)
+  constexpr bool Q1MERGED = HAS1 && !FF::DIRECT;
+  const long long nt1 = HAS1 && !Q1MERGED ? (m1.pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE : 0;
   const long long U0 = nt0 + nn0, U = U0 + nn1 + nt1;
   int* scol = reinterpret_cast<int*>(dyn + wid * FF::BYTES_PER_WARP);
   double* sval = reinterpret_cast<double*>(dyn + wid * FF::BYTES_PER_WARP + FF::COLW * 4);
@@ -1219,6 +1260,7 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
         fill_direct_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, m0.cnt, m0.fo);
       else
         fill_far_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, cur, m0.fo, scol, sval);
+      if constexpr (Q1MERGED) fill_q1_chunk(prf1, m1.pr.npt, idx, m1.cnt, m1.fo);
     } else if (kind == 1) {
 #ifndef SUN_EXP_NO_NEAR
       fill_near_unit(m0.pr, idx, m0.cnt, m0.fo, m0.side);
