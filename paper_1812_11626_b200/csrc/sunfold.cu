@@ -1213,11 +1213,15 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
   }
   // near units: NEAR_UNIT_ROWS side rows each (2 per near item)
   const long long nn0 = near_units1(m0.pr.n, m0.pr.W);
-  const long long nn1 = HAS1 ? near_units1(m1.pr.n, m1.pr.W) : 0;
-  // fill tiles: SLOTS_PER_TILE scan slots (one per warp) each
-  const long long nt0 = (m0.pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE;
   // Q1 tiles: none when the Q0 far tiles write Q1's rows (staged Q0 tiles of 256 pairs)
   constexpr bool Q1MERGED = HAS1 && !FF::DIRECT;
+  // Q1's near items are its D rows; with the diagonal drive they are empty (count pass), so
+  // their row pointers all equal nnz(Q1): CTA 0 writes them instead of near units
+  const long long nn1 = HAS1 && !Q1MERGED ? near_units1(m1.pr.n, m1.pr.W) : 0;
+  if (Q1MERGED && blockIdx.x == 0)
+    for (long long l = threadIdx.x; l < m1.pr.n - 1; l += blockDim.x) m1.fo.row_ptr[2 * m1.pr.np + l] = *m1.fo.nnz;
+  // fill tiles: SLOTS_PER_TILE scan slots (one per warp) each
+  const long long nt0 = (m0.pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE;
   const long long nt1 = HAS1 && !Q1MERGED ? (m1.pr.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE : 0;
   const long long U0 = nt0 + nn0, U = U0 + nn1 + nt1;
   int* scol = reinterpret_cast<int*>(dyn + wid * FF::BYTES_PER_WARP);
