@@ -296,6 +296,21 @@ struct ExpandArgs {
   int nrb, nA, nB, P;
 };
 
+// entry (r, c) of a banded CSR operator of planned half-width w: a complete band row stores
+// column c at rp[r] + c - max(r - w, 0), so the column index and the value are fetched in
+// parallel right after rp (two dependent loads); a search only if the guess misses
+__device__ __forceinline__ double2 csr_get(const OpDesc& d, int r, int c);
+__device__ __forceinline__ double2 csr_get_band(const OpDesc& d, int r, int c, int w) {
+  const int64_t b = __ldg(d.rp + r), e = __ldg(d.rp + r + 1);
+  const int lo = r - w > 0 ? r - w : 0;
+  const int64_t g = b + (int64_t)(c - lo);
+  if (c >= lo && g < e) {
+    const int cc = __ldg(d.ci + g);
+    const double2 vv = __ldg(d.v + g);
+    if (cc == c) return vv;
+  }
+  return csr_get(d, r, c);
+}
 __device__ __forceinline__ double2 csr_get(const OpDesc& d, int r, int c) {
   for (int64_t k = d.rp[r], e = d.rp[r + 1]; k < e; ++k) {
     const int cc = d.ci[k];
@@ -392,21 +407,22 @@ __global__ void __launch_bounds__(EXP_THREADS) k_expand(const ExpandArgs A) {
             const OpDesc L = ops.op[2 + p];
             double px = 0.0, py = 0.0;
             for (int x = lo; x <= hi; ++x) {
-              const double2 a = csr_get(L, x, r), b = csr_get(L, x, c);  // conj(L_xr) L_xc
+              const double2 a = csr_get_band(L, x, r, A.wL), b = csr_get_band(L, x, c, A.wL);  // conj(L_xr) L_xc
               px += a.x * b.x + a.y * b.y;
               py += a.x * b.y - a.y * b.x;
             }
             mx += ops.gamma[2 + p] * px;
             my += ops.gamma[2 + p] * py;
           }
-          const double2 h = csr_get(ops.op[0], r, c), ht = csr_get(ops.op[0], c, r);
+          const int wh = ops.wplan[0] >= 0 ? ops.wplan[0] : A.wK;
+          const double2 h = csr_get_band(ops.op[0], r, c, wh), ht = csr_get_band(ops.op[0], c, r, wh);
           kv = make_double2(h.x - 0.5 * my, h.y + 0.5 * mx);
           d0 = (unsigned long long)__double_as_longlong(fmax(fabs(h.x - ht.x), fabs(h.y + ht.y)));
         }
         A.kb0[(long long)r * (2 * A.wK + 1) + (o + A.wK)] = kv;
       }
       if (in && ops.has_h1 && o >= -A.wH1 && o <= A.wH1) {
-        const double2 g = csr_get(ops.op[1], r, c), gt = csr_get(ops.op[1], c, r);
+        const double2 g = csr_get_band(ops.op[1], r, c, A.wH1), gt = csr_get_band(ops.op[1], c, r, A.wH1);
         d1 = (unsigned long long)__double_as_longlong(fmax(fabs(g.x - gt.x), fabs(g.y + gt.y)));
       }
     }
