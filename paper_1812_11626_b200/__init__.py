@@ -123,7 +123,10 @@ def gen_index(n: int, kind: str, a: int, b: int = -1) -> int:
 class Plan:
     """A validated, analysed unfold problem bound to a device workspace (sun_plan_create)."""
 
-    def __init__(self, H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), stream=None):
+    def __init__(self, H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), stream=None,
+                 guard_bytes: int = 0):
+        """guard_bytes > 0 (tests): the workspace gets a tail of that many 0xA5 bytes beyond the
+        size the library is told; workspace_guard_intact() checks it (out-of-bounds writes)."""
         L = lib()
         self.stream = stream
         self.H0 = _to_device(H0)
@@ -138,7 +141,10 @@ class Plan:
         nbytes = int(L.sun_workspace_bytes(self.n, self.P))
         if nbytes == 0:
             _check(2, "sun_workspace_bytes")
-        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        self.workspace = torch.empty(nbytes + guard_bytes, dtype=torch.uint8, device="cuda")
+        self._guard = guard_bytes
+        if guard_bytes:
+            self.workspace[nbytes:].fill_(0xA5)
         self._s_h0 = _zcsr_struct(self.H0)
         self._s_h1 = _zcsr_struct(self.H1) if self.H1 is not None else None
         self._s_ls = [_zcsr_struct(x) for x in self.Ls]
@@ -157,6 +163,11 @@ class Plan:
         _check(st, "sun_plan_create")
         self._plan = plan
         self._caps = None  # output capacities for run(): previous nnz
+
+    def workspace_guard_intact(self) -> bool:
+        if not self._guard:
+            return True
+        return bool((self.workspace[-self._guard:] == 0xA5).all().item())
 
     # -- the three phases ----------------------------------------------------------------
     def count(self):
