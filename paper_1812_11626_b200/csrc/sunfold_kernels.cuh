@@ -239,35 +239,6 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* warp_tot, int& t
   return before + x - v;
 }
 
-// Block-wide exclusive scans of two ints per thread at once (one pass, two barriers).
-// Assumes every warp of the block is converged and blockDim.x <= 1024.
-__device__ __forceinline__ int2 block_exclusive_scan2(int v1, int v2, int2* warp_tot, int2& total) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  int x = v1, y = v2;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int a = __shfl_up_sync(FULL, x, o), b = __shfl_up_sync(FULL, y, o);
-    if (lane >= o) {
-      x += a;
-      y += b;
-    }
-  }
-  if (lane == 31) warp_tot[wid] = make_int2(x, y);
-  __syncthreads();
-  int2 before = make_int2(0, 0), tot = make_int2(0, 0);
-  for (int w = 0; w < nwarps; ++w) {  // <= 32 broadcast reads
-    const int2 t = warp_tot[w];
-    if (w < wid) {
-      before.x += t.x;
-      before.y += t.y;
-    }
-    tot.x += t.x;
-    tot.y += t.y;
-  }
-  total = tot;
-  return make_int2(before.x + x - v1, before.y + y - v2);
-}
-
 // ---------------------------------------------------------------------------------------
 // Last l in (hi, n-1] with |tr * inv[l]| > tau (hi if none).  The predicate is monotone
 // (non-increasing) in l, so the answer is unique; it is located from the estimate
