@@ -198,8 +198,8 @@ size_t sun_rk4_work_bytes(int64_t m);
  * regenerates the far-pair entries from the plan's band storage with the count/fill
  * expressions and tau masks, takes the near and D rows from the count pass's side buffer
  * (chain tails in O(1) from a per-stage prefix over the D coefficients), K from the same data.
- * Supported: mode-0 plans (sun_plan_info mode_q0 = 0) without a drive or with a diagonal H1;
- * else SUN_ERR_BANDWIDTH.  v: device float64[M], in/out.  work: device scratch of
+ * Supported: mode-0 plans and mode-2 plans (sun_plan_info mode_q0 = 0 or 2) without a drive or
+ * with a diagonal H1; else SUN_ERR_BANDWIDTH.  v: device float64[M], in/out.  work: device scratch of
  * sun_rk4_plan_work_bytes(plan) bytes (4 M + N doubles).  Asynchronous on `stream`.
  * Errors: SUN_ERR_ARG, SUN_ERR_STATE (plan not counted), SUN_ERR_BANDWIDTH, SUN_ERR_CAPACITY,
  * SUN_ERR_CUDA. */

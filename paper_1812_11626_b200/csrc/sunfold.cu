@@ -1921,24 +1921,24 @@ __global__ void __launch_bounds__(256) k_mf_stage(const MfStage S) {
     if (p >= np || b - a <= 2 * MC::W) return;  // near pairs: the side-row part
     double ux[NPOS], uy[NPOS];
     far_values<WK, WL, PT>(f0, a, b, ux, uy);
-    unsigned mr, mi;
-    far_masks<WK, WL>(f0.n, f0.tau, a, b, ux, uy, mr, mi);
     int q[NPOS];
     far_cols<WK, WL>(f0.n, a, b, q);
     double yS = 0.0, yJ = 0.0;
-#pragma unroll
-    for (int k = 0; k < NPOS; ++k) {
-      const double xs = ((mr | mi) >> k) & 1u ? mf_x(S, q[k]) : 0.0;
-      const double xj = ((mr | mi) >> k) & 1u ? mf_x(S, np + q[k]) : 0.0;
-      if ((mr >> k) & 1u) {
+    // kept entries as in far_masks (in range and |.| > tau), inline: NPOS may exceed 32
+    far_foreach<WK, WL>([&](int k, int dc, int dd) {
+      const bool ok = (dc >= 0 || a + dc >= 0) && (dd <= 0 || b + dd < f0.n);
+      const bool kr = ok && fabs(ux[k]) > f0.tau, ki = ok && fabs(uy[k]) > f0.tau;
+      const double xs = (kr || ki) ? mf_x(S, q[k]) : 0.0;
+      const double xj = (kr || ki) ? mf_x(S, np + q[k]) : 0.0;
+      if (kr) {
         yS += ux[k] * xs;
         yJ += ux[k] * xj;
       }
-      if ((mi >> k) & 1u) {
+      if (ki) {
         yS -= uy[k] * xj;
         yJ += uy[k] * xs;
       }
-    }
+    });
     if (S.has1) {
       yS += S.eps * mf_q1(S, f1, a, b, p, 0);
       yJ += S.eps * mf_q1(S, f1, a, b, p, 1);
@@ -2364,6 +2364,8 @@ cudaError_t launch_mf_t(const MfStage& S, unsigned grid, cudaStream_t st) {
   return cudaGetLastError();
 }
 cudaError_t dispatch_mf(const MfStage& S, unsigned grid, cudaStream_t st) {
+  if (S.p0.mode == 2 && S.p0.wK == 4 && S.p0.wL == 2)  // mode-2 widths (c3)
+    return S.p0.P == 1 ? launch_mf_t<4, 2, 1>(S, grid, st) : launch_mf_t<4, 2, -1>(S, grid, st);
   const int pt_ = mode0_pt(S.p0.P);
 #define SUN_XM(WK, WL, PT) \
   if (S.p0.wK == WK && S.p0.wL == WL && pt_ == PT) return launch_mf_t<WK, WL, PT>(S, grid, st);
@@ -3017,7 +3019,8 @@ int sun_rk4_plan(sun_plan pl, double eps0, double eps1, double omega, double t0,
                  double* v, void* work, size_t work_bytes, void* stream) {
   if (!pl || !v || !work || nsteps < 0) return SUN_ERR_ARG;
   if (!pl->counted) return SUN_ERR_STATE;
-  if (pl->pr[0].mode != 0 || (pl->has_h1 && pl->wH1 != 0)) return SUN_ERR_BANDWIDTH;
+  if (!(pl->pr[0].mode == 0 || (pl->pr[0].mode == 2 && pl->wK == 4 && pl->wL == 2)) || (pl->has_h1 && pl->wH1 != 0))
+    return SUN_ERR_BANDWIDTH;
   if (work_bytes < sun_rk4_plan_work_bytes(pl)) return SUN_ERR_CAPACITY;
   if (nsteps == 0) return SUN_OK;
   cudaStream_t st = (cudaStream_t)stream;

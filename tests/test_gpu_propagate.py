@@ -10,7 +10,7 @@ import scipy.sparse as sp
 import torch
 
 from oracle import basis, propagate, sparse
-from workloads import ZCSR, config, dimer_problem
+from workloads import ZCSR, banded_random_problem, config, dimer_problem
 
 pytestmark = pytest.mark.gpu
 
@@ -191,9 +191,30 @@ def test_rk4_matrix_free_full_size_and_errors():
     with pytest.raises(sun.SunError):
         p2.rk4(v0.clone(), 1e-5, 1)
     p2.close()
-    c3 = config(3)
-    p3 = sun.Plan(c3.H0, c3.H1, c3.Ls, c3.gammas)
-    p3.run()
+    # a mode-1 plan (runtime widths) -> unsupported
+    p1 = banded_random_problem(70, seed=9, wH=15, wL=7, P=1)
+    pm = sun.Plan(p1.H0, p1.H1, p1.Ls, p1.gammas)
+    pm.run()
     with pytest.raises(sun.SunError, match="bandwidth"):
-        p3.rk4(sun.expand_state(ZCSR.from_triplets(c3.n, [0], [0], [1.0])), 1e-5, 1)
-    p3.close()
+        pm.rk4(sun.expand_state(ZCSR.from_triplets(p1.n, [0], [0], [1.0])), 1e-5, 1)
+    pm.close()
+
+
+@pytest.mark.parametrize("which", ["small_P1", "small_P4", "c3"])
+def test_rk4_matrix_free_mode2(which):
+    """Mode-2 plans (widths (4, 2)): the matrix-free RK4 against the CSR RK4."""
+    sun = _sun()
+    prob = {"small_P1": lambda: banded_random_problem(50, seed=11, wH=4, wL=2, P=1),
+            "small_P4": lambda: banded_random_problem(64, seed=6),
+            "c3": lambda: config(3)}[which]()
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    Q0, Q1, K = plan.run()
+    assert plan.info()["mode_q0"] == 2
+    v0 = sun.expand_state(ZCSR.from_triplets(prob.n, [0], [0], [1.0]))
+    va, vb = v0.clone(), v0.clone()
+    h, steps = 1e-4, 5
+    sun.rk4(Q0, None, K, va, h, steps)
+    plan.rk4(vb, h, steps)
+    a, b = va.cpu().numpy(), vb.cpu().numpy()
+    assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
+    plan.close()
