@@ -449,7 +449,6 @@ def main():
         mf_ms = a.elapsed_time(b) / nst
         rk4["matrix_free"] = {"ms_per_step": mf_ms, "speedup_vs_csr": rk_ms / mf_ms, "max_rel_diff_vs_csr": diff,
                               "kernels": "k_mf_prefix + k_mf_stage per stage (8 launches per step)",
-                              "config3_note": "c3 (mode 2): 0.190 ms vs 0.447 ms per step on the CSR (tools/time_rk4_mf3.py)",
                               "note": "no matrix traffic: x gathered (L2), v/acc/next-x streamed, the U values "
                                       "recomputed in fp64 (latency / fp64-issue bound)"}
     # F3: batched dense unfold from random rate matrices A (Eq. 7) at
