@@ -1321,31 +1321,31 @@ __global__ void __launch_bounds__(32) k_count2(const MatCount mc) {
     count_near_item<WK, WL>(pr, u, scr, mc.cnt, mc.tsum, mc.side);
     return;
   }
-  u -= p0.nb_near;  // far warp u: pairs [32 u, 32 u + 32), one after the other
+  u -= p0.nb_near;  // far warp u: pairs [32 u, 32 u + 32), thread per pair
   const int lane = threadIdx.x & 31;
   const long long np = pr.np;
-  const Seg none = {nullptr, nullptr, 0};
-  long long pw = u * 32;
-  int a = 0, b = 1;
-  if (pw < np) pair_decode(pr.n, pw, a, b);
+  const long long pw = u * 32;
+  int a, b;
+  warp_pairs(pr.n, pw, a, b);
+  const long long p = pw + lane;
   int tot = 0;
-  for (int j = 0; j < 32 && pw + j < np; ++j) {
-    if (j) {
-      if (++b == pr.n) {
-        ++a;
-        b = a + 1;
+  if (p < np && b - a > 2 * MC::W) {
+    // the positions one by one with the fill's per-position expression (far_value_at)
+    int nR = 0, nI = 0;
+    for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
+      double x, y;
+      int c, d;
+      if (far_value_at<WK, WL, PT>(pr, a, b, k, x, y, c, d)) {
+        nR += fabs(x) > pr.tau;
+        nI += fabs(y) > pr.tau;
       }
     }
-    if (b - a > 2 * MC::W) {
-      int nR;
-      const int c = far_warp_pair<WK, WL, PT, false>(pr, a, b, none, 0, none, 0, &nR);
-      if (lane == 0) {
-        mc.cnt[pw + j] = c | (nR << CNT_BITS);
-        mc.cnt[np + pw + j] = c;
-      }
-      tot += c;
-    }
+    tot = nR + nI;
+    mc.cnt[p] = tot | (nR << CNT_BITS);
+    mc.cnt[np + p] = tot;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
   if (lane == 0 && tot) {  // scan slot u = this warp's 32 pairs
     atomicAdd(&mc.tsum[u], tot);
     atomicAdd(&mc.tsum[pr.npt + u], tot);

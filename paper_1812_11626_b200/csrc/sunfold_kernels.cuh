@@ -838,11 +838,52 @@ __device__ __forceinline__ void far_pos(int k, int& dc, int& dd) {
   }
 }
 
+// U at far position k of pair (a, b) (the same expression wherever it is evaluated: the count
+// and fill passes must take identical tau decisions); returns whether the position is in range
+template <int WK, int WL, int PT>
+__device__ __forceinline__ bool far_value_at(const Prob& pr, int a, int b, int k, double& x, double& y, int& c,
+                                             int& d) {
+  constexpr int NPOS = FarT<WK, WL>::NPOS;
+  constexpr int SK = 2 * WK + 1, SL = 2 * WL + 1;
+  const int n = pr.n;
+  const int P = PT < 0 ? pr.P : PT;
+  int dc, dd;
+  far_pos<WK, WL>(k < NPOS ? k : 0, dc, dd);
+  c = a + dc;
+  d = b + dd;
+  const bool ok = k < NPOS && c >= 0 && d < n;
+  x = 0.0;
+  y = 0.0;
+  if (ok) {
+    const int adc = dc < 0 ? -dc : dc, add = dd < 0 ? -dd : dd;
+    if (PT != 0 && adc <= WL && add <= WL) {
+      const double2* La = pr.L + (long long)a * SL + (dc + WL);
+      const double2* Lb = pr.L + (long long)b * SL + (dd + WL);
+      const long long ps = (long long)n * SL;
+      for (int p = 0; p < P; ++p) {
+        const double2 la = __ldg(La + p * ps), lb = __ldg(Lb + p * ps);
+        x += la.x * lb.x + la.y * lb.y;  // conj(Lt_p,ac) Lt_p,bd
+        y += la.x * lb.y - la.y * lb.x;
+      }
+    }
+    if (dd == 0) {  // + i K_ca
+      const double2 kv = __ldg(&pr.K.v[(long long)c * SK + (WK - dc)]);
+      x -= kv.y;
+      y += kv.x;
+    }
+    if (dc == 0) {  // - i conj(K_db)
+      const double2 kv = __ldg(&pr.K.v[(long long)d * SK + (WK - dd)]);
+      x -= kv.y;
+      y -= kv.x;
+    }
+  }
+  return ok;
+}
+
 template <int WK, int WL, int PT, bool EMIT>
 __device__ __forceinline__ int far_warp_pair(const Prob& pr, int a, int b, const Seg& sS, long long offS,
                                              const Seg& sJ, long long offJ, int* nR_out = nullptr) {
   constexpr int NPOS = FarT<WK, WL>::NPOS, NCH = (NPOS + 31) / 32;
-  constexpr int SK = 2 * WK + 1, SL = 2 * WL + 1;
   const int lane = threadIdx.x & 31;
   const int n = pr.n, np = (int)pr.np;
   const double tau = pr.tau;
@@ -851,38 +892,12 @@ __device__ __forceinline__ int far_warp_pair(const Prob& pr, int a, int b, const
   unsigned mr[NCH], mi[NCH];
   int qq[NCH];
   int nR = 0, nI = 0;
-  const int P = PT < 0 ? pr.P : PT;
 #pragma unroll
   for (int h = 0; h < NCH; ++h) {
     const int k = h * 32 + lane;
-    int dc, dd;
-    far_pos<WK, WL>(k < NPOS ? k : 0, dc, dd);
-    const int c = a + dc, d = b + dd;
-    const bool ok = k < NPOS && c >= 0 && d < n;
-    double x = 0.0, y = 0.0;
-    if (ok) {
-      const int adc = dc < 0 ? -dc : dc, add = dd < 0 ? -dd : dd;
-      if (PT != 0 && adc <= WL && add <= WL) {
-        const double2* La = pr.L + (long long)a * SL + (dc + WL);
-        const double2* Lb = pr.L + (long long)b * SL + (dd + WL);
-        const long long ps = (long long)n * SL;
-        for (int p = 0; p < P; ++p) {
-          const double2 la = __ldg(La + p * ps), lb = __ldg(Lb + p * ps);
-          x += la.x * lb.x + la.y * lb.y;  // conj(Lt_p,ac) Lt_p,bd
-          y += la.x * lb.y - la.y * lb.x;
-        }
-      }
-      if (dd == 0) {  // + i K_ca
-        const double2 kv = __ldg(&pr.K.v[(long long)c * SK + (WK - dc)]);
-        x -= kv.y;
-        y += kv.x;
-      }
-      if (dc == 0) {  // - i conj(K_db)
-        const double2 kv = __ldg(&pr.K.v[(long long)d * SK + (WK - dd)]);
-        x -= kv.y;
-        y -= kv.x;
-      }
-    }
+    double x, y;
+    int c, d;
+    const bool ok = far_value_at<WK, WL, PT>(pr, a, b, k, x, y, c, d);
     ux[h] = x;
     uy[h] = y;
     qq[h] = ok ? pidx32(n, c, d) : 0;
