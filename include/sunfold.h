@@ -207,6 +207,12 @@ int sun_rk4_plan(sun_plan plan, double eps0, double eps1, double omega, double t
                  double* v, void* work, size_t work_bytes, void* stream);
 size_t sun_rk4_plan_work_bytes(sun_plan plan);
 
+/* dv/dt = (Q0 + eps Q1) v + K matrix-free (the stage of sun_rk4_plan with a plain output): the
+ * same support and state requirements as sun_rk4_plan.  v, dvdt: device float64[M] (distinct).
+ * work: device scratch of >= N doubles.  Asynchronous.  Errors: as sun_rk4_plan. */
+int sun_apply_plan(sun_plan plan, double eps, const double* v, double* dvdt, void* work, size_t work_bytes,
+                   void* stream);
+
 /* Enable (1, the default) or disable (0) CUDA-graph replay of this plan's enqueue sequences.
  * With graphs, sun_count / sun_unfold / sun_run capture their launches once per distinct
  * output buffer set and replay the graph (one launch); without, every kernel is launched

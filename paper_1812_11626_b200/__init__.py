@@ -267,6 +267,16 @@ class Plan:
                               ctypes.c_void_p(_stream_handle(self.stream))), "sun_rk4_plan")
         return v
 
+    def apply(self, v: torch.Tensor, eps: float = 0.0, out: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """dv/dt = (Q0 + eps Q1) v + K without reading Q (sun_apply_plan); needs a counted plan."""
+        y = out if out is not None else torch.empty_like(v)
+        w = torch.empty(self.n, dtype=torch.float64, device=v.device)
+        _check(lib().sun_apply_plan(self._plan, ctypes.c_double(eps), ctypes.c_void_p(v.data_ptr()),
+                                    ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(w.data_ptr()),
+                                    ctypes.c_size_t(w.numel() * 8), ctypes.c_void_p(_stream_handle(self.stream))),
+               "sun_apply_plan")
+        return y
+
     def launches_per_run(self) -> int:
         """Kernels of this library launched by one run() (sun_run: count + fill)."""
         inf = self.info()

@@ -1848,8 +1848,10 @@ __device__ __forceinline__ void mf_epilogue(const MfStage& S, long long row, dou
   } else if (S.mode == 1) {
     S.acc[row] += 2.0 * y;
     S.xn[row] = S.v[row] + S.cn * y;
-  } else {
+  } else if (S.mode == 2) {
     S.vout[row] = S.v[row] + S.h6 * (S.acc[row] + y);
+  } else {  // 3: plain apply, vout = y
+    S.vout[row] = y;
   }
 }
 
@@ -3013,6 +3015,36 @@ size_t sun_rk4_plan_work_bytes(sun_plan pl) {
   if (!pl) return 0;
   const long long m = (long long)pl->n * pl->n - 1;
   return (size_t)(4 * m + pl->n) * sizeof(double);
+}
+
+int sun_apply_plan(sun_plan pl, double eps, const double* v, double* dvdt, void* work, size_t work_bytes,
+                   void* stream) {
+  if (!pl || !v || !dvdt || !work || v == dvdt) return SUN_ERR_ARG;
+  if (!pl->counted) return SUN_ERR_STATE;
+  if (!(pl->pr[0].mode == 0 || (pl->pr[0].mode == 2 && pl->wK == 4 && pl->wL == 2)) || (pl->has_h1 && pl->wH1 != 0))
+    return SUN_ERR_BANDWIDTH;
+  if (work_bytes < (size_t)pl->n * sizeof(double)) return SUN_ERR_CAPACITY;
+  cudaStream_t st = (cudaStream_t)stream;
+  MfStage S{};
+  S.p0 = pl->pr[0];
+  S.p1 = pl->has_h1 ? pl->pr[1] : pl->pr[0];
+  S.has1 = pl->has_h1;
+  S.side = pl->side[0];
+  S.pref = (double*)work;
+  S.pref_out = (double*)work;
+  S.x = v;
+  S.v = v;
+  S.vout = dvdt;
+  S.eps = eps;
+  S.mode = 3;
+  S.m = pl->pr[0].m;
+  S.nfar_blocks = (int)((pl->pr[0].np + 255) / 256);
+  const long long nside = 2 * ((long long)pl->n * 2 * S.p0.W + pl->n - 1);
+  const unsigned grid = (unsigned)(S.nfar_blocks + (nside + 7) / 8);
+  k_mf_prefix<<<1, 1024, 0, st>>>(S);
+  CK(cudaGetLastError());
+  CK(dispatch_mf(S, grid, st));
+  return SUN_OK;
 }
 
 int sun_rk4_plan(sun_plan pl, double eps0, double eps1, double omega, double t0, double h, int64_t nsteps,

@@ -218,3 +218,17 @@ def test_rk4_matrix_free_mode2(which):
     a, b = va.cpu().numpy(), vb.cpu().numpy()
     assert np.abs(a - b).max() <= 1e-12 * np.abs(a).max()
     plan.close()
+
+
+@pytest.mark.parametrize("idx", [1, 2, 3, 4])
+def test_apply_matrix_free_matches_csr_apply(idx):
+    """sun_apply_plan (Q regenerated) against sun_apply on the assembled CSR."""
+    sun = _sun()
+    prob = config(idx)
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    Q0, Q1, K = plan.run()
+    v = torch.linspace(-1.0, 1.0, prob.m, dtype=torch.float64, device="cuda")
+    a = sun.apply(Q0, Q1, 1.3, K, v).cpu().numpy()
+    b = plan.apply(v, 1.3).cpu().numpy()
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
+    plan.close()

@@ -27,3 +27,17 @@ ts = sorted(ts[2:])
 nz = Q0.nnz + (Q1.nnz if Q1 is not None else 0)
 byts = 12 * nz + 8 * (Q0.m + 1) * (2 if Q1 is not None else 1) + 8 * Q0.m * 3
 print(f"config {idx} apply {ts[len(ts)//2]*1e3:.1f} us, {byts / (ts[len(ts)//2]*1e-3) / 1e9:.0f} GB/s algorithmic")
+# matrix-free (sun_apply_plan) on the plan of the same problem
+plan = sun.Plan(p.H0, p.H1, p.Ls, p.gammas)
+plan.run()
+tm = []
+for i in range(12):
+    flush.fill_(1.0)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    plan.apply(v, 1.3, out=y)
+    b.record()
+    torch.cuda.synchronize()
+    tm.append(a.elapsed_time(b))
+tm = sorted(tm[2:])
+print(f"config {idx} apply matrix-free {tm[len(tm)//2]*1e3:.1f} us")
