@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(DT) k_dense_zdiag(const DenseArgs g) {
   const double2* ud = g.UD + (long long)r * (n - 1) * n2 + t;
   double2* Z = g.Z + (long long)r * n2 * n2 + (long long)b * n2 * n + d;  // + (x N + x) N
   double2 S = make_double2(0.0, 0.0);
+#pragma unroll 8
   for (int l = n - 1; l >= 1; --l) {
     const double2 w = cscale(ud[(long long)(l - 1) * n2], inv_ll1(l));
     Z[((long long)l * n + l) * n] = csub(S, cscale(w, (double)l));
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(DT) k_dense_kh(const DenseArgs g) {
   double2 G = make_double2(0.0, 0.0);
   if (g.A) {
     const double2* Z = g.Z + (long long)r * n2 * n2 + t;
+#pragma unroll 8
     for (int x = 0; x < n; ++x) G = cadd(G, Z[((long long)x * n + x) * n2]);
   }
   const double2 h = g.H[(long long)(g.r0 + r) * n2 + (long long)c * n + e];
@@ -423,6 +425,7 @@ __global__ void __launch_bounds__(DT) k_dense_vdiag(const DenseArgs g) {
   const double2* kh = g.Kh + (long long)r * n2;
   double2* vd = g.UD + (long long)r * (n - 1) * n2 + t;
   double2 P = make_double2(0.0, 0.0);
+#pragma unroll 8
   for (int xx = 0; xx < n; ++xx) {
     const double2 z = zprime(Z + ((long long)xx * n + xx) * n2, kh, n, has_a, xx, xx, c, d);
     if (xx >= 1) vd[(long long)(xx - 1) * n2] = cscale(csub(P, cscale(z, (double)xx)), inv_ll1(xx));
