@@ -92,6 +92,7 @@ SMALL = [
     banded_random_problem(50, seed=11, wH=4, wL=2, P=1),   # mode 2, one dissipator
     banded_random_problem(45, seed=12, wH=3, wL=0, P=1),   # mode 0 widths (3, 0)
     banded_random_problem(77, seed=13, wH=1, wL=1, P=2),   # mode 0 widths (2, 1), runtime P
+    dimer_problem(1300, True),                               # fill with a barrier per far tile (N >= 1200)
 ]
 
 
