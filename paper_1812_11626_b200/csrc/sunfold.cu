@@ -792,6 +792,72 @@ __device__ __forceinline__ void fill_near_unit(const Prob& pr, long long j, cons
   }
 }
 
+// Mode-0 near unit j with two rows per warp (16-lane halves): side rows 16 j .. 16 j + 15.  The
+// two rows' dependent lookups (slot prefix, offsets, metadata) overlap in one instruction
+// stream; every shuffle is on convergent code, the copies are half-warp strided loops.
+__device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, const int* __restrict__ cnt,
+                                                 const FillOut& fo, const NearSide& side) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int hl = lane & 15;
+  const long long np = pr.np;
+  const long long nside = 2 * ((long long)pr.n * 2 * pr.W + pr.n - 1);
+  const long long srow = j * 16 + wid * 2 + (lane >> 4);
+  int kind = 0, half = 0, a = 0, b = 0, lam = 0;
+  long long p = 0;
+  if (srow < nside) {
+    half = (int)(srow & 1);
+    kind = near_item(pr, srow >> 1, a, b, lam);
+    if (kind == 2 && half) kind = 0;
+    if (kind == 1) p = (long long)pidx32(pr.n, a, b);
+  }
+  int s1 = 0;
+  if (kind == 1) {
+    const long long ts = (p / pr.tp) * pr.tp;
+    const int* c = cnt + (half ? np : 0);
+    for (long long q = ts + hl; q < p; q += 16) s1 += __ldg(&c[q]) & CNT_MASK;  // mode 2 packs nR above
+  }
+#pragma unroll
+  for (int sh = 8; sh > 0; sh >>= 1) s1 += __shfl_xor_sync(FULL, s1, sh);  // within each half
+  if (kind == 0) return;  // no shuffles below
+  const NearMeta m = side.meta[srow];
+  long long o;
+  if (kind == 1) {
+    o = fo.toff[(half ? pr.npt : 0) + p / pr.tp] + s1;
+    if (hl == 0 && fo.K) fo.K[(half ? np : 0) + p] = m.k;
+  } else {
+    o = fo.toff[2 * pr.npt + lam - 1];
+    if (hl == 0) {
+      fo.row_ptr[2 * np + lam - 1] = o;
+      if (fo.K) fo.K[2 * np + lam - 1] = m.k;
+    }
+  }
+  const long long lim = fo.cap - o;
+  const int32_t* sc = side.col + srow * side.nc;
+  const double* sv = side.val + srow * side.nc;
+  const int nwin = m.n1 + m.n2 + m.nd, b2 = m.n1 + m.n2;
+#pragma unroll 2
+  for (int k = hl; k < nwin; k += 16) {
+    const int sidx = k < m.n1 ? k : (k < b2 ? side.seg + (k - m.n1) : 2 * side.seg + (k - b2));
+    const int c = __ldg(&sc[sidx]);
+    const double v = __ldg(&sv[sidx]);
+    if (k < lim) {
+      fo.col[o + k] = c;
+      fo.val[o + k] = v;
+    }
+  }
+  const long long ot = o + nwin, limt = lim - nwin;
+  const int dbase = (int)(2 * np - 1);
+#pragma unroll 4
+  for (int l = m.hi + 1 + hl; l <= m.lend; l += 16) {
+    const int k = l - m.hi - 1;
+    const double v = m.tr * __ldg(&pr.inv[l]);
+    if (k < limt) {
+      fo.col[ot + k] = dbase + l;
+      fo.val[ot + k] = v;
+    }
+  }
+}
+
 __host__ __device__ inline long long near_units1(long long n, long long W) {  // units of 8 side rows
   return (2 * (n * 2 * W + n - 1) + 7) / 8;
 }
@@ -1233,7 +1299,7 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
     if (HAS1) m1.fo.row_ptr[m1.pr.m] = *m1.fo.nnz;
   }
   // near units: NEAR_UNIT_ROWS side rows each (2 per near item)
-  const long long nn0 = near_units1(m0.pr.n, m0.pr.W);
+  const long long nn0 = (2 * (m0.pr.n * 2LL * m0.pr.W + m0.pr.n - 1) + 15) / 16;  // 16 side rows per unit
   // Q1 tiles: none when the Q0 far tiles write Q1's rows (staged Q0 tiles of 256 pairs)
   constexpr bool Q1MERGED = HAS1 && !FF::DIRECT;
   // Q1's near items are its D rows; with the diagonal drive they are empty (count pass), so
@@ -1292,7 +1358,7 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
       if constexpr (Q1MERGED) fill_q1_chunk(prf1, m1.pr.npt, idx, m1.cnt, m1.fo);
     } else if (kind == 1) {
 #ifndef SUN_EXP_NO_NEAR
-      fill_near_unit(m0.pr, idx, m0.cnt, m0.fo, m0.side);
+      fill_near_unit_h(m0.pr, idx, m0.cnt, m0.fo, m0.side);
 #endif
     } else if (kind == 2) {
       if constexpr (HAS1) fill_near_unit(m1.pr, idx, m1.cnt, m1.fo, m1.side);
@@ -2306,7 +2372,7 @@ cudaError_t attr_fill0(const Prob& p0, const Prob* p1, long long& grid) {
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fill0<WK, WL, PT, Q1W>, 256, smem);
   if (e != cudaSuccess) return e;
   auto tiles = [](const Prob& p) { return (p.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE; };
-  long long U = tiles(p0) + near_units1(p0.n, p0.W);
+  long long U = tiles(p0) + (2 * (p0.n * 2LL * p0.W + p0.n - 1) + 15) / 16;
   if (Q1W >= 0 && p1) U += tiles(*p1) + near_units1(p1->n, p1->W);
   grid = (long long)(nb > 0 ? nb : 1) * sms;
   if (grid > U) grid = U;
