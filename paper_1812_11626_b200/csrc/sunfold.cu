@@ -795,13 +795,19 @@ __device__ __forceinline__ void fill_near_unit(const Prob& pr, long long j, cons
 // Mode-0 near unit j with two rows per warp (16-lane halves): side rows 16 j .. 16 j + 15.  The
 // two rows' dependent lookups (slot prefix, offsets, metadata) overlap in one instruction
 // stream; every shuffle is on convergent code, the copies are half-warp strided loops.
+#ifndef SUN_NEAR_RPW
+#define SUN_NEAR_RPW 2
+#endif
+constexpr int NEAR_RPW = SUN_NEAR_RPW;        // near rows per warp (lane groups of 32 / NEAR_RPW)
+constexpr int NEAR_GL = 32 / NEAR_RPW;        // lanes per row
+constexpr int NEAR_UROWS = 8 * NEAR_RPW;      // side rows per near unit
 __device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, const int* __restrict__ cnt,
                                                  const FillOut& fo, const NearSide& side) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int hl = lane & 15;
+  const int hl = lane & (NEAR_GL - 1);
   const long long np = pr.np;
   const long long nside = 2 * ((long long)pr.n * 2 * pr.W + pr.n - 1);
-  const long long srow = j * 16 + wid * 2 + (lane >> 4);
+  const long long srow = j * NEAR_UROWS + wid * NEAR_RPW + lane / NEAR_GL;
   int kind = 0, half = 0, a = 0, b = 0, lam = 0;
   long long p = 0;
   if (srow < nside) {
@@ -814,10 +820,10 @@ __device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, co
   if (kind == 1) {
     const long long ts = (p / pr.tp) * pr.tp;
     const int* c = cnt + (half ? np : 0);
-    for (long long q = ts + hl; q < p; q += 16) s1 += __ldg(&c[q]) & CNT_MASK;  // mode 2 packs nR above
+    for (long long q = ts + hl; q < p; q += NEAR_GL) s1 += __ldg(&c[q]) & CNT_MASK;  // mode 2 packs nR above
   }
 #pragma unroll
-  for (int sh = 8; sh > 0; sh >>= 1) s1 += __shfl_xor_sync(FULL, s1, sh);  // within each half
+  for (int sh = NEAR_GL / 2; sh > 0; sh >>= 1) s1 += __shfl_xor_sync(FULL, s1, sh);  // within each group
   if (kind == 0) return;  // no shuffles below
   const NearMeta m = side.meta[srow];
   long long o;
@@ -836,7 +842,7 @@ __device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, co
   const double* sv = side.val + srow * side.nc;
   const int nwin = m.n1 + m.n2 + m.nd, b2 = m.n1 + m.n2;
 #pragma unroll 2
-  for (int k = hl; k < nwin; k += 16) {
+  for (int k = hl; k < nwin; k += NEAR_GL) {
     const int sidx = k < m.n1 ? k : (k < b2 ? side.seg + (k - m.n1) : 2 * side.seg + (k - b2));
     const int c = __ldg(&sc[sidx]);
     const double v = __ldg(&sv[sidx]);
@@ -848,7 +854,7 @@ __device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, co
   const long long ot = o + nwin, limt = lim - nwin;
   const int dbase = (int)(2 * np - 1);
 #pragma unroll 4
-  for (int l = m.hi + 1 + hl; l <= m.lend; l += 16) {
+  for (int l = m.hi + 1 + hl; l <= m.lend; l += NEAR_GL) {
     const int k = l - m.hi - 1;
     const double v = m.tr * __ldg(&pr.inv[l]);
     if (k < limt) {
@@ -1299,7 +1305,7 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
     if (HAS1) m1.fo.row_ptr[m1.pr.m] = *m1.fo.nnz;
   }
   // near units: NEAR_UNIT_ROWS side rows each (2 per near item)
-  const long long nn0 = (2 * (m0.pr.n * 2LL * m0.pr.W + m0.pr.n - 1) + 15) / 16;  // 16 side rows per unit
+  const long long nn0 = (2 * (m0.pr.n * 2LL * m0.pr.W + m0.pr.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
   // Q1 tiles: none when the Q0 far tiles write Q1's rows (staged Q0 tiles of 256 pairs)
   constexpr bool Q1MERGED = HAS1 && !FF::DIRECT;
   // Q1's near items are its D rows; with the diagonal drive they are empty (count pass), so
@@ -2372,7 +2378,7 @@ cudaError_t attr_fill0(const Prob& p0, const Prob* p1, long long& grid) {
   if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fill0<WK, WL, PT, Q1W>, 256, smem);
   if (e != cudaSuccess) return e;
   auto tiles = [](const Prob& p) { return (p.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE; };
-  long long U = tiles(p0) + (2 * (p0.n * 2LL * p0.W + p0.n - 1) + 15) / 16;
+  long long U = tiles(p0) + (2 * (p0.n * 2LL * p0.W + p0.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
   if (Q1W >= 0 && p1) U += tiles(*p1) + near_units1(p1->n, p1->W);
   grid = (long long)(nb > 0 ? nb : 1) * sms;
   if (grid > U) grid = U;
