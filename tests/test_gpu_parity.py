@@ -268,3 +268,36 @@ def test_wrapper_accepts_dense_and_sparse_torch_inputs():
     for s in (0, 5, ref[0].m - 1):
         assert np.array_equal(np.nonzero(D[s])[0], c[rp[s]:rp[s + 1]])
         assert np.array_equal(D[s, c[rp[s]:rp[s + 1]]], v[rp[s]:rp[s + 1]])
+
+
+def test_side_stream_matches_default_stream():
+    """Every call takes the caller's stream (C-ABI `void* stream`): a plan bound to a side stream
+    gives the default stream's results bit for bit (unfold, run, apply, both RK4 paths)."""
+    sun = _gpu()
+    prob = dimer_problem(60, True)
+    ref_plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    R = ref_plan.run()
+    v = torch.linspace(-1, 1, prob.m, dtype=torch.float64, device="cuda")
+    ya = sun.apply(R[0], R[1], 0.9, R[2], v)
+    va = v.clone()
+    sun.rk4(R[0], R[1], R[2], va, 1e-4, 3, eps0=1.0, eps1=0.5)
+    vma = v.clone()
+    ref_plan.rk4(vma, 1e-4, 3, eps0=1.0, eps1=0.5)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas, stream=s)
+        S1 = plan.run()
+        S2 = plan.run()
+        yb = sun.apply(S2[0], S2[1], 0.9, S2[2], v, stream=s)
+        vb = v.clone()
+        sun.rk4(S2[0], S2[1], S2[2], vb, 1e-4, 3, eps0=1.0, eps1=0.5, stream=s)
+        vmb = v.clone()
+        plan.rk4(vmb, 1e-4, 3, eps0=1.0, eps1=0.5)
+    s.synchronize()
+    for A, B in ((R, S1), (R, S2)):
+        assert torch.equal(A[0].row_ptr, B[0].row_ptr) and torch.equal(A[0].col, B[0].col)
+        assert torch.equal(A[0].val, B[0].val) and torch.equal(A[1].val, B[1].val) and torch.equal(A[2], B[2])
+    assert torch.equal(ya, yb) and torch.equal(va, vb) and torch.equal(vma, vmb)
+    plan.close()
+    ref_plan.close()
