@@ -47,3 +47,39 @@ def test_zcsr_roundtrip():
     z = ZCSR.from_dense(A + 0j)
     assert np.array_equal(z.to_dense(), A + 0j)
     assert all((np.diff(z.col[z.row_ptr[r]:z.row_ptr[r + 1]]) > 0).all() for r in range(7))
+
+
+def test_gks_ensemble_recipe():
+    """F3 inputs (F3 'ensemble reading'): H Hermitian (GUE), A = G G^+ Hermitian
+    positive semidefinite with Tr A = N; seeded, so two draws with one seed agree."""
+    import numpy as np
+
+    from workloads import gks_ensemble
+
+    n, B = 4, 3
+    H, A = gks_ensemble(n, B, seed=9)
+    H2, A2 = gks_ensemble(n, B, seed=9)
+    assert np.array_equal(H, H2) and np.array_equal(A, A2)
+    for b in range(B):
+        assert np.abs(H[b] - H[b].conj().T).max() == 0.0
+        assert np.abs(A[b] - A[b].conj().T).max() < 1e-12 * np.abs(A[b]).max()
+        assert abs(np.trace(A[b]).real - n) < 1e-12
+        assert np.linalg.eigvalsh(A[b]).min() > -1e-12
+
+
+def test_rank_p_coefficients_band():
+    """band > 0: only S_ab / J_ab with b - a <= band (and all D^l) carry a coefficient, so
+    L = sum_j l_j F_j is banded (checked through the oracle's basis)."""
+    import numpy as np
+
+    from oracle import basis
+    from workloads import rank_p_coefficients
+
+    n = 9
+    l, g = rank_p_coefficients(n, 2, seed=1, band=2)
+    F = basis.generators(n)
+    for p in range(2):
+        L = np.einsum("j,jab->ab", l[p], F)
+        r, c = np.nonzero(np.abs(L) > 0)
+        assert np.abs(r - c).max() <= 2
+    assert np.all((g >= 0.05) & (g <= 0.5))
