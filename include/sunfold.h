@@ -61,8 +61,11 @@ typedef enum {
   SUN_ERR_RATE = 4,          /* gamma_p < 0 or non-finite                   */
   SUN_ERR_CAPACITY = 5,      /* an output CSR capacity is below the required nnz            */
   SUN_ERR_CUDA = 6,          /* CUDA runtime error; sun_status_string() reports it          */
-  SUN_ERR_BANDWIDTH = 7,     /* half-bandwidth beyond the banded kernels' limit  */
-  SUN_ERR_STATE = 8          /* call out of sequence (e.g. sun_unfold before sun_count)     */
+  SUN_ERR_UNSUPPORTED = 7,   /* operation not available for this plan: the matrix-free RK4 /
+                                apply on a general-pattern (mode 3) plan; a single output row
+                                with >= 2^32 candidate terms                                 */
+  SUN_ERR_STATE = 8          /* call out of sequence (e.g. sun_unfold before sun_count), or
+                                operator values outside the pattern fixed by the plan       */
 } sun_status;
 
 /* N x N complex operator, CSR, device memory.  row_ptr int64[n+1]; col int32[nnz], strictly
@@ -93,7 +96,8 @@ typedef struct {
   int32_t w_h0, w_h1, w_l, w_k; /* half-bandwidths: H0, H1, max_p L_p, K = H0 + i/2 sum gamma L^+L */
   double tau_q0, tau_q1;        /* drop thresholds (R6) */
   int32_t mode_q0, mode_q1;     /* 0: thread-per-pair far tiles (compile-time widths); 1: warp-per-pair,
-                                   runtime widths; 2: warp-per-pair far path, compile-time widths */
+                                   runtime widths; 2: warp-per-pair far path, compile-time widths;
+                                   3: general pattern (candidate merge, sunfold_general.cu) */
   int32_t pairs_per_tile_q0, pairs_per_tile_q1;
   int64_t tiles_q0, tiles_q1;   /* scan slots (S tiles, J tiles, D slots) */
   int32_t has_h1;
@@ -102,13 +106,23 @@ typedef struct {
   int32_t launches_fill;        /* kernels enqueued by sun_unfold (sun_run = both) */
 } sun_plan_info_t;
 
-/* Bytes of device workspace a plan for dimension n with P dissipators needs (0 if n or P is
- * out of range).  The workspace holds the band-expanded operators, the per-row counts
- * (2 x 4 bytes per output row) and the tile offsets; it must be 256-byte aligned. */
+/* Bytes of device workspace a plan for dimension n with P dissipators needs when its operators
+ * are banded (0 if n or P is out of range): the band-expanded operators, the per-row counts
+ * (2 x 4 bytes per output row) and the tile offsets; 256-byte aligned.  Operators of any other
+ * pattern need sun_workspace_bytes_ops. */
 size_t sun_workspace_bytes(int32_t n, int32_t P);
 
+/* Bytes of device workspace that suffice for these operators whatever their pattern (host-only:
+ * reads the n and nnz fields): sun_workspace_bytes(n, P) plus, for the general-pattern mode,
+ * column access to every L_p (8 bytes per nonzero, 8 bytes per column) and the heavy-row lists
+ * (8 bytes per generator pair).  0 for invalid arguments. */
+size_t sun_workspace_bytes_ops(const sun_zcsr* H0, const sun_zcsr* H1, const sun_zcsr* const* L, int32_t P);
+
 /* Validate the inputs and analyse their patterns (half-bandwidths, Frobenius norms) on the
- * device, then build the plan.
+ * device, then build the plan.  Operators of ANY pattern are accepted ("any complex N x N matrix
+ * could be chosen as an operator L_p"): banded ones (max(w_H0, 2 w_L) <= 15, w_L <= 7,
+ * w_H1 <= 15) take the band kernels (modes 0-2), every other pattern the general mode (mode 3,
+ * candidate terms merged per row by a sort and a segmented reduction).
  *   H0: required.  H1: NULL if there is no periodic drive (then Q1 is not produced).
  *   L: array of P pointers to operators (may be NULL if P == 0); gamma: HOST array of P rates.
  *   workspace: device, >= sun_workspace_bytes(H0->n, P); owned by the caller, bound to the
@@ -116,9 +130,20 @@ size_t sun_workspace_bytes(int32_t n, int32_t P);
  * Runs one kernel on `stream` and synchronises on a small readback.  The input operators
  * must stay valid until sun_count has completed on the stream (their values are read there;
  * their patterns, i.e. bandwidths, are fixed by the plan).  Errors: SUN_ERR_DIM, _ARG (also
- * malformed CSR: unsorted/out-of-range columns), _RATE, _BANDWIDTH, _CUDA; *out is NULL then. */
+ * malformed CSR: unsorted/out-of-range columns), _RATE, _CAPACITY (a general-pattern plan with a
+ * workspace smaller than sun_workspace_bytes_ops), _CUDA; *out is NULL then. */
 int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const sun_zcsr* const* L,
                     const double* gamma, int32_t P, void* workspace, size_t workspace_bytes, void* stream);
+
+/* sun_plan_create with options.  flags: SUN_PLAN_GENERAL = take the general mode even for banded
+ * operators (cross-checks); SUN_PLAN_SMALLCAP = general mode with a 16-candidate merge buffer
+ * (tests: forces the key-range chunks and the single-key reduction at small N; slow);
+ * 0 = sun_plan_create. */
+#define SUN_PLAN_GENERAL 1
+#define SUN_PLAN_SMALLCAP 2
+int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const sun_zcsr* const* L,
+                       const double* gamma, int32_t P, int32_t flags, void* workspace, size_t workspace_bytes,
+                       void* stream);
 
 /* Expand H0/H1/L_p into band storage, form K = H0 + (i/2) sum_p gamma_p L_p^+ L_p and the drop
  * thresholds from the operators' current values, run the count pass and the prefix scan for
@@ -127,8 +152,9 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
 int sun_count(sun_plan plan, void* stream);
 
 /* Synchronise the sun_count stream and return nnz(Q0) and nnz(Q1) (0 if no drive); reports
- * SUN_ERR_NOT_HERMITIAN / SUN_ERR_ARG found by the device-side validation, and
- * SUN_ERR_BANDWIDTH if an operator's values now exceed the half-bandwidth fixed by the plan. */
+ * SUN_ERR_NOT_HERMITIAN / SUN_ERR_ARG found by the device-side validation,
+ * SUN_ERR_STATE if an operator's values now exceed the half-bandwidth fixed by a banded plan, and
+ * SUN_ERR_UNSUPPORTED for a row with >= 2^32 candidate terms (general mode). */
 int sun_plan_nnz(sun_plan plan, int64_t* nnz_q0, int64_t* nnz_q1);
 
 /* Fill pass: write Q0 (CSR), K (float64[M]) and, if the plan has H1, Q1.  Q1 may be NULL
@@ -199,9 +225,9 @@ size_t sun_rk4_work_bytes(int64_t m);
  * expressions and tau masks, takes the near and D rows from the count pass's side buffer
  * (chain tails in O(1) from a per-stage prefix over the D coefficients), K from the same data.
  * Supported: mode-0 plans and mode-2 plans (sun_plan_info mode_q0 = 0 or 2) without a drive or
- * with a diagonal H1; else SUN_ERR_BANDWIDTH.  v: device float64[M], in/out.  work: device scratch of
+ * with a diagonal H1; else SUN_ERR_UNSUPPORTED.  v: device float64[M], in/out.  work: device scratch of
  * sun_rk4_plan_work_bytes(plan) bytes (4 M + N doubles).  Asynchronous on `stream`.
- * Errors: SUN_ERR_ARG, SUN_ERR_STATE (plan not counted), SUN_ERR_BANDWIDTH, SUN_ERR_CAPACITY,
+ * Errors: SUN_ERR_ARG, SUN_ERR_STATE (plan not counted), SUN_ERR_UNSUPPORTED, SUN_ERR_CAPACITY,
  * SUN_ERR_CUDA. */
 int sun_rk4_plan(sun_plan plan, double eps0, double eps1, double omega, double t0, double h, int64_t nsteps,
                  double* v, void* work, size_t work_bytes, void* stream);

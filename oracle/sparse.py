@@ -41,6 +41,7 @@ def _load():
         lib.o2_nnz.argtypes = [P]
         lib.o2_gap.argtypes = [P, P]
         lib.o2_fetch.argtypes = [P, P, P, P, P]
+        lib.o2_fetch_abs.argtypes = [P, P]
         lib.o2_free.argtypes = [P]
         lib.o2_max_threads.restype = ctypes.c_int
         _lib = lib
@@ -107,13 +108,17 @@ def unfold_csr(H, Ls=(), gammas=(), tau: float = 0.0, with_k: bool = True, nthre
         val = np.empty(max(nnz, 1), dtype=np.float64)
         K = np.empty(m, dtype=np.float64)
         lib.o2_fetch(res, _ptr(row_ptr), _ptr(col), _ptr(val), _ptr(K))
-        gap = np.empty(3, dtype=np.float64)
+        absv = np.empty(max(nnz, 1), dtype=np.float64)
+        lib.o2_fetch_abs(res, _ptr(absv))
+        gap = np.empty(4, dtype=np.float64)
         lib.o2_gap(res, _ptr(gap))
     finally:
         lib.o2_free(res)
     return {
         "row_ptr": row_ptr, "col": col[:nnz], "val": val[:nnz], "K": K if with_k else None,
-        "gap": {"max_dropped": float(gap[0]), "min_kept": float(gap[1]), "max_imag": float(gap[2])},
+        "absum": absv[:nnz],
+        "gap": {"max_dropped": float(gap[0]), "min_kept": float(gap[1]), "max_imag": float(gap[2]),
+                "min_margin": float(gap[3])},
         "seconds": seconds,
     }
 
@@ -127,7 +132,76 @@ def unfold_problem(problem, nthreads: int = 0):
 
 
 def assert_gap(res, tau: float, factor: float = 1e3):
-    """R6: the largest dropped |q| must be < tau/factor and the smallest kept > tau*factor."""
+    """R6: the largest dropped |q| must be < tau/factor and the smallest kept
+    > tau*factor (factor 1e3 as adopted; configs where this fails are FLAGGED in DESIGN.md R6
+    and checked with assert_margin instead)."""
     gap = res["gap"]
     assert gap["max_dropped"] < tau / factor, f"dropped {gap['max_dropped']} vs tau {tau}"
     assert gap["min_kept"] > tau * factor, f"kept {gap['min_kept']} vs tau {tau}"
+
+
+MARGIN_MIN = 50.0  # DESIGN.md R6: entries near tau lie >= 50 per-entry roundoff bounds away from it
+
+
+def assert_margin(res, min_margin: float = MARGIN_MIN):
+    """R6, the quantity that protects the pattern: for every entry with |q| <= 1e6 tau (kept or
+    dropped), ||q| - tau| >= min_margin * 1e-16 * sum|terms| (sum|terms| = the absolute sum of
+    the products that make up the entry, accumulated by O2), i.e. no ordering of the
+    floating-point sum can move the entry across tau."""
+    m = res["gap"]["min_margin"]
+    assert m >= min_margin, f"roundoff margin {m} < {min_margin}"
+
+
+# Configs on which the adopted R6 gap rule (kept > 1e3 tau) fails, with the measured
+# min_kept / tau (DESIGN.md R6 "flagged configs"); they are checked with assert_margin.
+R6_FLAGGED = {"c3_banded_N512_P4": 543.45, "ring_N256_drive": 138.68, "sparse_N300_s21_P2": 520.36}
+
+
+def assert_r6(res, tau: float, name: str = ""):
+    """The stored-pattern checks of DESIGN.md R6 on an oracle result: the roundoff margin always;
+    the 1e3 gap rule unless `name` is a flagged config, whose measured gap is asserted instead
+    (within 1 % of the recorded value, so a change is noticed)."""
+    assert_margin(res)
+    if name in R6_FLAGGED:
+        ratio = res["gap"]["min_kept"] / tau
+        assert abs(ratio / R6_FLAGGED[name] - 1.0) < 1e-2, f"{name}: min_kept/tau {ratio} changed"
+        assert res["gap"]["max_dropped"] < tau / 1e3
+    else:
+        assert_gap(res, tau)
+
+
+def assert_entries_close(val_got, res, name: str = "Q"):
+    """R7: normwise max |q_gpu - q_oracle| <= 1e-12 max |Q_oracle|, and per entry
+    |q_gpu - q_oracle| <= 1e-12 |q_oracle| wherever the entry is well conditioned, cond =
+    sum|terms| / |q| <= 100 (sum|terms| from O2).  Returns (normwise error, fraction of entries
+    with cond <= 100, their worst relative error)."""
+    val_got = np.asarray(val_got)
+    ref = res["val"]
+    if ref.size == 0:
+        return 0.0, 1.0, 0.0
+    scale = float(np.abs(ref).max())
+    err = np.abs(val_got - ref)
+    assert err.max() <= 1e-12 * scale, f"{name}: max err {err.max()} vs 1e-12 * {scale}"
+    cond = res["absum"] / np.abs(ref)
+    good = cond <= 100.0
+    rel = err[good] / np.abs(ref[good])
+    worst = float(rel.max()) if rel.size else 0.0
+    assert worst <= 1e-12, f"{name}: per-entry rel err {worst} on an entry with cond <= 100"
+    return float(err.max() / scale), float(good.mean()), worst
+
+
+def assert_k_close(k_got, k_ref, what: str = "K", tau: float = 0.0):
+    """R7 for K: max |K_gpu - K_oracle| <= 1e-12 max |K_oracle|.  Where K is numerically zero
+    (max |K_oracle| <= tau, the R6 threshold of the problem: e.g. Hermitian or diagonal L_p, for
+    which K == 0 exactly and the oracle holds only roundoff), max |K_gpu| <= tau; with tau = 0
+    that is an exact-zero check."""
+    k_got = np.asarray(k_got)
+    k_ref = np.asarray(k_ref)
+    scale = float(np.abs(k_ref).max()) if k_ref.size else 0.0
+    if scale <= tau:
+        got = float(np.abs(k_got).max()) if k_got.size else 0.0
+        assert got <= tau, f"{what}: K is numerically zero (max |K_oracle| {scale} <= tau {tau}) but GPU has {got}"
+        return 0.0
+    err = float(np.abs(k_got - k_ref).max())
+    assert err <= 1e-12 * scale, f"{what}: max err {err} vs 1e-12 * {scale}"
+    return err / scale

@@ -46,6 +46,7 @@ typedef struct {
 typedef struct {
   int32_t r, c;
   zd v;
+  double a; /* sum of |term| merged into this entry (roundoff yardstick, R6) */
 } term_t;
 
 typedef struct {
@@ -61,6 +62,7 @@ static void tpush(tvec_t *tv, int32_t r, int32_t c, zd v) {
   tv->t[tv->len].r = r;
   tv->t[tv->len].c = c;
   tv->t[tv->len].v = v;
+  tv->t[tv->len].a = cabs(v);
   tv->len++;
 }
 
@@ -68,19 +70,22 @@ typedef struct {
   int32_t *s;
   int32_t *m;
   double *v;
+  double *a; /* sum|terms| of the entry (condition number = a / |v|; R7) */
   int64_t len, cap;
 } ovec_t;
 
-static void opush(ovec_t *o, int32_t s, int32_t m, double v) {
+static void opush(ovec_t *o, int32_t s, int32_t m, double v, double a) {
   if (o->len == o->cap) {
     o->cap = o->cap ? 2 * o->cap : 1024;
     o->s = (int32_t *)realloc(o->s, (size_t)o->cap * sizeof(int32_t));
     o->m = (int32_t *)realloc(o->m, (size_t)o->cap * sizeof(int32_t));
     o->v = (double *)realloc(o->v, (size_t)o->cap * sizeof(double));
+    o->a = (double *)realloc(o->a, (size_t)o->cap * sizeof(double));
   }
   o->s[o->len] = s;
   o->m[o->len] = m;
   o->v[o->len] = v;
+  o->a[o->len] = a;
   o->len++;
 }
 
@@ -219,23 +224,27 @@ static int64_t sum_terms(tvec_t *tv) {
   qsort(tv->t, (size_t)tv->len, sizeof(term_t), cmp_term);
   int64_t u = 0;
   for (int64_t i = 1; i < tv->len; ++i) {
-    if (tv->t[i].r == tv->t[u].r && tv->t[i].c == tv->t[u].c)
+    if (tv->t[i].r == tv->t[u].r && tv->t[i].c == tv->t[u].c) {
       tv->t[u].v += tv->t[i].v;
-    else
+      tv->t[u].a += tv->t[i].a;
+    } else
       tv->t[++u] = tv->t[i];
   }
   tv->len = u + 1;
   return tv->len;
 }
 
-/* X_rc from the sorted unique terms (0 if absent); *found tells whether it is stored. */
-static zd lookup(const tvec_t *tv, int32_t r, int32_t c, int *found) {
+/* X_rc from the sorted unique terms (0 if absent); *found tells whether it is stored;
+ * *absum (if given) receives the sum of |terms| merged into it. */
+static zd lookup_a(const tvec_t *tv, int32_t r, int32_t c, int *found, double *absum) {
   int64_t lo = 0, hi = tv->len - 1;
+  if (absum) *absum = 0.0;
   while (lo <= hi) {
     int64_t mid = (lo + hi) / 2;
     const term_t *t = &tv->t[mid];
     if (t->r == r && t->c == c) {
       if (found) *found = 1;
+      if (absum) *absum = t->a;
       return t->v;
     }
     if (t->r < r || (t->r == r && t->c < c))
@@ -246,6 +255,7 @@ static zd lookup(const tvec_t *tv, int32_t r, int32_t c, int *found) {
   if (found) *found = 0;
   return 0;
 }
+static zd lookup(const tvec_t *tv, int32_t r, int32_t c, int *found) { return lookup_a(tv, r, c, found, NULL); }
 
 static inline int64_t pidx(int64_t n, int64_t a, int64_t b) { return a * (2 * n - a - 1) / 2 + (b - a - 1); }
 
@@ -278,9 +288,20 @@ static int generator_entries(int n, int64_t m, int32_t *fr, int32_t *fc, zd *fv)
   return l + 1;
 }
 
+/* Gap diagnostics of the stored-pattern rule (R6).  min_margin: over every entry
+ * with |q| <= 1e6 tau, the smallest ||q| - tau| / (1e-16 sum|terms|) -- how many per-entry
+ * roundoff bounds separate the entry from the threshold (large = the keep/drop decision
+ * cannot depend on the order of summation). */
 typedef struct {
-  double max_dropped, min_kept, max_imag;
+  double max_dropped, min_kept, max_imag, min_margin;
 } gap_t;
+
+static void note_margin(gap_t *g, double v, double absum, double tau) {
+  if (tau <= 0.0 || fabs(v) > 1e6 * tau) return;
+  double bound = 1e-16 * absum;
+  double r = bound > 0.0 ? fabs(fabs(v) - tau) / bound : INFINITY;
+  if (r < g->min_margin) g->min_margin = r;
+}
 
 /* Project X (unique sorted terms) on every F_s: emit (s, col, Re Tr(F_s X)) with |.| > tau. */
 static void project_emit(int n, const tvec_t *X, int32_t col, double tau, ovec_t *out, double *dense_out,
@@ -297,7 +318,9 @@ static void project_emit(int n, const tvec_t *X, int32_t col, double tau, ovec_t
       (void)lookup(X, c, r, &up);
       if (up) continue;
     }
-    zd xab = lookup(X, a, b, NULL), xba = lookup(X, b, a, NULL);
+    double aab, aba;
+    zd xab = lookup_a(X, a, b, NULL, &aab), xba = lookup_a(X, b, a, NULL, &aba);
+    double absum = (aab + aba) * is2; /* sum|terms| of both Tr(S_ab X) and Tr(J_ab X) */
     zd trS = (xba + xab) * is2;          /* Tr(S_ab X) */
     zd trJ = (-I * xba + I * xab) * is2; /* Tr(J_ab X) */
     int64_t p = pidx(n, a, b);
@@ -306,10 +329,11 @@ static void project_emit(int n, const tvec_t *X, int32_t col, double tau, ovec_t
     int64_t rows[2] = {p, np + p};
     for (int q = 0; q < 2; ++q) {
       if (fabs(ims[q]) > gap->max_imag) gap->max_imag = fabs(ims[q]);
+      if (!dense_out) note_margin(gap, vals[q], absum, tau);
       if (dense_out) {
         dense_out[rows[q]] = vals[q];
       } else if (fabs(vals[q]) > tau) {
-        opush(out, (int32_t)rows[q], col, vals[q]);
+        opush(out, (int32_t)rows[q], col, vals[q], absum);
         if (fabs(vals[q]) < gap->min_kept) gap->min_kept = fabs(vals[q]);
       } else if (fabs(vals[q]) > gap->max_dropped) {
         gap->max_dropped = fabs(vals[q]);
@@ -321,29 +345,34 @@ static void project_emit(int n, const tvec_t *X, int32_t col, double tau, ovec_t
   for (int64_t i = 0; i < X->len; ++i)
     if (X->t[i].r == X->t[i].c) ++ndiag;
   if (ndiag == 0) return;
-  for (int c = 0; c < n; ++c) diagbuf[2 * c] = diagbuf[2 * c + 1] = 0.0;
+  for (int c = 0; c < n; ++c) diagbuf[3 * c] = diagbuf[3 * c + 1] = diagbuf[3 * c + 2] = 0.0;
   for (int64_t i = 0; i < X->len; ++i)
     if (X->t[i].r == X->t[i].c) {
-      diagbuf[2 * X->t[i].r] = creal(X->t[i].v);
-      diagbuf[2 * X->t[i].r + 1] = cimag(X->t[i].v);
+      diagbuf[3 * X->t[i].r] = creal(X->t[i].v);
+      diagbuf[3 * X->t[i].r + 1] = cimag(X->t[i].v);
+      diagbuf[3 * X->t[i].r + 2] = X->t[i].a;
     }
   double pre_re = diagbuf[0], pre_im = diagbuf[1]; /* sum_{c<l} X_cc, starting at l = 1 */
+  double pre_a = diagbuf[2];                        /* sum_{c<l} sum|terms of X_cc| */
   for (int l = 1; l < n; ++l) {
     double nrm = 1.0 / sqrt((double)l * (l + 1.0));
-    double v = (pre_re - (double)l * diagbuf[2 * l]) * nrm;
-    double im = (pre_im - (double)l * diagbuf[2 * l + 1]) * nrm;
+    double v = (pre_re - (double)l * diagbuf[3 * l]) * nrm;
+    double im = (pre_im - (double)l * diagbuf[3 * l + 1]) * nrm;
     if (fabs(im) > gap->max_imag) gap->max_imag = fabs(im);
     int64_t row = 2 * np + l - 1;
+    const double dabs = (pre_a + (double)l * diagbuf[3 * l + 2]) * nrm;
+    if (!dense_out) note_margin(gap, v, dabs, tau);
     if (dense_out) {
       dense_out[row] = v;
     } else if (fabs(v) > tau) {
-      opush(out, (int32_t)row, col, v);
+      opush(out, (int32_t)row, col, v, dabs);
       if (fabs(v) < gap->min_kept) gap->min_kept = fabs(v);
     } else if (fabs(v) > gap->max_dropped) {
       gap->max_dropped = fabs(v);
     }
-    pre_re += diagbuf[2 * l];
-    pre_im += diagbuf[2 * l + 1];
+    pre_re += diagbuf[3 * l];
+    pre_im += diagbuf[3 * l + 1];
+    pre_a += diagbuf[3 * l + 2];
   }
 }
 
@@ -352,6 +381,7 @@ typedef struct {
   int64_t *row_ptr;
   int32_t *col;
   double *val;
+  double *absv;
   double *K;
   gap_t gap;
 } o2_result;
@@ -403,10 +433,10 @@ void *o2_unfold(int n, const int64_t *h_rp, const int32_t *h_ci, const double *h
     int32_t *fr = (int32_t *)malloc((size_t)n * sizeof(int32_t));
     int32_t *fc = (int32_t *)malloc((size_t)n * sizeof(int32_t));
     zd *fv = (zd *)malloc((size_t)n * sizeof(zd));
-    double *diagbuf = (double *)malloc((size_t)2 * n * sizeof(double));
+    double *diagbuf = (double *)malloc((size_t)3 * n * sizeof(double));
 #pragma omp for schedule(dynamic, 1)
     for (int64_t ch = 0; ch < nch; ++ch) {
-      gap_t g = {0.0, INFINITY, 0.0};
+      gap_t g = {0.0, INFINITY, 0.0, INFINITY};
       for (int64_t m = ch * CH; m < (ch + 1) * CH && m < M; ++m) {
         int nf = generator_entries(n, m, fr, fc, fv);
         tv.len = 0;
@@ -427,17 +457,20 @@ void *o2_unfold(int n, const int64_t *h_rp, const int32_t *h_ci, const double *h
   res->gap.max_dropped = 0.0;
   res->gap.min_kept = INFINITY;
   res->gap.max_imag = 0.0;
+  res->gap.min_margin = INFINITY;
   int64_t nnz = 0;
   for (int64_t ch = 0; ch < nch; ++ch) {
     nnz += outs[ch].len;
     if (gaps[ch].max_dropped > res->gap.max_dropped) res->gap.max_dropped = gaps[ch].max_dropped;
     if (gaps[ch].min_kept < res->gap.min_kept) res->gap.min_kept = gaps[ch].min_kept;
     if (gaps[ch].max_imag > res->gap.max_imag) res->gap.max_imag = gaps[ch].max_imag;
+    if (gaps[ch].min_margin < res->gap.min_margin) res->gap.min_margin = gaps[ch].min_margin;
   }
   res->nnz = nnz;
   res->row_ptr = (int64_t *)calloc((size_t)M + 1, sizeof(int64_t));
   res->col = (int32_t *)malloc((size_t)(nnz ? nnz : 1) * sizeof(int32_t));
   res->val = (double *)malloc((size_t)(nnz ? nnz : 1) * sizeof(double));
+  res->absv = (double *)malloc((size_t)(nnz ? nnz : 1) * sizeof(double));
   /* stable counting sort by row; chunks are visited in column order */
   for (int64_t ch = 0; ch < nch; ++ch)
     for (int64_t i = 0; i < outs[ch].len; ++i) res->row_ptr[outs[ch].s[i] + 1]++;
@@ -449,10 +482,12 @@ void *o2_unfold(int n, const int64_t *h_rp, const int32_t *h_ci, const double *h
       int64_t d = pos[outs[ch].s[i]]++;
       res->col[d] = outs[ch].m[i];
       res->val[d] = outs[ch].v[i];
+      res->absv[d] = outs[ch].a[i];
     }
     free(outs[ch].s);
     free(outs[ch].m);
     free(outs[ch].v);
+    free(outs[ch].a);
   }
   free(pos);
   free(outs);
@@ -463,12 +498,12 @@ void *o2_unfold(int n, const int64_t *h_rp, const int32_t *h_ci, const double *h
     int32_t *fr = (int32_t *)malloc((size_t)n * sizeof(int32_t));
     int32_t *fc = (int32_t *)malloc((size_t)n * sizeof(int32_t));
     zd *fv = (zd *)malloc((size_t)n * sizeof(zd));
-    double *diagbuf = (double *)malloc((size_t)2 * n * sizeof(double));
+    double *diagbuf = (double *)malloc((size_t)3 * n * sizeof(double));
     for (int c = 0; c < n; ++c) { fr[c] = c; fc[c] = c; fv[c] = 1.0 / n; }
     tvec_t tv = {0, 0, 0};
     lindblad_terms(&md, n, fr, fc, fv, &tv);
     sum_terms(&tv);
-    gap_t g = {0.0, INFINITY, 0.0};
+    gap_t g = {0.0, INFINITY, 0.0, INFINITY};
     project_emit(n, &tv, 0, 0.0, NULL, res->K, diagbuf, &g);
     if (g.max_imag > res->gap.max_imag) res->gap.max_imag = g.max_imag;
     free(tv.t);
@@ -489,11 +524,12 @@ void *o2_unfold(int n, const int64_t *h_rp, const int32_t *h_ci, const double *h
 
 int64_t o2_nnz(void *r) { return ((o2_result *)r)->nnz; }
 
-void o2_gap(void *r, double *out3) {
+void o2_gap(void *r, double *out4) {
   o2_result *res = (o2_result *)r;
-  out3[0] = res->gap.max_dropped;
-  out3[1] = res->gap.min_kept;
-  out3[2] = res->gap.max_imag;
+  out4[0] = res->gap.max_dropped;
+  out4[1] = res->gap.min_kept;
+  out4[2] = res->gap.max_imag;
+  out4[3] = res->gap.min_margin;
 }
 
 void o2_fetch(void *r, int64_t *row_ptr, int32_t *col, double *val, double *K) {
@@ -506,11 +542,18 @@ void o2_fetch(void *r, int64_t *row_ptr, int32_t *col, double *val, double *K) {
   if (K) memcpy(K, res->K, (size_t)res->m * sizeof(double));
 }
 
+/* per-entry sum|terms| (same order as o2_fetch's col / val) */
+void o2_fetch_abs(void *r, double *absv) {
+  o2_result *res = (o2_result *)r;
+  if (res->nnz) memcpy(absv, res->absv, (size_t)res->nnz * sizeof(double));
+}
+
 void o2_free(void *r) {
   o2_result *res = (o2_result *)r;
   free(res->row_ptr);
   free(res->col);
   free(res->val);
+  free(res->absv);
   free(res->K);
   free(res);
 }

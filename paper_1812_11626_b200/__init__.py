@@ -18,6 +18,7 @@ K float64[M].  Generator order and the stored-pattern rule are those of include/
 from __future__ import annotations
 
 import ctypes
+import contextlib
 from typing import NamedTuple, Optional, Sequence
 
 import numpy as np
@@ -83,6 +84,24 @@ def _stream_handle(stream) -> int:
     return int(s.cuda_stream)
 
 
+@contextlib.contextmanager
+def _on(stream):
+    """Run a call's marshalling and allocations on `stream`: the stream first waits for the
+    caller's current stream (inputs made there are ordered before the kernels), and every
+    tensor allocated inside (workspace, outputs, scratch) belongs to `stream`, so the caching
+    allocator never hands its memory to another stream while the kernels still use it."""
+    if stream is None:
+        yield
+        return
+    cur = torch.cuda.current_stream(stream.device)
+    if stream == cur:
+        yield
+        return
+    stream.wait_stream(cur)
+    with torch.cuda.stream(stream):
+        yield
+
+
 def _to_device(A) -> DeviceZCSR:
     """Operator marshalling: DeviceZCSR as is; host ZCSR (workloads); a torch sparse-CSR tensor;
     a dense N x N torch tensor or numpy array (its nonzero entries, row-major)."""
@@ -124,9 +143,16 @@ class Plan:
     """A validated, analysed unfold problem bound to a device workspace (sun_plan_create)."""
 
     def __init__(self, H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), stream=None,
-                 guard_bytes: int = 0):
+                 guard_bytes: int = 0, general: bool = False, small_cap: bool = False):
         """guard_bytes > 0 (tests): the workspace gets a tail of that many 0xA5 bytes beyond the
-        size the library is told; workspace_guard_intact() checks it (out-of-bounds writes)."""
+        size the library is told; workspace_guard_intact() checks it (out-of-bounds writes).
+        general=True: the general-pattern mode even for banded operators (SUN_PLAN_GENERAL);
+        operators of any other pattern take it anyway.  small_cap=True (tests): general mode with a
+        16-candidate merge buffer (SUN_PLAN_SMALLCAP)."""
+        with _on(stream):
+            self._init(H0, H1, Ls, gammas, stream, guard_bytes, (1 if general else 0) | (2 if small_cap else 0))
+
+    def _init(self, H0, H1, Ls, gammas, stream, guard_bytes, flags=0):
         L = lib()
         self.stream = stream
         self.H0 = _to_device(H0)
@@ -138,13 +164,6 @@ class Plan:
         self.n = self.H0.n
         self.m = self.n * self.n - 1
         self.P = len(self.Ls)
-        nbytes = int(L.sun_workspace_bytes(self.n, self.P))
-        if nbytes == 0:
-            _check(2, "sun_workspace_bytes")
-        self.workspace = torch.empty(nbytes + guard_bytes, dtype=torch.uint8, device="cuda")
-        self._guard = guard_bytes
-        if guard_bytes:
-            self.workspace[nbytes:].fill_(0xA5)
         self._s_h0 = _zcsr_struct(self.H0)
         self._s_h1 = _zcsr_struct(self.H1) if self.H1 is not None else None
         self._s_ls = [_zcsr_struct(x) for x in self.Ls]
@@ -152,13 +171,20 @@ class Plan:
         for i, s in enumerate(self._s_ls):
             arr[i] = ctypes.addressof(s)
         self._arr = arr
+        s_h1 = ctypes.addressof(self._s_h1) if self._s_h1 is not None else None
+        s_ls = ctypes.addressof(arr) if self.P else None
+        nbytes = int(L.sun_workspace_bytes_ops(ctypes.addressof(self._s_h0), s_h1, s_ls, self.P))
+        if nbytes == 0:
+            _check(2, "sun_workspace_bytes_ops")
+        self.workspace = torch.empty(nbytes + guard_bytes, dtype=torch.uint8, device="cuda")
+        self._guard = guard_bytes
+        if guard_bytes:
+            self.workspace[nbytes:].fill_(0xA5)
         plan = ctypes.c_void_p()
-        st = L.sun_plan_create(
-            ctypes.addressof(plan), ctypes.addressof(self._s_h0),
-            ctypes.addressof(self._s_h1) if self._s_h1 is not None else None,
-            ctypes.addressof(arr) if self.P else None,
+        st = L.sun_plan_create_ex(
+            ctypes.addressof(plan), ctypes.addressof(self._s_h0), s_h1, s_ls,
             self.gammas.ctypes.data_as(ctypes.c_void_p) if self.P else None,
-            self.P, ctypes.c_void_p(self.workspace.data_ptr()), ctypes.c_size_t(nbytes),
+            self.P, flags, ctypes.c_void_p(self.workspace.data_ptr()), ctypes.c_size_t(nbytes),
             ctypes.c_void_p(_stream_handle(stream)))
         _check(st, "sun_plan_create")
         self._plan = plan
@@ -171,7 +197,8 @@ class Plan:
 
     # -- the three phases ----------------------------------------------------------------
     def count(self):
-        _check(lib().sun_count(self._plan, _stream_handle(self.stream)), "sun_count")
+        with _on(self.stream):
+            _check(lib().sun_count(self._plan, _stream_handle(self.stream)), "sun_count")
 
     def nnz(self):
         a, b = ctypes.c_int64(), ctypes.c_int64()
@@ -208,11 +235,13 @@ class Plan:
 
     def fill(self, nnz0: int, nnz1: int, out=None):
         """Allocate (unless `out` is given) and fill Q0, Q1 and K (sun_unfold, after count/nnz)."""
-        bufs = out if out is not None else self._alloc(nnz0, nnz1)
-        s0, s1 = self._structs(bufs)
-        _check(lib().sun_unfold(self._plan, ctypes.addressof(s0), ctypes.addressof(s1) if s1 is not None else None,
-                                bufs[2].data_ptr(), _stream_handle(self.stream)), "sun_unfold")
-        return self._trim(bufs, nnz0, nnz1)
+        with _on(self.stream):
+            bufs = out if out is not None else self._alloc(nnz0, nnz1)
+            s0, s1 = self._structs(bufs)
+            _check(lib().sun_unfold(self._plan, ctypes.addressof(s0),
+                                    ctypes.addressof(s1) if s1 is not None else None,
+                                    bufs[2].data_ptr(), _stream_handle(self.stream)), "sun_unfold")
+            return self._trim(bufs, nnz0, nnz1)
 
     def nnz_bound(self):
         b0 = int(lib().sun_nnz_bound(self._plan, 0))
@@ -224,6 +253,10 @@ class Plan:
         readback.  Output capacity: `out`, else the previous call's nnz (the first call of a
         plan uses the two-step path, which sizes the outputs exactly).
         Returns (Q0, Q1 or None, K) trimmed to the produced nnz."""
+        with _on(self.stream):
+            return self._run(out)
+
+    def _run(self, out):
         L = lib()
         if out is None:
             if self._caps is None:  # first call: exact sizes from the two-step path
@@ -257,6 +290,10 @@ class Plan:
             omega: float = 1.0, work=None) -> torch.Tensor:
         """Matrix-free RK4 of this plan's system in place on v (sun_rk4_plan; F1): Q0 / Q1 are
         regenerated in every stage instead of read.  Needs a counted plan (after run())."""
+        with _on(self.stream):
+            return self._rk4(v, h, nsteps, t0, eps0, eps1, omega, work)
+
+    def _rk4(self, v, h, nsteps, t0, eps0, eps1, omega, work):
         L = lib()
         nb = int(L.sun_rk4_plan_work_bytes(self._plan))
         w = work if work is not None else torch.empty((nb + 7) // 8, dtype=torch.float64, device=v.device)
@@ -269,13 +306,17 @@ class Plan:
 
     def apply(self, v: torch.Tensor, eps: float = 0.0, out: Optional[torch.Tensor] = None) -> torch.Tensor:
         """dv/dt = (Q0 + eps Q1) v + K without reading Q (sun_apply_plan); needs a counted plan."""
-        y = out if out is not None else torch.empty_like(v)
-        w = torch.empty(self.n, dtype=torch.float64, device=v.device)
+        with _on(self.stream):
+            y = out if out is not None else torch.empty_like(v)
+            w = torch.empty(self.n, dtype=torch.float64, device=v.device)
+            self._apply(v, eps, y, w)
+            return y
+
+    def _apply(self, v, eps, y, w):
         _check(lib().sun_apply_plan(self._plan, ctypes.c_double(eps), ctypes.c_void_p(v.data_ptr()),
                                     ctypes.c_void_p(y.data_ptr()), ctypes.c_void_p(w.data_ptr()),
                                     ctypes.c_size_t(w.numel() * 8), ctypes.c_void_p(_stream_handle(self.stream))),
                "sun_apply_plan")
-        return y
 
     def launches_per_run(self) -> int:
         """Kernels of this library launched by one run() (sun_run: count + fill)."""
@@ -304,12 +345,15 @@ class Plan:
 
 
 def unfold(H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), stream=None):
-    """expand(H, {L_p, gamma_p}) -> (Q0 CSR, Q1 CSR or None, K), all on the GPU."""
-    plan = Plan(H0, H1, Ls, gammas, stream)
-    try:
-        return plan.run()
-    finally:
-        plan.close()
+    """expand(H, {L_p, gamma_p}) -> (Q0 CSR, Q1 CSR or None, K), all on the GPU.  With `stream`,
+    the work (and every allocation) is on that stream, after the caller's current stream; the
+    outputs belong to `stream` (synchronise with it before using them elsewhere)."""
+    with _on(stream):
+        plan = Plan(H0, H1, Ls, gammas, stream)
+        try:
+            return plan.run()
+        finally:
+            plan.close()
 
 
 def unfold_split(H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), stream=None):
@@ -317,6 +361,11 @@ def unfold_split(H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), s
     and R, K from the dissipators (Eqs. 10-11), as separate CSR matrices.
     Two unfolds through the same C-ABI: (H0, no dissipators) and (0, {L_p, gamma_p}); a trace of
     L_p contributes its unitary part to R (reading R3).  Returns (QH, R, Q1 or None, K)."""
+    with _on(stream):
+        return _unfold_split(H0, H1, Ls, gammas, stream)
+
+
+def _unfold_split(H0, H1, Ls, gammas, stream):
     H0d = _to_device(H0)
     zero = DeviceZCSR(H0d.n, torch.zeros(H0d.n + 1, dtype=torch.int64, device=H0d.row_ptr.device),
                       torch.zeros(0, dtype=torch.int32, device=H0d.row_ptr.device),
@@ -331,21 +380,23 @@ def unfold_split(H0, H1=None, Ls: Sequence = (), gammas: Sequence[float] = (), s
 
 def expand_state(rho, stream=None) -> torch.Tensor:
     """v = Re Tr(F_s rho) (Eq. 5; sun_expand_state).  rho: DeviceZCSR or host CSR object."""
-    R = _to_device(rho)
-    s = _zcsr_struct(R)
-    v = torch.empty(R.n * R.n - 1, dtype=torch.float64, device=R.row_ptr.device)
-    _check(lib().sun_expand_state(ctypes.addressof(s), ctypes.c_void_p(v.data_ptr()),
-                                  ctypes.c_void_p(_stream_handle(stream))), "sun_expand_state")
-    return v
+    with _on(stream):
+        R = _to_device(rho)
+        s = _zcsr_struct(R)
+        v = torch.empty(R.n * R.n - 1, dtype=torch.float64, device=R.row_ptr.device)
+        _check(lib().sun_expand_state(ctypes.addressof(s), ctypes.c_void_p(v.data_ptr()),
+                                      ctypes.c_void_p(_stream_handle(stream))), "sun_expand_state")
+        return v
 
 
 def state_diag(v: torch.Tensor, n: int, stream=None) -> torch.Tensor:
     """Populations <a|rho|a> of the state with coherence vector v (sun_state_diag)."""
     assert v.is_cuda and v.dtype == torch.float64 and v.shape[0] == n * n - 1
-    d = torch.empty(n, dtype=torch.float64, device=v.device)
-    _check(lib().sun_state_diag(ctypes.c_void_p(v.data_ptr()), n, ctypes.c_void_p(d.data_ptr()),
-                                ctypes.c_void_p(_stream_handle(stream))), "sun_state_diag")
-    return d
+    with _on(stream):
+        d = torch.empty(n, dtype=torch.float64, device=v.device)
+        _check(lib().sun_state_diag(ctypes.c_void_p(v.data_ptr()), n, ctypes.c_void_p(d.data_ptr()),
+                                    ctypes.c_void_p(_stream_handle(stream))), "sun_state_diag")
+        return d
 
 
 def rk4(Q0: CSR, Q1: Optional[CSR], K: Optional[torch.Tensor], v: torch.Tensor, h: float, nsteps: int,
@@ -353,6 +404,11 @@ def rk4(Q0: CSR, Q1: Optional[CSR], K: Optional[torch.Tensor], v: torch.Tensor, 
         stream=None) -> torch.Tensor:
     """Fixed-step RK4 of dv/dt = (Q0 + eps(t) Q1) v + K in place on v (sun_rk4, Step 3.1)."""
     assert v.is_cuda and v.dtype == torch.float64 and v.shape[0] == Q0.m
+    with _on(stream):
+        return _rk4_csr(Q0, Q1, K, v, h, nsteps, t0, eps0, eps1, omega, work, stream)
+
+
+def _rk4_csr(Q0, Q1, K, v, h, nsteps, t0, eps0, eps1, omega, work, stream):
     nb = int(lib().sun_rk4_work_bytes(Q0.m))
     w = work if work is not None else torch.empty((nb + 7) // 8, dtype=torch.float64, device=v.device)
     assert w.numel() * w.element_size() >= nb
@@ -369,17 +425,23 @@ def rk4(Q0: CSR, Q1: Optional[CSR], K: Optional[torch.Tensor], v: torch.Tensor, 
 def state_reconstruct(v: torch.Tensor, n: int, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """rho = I/N + sum_j v_j F_j as a dense complex128 N x N tensor (Step 3.2; sun_state_reconstruct)."""
     assert v.is_cuda and v.dtype == torch.float64 and v.numel() == n * n - 1
-    rho = out if out is not None else torch.empty((n, n), dtype=torch.complex128, device=v.device)
-    assert rho.dtype == torch.complex128 and rho.is_contiguous() and rho.numel() == n * n
-    _check(lib().sun_state_reconstruct(ctypes.c_void_p(v.data_ptr()), n, ctypes.c_void_p(rho.data_ptr()),
-                                       ctypes.c_void_p(_stream_handle(stream))), "sun_state_reconstruct")
-    return rho
+    with _on(stream):
+        rho = out if out is not None else torch.empty((n, n), dtype=torch.complex128, device=v.device)
+        assert rho.dtype == torch.complex128 and rho.is_contiguous() and rho.numel() == n * n
+        _check(lib().sun_state_reconstruct(ctypes.c_void_p(v.data_ptr()), n, ctypes.c_void_p(rho.data_ptr()),
+                                           ctypes.c_void_p(_stream_handle(stream))), "sun_state_reconstruct")
+        return rho
 
 
 def structure_constants(n: int, which: str = "f", count_only: bool = False, stream=None):
     """Nonzero f_mns ('f') or d_mns ('d') of SU(N), every ordered triple, generated on the GPU from
     index arithmetic (sun_structure_constants; Step 2.2).  Returns (idx int32 (nnz, 3),
     val float64 (nnz,)) on the device, or the count only."""
+    with _on(stream):
+        return _structure_constants(n, which, count_only, stream)
+
+
+def _structure_constants(n, which, count_only, stream):
     w = {"f": 0, "d": 1}[which]
     dev = torch.device("cuda")
     nb = int(lib().sun_sc_work_bytes(n))
@@ -417,6 +479,11 @@ def unfold_dense(H: torch.Tensor, A: Optional[torch.Tensor] = None, Q: Optional[
     K (B, M) float64), squeezed like H.  `work` (any dtype, >= dense_work_bytes(N, 1)
     bytes) may be passed to reuse scratch; else `chunk` realisations' worth is allocated.
     """
+    with _on(stream):
+        return _unfold_dense(H, A, Q, K, work, chunk, stream)
+
+
+def _unfold_dense(H, A, Q, K, work, chunk, stream):
     squeeze = H.dim() == 2
     Hb = H.unsqueeze(0) if squeeze else H
     assert Hb.is_cuda and Hb.dtype == torch.complex128 and Hb.dim() == 3 and Hb.shape[1] == Hb.shape[2]
@@ -452,11 +519,16 @@ def apply(Q0: CSR, Q1: Optional[CSR], eps: float, K: Optional[torch.Tensor], v: 
           out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
     """dv/dt = Q0 v + eps Q1 v + K (Eq. 9) via sun_apply."""
     assert v.is_cuda and v.dtype == torch.float64 and v.shape[0] == Q0.m
-    y = out if out is not None else torch.empty_like(v)
+    with _on(stream):
+        y = out if out is not None else torch.empty_like(v)
+        _apply_csr(Q0, Q1, eps, K, v, y, stream)
+        return y
+
+
+def _apply_csr(Q0, Q1, eps, K, v, y, stream):
     s0 = _dcsr_struct(Q0)
     s1 = _dcsr_struct(Q1) if Q1 is not None else None
     _check(lib().sun_apply(ctypes.addressof(s0), ctypes.addressof(s1) if s1 is not None else None, ctypes.c_double(eps),
                            ctypes.c_void_p(K.data_ptr()) if K is not None else None,
                            ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(y.data_ptr()),
                            ctypes.c_void_p(_stream_handle(stream))), "sun_apply")
-    return y

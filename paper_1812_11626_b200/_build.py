@@ -8,8 +8,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsunfold.so")
-SOURCES = [os.path.join(CSRC, "sunfold.cu"), os.path.join(CSRC, "sunfold_dense.cu"), os.path.join(CSRC, "sunfold_sc.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "sunfold_kernels.cuh"), os.path.join(ROOT, "include", "sunfold.h")]
+SOURCES = [os.path.join(CSRC, "sunfold.cu"), os.path.join(CSRC, "sunfold_dense.cu"), os.path.join(CSRC, "sunfold_sc.cu"),
+           os.path.join(CSRC, "sunfold_general.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, "sunfold_kernels.cuh"), os.path.join(CSRC, "sunfold_general.cuh"),
+                  os.path.join(ROOT, "include", "sunfold.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

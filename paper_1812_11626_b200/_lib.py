@@ -36,7 +36,9 @@ class SunPlanInfo(ctypes.Structure):
 
 SIGNATURES = {
     "sun_workspace_bytes": (ctypes.c_size_t, [ctypes.c_int32, ctypes.c_int32]),
+    "sun_workspace_bytes_ops": (ctypes.c_size_t, [P, P, P, ctypes.c_int32]),
     "sun_plan_create": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int32, P, ctypes.c_size_t, P]),
+    "sun_plan_create_ex": (ctypes.c_int, [P, P, P, P, P, ctypes.c_int32, ctypes.c_int32, P, ctypes.c_size_t, P]),
     "sun_count": (ctypes.c_int, [P, P]),
     "sun_plan_nnz": (ctypes.c_int, [P, P, P]),
     "sun_unfold": (ctypes.c_int, [P, P, P, P, P]),

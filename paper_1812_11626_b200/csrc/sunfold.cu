@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "../../include/sunfold.h"
+#include "sunfold_general.cuh"
 #include "sunfold_kernels.cuh"
 
 using namespace sunk;
@@ -33,7 +34,7 @@ namespace {
 
 constexpr int MAXOPS = 66;       // H0, H1 and up to 64 dissipators
 constexpr int WLMAX = WMAX / 2;  // wK >= 2 wL
-constexpr int F_MALFORMED = 1, F_PATTERN = 8;
+constexpr int F_MALFORMED = 1, F_PATTERN = 8, F_TOOBIG = 16;  // F_TOOBIG: sunfold_general.cu
 constexpr int TP0 = 256;          // modes 0/2: pairs per fill tile == threads per fill CTA
 constexpr int SLOTS_PER_TILE = 8;
 #ifndef SUN_TILE_SYNC_MIN_N
@@ -193,6 +194,11 @@ struct sun_plan_s {
   };
   cudaStream_t cap_stream = nullptr;
   std::vector<GraphEntry> graphs;
+  // mode 3 (general-pattern operators, sunfold_general.cu)
+  int general = 0;
+  int small_cap = 0;  // SUN_PLAN_SMALLCAP (tests)
+  sung::GLayout glay;
+  sung::GProb gp[2];
   unsigned long long graph_clock = 0;
   bool use_graphs = true;
   HeaderPrefix* hpin = nullptr;  // pinned host copy of the header prefix (nnz readback)
@@ -2472,6 +2478,61 @@ cudaError_t launch_mode1(const Prob& pr, const FarPos* fp, int npos, int* cnt, i
   return launch_mode1_t<-1, 0, 0>(pr, fp, npos, cnt, ts, fo, st);
 }
 
+// mode 3: general-pattern operators (sunfold_general.cu).  Slot layout as modes 0/2: S slots and
+// J slots of 32 pairs, one slot per D row.
+void setup_general(sun_plan_s* pl) {
+  const Layout& L = pl->lay;
+  const sung::GLayout& g = pl->glay;
+  char* ws = pl->ws;
+  DevHeader* hdr = (DevHeader*)(ws + L.hdr);
+  for (int which = 0; which < 1 + pl->has_h1; ++which) {
+    Prob& pr = pl->pr[which];
+    memset(&pr, 0, sizeof(pr));
+    pr.n = pl->n;
+    pr.np = (long long)pl->n * (pl->n - 1) / 2;
+    pr.m = (long long)pl->n * pl->n - 1;
+    pr.P = which ? 0 : pl->P;
+    pr.mode = 3;
+    pr.tp = sung::GSLOT;
+    pr.npt = (pr.np + sung::GSLOT - 1) / sung::GSLOT;
+    pr.ndt = pl->n - 1;
+    pr.inv = reinterpret_cast<const double*>(ws + L.inv);
+    pr.tau_ptr = &hdr->tau[which];
+    pl->npos_far[which] = 0;
+    sung::GProb& G = pl->gp[which];
+    memset(&G, 0, sizeof(G));
+    G.n = pl->n;
+    G.P = pr.P;
+    G.np = pr.np;
+    G.m = pr.m;
+    const OpDesc& h = pl->ops.op[which];
+    G.H = {h.rp, h.ci, h.v};
+    for (int p = 0; p < G.P; ++p) {
+      const OpDesc& d = pl->ops.op[2 + p];
+      G.L[p] = {d.rp, d.ci, d.v};
+      G.C[p] = {reinterpret_cast<const int*>(ws + g.cp) + (long long)p * (pl->n + 1),
+                reinterpret_cast<const int2*>(ws + g.xr) + g.xr_off[p]};
+      G.g[p] = pl->gamma[p];
+    }
+    G.inv = pr.inv;
+    G.tau_ptr = pr.tau_ptr;
+    G.npt = pr.npt;
+    G.heavy = reinterpret_cast<int*>(ws + (which ? g.heavy1 : g.heavy0));
+    G.nheavy = reinterpret_cast<int*>(ws + g.nheavy) + which;
+    G.flags = &hdr->flags;
+    G.cap = pl->small_cap ? 16 : (1 << 30);
+  }
+}
+
+long long general_nnz(const sun_zcsr* const* L, int P, long long* nnzL) {
+  long long tot = 0;
+  for (int p = 0; p < P; ++p) {
+    nnzL[p] = L[p]->nnz;
+    tot += nnzL[p];
+  }
+  return tot;
+}
+
 }  // namespace
 
 extern "C" {
@@ -2487,9 +2548,10 @@ const char* sun_status_string(int status) {
     case SUN_ERR_RATE: return "invalid rate (gamma_p must be finite and >= 0)";
     case SUN_ERR_CAPACITY: return "output CSR capacity below the required nnz";
     case SUN_ERR_CUDA: return g_errbuf[0] ? g_errbuf : "CUDA error";
-    case SUN_ERR_BANDWIDTH:
-      return "operator half-bandwidth exceeds the banded kernels' limit (max(w_H, 2 w_L) <= 15, w_L <= 7)";
-    case SUN_ERR_STATE: return "call out of sequence";
+    case SUN_ERR_UNSUPPORTED:
+      return "unsupported for this plan (matrix-free propagation needs a banded plan; or a row with >= 2^32 "
+             "candidate terms)";
+    case SUN_ERR_STATE: return "call out of sequence (or operator values outside the plan's pattern: new plan)";
     default: return "unknown status";
   }
 }
@@ -2514,8 +2576,28 @@ size_t sun_workspace_bytes(int32_t n, int32_t P) {
   return make_layout(n, P).total;
 }
 
+size_t sun_workspace_bytes_ops(const sun_zcsr* H0, const sun_zcsr* H1, const sun_zcsr* const* L, int32_t P) {
+  (void)H1;
+  if (!H0 || P < 0 || P > MAXOPS - 2 || (P > 0 && !L)) return 0;
+  const int n = H0->n;
+  if (n < 2 || n > 46340) return 0;
+  long long nnzL[MAXOPS];
+  for (int p = 0; p < P; ++p) {
+    if (!L[p] || L[p]->nnz < 0) return 0;
+    nnzL[p] = L[p]->nnz;
+  }
+  const size_t base = make_layout(n, P).total;
+  return sung::g_layout(n, P, nnzL, base).total;
+}
+
 int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const sun_zcsr* const* L,
                     const double* gamma, int32_t P, void* workspace, size_t workspace_bytes, void* stream) {
+  return sun_plan_create_ex(out, H0, H1, L, gamma, P, 0, workspace, workspace_bytes, stream);
+}
+
+int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const sun_zcsr* const* L,
+                       const double* gamma, int32_t P, int32_t flags, void* workspace, size_t workspace_bytes,
+                       void* stream) {
   if (!out) return SUN_ERR_ARG;
   *out = nullptr;
   g_errbuf[0] = 0;
@@ -2580,10 +2662,9 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
   pl->wK = pl->wH0 > 2 * wL ? pl->wH0 : 2 * wL;
   if (pl->wK > n - 1) pl->wK = n - 1;  // M = L^+L has half-bandwidth <= n-1
   if (pl->wK < pl->wH0) pl->wK = pl->wH0;
-  if (pl->wK > WMAX || pl->wL > WLMAX || pl->wH1 > WMAX) {
-    delete pl;
-    return SUN_ERR_BANDWIDTH;
-  }
+  // operators beyond the banded kernels' widths (or SUN_PLAN_GENERAL): mode 3
+  pl->general = (flags & (SUN_PLAN_GENERAL | SUN_PLAN_SMALLCAP)) || pl->wK > WMAX || pl->wL > WLMAX || pl->wH1 > WMAX;
+  pl->small_cap = (flags & SUN_PLAN_SMALLCAP) != 0;
   double s0 = sqrt(h.nrm2[0]);
   for (int p = 0; p < P; ++p) s0 += gamma[p] * h.nrm2[2 + p];
   pl->tau0 = 1e-14 * s0;
@@ -2595,11 +2676,26 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
     pl->ops.wplan[2 + p] = pl->wL;
     pl->gam.g[p] = gamma[p];
   }
-  setup_prob(pl, 0);
-  if (pl->has_h1) setup_prob(pl, 1);
-  if (pl->npos_far[0] > FAR_MAXPOS || (pl->has_h1 && pl->npos_far[1] > FAR_MAXPOS)) {
-    delete pl;
-    return SUN_ERR_BANDWIDTH;
+  if (!pl->general) {
+    setup_prob(pl, 0);
+    if (pl->has_h1) setup_prob(pl, 1);
+    pl->general = pl->npos_far[0] > FAR_MAXPOS || (pl->has_h1 && pl->npos_far[1] > FAR_MAXPOS);
+  }
+  if (pl->general) {
+    long long nnzL[MAXOPS];
+    general_nnz(L, P, nnzL);
+    pl->glay = sung::g_layout(n, P, nnzL, lay.total);
+    if (workspace_bytes < pl->glay.total) {
+      delete pl;
+      return SUN_ERR_CAPACITY;  // general-pattern operators: size from sun_workspace_bytes_ops
+    }
+    for (int i = 0; i < MAXOPS; ++i) pl->ops.wplan[i] = -1;
+    setup_general(pl);
+    cudaError_t e1 = sung::g_prepare();
+    if (e1 != cudaSuccess) {
+      delete pl;
+      return cuda_fail(e1);
+    }
   }
   const int nmat = 1 + pl->has_h1;
   {
@@ -2609,6 +2705,10 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
   }
   pl->launches_count = 1 + (pl->combined ? 1 : nmat) + 1;  // expand, count, scan
   pl->launches_fill = pl->combined ? 1 : nmat;
+  if (pl->general) {
+    pl->launches_count = (P > 0 ? sung::G_LAUNCHES_EXPAND : 1) + sung::G_LAUNCHES_COUNT * nmat + 1;
+    pl->launches_fill = sung::G_LAUNCHES_FILL * nmat;
+  }
   for (int i = 0; i < 2; ++i) {
     cudaError_t e1 = cudaStreamCreateWithFlags(&pl->aux[i], cudaStreamNonBlocking);
     if (e1 == cudaSuccess) e1 = cudaEventCreateWithFlags(&pl->ev_join[i], cudaEventDisableTiming);
@@ -2626,7 +2726,9 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
     }
     const char* ng = getenv("SUNFOLD_NO_GRAPHS");
     pl->use_graphs = !(ng && ng[0] && ng[0] != '0');
-    if (pl->combined) {
+    if (pl->general) {
+      // no band kernels
+    } else if (pl->combined) {
       e1 = dispatch_attr0(pl->pr[0], pl->has_h1 ? &pl->pr[1] : nullptr, pl->has_h1 ? 0 : -1, pl->fill_grid[0]);
     } else {
       for (int which = 0; which < nmat && e1 == cudaSuccess; ++which) {
@@ -2655,7 +2757,50 @@ int sun_plan_create(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, const
   return SUN_OK;
 }
 
+static int enqueue_count_general(sun_plan pl, cudaStream_t st) {
+  const Layout& L = pl->lay;
+  char* ws = pl->ws;
+  DevHeader* hdr = (DevHeader*)(ws + L.hdr);
+  sung::GExpandIn in;
+  memset(&in, 0, sizeof(in));
+  in.n = pl->n;
+  in.nops = pl->ops.nops;
+  in.has_h1 = pl->has_h1;
+  for (int op = 0; op < in.nops; ++op) {
+    in.rp[op] = pl->ops.op[op].rp;
+    in.ci[op] = pl->ops.op[op].ci;
+    in.v[op] = pl->ops.op[op].v;
+    in.gamma[op] = pl->ops.gamma[op];
+  }
+  sung::GHeaderRef hr{&hdr->flags, hdr->tau, hdr->herm_dev, hdr->nrm2_h, hdr->nrm2, &hdr->done, hdr->ticket};
+  const long long nz32 = (long long)((L.st0 - L.ts0) / sizeof(int));
+  const long long nz64 = (long long)((L.toff0 - L.st0) / sizeof(unsigned long long));
+  CK(sung::g_expand(in, ws, pl->glay, (double*)(ws + L.inv), (int*)(ws + L.ts0), nz32,
+                    (unsigned long long*)(ws + L.st0), nz64, hr, st));
+  const int nmat = 1 + pl->has_h1;
+  ScanArgs sa;
+  memset(&sa, 0, sizeof(sa));
+  long long maxchunks = 1;
+  for (int which = 0; which < nmat; ++which) {
+    int* cnt = (int*)(ws + (which ? L.cnt1 : L.cnt0));
+    int* ts = (int*)(ws + (which ? L.ts1 : L.ts0));
+    CK(sung::g_count(pl->gp[which], cnt, ts, st));
+    sa.ts[which] = ts;
+    sa.toff[which] = (long long*)(ws + (which ? L.toff1 : L.toff0));
+    sa.status[which] = (unsigned long long*)(ws + (which ? L.st1 : L.st0));
+    sa.nnz[which] = &hdr->nnz[which];
+    sa.nslots[which] = nslots_of(pl->pr[which]);
+    const long long nc = (sa.nslots[which] + SCAN_TILE - 1) / SCAN_TILE;
+    if (nc > maxchunks) maxchunks = nc;
+  }
+  sa.ticket = hdr->ticket;
+  k_scan_chain<<<dim3((unsigned)maxchunks, nmat), SCAN_THREADS, 0, st>>>(sa);
+  CK(cudaGetLastError());
+  return SUN_OK;
+}
+
 static int enqueue_count(sun_plan pl, cudaStream_t st) {
+  if (pl->general) return enqueue_count_general(pl, st);
   const Layout& L = pl->lay;
   const int n = pl->n;
   char* ws = pl->ws;
@@ -2757,7 +2902,8 @@ int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
     memcpy(&dev, &h.herm_dev[k], sizeof(dev));
     if (dev > 1e-12 * sqrt(h.nrm2_h[k])) return SUN_ERR_NOT_HERMITIAN;
   }
-  if (h.flags & F_PATTERN) return SUN_ERR_BANDWIDTH;
+  if (h.flags & F_PATTERN) return SUN_ERR_STATE;        // values outside the plan's bands: new plan
+  if (h.flags & F_TOOBIG) return SUN_ERR_UNSUPPORTED;   // a row with >= 2^32 candidate terms
   pl->tau0 = h.tau[0];
   pl->tau1 = pl->has_h1 ? h.tau[1] : 0.0;
   pl->nnz[0] = h.nnz[0];
@@ -2785,6 +2931,14 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
                         pl->n >= SUN_TILE_SYNC_MIN_N ? 1 : 0};
   }
   if (nmat == 1) mf[1] = mf[0];
+  if (pl->general) {
+    for (int which = 0; which < nmat; ++which) {
+      const FillOut& fo = mf[which].fo;
+      const sung::GOut go{fo.row_ptr, fo.col, fo.val, fo.cap, fo.K, fo.toff, fo.nnz};
+      CK(sung::g_fill(pl->gp[which], mf[which].cnt, go, st));
+    }
+    return SUN_OK;
+  }
   if (pl->combined) {
     CK(dispatch_fill0(mf[0], mf[1], pl->has_h1 ? 0 : -1, pl->fill_grid[0], st));
     return SUN_OK;
@@ -2938,6 +3092,7 @@ int64_t sun_nnz_bound(sun_plan pl, int32_t which) {
   if (!pl || which < 0 || which > 1 || (which == 1 && !pl->has_h1)) return -1;
   const Prob& pr = pl->pr[which];
   const long long n = pl->n;
+  if (pl->general) return pr.m * pr.m;  // no structural bound short of dense
   const long long W = pr.W;
   const long long nw = 4 * W + 1 < n ? 4 * W + 1 : n;          // near-pair window
   const long long nwd = 2 * pr.wK + 1 < n ? 2 * pr.wK + 1 : n;  // D-row window
@@ -3094,7 +3249,7 @@ int sun_apply_plan(sun_plan pl, double eps, const double* v, double* dvdt, void*
   if (!pl || !v || !dvdt || !work || v == dvdt) return SUN_ERR_ARG;
   if (!pl->counted) return SUN_ERR_STATE;
   if (!(pl->pr[0].mode == 0 || (pl->pr[0].mode == 2 && pl->wK == 4 && pl->wL == 2)) || (pl->has_h1 && pl->wH1 != 0))
-    return SUN_ERR_BANDWIDTH;
+    return SUN_ERR_UNSUPPORTED;
   if (work_bytes < (size_t)pl->n * sizeof(double)) return SUN_ERR_CAPACITY;
   cudaStream_t st = (cudaStream_t)stream;
   MfStage S{};
@@ -3124,7 +3279,7 @@ int sun_rk4_plan(sun_plan pl, double eps0, double eps1, double omega, double t0,
   if (!pl || !v || !work || nsteps < 0) return SUN_ERR_ARG;
   if (!pl->counted) return SUN_ERR_STATE;
   if (!(pl->pr[0].mode == 0 || (pl->pr[0].mode == 2 && pl->wK == 4 && pl->wL == 2)) || (pl->has_h1 && pl->wH1 != 0))
-    return SUN_ERR_BANDWIDTH;
+    return SUN_ERR_UNSUPPORTED;
   if (work_bytes < sun_rk4_plan_work_bytes(pl)) return SUN_ERR_CAPACITY;
   if (nsteps == 0) return SUN_OK;
   cudaStream_t st = (cudaStream_t)stream;

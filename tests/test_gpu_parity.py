@@ -3,8 +3,10 @@
 Bar (BASELINE.json north_star; R6/R7):
   * CSR pattern (row_ptr, col) bit-exact;
   * values: max |q_gpu - q_oracle| <= 1e-12 max |q_oracle| per matrix (normwise, R7),
-    and per-entry relative error <= 1e-12 on >= 99% of the entries;
-  * K: max |K_gpu - K_oracle| <= 1e-12 max(1, max |K_oracle|);
+    and per-entry relative error <= 1e-12 wherever the entry has cond = sum|terms|/|q| <= 100;
+  * K: max |K_gpu - K_oracle| <= 1e-12 max |K_oracle| (exact zeros where K == 0);
+  * the oracle's pattern is robust (R6): gap kept > 1e3 tau > 1e6 dropped (flagged configs
+    excepted, DESIGN.md R6) and every entry near tau >= 50 roundoff bounds away from it;
   * bitwise determinism across runs; Q1 of a diagonal drive exactly skew-symmetric.
 """
 import numpy as np
@@ -29,18 +31,12 @@ def _np(t):
     return t.detach().cpu().numpy()
 
 
-def _compare_csr(gpu_csr, ref, name):
-    rp, col, val = _np(gpu_csr.row_ptr), _np(gpu_csr.col), _np(gpu_csr.val)
+def _compare_csr(got, ref, name):
+    """Bit-exact pattern; values per R7 (normwise 1e-12, and 1e-12 per entry where cond <= 100)."""
+    rp, col, val = _np(got.row_ptr), _np(got.col), _np(got.val)
     assert np.array_equal(rp, ref["row_ptr"]), f"{name}: row_ptr differs"
     assert np.array_equal(col, ref["col"]), f"{name}: col differs"
-    if val.size == 0:
-        return 0.0
-    scale = np.abs(ref["val"]).max()
-    err = np.abs(val - ref["val"])
-    assert err.max() <= 1e-12 * scale, f"{name}: max err {err.max()} vs scale {scale}"
-    rel = err / np.abs(ref["val"])
-    assert np.mean(rel <= 1e-12) >= 0.99, f"{name}: per-entry rel err too large: {np.quantile(rel, 0.99)}"
-    return float(err.max() / scale)
+    return sparse.assert_entries_close(val, ref, name)[0]
 
 
 def _run(sun, prob):
@@ -54,12 +50,13 @@ def _run(sun, prob):
 def _check_problem(sun, prob, determinism=True):
     ref = sparse.unfold_problem(prob)
     tau0 = sparse.tau_q0(prob)
-    sparse.assert_gap(ref["Q0"], tau0, factor=100)
+    sparse.assert_r6(ref["Q0"], tau0, prob.name)
+    if prob.H1 is not None:
+        sparse.assert_r6(ref["Q1"], sparse.tau_q1(prob), prob.name + ":Q1")
     plan, Q0, Q1, K, info = _run(sun, prob)
     assert abs(info["tau_q0"] - tau0) <= 1e-12 * tau0
     _compare_csr(Q0, ref["Q0"], prob.name + ":Q0")
-    kref = ref["Q0"]["K"]
-    assert np.abs(_np(K) - kref).max() <= 1e-12 * max(1.0, np.abs(kref).max())
+    sparse.assert_k_close(_np(K), ref["Q0"]["K"], prob.name + ":K", tau0)
     if prob.H1 is not None:
         _compare_csr(Q1, ref["Q1"], prob.name + ":Q1")
     else:
@@ -186,9 +183,8 @@ def test_error_codes():
     H = ZCSR.from_dense(A + A.conj().T)
     with pytest.raises(sun.SunError, match="rate"):
         sun.Plan(H, None, [ZCSR.from_dense(A)], [-0.1])
-    big = banded_random_problem(60, seed=1, wH=16, wL=0, P=0)
-    with pytest.raises(sun.SunError, match="bandwidth"):
-        sun.Plan(big.H0, None, [], [])
+    big = banded_random_problem(60, seed=1, wH=16, wL=0, P=0)  # beyond the band kernels: general mode
+    assert sun.Plan(big.H0, None, [], []).info()["mode_q0"] == 3
     p = dimer_problem(8, True)
     plan = sun.Plan(p.H0, p.H1, p.Ls, p.gammas)
     plan.count()
@@ -246,7 +242,7 @@ def test_plan_rerun_uses_current_operator_values():
         ref = sparse.unfold_problem(cur)
         _compare_csr(Q0, ref["Q0"], "rerun:Q0")
         _compare_csr(Q1, ref["Q1"], "rerun:Q1")
-        assert np.abs(_np(K) - ref["Q0"]["K"]).max() <= 1e-12 * max(1.0, np.abs(ref["Q0"]["K"]).max())
+        sparse.assert_k_close(_np(K), ref["Q0"]["K"], "rerun:K", sparse.tau_q0(cur))
     plan.close()
 
 
@@ -301,3 +297,35 @@ def test_side_stream_matches_default_stream():
     assert torch.equal(ya, yb) and torch.equal(va, vb) and torch.equal(vma, vmb)
     plan.close()
     ref_plan.close()
+
+
+def test_stream_argument_without_stream_context():
+    """A call given `stream=s` while the caller's current stream stays the default one: the work
+    is ordered after the current stream (inputs copied there just before) and the workspace,
+    outputs and scratch belong to `s`, so memory freed by unfold()'s plan is not reused by the
+    current stream while `s` still runs.  Results equal the default-stream ones."""
+    sun = _gpu()
+    prob = dimer_problem(60, True)
+    R = sun.unfold(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    v = torch.linspace(-1, 1, prob.m, dtype=torch.float64, device="cuda")
+    ya = sun.apply(R[0], R[1], 0.9, R[2], v)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    outs = []
+    for k in range(3):
+        H0 = sun.DeviceZCSR.from_host(prob.H0)  # made on the current stream
+        H1 = sun.DeviceZCSR.from_host(prob.H1)
+        Ls = [sun.DeviceZCSR.from_host(x) for x in prob.Ls]
+        S = sun.unfold(H0, H1, Ls, prob.gammas, stream=s)
+        junk = torch.full((1 << 22,), float(k), dtype=torch.float64, device="cuda")  # reuse pressure
+        y = sun.apply(S[0], S[1], 0.9, S[2], v, stream=s)
+        outs.append((S, y))
+        del junk
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas, stream=s)
+    P1 = plan.run()
+    s.synchronize()
+    for S, y in outs + [(P1, ya)]:
+        assert torch.equal(R[0].row_ptr, S[0].row_ptr) and torch.equal(R[0].col, S[0].col)
+        assert torch.equal(R[0].val, S[0].val) and torch.equal(R[1].val, S[1].val) and torch.equal(R[2], S[2])
+        assert torch.equal(ya, y)
+    plan.close()

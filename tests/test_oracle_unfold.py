@@ -161,7 +161,7 @@ def test_o2_equals_o1(prob):
     assert np.array_equal(rp, r["row_ptr"]) and np.array_equal(ci, r["col"])
     assert np.abs(val - r["val"]).max() <= 1e-13 * np.abs(val).max()
     assert np.abs(K - r["K"]).max() <= 1e-13 * max(1.0, np.abs(K).max())
-    sparse.assert_gap(r, tau, factor=100)
+    sparse.assert_r6(r, tau, prob.name)
     if prob.H1 is not None:
         Q1, _ = dense.unfold_dense(prob.H1.to_dense())
         t1 = sparse.tau_q1(prob)
@@ -201,7 +201,7 @@ def test_o2_apply_check_baseline_configs(idx):
     """Q(t) v + K = proj L(t)(rho) at BASELINE configs[2], configs[3] (global invariant)."""
     prob = config(idx)
     r = sparse.unfold_problem(prob)
-    sparse.assert_gap(r["Q0"], sparse.tau_q0(prob), factor=100)
+    sparse.assert_r6(r["Q0"], sparse.tau_q0(prob), prob.name)
     rng = np.random.default_rng(idx)
     rho = _random_density(prob.n, rng)
     v = basis.project(rho).real

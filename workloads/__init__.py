@@ -207,6 +207,75 @@ def banded_random_problem(n: int = 512, seed: int = 3, wH: int = 3, wL: int = 2,
                    [ZCSR.from_dense(L) for L in Ls], gammas)
 
 
+def ring_dimer_problem(n: int, drive: bool = True, gamma: float = 0.1, J: float = 1.0) -> Problem:
+    """General-pattern case (i): the dimer of R8/R9/R11 closed into a ring -- H gains the hopping
+    -J (E_{0,N-1} + E_{N-1,0}) and L the antisymmetric pair +E_{0,N-1} - E_{N-1,0} (entry (0, N-1):
+    half-bandwidth N-1, beyond every banded mode).  Deterministic."""
+    base = dimer_problem(n, drive, gamma=gamma)
+    H = base.H0.to_dense()
+    H[0, n - 1] += -J
+    H[n - 1, 0] += -J
+    L = base.Ls[0].to_dense()
+    L[0, n - 1] += 1.0
+    L[n - 1, 0] -= 1.0
+    return Problem(f"ring_N{n}" + ("_drive" if drive else ""), n, ZCSR.from_dense(H), base.H1, [ZCSR.from_dense(L)],
+                   [gamma])
+
+
+def random_sparse_problem(n: int = 300, seed: int = 21, per_row: int = 4, P: int = 2, drive: bool = False) -> Problem:
+    """General-pattern case (ii): H and every L_p with `per_row` nonzeros per row at uniformly
+    random columns (no band).  rng = default_rng(seed).  H: for each row a, `per_row // 2` columns
+    drawn without replacement (excluding a), entries g + i g (real then imaginary draw per row)
+    mirrored conjugate (so rows hold about per_row entries), then a real diagonal g(N).  Then for
+    p = 1..P: for each row, `per_row` distinct columns and entries g + i g.  gamma ~ U[0.05, 0.5].
+    drive: H1 = the same recipe's real symmetric pattern with entries g (one more draw)."""
+    rng = np.random.default_rng(seed)
+    H = np.zeros((n, n), dtype=np.complex128)
+    k = max(per_row // 2, 1)
+    for a in range(n):
+        cols = rng.choice(np.delete(np.arange(n), a), size=k, replace=False)
+        re, im = rng.standard_normal(k), rng.standard_normal(k)
+        H[a, cols] += re + 1j * im
+        H[cols, a] += re - 1j * im
+    H[np.arange(n), np.arange(n)] += rng.standard_normal(n)
+    Ls = []
+    for _ in range(P):
+        L = np.zeros((n, n), dtype=np.complex128)
+        for a in range(n):
+            cols = rng.choice(n, size=per_row, replace=False)
+            L[a, cols] = rng.standard_normal(per_row) + 1j * rng.standard_normal(per_row)
+        Ls.append(ZCSR.from_dense(L))
+    gammas = list(rng.uniform(0.05, 0.5, size=P))
+    H1 = None
+    if drive:
+        D = np.zeros((n, n), dtype=np.complex128)
+        for a in range(n):
+            cols = rng.choice(np.delete(np.arange(n), a), size=k, replace=False)
+            v = rng.standard_normal(k)
+            D[a, cols] += v
+            D[cols, a] += v
+        H1 = ZCSR.from_dense(D)
+    return Problem(f"sparse_N{n}_s{seed}_P{P}", n, ZCSR.from_dense(H), H1, Ls, gammas)
+
+
+def dense_dissipator_problem(n: int, seed: int = 0, P: int = 1, gamma: float = 0.5) -> Problem:
+    """General-pattern case (iii), the paper's dense-L case (Table II): the
+    dimer Hamiltonian with P dense random dissipators L_p = g + i g (traceful).  rng = default_rng(seed)."""
+    rng = np.random.default_rng(seed)
+    Ls = [ZCSR.from_dense(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) for _ in range(P)]
+    return Problem(f"denseL_N{n}_s{seed}_P{P}", n, dimer_hamiltonian(n), None, Ls, [gamma] * P)
+
+
+def column_jump_problem(n: int, seed: int = 0) -> Problem:
+    """A jump into a superposition, L = |psi><0| (one dense column), plus the dimer H: many
+    candidate terms share one output key (the single-key path of the general mode)."""
+    rng = np.random.default_rng(seed)
+    psi = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    L = np.zeros((n, n), dtype=np.complex128)
+    L[:, 0] = psi
+    return Problem(f"coljump_N{n}_s{seed}", n, dimer_hamiltonian(n), None, [ZCSR.from_dense(L)], [0.3])
+
+
 def config(idx: int) -> Problem:
     """The five BASELINE.json configurations (index = position in configs[])."""
     if idx == 0:
