@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-rk4", action="store_true")
     ap.add_argument("--no-f3", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs and general workloads")
     return ap.parse_args()
 
 
@@ -107,7 +108,7 @@ def barrier(world):
 # clocks sampling during the timed region
 # ---------------------------------------------------------------------------------------
 class ClockSampler:
-    """SM clock and throttle reasons sampled every ~5 ms by NVML (nvidia-smi's library) while the
+    """SM clock and throttle reasons sampled every ~0.5 ms by NVML (nvidia-smi's library) while the
     timed region runs; falls back to nvidia-smi queries if NVML is unavailable."""
 
     # NVML clocks-event-reason bits (nvmlClocksEventReason*)
@@ -133,7 +134,7 @@ class ClockSampler:
                 rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
                 self.rows.append((time.perf_counter(), float(sm), float(smax), int(rs)))
                 self._ready.set()
-                self._stop.wait(0.005)
+                self._stop.wait(0.0005)
         finally:
             pynvml.nvmlShutdown()
 
@@ -176,7 +177,7 @@ class ClockSampler:
         if not inside and self.rows:  # region shorter than the sampling period: nearest sample before it
             before = [r for r in self.rows if self.t0 is None or r[0] < self.t0]
             inside = before[-1:] if before else self.rows[:1]
-            window = "last sample before the timed region (region shorter than the 5 ms period)"
+            window = "last sample before the timed region (region shorter than the sampling period)"
         if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
         reasons = set()
@@ -191,7 +192,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------
 # CPU baseline: the oracle (O2) as it stands
 # ---------------------------------------------------------------------------------------
-def cpu_oracle_run(prob, reps: int = 1):
+def cpu_oracle_run(prob, reps: int = 1, keep: list = None):
     from oracle import sparse
 
     times = []
@@ -201,7 +202,42 @@ def cpu_oracle_run(prob, reps: int = 1):
         r = sparse.unfold_problem(prob)
         times.append(time.perf_counter() - t0)
         nnz = len(r["Q0"]["col"]) + (len(r["Q1"]["col"]) if "Q1" in r else 0)
+    if keep is not None:
+        keep.append(r)
     return nnz, times, sparse.max_threads()
+
+
+def bench_config(idx: int, prob) -> dict:
+    """The `config` dict of the JSON line: identical in both arms (the workload's identity only)."""
+    from workloads import CONFIG_NAMES
+
+    return {"workload": CONFIG_NAMES[idx] if idx is not None else prob.name, "N": prob.n, "M": prob.m}
+
+
+def oracle_errors(out, ref, tau0) -> dict:
+    """GPU outputs (Q0, Q1, K) against an oracle result: bit-exact pattern, normwise value errors
+    (max |q_gpu - q_oracle| / max |q_oracle|, R7), K the same."""
+    import numpy as np
+
+    Q0, Q1, K = out
+    res = {}
+    exact = True
+    for nm, Q in (("Q0", Q0), ("Q1", Q1)):
+        if Q is None or nm not in ref:
+            continue
+        r = ref[nm]
+        rp, col, val = Q.row_ptr.cpu().numpy(), Q.col.cpu().numpy(), Q.val.cpu().numpy()
+        same = bool(np.array_equal(rp, r["row_ptr"]) and np.array_equal(col, r["col"]))
+        exact &= same
+        sc = float(np.abs(r["val"]).max()) if r["val"].size else 0.0
+        res[nm] = float(np.abs(val - r["val"]).max() / sc) if same and sc > 0 else (0.0 if same else None)
+    kr = ref["Q0"]["K"]
+    kg = K.cpu().numpy()
+    ks = float(np.abs(kr).max())
+    res["K"] = float(np.abs(kg - kr).max() / ks) if ks > tau0 else float(np.abs(kg).max())
+    res["K_normalisation"] = "max|K_oracle|" if ks > tau0 else "absolute (K numerically zero, <= tau)"
+    return {"pattern_exact": exact, "max_err_normwise": res,
+            "tolerance": "pattern bit-exact; values <= 1e-12 normwise (DESIGN.md R7)"}
 
 
 def cpu_model() -> str:
@@ -214,8 +250,8 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def cpu_baseline(prob, reps: int = 2):
-    nnz, times, cores = cpu_oracle_run(prob, reps)
+def cpu_baseline(prob, reps: int = 2, keep: list = None):
+    nnz, times, cores = cpu_oracle_run(prob, reps, keep)
     t = statistics.mean(times)
     # one single-threaded unfold as well
     from oracle import sparse
@@ -250,7 +286,7 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_NAMES[args.config], "N": prob.n, "M": prob.m, "nnz_total": nnz},
+        "config": bench_config(args.config, prob), "nnz_per_step": nnz,
         "cpu_baseline": {"value": v, "unit": UNIT, "kind": "oracle", "cores": cores,
                          "sample": f"{steps} full unfolds of {prob.name} by oracle O2 (sparse_o2.c, OpenMP), "
                                    f"{args.steps} requested, capped at ~90 s of CPU work"},
@@ -263,6 +299,75 @@ def run_reference(args):
 # ---------------------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------------------
+def measure_problem(sun, prob, steps: int, flush, peak: float, label: str, oracle: bool = True, **plan_kw) -> dict:
+    """One workload beside the headline: the sun_run step (L2 flushed between steps, device
+    time), the fill pass alone (graphs off, GPU kept busy while the host enqueues), nnz/s, the
+    fill's HBM fraction on algorithmic bytes (12 B/nnz + 8 B/row per matrix + 8 B/row for K),
+    and the GPU outputs against the oracle O2 (timed on the host cores: the CPU baseline)."""
+    import torch
+
+    stream = torch.cuda.current_stream()
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    H0 = sun.DeviceZCSR.from_host(prob.H0)
+    H1 = sun.DeviceZCSR.from_host(prob.H1) if prob.H1 is not None else None
+    Ls = [sun.DeviceZCSR.from_host(x) for x in prob.Ls]
+    plan = sun.Plan(H0, H1, Ls, prob.gammas, **plan_kw)
+    out = None
+    for _ in range(3):
+        out = plan.run()
+    torch.cuda.synchronize()
+    tm = []
+    for _ in range(steps):
+        flush.fill_(1.0)
+        a, b = ev(), ev()
+        a.record(stream)
+        out = plan.run()
+        b.record(stream)
+        tm.append((a, b))
+    torch.cuda.synchronize()
+    step_ms = statistics.median([a.elapsed_time(b) for a, b in tm])
+    Q0, Q1, K = out
+    nnz = Q0.nnz + (Q1.nnz if Q1 is not None else 0)
+    m = prob.m
+    fill_bytes = 8 * (m + 1) + 12 * Q0.nnz + 8 * m + ((8 * (m + 1) + 12 * Q1.nnz) if Q1 is not None else 0)
+    plan.set_graphs(False)
+    plan.count()
+    n0, n1 = plan.nnz()
+    bufs = plan.fill(n0, n1)
+    iso = []
+    for _ in range(max(5, min(steps, 30))):
+        flush.fill_(1.0)
+        torch.cuda._sleep(200_000)
+        a, b = ev(), ev()
+        a.record(stream)
+        plan.fill(n0, n1, out=bufs)
+        b.record(stream)
+        iso.append((a, b))
+    torch.cuda.synchronize()
+    fill_ms = statistics.median([a.elapsed_time(b) for a, b in iso])
+    info = plan.info()
+    res = {"workload": label, "N": prob.n, "M": m, "P": len(prob.Ls), "mode_q0": info["mode_q0"],
+           "nnz_q0": int(Q0.nnz), "nnz_q1": int(Q1.nnz) if Q1 is not None else 0, "steps": steps,
+           "ms_per_step": step_ms, "nnz_per_s": nnz / (step_ms * 1e-3),
+           "fill": {"launch_ms": fill_ms, "algorithmic_bytes": fill_bytes,
+                    "achieved_gbs": fill_bytes / (fill_ms * 1e-3) / 1e9,
+                    "frac": fill_bytes / (fill_ms * 1e-3) / 1e9 / peak,
+                    "note": "outputs below the 126 MB L2 stay L2-resident: fraction not meaningful"
+                    if fill_bytes < 126e6 else "HBM-bound size"}}
+    if oracle:
+        from oracle import sparse
+
+        keep = []
+        onnz, otimes, cores = cpu_oracle_run(prob, 1, keep)
+        res["oracle_check"] = oracle_errors((Q0, Q1, K), keep[0], sparse.tau_q0(prob))
+        res["cpu_baseline"] = {"seconds_per_unfold": otimes[0], "value": onnz / otimes[0], "unit": UNIT,
+                               "cores": cores, "kind": "oracle", "speedup_gpu_vs_oracle": otimes[0] / (step_ms * 1e-3)}
+    plan.close()
+    del bufs, out, Q0, Q1, K
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -487,7 +592,24 @@ def main():
         torch.cuda.empty_cache()
     info = plan.info()
     launches_per_step = plan.launches_per_run()
+    Q0h, Q1h, Kh = keep[-1]
     plan.close()
+    # every other BASELINE config (parity-test cases) and the general-pattern
+    # workloads (operators beyond the band kernels, mode 3), measured the same way
+    extra = {}
+    general = {}
+    if rank == 0 and not args.no_configs:
+        for idx in range(5):
+            if idx == args.config:
+                continue
+            p_i = config(idx)
+            extra[CONFIG_NAMES[idx]] = measure_problem(sun, p_i, 50, flush, peak, CONFIG_NAMES[idx])
+        from workloads import dense_dissipator_problem, random_sparse_problem, ring_dimer_problem
+
+        for p_g, lab in ((random_sparse_problem(300, seed=21, P=2), "(ii) random sparse H, L_p: 4 nnz/row, N=300, P=2"),
+                         (ring_dimer_problem(256, drive=True), "(i) ring dimer N=256 (entry (0, N-1)), driven"),
+                         (dense_dissipator_problem(48, seed=0), "(iii) dense L_p, dimer H, N=48")):
+            general[p_g.name] = measure_problem(sun, p_g, 30, flush, peak, lab)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "fill_traffic.json")
     if os.path.exists(tpath):
@@ -542,19 +664,26 @@ def main():
                "note": "sun.unfold() on host (pinned) CSR inputs; full Q0/Q1/K copied back to pinned host memory"}
 
     cpu = None
+    check = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(prob)
+        keep_ref = []
+        cpu = cpu_baseline(prob, keep=keep_ref)
+        from oracle import sparse as _sp
+
+        check = oracle_errors((Q0h, Q1h, Kh), keep_ref[0], _sp.tau_q0(prob))
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": CONFIG_NAMES[args.config], "N": prob.n, "M": prob.m, "P": len(prob.Ls),
-                   "nnz_q0": int(Q0.nnz), "nnz_q1": int(Q1.nnz) if Q1 is not None else 0,
-                   "l2": "flushed between timed steps (512 MiB write, outside step events)",
-                   "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                   "step": "sun_run (expand+count+scan+fill+K+Q1, no host round trip) + sun_plan_nnz readback "
-                           "+ output allocation, on a plan built once; unfold_cold_ms adds sun_plan_create"},
+        "config": bench_config(args.config, prob),
+        "config_detail": {"P": len(prob.Ls), "nnz_q0": int(Q0.nnz), "nnz_q1": int(Q1.nnz) if Q1 is not None else 0,
+                          "l2": "flushed between timed steps (512 MiB write, outside step events)",
+                          "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                          "step": "sun_run (expand+count+scan+fill+K+Q1, no host round trip) + sun_plan_nnz "
+                                  "readback + output allocation, on a plan built once; unfold_cold_ms adds "
+                                  "sun_plan_create"},
+        "oracle_check": check,
         "unfold_wall_ms": ms,
         "unfold_cold_ms": cold_ms,
         "phases_ms": {"count device (expand+count+scan)": count_dev_ms, "fill isolated": iso_ms,
@@ -566,6 +695,8 @@ def main():
         "cpu_baseline": cpu,
         "rk4": rk4,
         "f3_dense": f3,
+        "configs": extra,
+        "general_pattern": general,
         "plan": {k: info[k] for k in ("w_h0", "w_l", "w_k", "mode_q0", "npos_far_q0", "tiles_q0")},
         "wall_s_timed_region": t_wall,
     }

@@ -22,3 +22,4 @@ def test_reference_arm_json_line():
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("c1_")
+    assert set(d["config"]) == {"workload", "N", "M"}  # the GPU arm prints the same dict (bench_config)
