@@ -2519,6 +2519,7 @@ void setup_general(sun_plan_s* pl) {
     G.npt = pr.npt;
     G.heavy = reinterpret_cast<int*>(ws + (which ? g.heavy1 : g.heavy0));
     G.nheavy = reinterpret_cast<int*>(ws + g.nheavy) + which;
+    G.dtot = reinterpret_cast<int*>(ws + (which ? g.dtot1 : g.dtot0));
     G.flags = &hdr->flags;
     G.cap = pl->small_cap ? 16 : (1 << 30);
   }
@@ -2781,10 +2782,11 @@ static int enqueue_count_general(sun_plan pl, cudaStream_t st) {
   ScanArgs sa;
   memset(&sa, 0, sizeof(sa));
   long long maxchunks = 1;
+  CK(fork_aux(pl, st, nmat));  // D rows of matrix `which` on aux[which], concurrent with the pairs
   for (int which = 0; which < nmat; ++which) {
     int* cnt = (int*)(ws + (which ? L.cnt1 : L.cnt0));
     int* ts = (int*)(ws + (which ? L.ts1 : L.ts0));
-    CK(sung::g_count(pl->gp[which], cnt, ts, st));
+    CK(sung::g_count(pl->gp[which], cnt, ts, st, pl->aux[which]));
     sa.ts[which] = ts;
     sa.toff[which] = (long long*)(ws + (which ? L.toff1 : L.toff0));
     sa.status[which] = (unsigned long long*)(ws + (which ? L.st1 : L.st0));
@@ -2793,6 +2795,7 @@ static int enqueue_count_general(sun_plan pl, cudaStream_t st) {
     const long long nc = (sa.nslots[which] + SCAN_TILE - 1) / SCAN_TILE;
     if (nc > maxchunks) maxchunks = nc;
   }
+  CK(join_aux(pl, st, nmat));
   sa.ticket = hdr->ticket;
   k_scan_chain<<<dim3((unsigned)maxchunks, nmat), SCAN_THREADS, 0, st>>>(sa);
   CK(cudaGetLastError());
@@ -2932,11 +2935,13 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
   }
   if (nmat == 1) mf[1] = mf[0];
   if (pl->general) {
+    CK(fork_aux(pl, st, nmat));  // heavy rows of matrix `which` on aux[which]
     for (int which = 0; which < nmat; ++which) {
       const FillOut& fo = mf[which].fo;
       const sung::GOut go{fo.row_ptr, fo.col, fo.val, fo.cap, fo.K, fo.toff, fo.nnz};
-      CK(sung::g_fill(pl->gp[which], mf[which].cnt, go, st));
+      CK(sung::g_fill(pl->gp[which], mf[which].cnt, go, st, pl->aux[which]));
     }
+    CK(join_aux(pl, st, nmat));
     return SUN_OK;
   }
   if (pl->combined) {

@@ -19,8 +19,14 @@ namespace {
 constexpr unsigned FULLM = 0xffffffffu;
 constexpr int GF_MALFORMED = 1, GF_TOOBIG = 16;  // header flags (sunfold.cu F_*)
 constexpr int GE_THREADS = 256;                  // expand: rows per CTA
-constexpr int GW_CAP = 128, GW_WARPS = 8;        // light engine: candidates per warp, warps per CTA
-constexpr int GH_CAP = 1024, GH_NT = 128;        // heavy engine: candidates per CTA, threads
+#ifndef SUN_GW_CAP
+#define SUN_GW_CAP 128
+#endif
+#ifndef SUN_GW_WARPS
+#define SUN_GW_WARPS 8
+#endif
+constexpr int GW_CAP = SUN_GW_CAP, GW_WARPS = SUN_GW_WARPS;  // light engine: candidates per warp, warps per CTA
+constexpr int GH_CAP = 2048, GH_NT = 256;        // heavy engine: candidates per CTA, threads
 constexpr int GH_NB = 256, GH_LEV = 4;           // heavy engine: histogram bins, levels
 constexpr double SQ2 = 1.4142135623730951;
 
@@ -340,10 +346,12 @@ __device__ __forceinline__ double fD(const Item& it, int c) {
 }
 
 // Source `src` of item `it`: number of candidates (COUNT_ONLY) or emit them as
-// vis(key, seq, value, transposed) with seq = seq0 + local index.
+// vis(key, seq, value, transposed) with seq = seq0 + local index.  part / nparts: emit only the
+// part-th of nparts interleaved slices (frame mode splits one source over a group; every source
+// emits pairwise distinct keys); seq is meaningful only for nparts == 1.
 template <bool COUNT_ONLY, bool NEEDVAL, class V>
 __device__ __forceinline__ unsigned long long source(const GProb& G, const Item& it, long long src, unsigned seq0,
-                                                     V& vis) {
+                                                     V& vis, int part = 0, int nparts = 1) {
   const int n = G.n;
   if (it.kind == 1) {  // ---- row D^lam
     const int lam = it.lam;
@@ -353,7 +361,7 @@ __device__ __forceinline__ unsigned long long source(const GProb& G, const Item&
       const long long k0 = lbound(G.H.ci, r0, r1, lam > c + 1 ? lam : c + 1);
       if (COUNT_ONLY) return (unsigned long long)(r1 - k0);
       const double fc = fD(it, c);
-      for (long long k = k0; k < r1; ++k) {
+      for (long long k = k0 + part; k < r1; k += nparts) {
         const int d = __ldg(G.H.ci + k);
         double2 w = make_double2(0.0, 0.0);
         if (NEEDVAL) {
@@ -402,13 +410,13 @@ __device__ __forceinline__ unsigned long long source(const GProb& G, const Item&
       vis(c == d ? (unsigned)(G.np + c) : (unsigned)sunk::pidx32(n, c, d), s++, w, 0);
     };
     if (cnt_case == 0) {
-      for (long long jj = j0; jj < r; ++jj)
+      for (long long jj = j0 + part; jj < r; jj += nparts)
         for (long long ii = 0; ii <= jj; ++ii) pairv(ii, jj);
     } else if (cnt_case == 1) {
-      for (long long ii = 0; ii < i1; ++ii)
+      for (long long ii = part; ii < i1; ii += nparts)
         for (long long jj = ii; jj < r; ++jj) pairv(ii, jj);
     } else {
-      for (long long ii = 0; ii < r; ++ii)
+      for (long long ii = part; ii < r; ii += nparts)
         for (long long jj = ii; jj < r; ++jj)
           if (!(jj == ii && __ldg(L.ci + r0 + ii) == lam)) pairv(ii, jj);
     }
@@ -420,7 +428,7 @@ __device__ __forceinline__ unsigned long long source(const GProb& G, const Item&
     const int row = src == 0 ? a : b;
     const long long r0 = G.H.rp[row], r1 = G.H.rp[row + 1];
     if (COUNT_ONLY) return (unsigned long long)(r1 - r0);
-    for (long long k = r0; k < r1; ++k) {
+    for (long long k = r0 + part; k < r1; k += nparts) {
       const int c = __ldg(G.H.ci + k);
       double2 U = make_double2(0.0, 0.0);
       if (NEEDVAL) {
@@ -448,7 +456,7 @@ __device__ __forceinline__ unsigned long long source(const GProb& G, const Item&
       const long long r0 = L.rp[x], r1 = L.rp[x + 1];
       if (COUNT_ONLY) return (unsigned long long)(r1 - r0);
       const double2 lx = NEEDVAL ? __ldg(L.v + e.y) : make_double2(0.0, 0.0);  // L_xa (T3) | L_xb (T4)
-      for (long long k = r0; k < r1; ++k) {
+      for (long long k = r0 + part; k < r1; k += nparts) {
         const int c = __ldg(L.ci + k);
         double2 U = make_double2(0.0, 0.0);
         if (NEEDVAL) {
@@ -468,7 +476,7 @@ __device__ __forceinline__ unsigned long long source(const GProb& G, const Item&
       if (COUNT_ONLY) return (unsigned long long)(rb1 - rb0);
       const int c = __ldg(L.ci + ra0 + i);
       const double2 lac = NEEDVAL ? __ldg(L.v + ra0 + i) : make_double2(0.0, 0.0);
-      for (long long k = rb0; k < rb1; ++k) {
+      for (long long k = rb0 + part; k < rb1; k += nparts) {
         const int d = __ldg(L.ci + k);
         double2 U = make_double2(0.0, 0.0);
         if (NEEDVAL) {
@@ -534,8 +542,8 @@ __device__ __forceinline__ unsigned long long gscan(unsigned long long v, unsign
 // Enumerate every candidate of the item: sources in rounds of NT (thread r of the group takes
 // source s0 + r), sequence bases from a group scan of the sources' sizes.
 template <int NT, bool NEEDVAL, class V>
-__device__ __forceinline__ void enumerate(const GProb& G, const Item& it, long long nsrc, unsigned long long* sc,
-                                          V& vis) {
+__device__ __forceinline__ unsigned enumerate(const GProb& G, const Item& it, long long nsrc, unsigned long long* sc,
+                                              V& vis) {
   unsigned carry = 0;
   for (long long s0 = 0; s0 < nsrc; s0 += NT) {
     const long long src = s0 + grank<NT>();
@@ -545,6 +553,7 @@ __device__ __forceinline__ void enumerate(const GProb& G, const Item& it, long l
     if (src < nsrc && c > 0) source<false, NEEDVAL>(G, it, src, carry + (unsigned)ex, vis);
     carry += (unsigned)tot;
   }
+  return carry;  // number of candidates
 }
 
 template <int NT>
@@ -648,7 +657,10 @@ __device__ void assemble_runs(const GProb& G, const Item& it, GBuf<CAP>& B, RowS
     double2 A = make_double2(0.0, 0.0), Bs = make_double2(0.0, 0.0);
     if (head) {
       for (int j = i; j < cnt && (unsigned)(B.key[j] >> 32) == k32; ++j) {
-        const unsigned short s = B.slot[j];
+        // light warps (register sort): value index and transposition in the key's low word;
+        // CTA groups: the slot array moved with the keys
+        const unsigned lw = (unsigned)B.key[j];
+        const unsigned short s = NT == 32 ? (unsigned short)((lw & 0x7fffu) | ((lw >> 16) & 0x8000u)) : B.slot[j];
         const double2 U = B.val[s & 0x7fff];
         if (s & 0x8000) {  // transposed candidate U_dc: conj for G_S, -conj for G_J
           A.x += U.x; A.y -= U.y;
@@ -700,19 +712,19 @@ __device__ void assemble_runs(const GProb& G, const Item& it, GBuf<CAP>& B, RowS
 // D chain over the chunk's diagonal list (warp 0 of the group): for each diagonal key c (in
 // order), the segment l in [prev, c) with coefficient P inv[l] (kept prefix by a binary
 // search), then l = c with (P - c g_c) inv[c]; P += g_c.  Both rows of a pair item.
-template <int NT, int CAP>
-__device__ void d_chain(const GProb& G, const Item& it, GBuf<CAP>& B, RowState& rs, int pass, double tau,
-                        const GOut& O) {
+template <int NT, class DG>
+__device__ void d_chain_f(const GProb& G, const Item& it, int nd, DG diag, RowState& rs, int pass, double tau,
+                          const GOut& O) {
   if (NT != 32 && threadIdx.x >= 32) return;  // CTA groups: warp 0 only
   const int lane = threadIdx.x & 31;
   const int nrow = it.kind == 0 ? 2 : 1;
   const int dbase = (int)(2 * G.np - 1);
-  const int nd = B.nd;
   for (int base = 0; base < nd; base += 32) {
     const int k = base + lane;
     const bool valid = k < nd;
-    const int c = valid ? B.dc[k] : 0x7fffffff;
-    const double2 g = valid ? B.dg[k] : make_double2(0.0, 0.0);
+    int c = 0x7fffffff;
+    double2 g = make_double2(0.0, 0.0);
+    if (valid) diag(k, c, g);
     const int nv = nd - base < 32 ? nd - base : 32;
     const int cprev = __shfl_up_sync(FULLM, c, 1);
     int s0 = lane == 0 ? rs.prev : cprev + 1;
@@ -762,6 +774,16 @@ __device__ void d_chain(const GProb& G, const Item& it, GBuf<CAP>& B, RowState& 
   }
 }
 
+template <int NT, int CAP>
+__device__ __forceinline__ void d_chain(const GProb& G, const Item& it, GBuf<CAP>& B, RowState& rs, int pass,
+                                        double tau, const GOut& O) {
+  auto dg = [&](int k, int& c, double2& g) {
+    c = B.dc[k];
+    g = B.dg[k];
+  };
+  d_chain_f<NT>(G, it, B.nd, dg, rs, pass, tau, O);
+}
+
 // tail of the D chain after the last diagonal key: l in [prev, n) with P inv[l]
 __device__ __forceinline__ void d_tail(const GProb& G, const Item& it, RowState& rs, int pass, double tau,
                                        const GOut& O) {
@@ -785,6 +807,16 @@ __device__ __forceinline__ void gather(const GProb& G, const Item& it, long long
                                        unsigned hi) {
   if (grank<NT>() == 0) B.cnt = 0;
   gsync<NT>();
+  if (NT == 32) {  // light warps: one chunk holding every candidate; index = sequence number
+    auto vis = [&](unsigned key, unsigned seq, double2 U, int tr) {
+      B.key[seq] = ((unsigned long long)key << 32) | ((unsigned)tr << 31) | seq;
+      B.val[seq] = U;
+    };
+    const unsigned c = enumerate<NT, true>(G, it, nsrc, B.sc, vis);
+    if ((threadIdx.x & 31) == 0) B.cnt = (int)c;
+    __syncwarp();
+    return;
+  }
   auto vis = [&](unsigned key, unsigned seq, double2 U, int tr) {
     if (key >= lo && key < hi) {
       const int i = atomicAdd(&B.cnt, 1);
@@ -797,12 +829,72 @@ __device__ __forceinline__ void gather(const GProb& G, const Item& it, long long
   gsync<NT>();
 }
 
+// bitonic sort of cnt <= 32 R 64-bit keys in registers (R per lane, element e = lane + 32 q)
+template <int R>
+__device__ __forceinline__ void warp_sort_regs(unsigned long long* key, int cnt) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long v[R];
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int e = lane + 32 * q;
+    v[q] = e < cnt ? key[e] : ~0ull;
+  }
+  int n2 = 2;
+  while (n2 < cnt) n2 <<= 1;
+  for (int k = 2; k <= n2; k <<= 1)
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= 32) {  // partner in another register of this lane
+        const int jq = j >> 5;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int q2 = q ^ jq;
+          if (q2 > q && q2 < R) {
+            const int e = lane + 32 * q;
+            const bool asc = (e & k) == 0;
+            const unsigned long long a = v[q], b = v[q2];
+            if ((a > b) == asc) {
+              v[q] = b;
+              v[q2] = a;
+            }
+          }
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int e = lane + 32 * q;
+          const unsigned long long o = __shfl_xor_sync(FULLM, v[q], j);
+          const bool lower = (lane & j) == 0, asc = (e & k) == 0;
+          v[q] = (lower == asc) ? (o < v[q] ? o : v[q]) : (o > v[q] ? o : v[q]);
+        }
+      }
+    }
+#pragma unroll
+  for (int q = 0; q < R; ++q) {
+    const int e = lane + 32 * q;
+    if (e < cnt) key[e] = v[q];
+  }
+  __syncwarp();
+}
+
+template <int NT, int CAP>
+__device__ __forceinline__ void sort_gathered(GBuf<CAP>& B) {
+  if constexpr (NT == 32) {
+    static_assert(CAP <= 128, "register sort holds <= 4 keys per lane");
+    const int c = B.cnt;
+    if (c <= 32) warp_sort_regs<1>(B.key, c);
+    else if (c <= 64) warp_sort_regs<2>(B.key, c);
+    else warp_sort_regs<CAP / 32>(B.key, c);
+  } else {
+    bitonic<NT>(B.key, B.slot, B.cnt);
+  }
+}
+
 // one chunk: gather, sort, runs (+ D chain)
 template <int NT, int CAP>
 __device__ __forceinline__ void chunk(const GProb& G, const Item& it, long long nsrc, GBuf<CAP>& B, RowState& rs,
                                       int pass, double tau, const GOut& O, unsigned lo, unsigned hi) {
   gather<NT, CAP>(G, it, nsrc, B, lo, hi);
-  bitonic<NT>(B.key, B.slot, B.cnt);
+  sort_gathered<NT, CAP>(B);
   assemble_runs<NT, CAP>(G, it, B, rs, pass, tau, O);
   if (pass != PASS_SJ) d_chain<NT, CAP>(G, it, B, rs, pass, tau, O);
   gsync<NT>();
@@ -844,6 +936,150 @@ __device__ void overflow_key(const GProb& G, const Item& it, long long nsrc, GBu
   assemble_runs<NT, CAP>(G, it, B, rs, pass, tau, O);
   if (pass != PASS_SJ) d_chain<NT, CAP>(G, it, B, rs, pass, tau, O);
   gsync<NT>();
+}
+
+// ---- frame mode: items whose keys span a window of the shared buffer (dense operators) ----
+// The group accumulates every candidate straight into a key-indexed frame (direct and
+// transposed sums apart), one source after another with a barrier in between: a source emits
+// pairwise distinct keys, so no two threads touch one key at a time and every key's sum is
+// formed in source order (deterministic).  The D chain reads the diagonal keys of the window.
+template <int CAP>
+__device__ __forceinline__ int frame_keys(const Item& it) {
+  constexpr int W2 = (46 * CAP) / 16;  // double2 slots in key[] .. dg[]
+  return it.kind == 0 ? W2 / 2 : W2;
+}
+
+template <int NT>
+__device__ __forceinline__ void key_span(const GProb& G, const Item& it, long long nsrc, unsigned long long* sc,
+                                         unsigned& kmin, unsigned& kmax) {
+  unsigned mn = 0xffffffffu, mx = 0u;
+  auto vis = [&](unsigned key, unsigned, double2, int) {
+    mn = key < mn ? key : mn;
+    mx = key > mx ? key : mx;
+  };
+  for (long long s = grank<NT>(); s < nsrc; s += NT) source<false, false>(G, it, s, 0u, vis);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned a = __shfl_xor_sync(FULLM, mn, o), b = __shfl_xor_sync(FULLM, mx, o);
+    mn = a < mn ? a : mn;
+    mx = b > mx ? b : mx;
+  }
+  if (NT != 32) {
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+      sc[threadIdx.x >> 5] = mn;
+      sc[16 + (threadIdx.x >> 5)] = mx;
+    }
+    __syncthreads();
+    for (int w = 0; w < NT / 32; ++w) {
+      mn = (unsigned)sc[w] < mn ? (unsigned)sc[w] : mn;
+      mx = (unsigned)sc[16 + w] > mx ? (unsigned)sc[16 + w] : mx;
+    }
+    __syncthreads();
+  }
+  kmin = mn;
+  kmax = mx;
+}
+
+template <int NT, int CAP>
+__device__ void frame_accum(const GProb& G, const Item& it, long long nsrc, GBuf<CAP>& B, unsigned lo, unsigned hi) {
+  double2* F = reinterpret_cast<double2*>(&B.key[0]);
+  const int W = frame_keys<CAP>(it);
+  const int span = (int)(hi - lo);
+  for (int i = grank<NT>(); i < span; i += NT) {
+    F[i] = make_double2(0.0, 0.0);
+    if (it.kind == 0) F[W + i] = make_double2(0.0, 0.0);
+  }
+  gsync<NT>();
+  auto vis = [&](unsigned key, unsigned, double2 U, int tr) {
+    if (key >= lo && key < hi) {
+      double2& a = F[(tr ? W : 0) + (int)(key - lo)];
+      a.x += U.x;
+      a.y += U.y;
+    }
+  };
+  for (long long src = 0; src < nsrc; ++src) {
+    source<false, true>(G, it, src, 0u, vis, grank<NT>(), NT);
+    gsync<NT>();
+  }
+}
+
+// off-diagonal keys of the window -> S / J entries (counted or written)
+template <int NT, int CAP>
+__device__ void assemble_frame(const GProb& G, const Item& it, GBuf<CAP>& B, unsigned lo, unsigned hi, RowState& rs,
+                               int pass, double tau, const GOut& O) {
+  const double2* F = reinterpret_cast<const double2*>(&B.key[0]);
+  const int W = frame_keys<CAP>(it);
+  const unsigned npk = (unsigned)G.np;
+  const int nrow = it.kind == 0 ? 2 : 1;
+  const unsigned ohi = hi < npk ? hi : npk;
+  for (unsigned base = lo; base < ohi; base += NT) {
+    const unsigned k = base + (unsigned)grank<NT>();
+    const bool valid = k < ohi;
+    double2 N = make_double2(0.0, 0.0), T = make_double2(0.0, 0.0);
+    if (valid) {
+      N = F[k - lo];
+      if (it.kind == 0) T = F[W + (k - lo)];
+    }
+    const double2 A = make_double2(N.x + T.x, N.y - T.y);   // direct + conj(transposed)
+    const double2 Bs = make_double2(N.x - T.x, N.y + T.y);  // direct - conj(transposed)
+    double v0S, v0J, v1S = 0.0, v1J = 0.0;
+    if (it.kind == 0) {
+      v0S = A.x; v0J = -A.y; v1S = Bs.y; v1J = Bs.x;
+    } else {
+      v0S = SQ2 * A.x; v0J = -SQ2 * A.y;
+    }
+    const bool f0S = valid && fabs(v0S) > tau, f0J = valid && fabs(v0J) > tau;
+    const bool f1S = valid && nrow == 2 && fabs(v1S) > tau, f1J = valid && nrow == 2 && fabs(v1J) > tau;
+    const unsigned long long fl = (unsigned long long)f0S | ((unsigned long long)f0J << 12) |
+                                  ((unsigned long long)f1S << 24) | ((unsigned long long)f1J << 36);
+    unsigned long long tot;
+    const unsigned long long ex = gscan<NT>(fl, &tot, B.sc);
+    auto fld = [](unsigned long long x, int q) { return (long long)((x >> (12 * q)) & 0xfff); };
+    if (pass == PASS_WRITE) {
+      if (f0S) put(O, rs.O[0] + rs.nS[0] + fld(ex, 0), (int)k, v0S);
+      if (f0J) put(O, rs.O[0] + rs.TS[0] + rs.nJ[0] + fld(ex, 1), (int)(npk + k), v0J);
+      if (f1S) put(O, rs.O[1] + rs.nS[1] + fld(ex, 2), (int)k, v1S);
+      if (f1J) put(O, rs.O[1] + rs.TS[1] + rs.nJ[1] + fld(ex, 3), (int)(npk + k), v1J);
+    }
+    rs.nS[0] += fld(tot, 0);
+    rs.nJ[0] += fld(tot, 1);
+    rs.nS[1] += fld(tot, 2);
+    rs.nJ[1] += fld(tot, 3);
+  }
+  gsync<NT>();
+}
+
+// D chain over the diagonal keys of the window (every key np + c in it, g = 0 where untouched)
+template <int NT, int CAP>
+__device__ __forceinline__ void frame_chain(const GProb& G, const Item& it, GBuf<CAP>& B, unsigned lo, unsigned hi,
+                                            RowState& rs, int pass, double tau, const GOut& O) {
+  const unsigned npk = (unsigned)G.np;
+  const unsigned dlo = lo > npk ? lo : npk;
+  const int nd = hi > dlo ? (int)(hi - dlo) : 0;
+  const double2* F = reinterpret_cast<const double2*>(&B.key[0]);
+  const bool pair = it.kind == 0;
+  auto dg = [&](int k, int& c, double2& g) {
+    c = (int)(dlo - npk) + k;
+    const double2 N = F[(dlo - lo) + k];
+    g = pair ? make_double2(SQ2 * N.x, SQ2 * N.y) : make_double2(N.x, 0.0);
+  };
+  d_chain_f<NT>(G, it, nd, dg, rs, pass, tau, O);
+  gsync<NT>();
+}
+
+// every window of [kmin, kmax] in key order: accumulate, emit, chain
+template <int NT, int CAP>
+__device__ void frame_sweep(const GProb& G, const Item& it, long long nsrc, GBuf<CAP>& B, unsigned kmin,
+                            unsigned kmax, RowState& rs, int pass, double tau, const GOut& O) {
+  const unsigned W = (unsigned)frame_keys<CAP>(it);
+  for (unsigned lo = kmin; lo <= kmax; lo += W) {
+    const unsigned hi = kmax - lo + 1 < W ? kmax + 1 : lo + W;
+    frame_accum<NT, CAP>(G, it, nsrc, B, lo, hi);
+    assemble_frame<NT, CAP>(G, it, B, lo, hi, rs, pass, tau, O);
+    if (pass != PASS_SJ) frame_chain<NT, CAP>(G, it, B, lo, hi, rs, pass, tau, O);
+    if (hi == kmax + 1) break;
+  }
 }
 
 // every chunk of the item in key order.  Items with at most CAP candidates: one chunk.
@@ -938,8 +1174,22 @@ __device__ void run_item(const GProb& G, const Item& it, long long idx, unsigned
   rs.prev = 1;
   const long long np = G.np;
   const int lane = threadIdx.x & 31;
+  const unsigned kend = (unsigned)(G.np + G.n);
+  // path: 0 one sorted chunk; 1 key-range chunks (sorted); 2 key-indexed frame (<= 2 windows)
+  const int cap = G.cap < CAP ? G.cap : CAP;
+  int path = 0;
+  unsigned kmin = 0, kmax = 0;
+  if (C > (unsigned long long)cap) {
+    path = 1;
+    if (X != nullptr && G.cap >= CAP) {
+      key_span<NT>(G, it, nsrc, B.sc, kmin, kmax);
+      const unsigned W = (unsigned)frame_keys<CAP>(it);
+      if ((unsigned long long)(kmax - kmin) + 1 <= 2ull * W) path = 2;
+    }
+  }
   if (!FILL) {
-    sweep<NT, CAP>(G, it, nsrc, C, B, X, rs, PASS_COUNT, tau, O);
+    if (path == 2) frame_sweep<NT, CAP>(G, it, nsrc, B, kmin, kmax, rs, PASS_COUNT, tau, O);
+    else sweep<NT, CAP>(G, it, nsrc, C, B, X, rs, PASS_COUNT, tau, O);
     d_tail(G, it, rs, PASS_COUNT, tau, O);
     if (grank<NT>() == 0) {
       if (it.kind == 0) {
@@ -952,6 +1202,8 @@ __device__ void run_item(const GProb& G, const Item& it, long long idx, unsigned
         const int t0 = (int)(rs.nS[0] + rs.nJ[0] + rs.nD[0]);
         cnt[2 * np + it.lam - 1] = t0;
         ts[2 * G.npt + it.lam - 1] = t0;
+        G.dtot[2 * (it.lam - 1)] = (int)rs.nS[0];  // S / J part lengths: the fill skips its counting sweep
+        G.dtot[2 * (it.lam - 1) + 1] = (int)rs.nJ[0];
       }
     }
     gsync<NT>();
@@ -999,12 +1251,22 @@ __device__ void run_item(const GProb& G, const Item& it, long long idx, unsigned
     }
   }
   // S / J totals first (the J part follows the whole S part, the D part follows both); a
-  // single-chunk row keeps its sorted candidates for the writing pass
-  const bool one = C <= (unsigned long long)(G.cap < CAP ? G.cap : CAP);
-  if (one) {
-    gather<NT, CAP>(G, it, nsrc, B, 0u, (unsigned)(G.np + G.n));
-    bitonic<NT>(B.key, B.slot, B.cnt);
+  // single chunk / window keeps its data for the writing pass
+  const bool frame1 = path == 2 && (unsigned long long)(kmax - kmin) + 1 <= (unsigned long long)frame_keys<CAP>(it);
+  const bool known = it.kind == 1 && path != 0;  // D row: S / J lengths from the count pass
+  if (known) {
+    rs.nS[0] = __ldg(G.dtot + 2 * (it.lam - 1));
+    rs.nJ[0] = __ldg(G.dtot + 2 * (it.lam - 1) + 1);
+    if (frame1) frame_accum<NT, CAP>(G, it, nsrc, B, kmin, kmax + 1);
+  } else if (path == 0) {
+    gather<NT, CAP>(G, it, nsrc, B, 0u, kend);
+    sort_gathered<NT, CAP>(B);
     assemble_runs<NT, CAP>(G, it, B, rs, PASS_SJ, tau, O);
+  } else if (frame1) {
+    frame_accum<NT, CAP>(G, it, nsrc, B, kmin, kmax + 1);
+    assemble_frame<NT, CAP>(G, it, B, kmin, kmax + 1, rs, PASS_SJ, tau, O);
+  } else if (path == 2) {
+    frame_sweep<NT, CAP>(G, it, nsrc, B, kmin, kmax, rs, PASS_SJ, tau, O);
   } else {
     sweep<NT, CAP>(G, it, nsrc, C, B, X, rs, PASS_SJ, tau, O);
   }
@@ -1014,10 +1276,15 @@ __device__ void run_item(const GProb& G, const Item& it, long long idx, unsigned
     rs.TJ[r] = rs.nJ[r];
     rs.nS[r] = rs.nJ[r] = 0;
   }
-  if (one) {
+  if (path == 0) {
     assemble_runs<NT, CAP>(G, it, B, rs, PASS_WRITE, tau, O);
     d_chain<NT, CAP>(G, it, B, rs, PASS_WRITE, tau, O);
     gsync<NT>();
+  } else if (frame1) {  // (frame accumulated above)
+    assemble_frame<NT, CAP>(G, it, B, kmin, kmax + 1, rs, PASS_WRITE, tau, O);
+    frame_chain<NT, CAP>(G, it, B, kmin, kmax + 1, rs, PASS_WRITE, tau, O);
+  } else if (path == 2) {
+    frame_sweep<NT, CAP>(G, it, nsrc, B, kmin, kmax, rs, PASS_WRITE, tau, O);
   } else {
     sweep<NT, CAP>(G, it, nsrc, C, B, X, rs, PASS_WRITE, tau, O);
   }
@@ -1055,16 +1322,17 @@ __global__ void __launch_bounds__(32 * GW_WARPS) k_g_light(const GProb G, int* c
   }
 }
 
-// heavy engine: a CTA per D row and per listed pair; key-range chunks
+// heavy engine: a CTA per D row and per listed pair; key-range chunks or a key-indexed frame.
+// part: 0 = the D rows only, 1 = the listed pairs only, 2 = both
 template <bool FILL>
-__global__ void __launch_bounds__(GH_NT) k_g_heavy(const GProb G, int* cnt, int* ts, const GOut O) {
+__global__ void __launch_bounds__(GH_NT) k_g_heavy(const GProb G, int* cnt, int* ts, const GOut O, int part) {
   extern __shared__ __align__(16) unsigned char gsm[];
   GBuf<GH_CAP>& B = *reinterpret_cast<GBuf<GH_CAP>*>(gsm);
   GHeavyExtra* X = reinterpret_cast<GHeavyExtra*>(gsm + sizeof(GBuf<GH_CAP>));
   const double tau = *G.tau_ptr;
-  const long long nd = G.n - 1;
-  const long long items = nd + *G.nheavy;
-  if (FILL && blockIdx.x == 0 && threadIdx.x == 0) O.row_ptr[G.m] = *O.nnz;
+  const long long nd = part == 1 ? 0 : G.n - 1;
+  const long long items = nd + (part == 0 ? 0 : *G.nheavy);
+  if (FILL && part != 1 && blockIdx.x == 0 && threadIdx.x == 0) O.row_ptr[G.m] = *O.nnz;
   for (long long t = blockIdx.x; t < items; t += gridDim.x) {
     const bool isd = t < nd;
     const long long p = isd ? 0 : (long long)__ldg(G.heavy + (t - nd));
@@ -1129,6 +1397,8 @@ GLayout g_layout(int n, int P, const long long* nnzL, size_t base) {
   g.nheavy = off; off = al256(off + 2 * sizeof(int));
   g.nrb = (n + GE_THREADS - 1) / GE_THREADS;
   g.blk = off;    off = al256(off + (size_t)(2 + P) * g.nrb * sizeof(GBlk));
+  g.dtot0 = off;  off = al256(off + (size_t)2 * n * sizeof(int));
+  g.dtot1 = off;  off = al256(off + (size_t)2 * n * sizeof(int));
   g.total = off;
   return g;
 }
@@ -1176,26 +1446,31 @@ cudaError_t g_prepare() {
   return set_attrs();
 }
 
-cudaError_t g_count(const GProb& pr, int* cnt, int* ts, cudaStream_t st) {
+// The D rows (heavy engine, part 0) run on `aux` concurrently with the light pairs on `st`; the
+// listed heavy pairs (part 1) follow the light count on `st` (the list is its output).  The
+// caller orders `aux` after `st` before and joins it afterwards.
+cudaError_t g_count(const GProb& pr, int* cnt, int* ts, cudaStream_t st, cudaStream_t aux) {
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
   GOut none{};
   const int sms = sm_count();
   const long long lw = (pr.np + GW_WARPS - 1) / GW_WARPS;
   const unsigned lg = (unsigned)(lw < 4LL * sms ? (lw > 0 ? lw : 1) : 4LL * sms);
+  const unsigned hd = (unsigned)(pr.n - 1 < 2LL * sms ? pr.n - 1 : 2LL * sms);
+  k_g_heavy<false><<<hd > 0 ? hd : 1, GH_NT, HEAVY_SMEM, aux>>>(pr, cnt, ts, none, 0);
   k_g_light<false><<<lg, 32 * GW_WARPS, LIGHT_SMEM, st>>>(pr, cnt, ts, none);
-  k_g_heavy<false><<<(unsigned)(4 * sms), GH_NT, HEAVY_SMEM, st>>>(pr, cnt, ts, none);
+  k_g_heavy<false><<<(unsigned)(2 * sms), GH_NT, HEAVY_SMEM, st>>>(pr, cnt, ts, none, 1);
   return cudaGetLastError();
 }
 
-cudaError_t g_fill(const GProb& pr, const int* cnt, const GOut& out, cudaStream_t st) {
+cudaError_t g_fill(const GProb& pr, const int* cnt, const GOut& out, cudaStream_t st, cudaStream_t aux) {
   cudaError_t e = set_attrs();
   if (e != cudaSuccess) return e;
   const int sms = sm_count();
   const long long lw = (pr.np + GW_WARPS - 1) / GW_WARPS;
   const unsigned lg = (unsigned)(lw < 4LL * sms ? (lw > 0 ? lw : 1) : 4LL * sms);
+  k_g_heavy<true><<<(unsigned)(2 * sms), GH_NT, HEAVY_SMEM, aux>>>(pr, const_cast<int*>(cnt), nullptr, out, 2);
   k_g_light<true><<<lg, 32 * GW_WARPS, LIGHT_SMEM, st>>>(pr, const_cast<int*>(cnt), nullptr, out);
-  k_g_heavy<true><<<(unsigned)(4 * sms), GH_NT, HEAVY_SMEM, st>>>(pr, const_cast<int*>(cnt), nullptr, out);
   return cudaGetLastError();
 }
 

@@ -59,6 +59,7 @@ struct GProb {
   int* heavy;             // heavy pair list (count pass appends, fill pass reads)
   int* nheavy;            // its length
   int* flags;             // header flags (F_* of sunfold.cu)
+  int* dtot;              // [2 (n-1)]: S / J part lengths of the D rows (count pass -> fill pass)
   int cap;                // candidate buffer limit (testing: a small value forces the chunked
                           // and single-key paths); the engines use min(their buffer, cap)
 };
@@ -77,7 +78,7 @@ constexpr int GSLOT = 32;  // pairs per scan slot (as modes 0/2: S slots, J slot
 
 // Host side (sunfold_general.cu).  Layout of the general region of the workspace.
 struct GLayout {
-  size_t colcnt, cp, xr, heavy0, heavy1, nheavy, blk, total;
+  size_t colcnt, cp, xr, heavy0, heavy1, nheavy, blk, dtot0, dtot1, total;
   long long xr_off[GMAXP];
   long long nrb;  // row blocks of the expand kernel
 };
@@ -106,11 +107,12 @@ cudaError_t g_expand(const GExpandIn& in, char* ws, const GLayout& gl, double* i
                      unsigned long long* zero64, long long nz64, GHeaderRef hdr, cudaStream_t st);
 // kernel attributes (dynamic shared memory); call outside any stream capture
 cudaError_t g_prepare();
-// count pass (a3) of one matrix: per-row counts and slot sums (modes 0/2 slot layout)
-cudaError_t g_count(const GProb& pr, int* cnt, int* ts, cudaStream_t st);
-// fill pass (a5): row_ptr, col, val (and K)
-cudaError_t g_fill(const GProb& pr, const int* cnt, const GOut& out, cudaStream_t st);
+// count pass (a3) of one matrix: per-row counts and slot sums (modes 0/2 slot layout); the D
+// rows on `aux` (ordered after `st` by the caller, joined afterwards)
+cudaError_t g_count(const GProb& pr, int* cnt, int* ts, cudaStream_t st, cudaStream_t aux);
+// fill pass (a5): row_ptr, col, val (and K); heavy rows on `aux`
+cudaError_t g_fill(const GProb& pr, const int* cnt, const GOut& out, cudaStream_t st, cudaStream_t aux);
 // kernels per count / fill call
-constexpr int G_LAUNCHES_EXPAND = 4, G_LAUNCHES_COUNT = 2, G_LAUNCHES_FILL = 2;
+constexpr int G_LAUNCHES_EXPAND = 4, G_LAUNCHES_COUNT = 3, G_LAUNCHES_FILL = 2;
 
 }  // namespace sung
