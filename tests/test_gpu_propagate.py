@@ -232,3 +232,63 @@ def test_apply_matrix_free_matches_csr_apply(idx):
     b = plan.apply(v, 1.3).cpu().numpy()
     assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
     plan.close()
+
+
+def _oracle_mats(prob):
+    ref = sparse.unfold_problem(prob)
+    m = prob.m
+    Q0 = _csr_np(ref["Q0"], m)
+    Q1 = _csr_np(ref["Q1"], m) if "Q1" in ref else None
+    return ref, Q0, Q1, ref["Q0"]["K"]
+
+
+@pytest.mark.parametrize("idx", [2, 3, 4])
+def test_matrix_free_apply_and_rk4_against_oracle(idx):
+    """The matrix-free apply (sun_apply_plan) and RK4 (sun_rk4_plan) directly against the oracle:
+    y = (Q0 + eps Q1) v + K and RK4 on v with O2's matrices (oracle.propagate.rk4_v), at c2-c4.
+    Bound: R7's entrywise tolerance 1e-12 max|Q| carried through the row sums (apply) and the
+    steps (RK4)."""
+    sun = _sun()
+    prob = config(idx)
+    ref, Qo0, Qo1, Ko = _oracle_mats(prob)
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    plan.run()
+    rng = np.random.default_rng(7 + idx)
+    rho = _dense_random_rho(prob.n, 90 + idx) if prob.n <= 512 else None
+    v = basis.project(rho).real if rho is not None else rng.standard_normal(prob.m) / prob.n
+    eps = 1.0 + 1.5 * np.sin(0.7)
+    y = plan.apply(torch.tensor(v, device="cuda"), eps).cpu().numpy()
+    yref = Qo0 @ v + Ko + (eps * (Qo1 @ v) if Qo1 is not None else 0.0)
+    rowlen = np.diff(ref["Q0"]["row_ptr"]).max()
+    qmax = np.abs(ref["Q0"]["val"]).max()
+    bound = 1e-12 * qmax * np.abs(v).max() * rowlen * (1 + abs(eps)) + 1e-12 * np.abs(Ko).max()
+    assert np.abs(y - yref).max() <= bound + 1e-13 * np.abs(yref).max()
+    v0 = sun.expand_state(ZCSR.from_triplets(prob.n, [0], [0], [1.0]))
+    h, steps = 1e-5, 3
+    kw = dict(eps0=1.0, eps1=1.5, omega=1.0) if Qo1 is not None else {}
+    vg = v0.clone()
+    plan.rk4(vg, h, steps, **kw)
+    vref = propagate.rk4_v(Qo0, Qo1, Ko, v0.cpu().numpy(), 0.0, h, steps, **kw)
+    b2 = steps * h * 3.5 * rowlen * 1e-12 * qmax * np.abs(vref).max() * 2
+    assert np.abs(vg.cpu().numpy() - vref).max() <= b2 + 1e-13 * np.abs(vref).max()
+    plan.close()
+
+
+@pytest.mark.parametrize("idx", [0, 2, 3])
+def test_unfold_split_against_oracle(idx):
+    """F4: Q_H (Eq. 6) and R (Eq. 10) of unfold_split, each against O2 directly: O2 on
+    (H0, no dissipators) and on (0, {L_p, gamma_p}); K against O2's K."""
+    sun = _sun()
+    prob = config(idx)
+    QH, R, Q1, K = sun.unfold_split(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    n = prob.n
+    zero = ZCSR.from_dense(np.zeros((n, n), complex))
+    tauH = sparse.TAU_REL * sparse.frob(prob.H0)
+    tauR = sparse.TAU_REL * sum(g * sparse.frob(L) ** 2 for L, g in zip(prob.Ls, prob.gammas))
+    rH = sparse.unfold_csr(prob.H0, (), (), tauH, with_k=False)
+    rR = sparse.unfold_csr(zero, prob.Ls, prob.gammas, tauR)
+    for got, want, nm in ((QH, rH, "QH"), (R, rR, "R")):
+        assert np.array_equal(got.row_ptr.cpu().numpy(), want["row_ptr"]), nm
+        assert np.array_equal(got.col.cpu().numpy(), want["col"]), nm
+        sparse.assert_entries_close(got.val.cpu().numpy(), want, nm)
+    sparse.assert_k_close(K.cpu().numpy(), rR["K"], "split:K", tauR)

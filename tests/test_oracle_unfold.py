@@ -9,6 +9,7 @@ import json
 import os
 
 import numpy as np
+import scipy.sparse as sp
 import pytest
 
 from oracle import basis, dense, paper_eqs, sparse
@@ -223,3 +224,46 @@ def test_o2_nnz_regression_dimer_banded():
         p = banded_random_problem(n, seed=3)
         r = sparse.unfold_csr(p.H0, p.Ls, p.gammas, sparse.tau_q0(p))
         assert len(r["col"]) == int(70.5 * n * n - 322.5 * n + 379)
+
+
+def _labels_of(n, m):
+    """(kind, a, b) of generator index m (R5)."""
+    np_ = n * (n - 1) // 2
+    if m < 2 * np_:
+        p = m if m < np_ else m - np_
+        a = 0
+        while p >= n - 1 - a:
+            p -= n - 1 - a
+            a += 1
+        return ("S" if m < np_ else "J"), a, a + 1 + p
+    return "D", m - 2 * np_ + 1, -1
+
+
+@pytest.mark.parametrize("idx,nrand,nd", [(2, 200, 255), (3, 60, 30), (4, 24, 8)])
+def test_o2_columns_match_o1_samples(idx, nrand, nd):
+    """O2 against the textbook definition O1 (Q_sm = Tr(F_s L(F_m)), dense
+    matrices) on sampled columns at the BASELINE sizes c2-c4 where O1 cannot run
+    whole: random S/J columns plus D columns (all at c2).  Pattern of each column bit-exact under
+    R6, values within 1e-12 max|Q| (R7)."""
+    prob = config(idx)
+    n, m = prob.n, prob.m
+    r = sparse.unfold_problem(prob)["Q0"]
+    tau = sparse.tau_q0(prob)
+    Qc = sp.csr_matrix((r["val"], r["col"], r["row_ptr"]), shape=(m, m)).tocsc()
+    scale = np.abs(r["val"]).max()
+    H = prob.H0.to_dense()
+    Ls = [L.to_dense() for L in prob.Ls]
+    rng = np.random.default_rng(100 + idx)
+    cols = list(rng.choice(n * (n - 1), size=nrand, replace=False))
+    dcols = n * (n - 1) + np.linspace(0, n - 2, nd).round().astype(int)
+    for mcol in cols + list(dcols):
+        kind, a, b = _labels_of(n, int(mcol))
+        F = basis.generator(n, kind, a, b)
+        col = basis.project(dense.lindbladian(H, Ls, prob.gammas, F))
+        assert np.abs(col.imag).max() <= 1e-12 * scale
+        col = col.real
+        keep = np.nonzero(np.abs(col) > tau)[0]
+        lo, hi = Qc.indptr[mcol], Qc.indptr[mcol + 1]
+        assert np.array_equal(Qc.indices[lo:hi], keep), (idx, mcol, kind, a, b)
+        assert np.abs(Qc.data[lo:hi] - col[keep]).max(initial=0.0) <= 1e-12 * scale
+        assert np.abs(np.delete(col, keep)).max(initial=0.0) < tau
