@@ -16,6 +16,7 @@
 //   sun_apply       : k_apply           (a7) dv/dt = Q0 v + eps Q1 v + K
 #include <cuda_runtime.h>
 #include <math.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -92,6 +93,13 @@ struct BlkInfo {  // k_expand: one per (operator, row block), reduced by the las
 
 struct Gammas {
   double g[MAXOPS];
+};
+
+// NVTX ranges: host-side ranges around the enqueue of each pass, named after the
+// paper's steps; with graphs they mark the capture (first call) or the replay launch.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
 };
 
 thread_local char g_errbuf[512];
@@ -2635,6 +2643,7 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
     ops.gamma[2 + p] = gamma[p];
   }
   for (int i = 0; i < MAXOPS; ++i) ops.wplan[i] = -1;
+  NvtxRange r_("sun_plan_create (analyse)");
   CK(cudaMemsetAsync(hdr, 0, sizeof(DevHeader), st));
   k_analyze<<<ops.nops, 256, 0, st>>>(ops, hdr);
   CK(cudaGetLastError());
@@ -2803,6 +2812,7 @@ static int enqueue_count_general(sun_plan pl, cudaStream_t st) {
 }
 
 static int enqueue_count(sun_plan pl, cudaStream_t st) {
+  NvtxRange r_("sunfold: expand (a1) + count (a3) + scan (a4)");
   if (pl->general) return enqueue_count_general(pl, st);
   const Layout& L = pl->lay;
   const int n = pl->n;
@@ -2888,6 +2898,7 @@ static int enqueue_count(sun_plan pl, cudaStream_t st) {
 
 int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
   if (!pl) return SUN_ERR_ARG;
+  NvtxRange r_("sun_plan_nnz (readback)");
   if (!pl->counted) return SUN_ERR_STATE;
   if (!pl->hpin && cudaMallocHost(&pl->hpin, sizeof(HeaderPrefix)) != cudaSuccess) {
     pl->hpin = nullptr;  // pageable fallback
@@ -2921,6 +2932,7 @@ int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
 }
 
 static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st) {
+  NvtxRange r_("sunfold: fill (a5) + K + Q1 (a6)");
   const Layout& L = pl->lay;
   char* ws = pl->ws;
   DevHeader* hdr = (DevHeader*)(ws + L.hdr);
@@ -2970,6 +2982,7 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
 // the sequence (captured on the plan's capture stream; kernel arguments, including the output
 // pointers and capacities, are part of the key), or enqueue directly if graphs are disabled.
 static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st) {
+  NvtxRange r_(kind == 0 ? "sun_count" : (kind == 1 ? "sun_unfold" : "sun_run"));
   // the nnz / flags readback of sun_plan_nnz rides in the same sequence (a memcpy node of the
   // graph into pinned host memory), so sun_plan_nnz only waits for the stream
   if (kind != 1 && !pl->hpin && cudaMallocHost(&pl->hpin, sizeof(HeaderPrefix)) != cudaSuccess) {
