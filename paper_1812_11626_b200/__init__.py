@@ -189,6 +189,7 @@ class Plan:
         _check(st, "sun_plan_create")
         self._plan = plan
         self._caps = None  # output capacities for run(): previous nnz
+        self._banded = self.info()["mode_q0"] != 3
 
     def workspace_guard_intact(self) -> bool:
         if not self._guard:
@@ -251,7 +252,8 @@ class Plan:
     def run(self, out=None):
         """Whole unfold with no host round trip between the passes (sun_run), then the nnz
         readback.  Output capacity: `out`, else the previous call's nnz (the first call of a
-        plan uses the two-step path, which sizes the outputs exactly).
+        banded plan uses the structural bound sun_nnz_bound -- the returned tensors are views of
+        those buffers -- and that of a general-pattern plan the exact two-step path).
         Returns (Q0, Q1 or None, K) trimmed to the produced nnz."""
         with _on(self.stream):
             return self._run(out)
@@ -259,11 +261,14 @@ class Plan:
     def _run(self, out):
         L = lib()
         if out is None:
-            if self._caps is None:  # first call: exact sizes from the two-step path
-                res = self.run_two_pass()
-                self._caps = (res[0].nnz, res[1].nnz if res[1] is not None else 0)
-                return res
-            bufs = self._alloc(*self._caps)
+            if self._caps is None:
+                if not self._banded:  # first call, general mode: exact sizes from the two-step path
+                    res = self.run_two_pass()
+                    self._caps = (res[0].nnz, res[1].nnz if res[1] is not None else 0)
+                    return res
+                bufs = self._alloc(*self.nnz_bound())  # banded: the structural bound, one pass
+            else:
+                bufs = self._alloc(*self._caps)
         else:
             bufs = out
         s0, s1 = self._structs(bufs)

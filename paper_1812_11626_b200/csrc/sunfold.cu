@@ -22,6 +22,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
 #include <type_traits>
 #include <vector>
 
@@ -162,6 +163,53 @@ Layout make_layout(int n, int P) {
   return L;
 }
 
+// Streams, events and the pinned readback slot of a plan, recycled across plans (creating and
+// destroying them, and cudaFreeHost in particular, dominated the cost of a one-shot unfold).
+struct PlanRes {
+  int device = -1;
+  cudaStream_t aux[2] = {nullptr, nullptr}, cap = nullptr;
+  cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
+  cudaEvent_t done = nullptr;  // recorded after each readback into hpin (released plans wait on it)
+  HeaderPrefix* hpin = nullptr;
+};
+std::mutex g_res_mu;
+std::vector<PlanRes> g_res_free;
+
+cudaError_t res_acquire(PlanRes& r) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  {
+    std::lock_guard<std::mutex> lk(g_res_mu);
+    for (size_t i = 0; i < g_res_free.size(); ++i)
+      if (g_res_free[i].device == dev) {
+        r = g_res_free[i];
+        g_res_free.erase(g_res_free.begin() + i);
+        return cudaSuccess;
+      }
+  }
+  r = PlanRes();
+  r.device = dev;
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = cudaStreamCreateWithFlags(&r.aux[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.join[i], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r.cap, cudaStreamNonBlocking);
+  if (e == cudaSuccess && cudaMallocHost(&r.hpin, sizeof(HeaderPrefix)) != cudaSuccess) {
+    r.hpin = nullptr;  // pageable fallback in sun_plan_nnz
+    (void)cudaGetLastError();
+  }
+  return e;
+}
+
+void res_release(const PlanRes& r) {
+  if (r.device < 0 || !r.aux[0] || !r.aux[1] || !r.cap || !r.fork || !r.join[0] || !r.join[1] || !r.done) return;
+  std::lock_guard<std::mutex> lk(g_res_mu);
+  g_res_free.push_back(r);
+}
+
 }  // namespace
 
 struct sun_plan_s {
@@ -211,15 +259,17 @@ struct sun_plan_s {
   bool use_graphs = true;
   HeaderPrefix* hpin = nullptr;  // pinned host copy of the header prefix (nnz readback)
   int hdr_enqueued = 0;          // the last count/run sequence already copies the header to hpin
+  PlanRes res;                   // pooled streams / events / pinned slot (res_acquire)
+  std::vector<std::vector<uintptr_t>> seen;  // enqueue keys run once directly (captured on reuse)
   ~sun_plan_s() {
-    if (hpin) cudaFreeHost(hpin);
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
-    for (int i = 0; i < 2; ++i) {
-      if (aux[i]) cudaStreamDestroy(aux[i]);
-      if (ev_join[i]) cudaEventDestroy(ev_join[i]);
+    if (aux[0]) {  // nothing of this plan may still run on the pooled streams or write hpin
+      cudaStreamSynchronize(aux[0]);
+      cudaStreamSynchronize(aux[1]);
+      cudaEventSynchronize(res.done);
+      (void)cudaGetLastError();  // a destructor reports nothing: leave no error for the next call
     }
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (cap_stream) cudaStreamDestroy(cap_stream);
+    res_release(res);
   }
 };
 
@@ -2385,12 +2435,18 @@ cudaError_t launch_count0(const MatCount& m0, const MatCount& m1, cudaStream_t s
 template <int WK, int WL, int PT, int Q1W>
 cudaError_t attr_fill0(const Prob& p0, const Prob* p1, long long& grid) {
   const int smem = FillFar<WK, WL>::SMEM;
-  cudaError_t e = cudaFuncSetAttribute(k_fill0<WK, WL, PT, Q1W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  int dev = 0, sms = 0, nb = 0;
-  if (e == cudaSuccess) e = cudaGetDevice(&dev);
-  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fill0<WK, WL, PT, Q1W>, 256, smem);
-  if (e != cudaSuccess) return e;
+  static int c_sms = 0, c_nb = 0;  // per instantiation: set once (attribute, occupancy)
+  int sms = c_sms, nb = c_nb;
+  if (!c_sms) {
+    cudaError_t e = cudaFuncSetAttribute(k_fill0<WK, WL, PT, Q1W>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int dev = 0;
+    if (e == cudaSuccess) e = cudaGetDevice(&dev);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_fill0<WK, WL, PT, Q1W>, 256, smem);
+    if (e != cudaSuccess) return e;
+    c_nb = nb;
+    c_sms = sms;
+  }
   auto tiles = [](const Prob& p) { return (p.npt + SLOTS_PER_TILE - 1) / SLOTS_PER_TILE; };
   long long U = tiles(p0) + (2 * (p0.n * 2LL * p0.W + p0.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
   if (Q1W >= 0 && p1) U += tiles(*p1) + near_units1(p1->n, p1->W);
@@ -2719,21 +2775,19 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
     pl->launches_count = (P > 0 ? sung::G_LAUNCHES_EXPAND : 1) + sung::G_LAUNCHES_COUNT * nmat + 1;
     pl->launches_fill = sung::G_LAUNCHES_FILL * nmat;
   }
-  for (int i = 0; i < 2; ++i) {
-    cudaError_t e1 = cudaStreamCreateWithFlags(&pl->aux[i], cudaStreamNonBlocking);
-    if (e1 == cudaSuccess) e1 = cudaEventCreateWithFlags(&pl->ev_join[i], cudaEventDisableTiming);
-    if (e1 != cudaSuccess) {
-      delete pl;
-      return cuda_fail(e1);
-    }
-  }
   {
-    cudaError_t e1 = cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming);
-    if (e1 == cudaSuccess) e1 = cudaStreamCreateWithFlags(&pl->cap_stream, cudaStreamNonBlocking);
+    cudaError_t e1 = res_acquire(pl->res);
     if (e1 != cudaSuccess) {
       delete pl;
       return cuda_fail(e1);
     }
+    for (int i = 0; i < 2; ++i) {
+      pl->aux[i] = pl->res.aux[i];
+      pl->ev_join[i] = pl->res.join[i];
+    }
+    pl->ev_fork = pl->res.fork;
+    pl->cap_stream = pl->res.cap;
+    pl->hpin = pl->res.hpin;
     const char* ng = getenv("SUNFOLD_NO_GRAPHS");
     pl->use_graphs = !(ng && ng[0] && ng[0] != '0');
     if (pl->general) {
@@ -2900,10 +2954,6 @@ int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
   if (!pl) return SUN_ERR_ARG;
   NvtxRange r_("sun_plan_nnz (readback)");
   if (!pl->counted) return SUN_ERR_STATE;
-  if (!pl->hpin && cudaMallocHost(&pl->hpin, sizeof(HeaderPrefix)) != cudaSuccess) {
-    pl->hpin = nullptr;  // pageable fallback
-    (void)cudaGetLastError();
-  }
   HeaderPrefix hloc;
   HeaderPrefix* hp = pl->hpin ? pl->hpin : &hloc;
   if (!pl->hdr_enqueued)
@@ -2985,10 +3035,6 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
   NvtxRange r_(kind == 0 ? "sun_count" : (kind == 1 ? "sun_unfold" : "sun_run"));
   // the nnz / flags readback of sun_plan_nnz rides in the same sequence (a memcpy node of the
   // graph into pinned host memory), so sun_plan_nnz only waits for the stream
-  if (kind != 1 && !pl->hpin && cudaMallocHost(&pl->hpin, sizeof(HeaderPrefix)) != cudaSuccess) {
-    pl->hpin = nullptr;  // pageable fallback in sun_plan_nnz
-    (void)cudaGetLastError();
-  }
   const bool readback = kind != 1 && pl->hpin;
   auto direct = [&](cudaStream_t s) -> int {
     int rc = SUN_OK;
@@ -3002,8 +3048,15 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
     return rc;
   };
   pl->hdr_enqueued = 0;
+  auto mark = [&](int rc) {  // the pooled pinned slot is written by this sequence: track its end
+    if (rc == SUN_OK && readback) {
+      const cudaError_t e = cudaEventRecord(pl->res.done, st);
+      if (e != cudaSuccess) return cuda_fail(e);
+    }
+    return rc;
+  };
   if (!pl->use_graphs) {
-    const int rc = direct(st);
+    const int rc = mark(direct(st));
     pl->hdr_enqueued = rc == SUN_OK && readback ? 1 : 0;
     return rc;
   }
@@ -3023,6 +3076,18 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
       g.used = ++pl->graph_clock;
       break;
     }
+  if (!exec) {  // first use of this sequence: launch directly; capture a graph when it recurs
+    std::vector<uintptr_t> kv(key, key + 12);
+    bool again = false;
+    for (const auto& k : pl->seen) again |= k == kv;
+    if (!again) {
+      if (pl->seen.size() >= 16) pl->seen.erase(pl->seen.begin());
+      pl->seen.push_back(kv);
+      const int rc = mark(direct(st));
+      pl->hdr_enqueued = rc == SUN_OK && readback ? 1 : 0;
+      return rc;
+    }
+  }
   if (!exec) {
     CK(cudaStreamBeginCapture(pl->cap_stream, cudaStreamCaptureModeThreadLocal));
     int rc = direct(pl->cap_stream);
@@ -3051,8 +3116,9 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
     pl->graphs.push_back(ge);
   }
   CK(cudaGraphLaunch(exec, st));
-  pl->hdr_enqueued = readback ? 1 : 0;
-  return SUN_OK;
+  const int rc = mark(SUN_OK);
+  pl->hdr_enqueued = rc == SUN_OK && readback ? 1 : 0;
+  return rc;
 }
 
 int sun_count(sun_plan pl, void* stream) {
