@@ -62,6 +62,15 @@ struct Prob {
   long long nb_near;   // mode 0: units of 8 near-pair / D-row items (one warp each)
 };
 
+// (x, y) += conj(la) lb with every rounding explicit: the compiler has no contraction choice
+// left, so each evaluation of a value (count pass, fill pass, matrix-free stages; whatever
+// kernel it is inlined into) performs the identical operations and the passes take identical
+// tau decisions.
+__device__ __forceinline__ void conj_mul_acc(double& x, double& y, const double2 la, const double2 lb) {
+  x = __dadd_rn(x, __fma_rn(la.x, lb.x, __dmul_rn(la.y, lb.y)));
+  y = __dadd_rn(y, __fma_rn(la.x, lb.y, -__dmul_rn(la.y, lb.x)));
+}
+
 __device__ __forceinline__ double2 bget(const Band B, int r, int c) {
   int o = c - r;
   if (o < -B.w || o > B.w) return make_double2(0.0, 0.0);
@@ -81,10 +90,12 @@ __device__ __forceinline__ int pidx32(int n, int c, int d) {
 }
 
 // pair index p -> (a, b), a < b < n, lexicographic (R5)
+// (fp32 square-root estimate, |error| <= a few rows for n <= 46340, fixed by the exact integer
+// corrections below)
 __device__ __forceinline__ void pair_decode(long long n, long long p, int& a_out, int& b_out) {
-  double t = (double)(2 * n - 1);
-  double disc = t * t - 8.0 * (double)p;
-  long long a = (long long)floor((t - sqrt(disc > 0.0 ? disc : 0.0)) * 0.5);
+  const float t = (float)(2 * n - 1);
+  const float disc = (float)((2 * n - 1) * (2 * n - 1) - 8 * p);
+  long long a = (long long)((t - sqrtf(disc > 0.0f ? disc : 0.0f)) * 0.5f);
   if (a < 0) a = 0;
   if (a > n - 2) a = n - 2;
   while (a > 0 && a * (2 * n - a - 1) / 2 > p) --a;
@@ -146,8 +157,7 @@ __device__ __forceinline__ double2 U_elem(const Prob& pr, int a, int b, int c, i
     for (int p = 0; p < pr.P; ++p) {
       double2 la = lget(pr, p, a, c);
       double2 lb = lget(pr, p, b, d);
-      ux += la.x * lb.x + la.y * lb.y;  // conj(la) * lb
-      uy += la.x * lb.y - la.y * lb.x;
+      conj_mul_acc(ux, uy, la, lb);  // conj(la) * lb
     }
   }
   return make_double2(ux, uy);
@@ -642,8 +652,7 @@ __device__ __forceinline__ void far_values(const FarCtx& pr, int a, int b, doubl
       for (int i = 0; i < SL; ++i)
 #pragma unroll
         for (int j = 0; j < SL; ++j) {
-          ox[i][j] += la[i].x * lb[j].x + la[i].y * lb[j].y;
-          oy[i][j] += la[i].x * lb[j].y - la[i].y * lb[j].x;
+          conj_mul_acc(ox[i][j], oy[i][j], la[i], lb[j]);
         }
     }
   }
@@ -862,8 +871,7 @@ __device__ __forceinline__ bool far_value_at(const Prob& pr, int a, int b, int k
       const long long ps = (long long)n * SL;
       for (int p = 0; p < P; ++p) {
         const double2 la = __ldg(La + p * ps), lb = __ldg(Lb + p * ps);
-        x += la.x * lb.x + la.y * lb.y;  // conj(Lt_p,ac) Lt_p,bd
-        y += la.x * lb.y - la.y * lb.x;
+        conj_mul_acc(x, y, la, lb);  // conj(Lt_p,ac) Lt_p,bd
       }
     }
     if (dd == 0) {  // + i K_ca
