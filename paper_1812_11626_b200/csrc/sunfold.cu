@@ -236,6 +236,7 @@ struct sun_plan_s {
   std::vector<int> pos_dc[2], pos_dd[2];
   NearSide side[2];
   int combined;         // mode 0 with Q1 absent or Q1 = Q_H[diagonal H1]: one launch per pass
+  int near_sep = 0;     // combined: near rows by k_near0 before the fill (SUNFOLD_NEAR_SEP=1)
   long long fill_grid[2];
   // auxiliary streams: the Q1 passes and the near-item fill run concurrently with Q0's far
   // tiles (fork/join with events on the caller's stream; also valid under graph capture)
@@ -865,8 +866,9 @@ __device__ __forceinline__ void fill_near_unit(const Prob& pr, long long j, cons
 constexpr int NEAR_RPW = SUN_NEAR_RPW;        // near rows per warp (lane groups of 32 / NEAR_RPW)
 constexpr int NEAR_GL = 32 / NEAR_RPW;        // lanes per row
 constexpr int NEAR_UROWS = 8 * NEAR_RPW;      // side rows per near unit
+// inv: the inv[l] table (global, or a shared-memory copy; generic loads).
 __device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, const int* __restrict__ cnt,
-                                                 const FillOut& fo, const NearSide& side) {
+                                                 const FillOut& fo, const NearSide& side, const double* inv) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int hl = lane & (NEAR_GL - 1);
   const long long np = pr.np;
@@ -917,10 +919,10 @@ __device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, co
   }
   const long long ot = o + nwin, limt = lim - nwin;
   const int dbase = (int)(2 * np - 1);
-#pragma unroll 4
+#pragma unroll 8
   for (int l = m.hi + 1 + hl; l <= m.lend; l += NEAR_GL) {
     const int k = l - m.hi - 1;
-    const double v = m.tr * __ldg(&pr.inv[l]);
+    const double v = m.tr * inv[l];
     if (k < limt) {
       fo.col[ot + k] = dbase + l;
       fo.val[ot + k] = v;
@@ -1353,6 +1355,7 @@ struct MatFill {
   FillOut fo;
   NearSide side;
   int tile_sync;  // keep a CTA's warps on the same far tile (large outputs; see k_fill0)
+  int near_sep;   // the near rows are written by k_near0 (launched before the fill), not by its units
 };
 
 // Fill pass of Q0 and, with Q1W >= 0, of Q1 (widths Q1W, 0, no dissipators; staging-free
@@ -1371,7 +1374,7 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
     if (HAS1) m1.fo.row_ptr[m1.pr.m] = *m1.fo.nnz;
   }
   // near units: NEAR_UNIT_ROWS side rows each (2 per near item)
-  const long long nn0 = (2 * (m0.pr.n * 2LL * m0.pr.W + m0.pr.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
+  const long long nn0 = m0.near_sep ? 0 : (2 * (m0.pr.n * 2LL * m0.pr.W + m0.pr.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
   // Q1 tiles: none when the Q0 far tiles write Q1's rows (staged Q0 tiles of 256 pairs)
   constexpr bool Q1MERGED = HAS1 && !FF::DIRECT;
   // Q1's near items are its D rows; with the diagonal drive they are empty (count pass), so
@@ -1431,7 +1434,7 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
       if constexpr (Q1MERGED) fill_q1_chunk(prf1, m1.pr.npt, idx, m1.cnt, m1.fo, a, b);
     } else if (kind == 1) {
 #ifndef SUN_EXP_NO_NEAR
-      fill_near_unit_h(m0.pr, idx, m0.cnt, m0.fo, m0.side);
+      fill_near_unit_h(m0.pr, idx, m0.cnt, m0.fo, m0.side, m0.pr.inv);
 #endif
     } else if (kind == 2) {
       if constexpr (HAS1) fill_near_unit(m1.pr, idx, m1.cnt, m1.fo, m1.side);
@@ -1440,6 +1443,25 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
     }
   }
   if (!FF::DIRECT && lane == 0) bulk_wait0();  // staging must outlive the bulk reads
+}
+
+// Near rows of a combined mode-0 plan (the near pairs' S and J rows, the D rows; K of those
+// rows) in a launch of their own between the scan and the fill: latency-bound copies from the
+// side buffer plus the chain tails, one wave of 8-warp CTAs at up to 64 warps per SM (inside
+// the fill they ran as its first units at 16 warps per SM).
+// The chain tails (up to n entries per row, tr * inv[l]) read inv[] from a shared-memory copy
+// when it fits (NEAR_SMEM_INV doubles), not one dependent L2 load per entry.
+constexpr int NEAR_SMEM_INV = 8192;
+__global__ void __launch_bounds__(256) k_near0(const MatFill m0) {
+  extern __shared__ double sinv[];
+  const int n = m0.pr.n;
+  const double* inv = m0.pr.inv;
+  if (n <= NEAR_SMEM_INV) {
+    for (int l = threadIdx.x; l < n; l += blockDim.x) sinv[l] = __ldg(&m0.pr.inv[l]);
+    __syncthreads();
+    inv = sinv;
+  }
+  fill_near_unit_h(m0.pr, blockIdx.x, m0.cnt, m0.fo, m0.side, inv);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -2773,7 +2795,11 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
     pl->combined = p0.mode == 0 && (!pl->has_h1 || (p1.mode == 0 && p1.wK == 0 && p1.wL == 0 && p1.P == 0));
   }
   pl->launches_count = 1 + (pl->combined ? 1 : nmat) + 1;  // expand, count, scan
-  pl->launches_fill = pl->combined ? 1 : nmat;
+  {  // measured equal at c4 (k_near0 10.2 us + fill 53.2 us vs fill 61 us): off by default
+    const char* nf = getenv("SUNFOLD_NEAR_SEP");
+    pl->near_sep = pl->combined && (nf && nf[0] && nf[0] != '0');
+  }
+  pl->launches_fill = pl->combined ? 1 + pl->near_sep : nmat;
   if (pl->general) {
     pl->launches_count = (P > 0 ? sung::G_LAUNCHES_EXPAND : 1) + sung::G_LAUNCHES_COUNT * nmat + 1;
     pl->launches_fill = sung::G_LAUNCHES_FILL * nmat;
@@ -2797,6 +2823,11 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
       // no band kernels
     } else if (pl->combined) {
       e1 = dispatch_attr0(pl->pr[0], pl->has_h1 ? &pl->pr[1] : nullptr, pl->has_h1 ? 0 : -1, pl->fill_grid[0]);
+      static bool near_attr = false;  // k_near0's shared inv[] table: up to 64 KB
+      if (e1 == cudaSuccess && !near_attr) {
+        e1 = cudaFuncSetAttribute(k_near0, cudaFuncAttributeMaxDynamicSharedMemorySize, NEAR_SMEM_INV * (int)sizeof(double));
+        near_attr = e1 == cudaSuccess;
+      }
     } else {
       for (int which = 0; which < nmat && e1 == cudaSuccess; ++which) {
         if (pl->pr[which].mode == 0) e1 = dispatch_attr0(pl->pr[which], nullptr, -1, pl->fill_grid[which]);
@@ -2996,7 +3027,7 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
     FillOut fo = {Q->row_ptr, Q->col, Q->val, (long long)Q->nnz, which ? nullptr : K,
                   (const long long*)(ws + (which ? L.toff1 : L.toff0)), &hdr->nnz[which]};
     mf[which] = MatFill{pl->pr[which], (const int*)(ws + (which ? L.cnt1 : L.cnt0)), fo, pl->side[which],
-                        pl->n >= SUN_TILE_SYNC_MIN_N ? 1 : 0};
+                        pl->n >= SUN_TILE_SYNC_MIN_N ? 1 : 0, 0};
   }
   if (nmat == 1) mf[1] = mf[0];
   if (pl->general) {
@@ -3010,6 +3041,14 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
     return SUN_OK;
   }
   if (pl->combined) {
+    if (pl->near_sep) {
+      mf[0].near_sep = 1;
+      const Prob& p0 = pl->pr[0];
+      const long long nn0 = (2 * (p0.n * 2LL * p0.W + p0.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
+      const size_t sm = p0.n <= NEAR_SMEM_INV ? (size_t)p0.n * sizeof(double) : 0;
+      if (nn0 > 0) k_near0<<<(unsigned)nn0, 256, sm, st>>>(mf[0]);
+      CK(cudaGetLastError());
+    }
     CK(dispatch_fill0(mf[0], mf[1], pl->has_h1 ? 0 : -1, pl->fill_grid[0], st));
     return SUN_OK;
   }
