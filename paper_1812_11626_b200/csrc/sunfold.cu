@@ -866,7 +866,8 @@ __device__ __forceinline__ void fill_near_unit(const Prob& pr, long long j, cons
 constexpr int NEAR_RPW = SUN_NEAR_RPW;        // near rows per warp (lane groups of 32 / NEAR_RPW)
 constexpr int NEAR_GL = 32 / NEAR_RPW;        // lanes per row
 constexpr int NEAR_UROWS = 8 * NEAR_RPW;      // side rows per near unit
-// inv: the inv[l] table (global, or a shared-memory copy; generic loads).
+// inv: the inv[l] table (SMEM_INV: a shared-memory copy, else global through the read-only path).
+template <bool SMEM_INV>
 __device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, const int* __restrict__ cnt,
                                                  const FillOut& fo, const NearSide& side, const double* inv) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -919,10 +920,10 @@ __device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, co
   }
   const long long ot = o + nwin, limt = lim - nwin;
   const int dbase = (int)(2 * np - 1);
-#pragma unroll 8
+#pragma unroll 4
   for (int l = m.hi + 1 + hl; l <= m.lend; l += NEAR_GL) {
     const int k = l - m.hi - 1;
-    const double v = m.tr * inv[l];
+    const double v = m.tr * (SMEM_INV ? inv[l] : __ldg(&inv[l]));
     if (k < limt) {
       fo.col[ot + k] = dbase + l;
       fo.val[ot + k] = v;
@@ -1434,7 +1435,7 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
       if constexpr (Q1MERGED) fill_q1_chunk(prf1, m1.pr.npt, idx, m1.cnt, m1.fo, a, b);
     } else if (kind == 1) {
 #ifndef SUN_EXP_NO_NEAR
-      fill_near_unit_h(m0.pr, idx, m0.cnt, m0.fo, m0.side, m0.pr.inv);
+      fill_near_unit_h<false>(m0.pr, idx, m0.cnt, m0.fo, m0.side, m0.pr.inv);
 #endif
     } else if (kind == 2) {
       if constexpr (HAS1) fill_near_unit(m1.pr, idx, m1.cnt, m1.fo, m1.side);
@@ -1455,13 +1456,13 @@ constexpr int NEAR_SMEM_INV = 8192;
 __global__ void __launch_bounds__(256) k_near0(const MatFill m0) {
   extern __shared__ double sinv[];
   const int n = m0.pr.n;
-  const double* inv = m0.pr.inv;
   if (n <= NEAR_SMEM_INV) {
     for (int l = threadIdx.x; l < n; l += blockDim.x) sinv[l] = __ldg(&m0.pr.inv[l]);
     __syncthreads();
-    inv = sinv;
+    fill_near_unit_h<true>(m0.pr, blockIdx.x, m0.cnt, m0.fo, m0.side, sinv);
+  } else {
+    fill_near_unit_h<false>(m0.pr, blockIdx.x, m0.cnt, m0.fo, m0.side, m0.pr.inv);
   }
-  fill_near_unit_h(m0.pr, blockIdx.x, m0.cnt, m0.fo, m0.side, inv);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1493,6 +1494,7 @@ __global__ void __launch_bounds__(32) k_count2(const MatCount mc) {
   if (p < np && b - a > 2 * MC::W) {
     // the positions one by one with the fill's per-position expression (far_value_at)
     int nR = 0, nI = 0;
+#pragma unroll 4
     for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
       double x, y;
       int c, d;

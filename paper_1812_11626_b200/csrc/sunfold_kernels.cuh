@@ -865,24 +865,33 @@ __device__ __forceinline__ bool far_value_at(const Prob& pr, int a, int b, int k
   y = 0.0;
   if (ok) {
     const int adc = dc < 0 ? -dc : dc, add = dd < 0 ? -dd : dd;
+    // every load is issued before the first use: the K terms, then the dissipators four at a
+    // time (the accumulation order, p = 0, 1, ..., is the same whatever the batching)
+    const double2 kca = dd == 0 ? __ldg(&pr.K.v[(long long)c * SK + (WK - dc)]) : make_double2(0.0, 0.0);
+    const double2 kdb = dc == 0 ? __ldg(&pr.K.v[(long long)d * SK + (WK - dd)]) : make_double2(0.0, 0.0);
     if (PT != 0 && adc <= WL && add <= WL) {
       const double2* La = pr.L + (long long)a * SL + (dc + WL);
       const double2* Lb = pr.L + (long long)b * SL + (dd + WL);
       const long long ps = (long long)n * SL;
-      for (int p = 0; p < P; ++p) {
-        const double2 la = __ldg(La + p * ps), lb = __ldg(Lb + p * ps);
-        conj_mul_acc(x, y, la, lb);  // conj(Lt_p,ac) Lt_p,bd
+      for (int p0 = 0; p0 < P; p0 += 4) {
+        double2 la[4], lb[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          la[i] = p0 + i < P ? __ldg(La + (p0 + i) * ps) : make_double2(0.0, 0.0);
+          lb[i] = p0 + i < P ? __ldg(Lb + (p0 + i) * ps) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (p0 + i < P) conj_mul_acc(x, y, la[i], lb[i]);  // conj(Lt_p,ac) Lt_p,bd
       }
     }
     if (dd == 0) {  // + i K_ca
-      const double2 kv = __ldg(&pr.K.v[(long long)c * SK + (WK - dc)]);
-      x -= kv.y;
-      y += kv.x;
+      x -= kca.y;
+      y += kca.x;
     }
     if (dc == 0) {  // - i conj(K_db)
-      const double2 kv = __ldg(&pr.K.v[(long long)d * SK + (WK - dd)]);
-      x -= kv.y;
-      y -= kv.x;
+      x -= kdb.y;
+      y -= kdb.x;
     }
   }
   return ok;
