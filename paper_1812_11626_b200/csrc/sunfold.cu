@@ -171,6 +171,7 @@ struct PlanRes {
   cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
   cudaEvent_t done = nullptr;  // recorded after each readback into hpin (released plans wait on it)
   HeaderPrefix* hpin = nullptr;
+  HeaderPrefix* dpin = nullptr;  // device alias of hpin (mapped): the scan writes the header there
 };
 std::mutex g_res_mu;
 std::vector<PlanRes> g_res_free;
@@ -197,8 +198,12 @@ cudaError_t res_acquire(PlanRes& r) {
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&r.done, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&r.cap, cudaStreamNonBlocking);
-  if (e == cudaSuccess && cudaMallocHost(&r.hpin, sizeof(HeaderPrefix)) != cudaSuccess) {
-    r.hpin = nullptr;  // pageable fallback in sun_plan_nnz
+  if (e == cudaSuccess) {  // mapped pinned slot: the scan kernel stores the header prefix into it
+    if (cudaHostAlloc(&r.hpin, sizeof(HeaderPrefix), cudaHostAllocMapped) == cudaSuccess) {
+      if (cudaHostGetDevicePointer(&r.dpin, r.hpin, 0) != cudaSuccess) r.dpin = nullptr;
+    } else if (cudaMallocHost(&r.hpin, sizeof(HeaderPrefix)) != cudaSuccess) {
+      r.hpin = nullptr;  // pageable fallback in sun_plan_nnz
+    }
     (void)cudaGetLastError();
   }
   return e;
@@ -1781,6 +1786,8 @@ struct ScanArgs {
   long long* nnz[2];
   long long nslots[2];
   unsigned int* ticket;
+  const DevHeader* hdr;  // with hout: the header prefix is also stored in mapped host memory
+  HeaderPrefix* hout;    // (sun_plan_nnz then reads it after the stream; no copy node)
 };
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_chain(ScanArgs A) {
@@ -1846,7 +1853,22 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_chain(ScanArgs A) {
     }
     if (lane == 0) {
       prefix_s = prefix;
-      if (chunk == nchunks - 1 || nchunks == 0) *A.nnz[y] = prefix + total;
+      if (chunk == nchunks - 1 || nchunks == 0) {
+        *A.nnz[y] = prefix + total;
+        if (A.hout) A.hout->nnz[y] = prefix + total;
+      }
+      if (A.hout && y == 0 && chunk == 0) {  // the rest of the prefix is final (expand / count kernels)
+        const DevHeader* h = A.hdr;
+        A.hout->flags = h->flags;
+        A.hout->pad = 0;
+        A.hout->tau[0] = h->tau[0];
+        A.hout->tau[1] = h->tau[1];
+        A.hout->herm_dev[0] = h->herm_dev[0];
+        A.hout->herm_dev[1] = h->herm_dev[1];
+        A.hout->nrm2_h[0] = h->nrm2_h[0];
+        A.hout->nrm2_h[1] = h->nrm2_h[1];
+        if (gridDim.y == 1) A.hout->nnz[1] = 0;
+      }
     }
   }
   __syncthreads();
@@ -2896,6 +2918,8 @@ static int enqueue_count_general(sun_plan pl, cudaStream_t st) {
   }
   CK(join_aux(pl, st, nmat));
   sa.ticket = hdr->ticket;
+  sa.hdr = hdr;
+  sa.hout = pl->res.dpin;
   k_scan_chain<<<dim3((unsigned)maxchunks, nmat), SCAN_THREADS, 0, st>>>(sa);
   CK(cudaGetLastError());
   return SUN_OK;
@@ -2962,6 +2986,8 @@ static int enqueue_count(sun_plan pl, cudaStream_t st) {
   }
   if (nmat == 1) mc[1] = mc[0];
   sa.ticket = hdr->ticket;
+  sa.hdr = hdr;
+  sa.hout = pl->res.dpin;
   if (pl->combined) {
     CK(dispatch_count0(mc[0], mc[1], pl->has_h1 ? 0 : -1, st));
   } else {
@@ -3080,11 +3106,12 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
   // the nnz / flags readback of sun_plan_nnz rides in the same sequence (a memcpy node of the
   // graph into pinned host memory), so sun_plan_nnz only waits for the stream
   const bool readback = kind != 1 && pl->hpin;
+  const bool mapped = pl->res.dpin != nullptr;  // the scan stores the header into hpin itself
   auto direct = [&](cudaStream_t s) -> int {
     int rc = SUN_OK;
     if (kind != 1) rc = enqueue_count(pl, s);
     if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s);
-    if (rc == SUN_OK && readback) {
+    if (rc == SUN_OK && readback && !mapped) {
       const cudaError_t e =
           cudaMemcpyAsync(pl->hpin, pl->ws + pl->lay.hdr, sizeof(HeaderPrefix), cudaMemcpyDeviceToHost, s);
       if (e != cudaSuccess) rc = cuda_fail(e);
