@@ -46,6 +46,7 @@ constexpr int WARP_TP = 64;       // mode 1: pairs per tile
 constexpr int WARP_THREADS = 256;
 constexpr int FAR_MAXPOS = 1024;
 constexpr int EXP_THREADS = 256;  // k_expand rows (or K-band entries) per CTA
+constexpr int EXP_LSTAGE = 2048;  // k_expand: staged dissipator band values per K block (32 KB)
 constexpr int SCAN_THREADS = 1024, SCAN_IPT = 4, SCAN_TILE = SCAN_THREADS * SCAN_IPT;
 constexpr unsigned long long SCAN_A = 1ull << 62, SCAN_P = 2ull << 62, SCAN_V = (1ull << 62) - 1;
 
@@ -402,6 +403,7 @@ __global__ void __launch_bounds__(EXP_THREADS) k_expand(const ExpandArgs A) {
   __shared__ int sbw[EXP_THREADS / 32], sfl[EXP_THREADS / 32];
   __shared__ unsigned long long sh0[EXP_THREADS / 32], sh1[EXP_THREADS / 32];
   __shared__ int last;
+  __shared__ double2 A_ls[EXP_LSTAGE];
   if ((int)blockIdx.x < A.nA) {
     const int op = blockIdx.x / A.nrb, rb = blockIdx.x % A.nrb;
     double acc = 0.0;
@@ -462,6 +464,21 @@ __global__ void __launch_bounds__(EXP_THREADS) k_expand(const ExpandArgs A) {
     if (t < n) A.inv[t] = t > 0 ? 1.0 / sqrt((double)t * (double)(t + 1)) : 0.0;
     unsigned long long d0 = 0ull, d1 = 0ull;
     const int sw = 2 * A.wX + 1;
+    // the block's dissipator rows x in [x0, x0 + nx) as dense band rows in shared memory
+    // (Ls[(p nx + x - x0) SL + o] = L_p(x, x + o - wL)): every CSR lookup issued at once,
+    // instead of two dependent lookups per (p, x) in each K entry's loop
+    const int SLd = 2 * A.wL + 1;
+    const long long tb = (long long)(blockIdx.x - A.nA) * blockDim.x;
+    const int rf = (int)(tb / sw), rl = (int)min((long long)n - 1, (tb + blockDim.x - 1) / sw);
+    const int x0 = max(0, rf - A.wL), nx = min(n - 1, rl + A.wL) - x0 + 1;
+    const bool staged = A.P > 0 && (long long)A.P * nx * SLd <= EXP_LSTAGE;
+    if (staged) {
+      for (int e = threadIdx.x; e < A.P * nx * SLd; e += blockDim.x) {
+        const int p = e / (nx * SLd), f = e % (nx * SLd), x = x0 + f / SLd, cc = x + f % SLd - A.wL;
+        A_ls[e] = (cc >= 0 && cc < n) ? csr_get_band(ops.op[2 + p], x, cc, A.wL) : make_double2(0.0, 0.0);
+      }
+    }
+    __syncthreads();
     if (t < (long long)n * sw) {
       const int r = (int)(t / sw), o = (int)(t % sw) - A.wX;
       const int c = r + o;
@@ -477,7 +494,15 @@ __global__ void __launch_bounds__(EXP_THREADS) k_expand(const ExpandArgs A) {
             const OpDesc L = ops.op[2 + p];
             double px = 0.0, py = 0.0;
             for (int x = lo; x <= hi; ++x) {
-              const double2 a = csr_get_band(L, x, r, A.wL), b = csr_get_band(L, x, c, A.wL);  // conj(L_xr) L_xc
+              double2 a, b;  // conj(L_xr) L_xc
+              if (staged) {
+                const double2* row = A_ls + ((long long)p * nx + (x - x0)) * SLd - x + A.wL;
+                a = row[r];
+                b = row[c];
+              } else {
+                a = csr_get_band(L, x, r, A.wL);
+                b = csr_get_band(L, x, c, A.wL);
+              }
               px += a.x * b.x + a.y * b.y;
               py += a.x * b.y - a.y * b.x;
             }
@@ -1362,7 +1387,23 @@ struct MatFill {
   NearSide side;
   int tile_sync;  // keep a CTA's warps on the same far tile (large outputs; see k_fill0)
   int near_sep;   // the near rows are written by k_near0 (launched before the fill), not by its units
+  const DevHeader* hdr;  // with hout (sun_run of modes 0 / 2): CTA 0 stores the header prefix into
+  HeaderPrefix* hout;    // mapped host memory at the start of the fill (final since the scan)
 };
+
+// header prefix -> mapped pinned host memory (sun_plan_nnz reads it after the stream)
+__device__ __forceinline__ void store_header(const DevHeader* h, HeaderPrefix* o, int has1) {
+  o->flags = h->flags;
+  o->pad = 0;
+  o->nnz[0] = h->nnz[0];
+  o->nnz[1] = has1 ? h->nnz[1] : 0;
+  o->tau[0] = h->tau[0];
+  o->tau[1] = h->tau[1];
+  o->herm_dev[0] = h->herm_dev[0];
+  o->herm_dev[1] = h->herm_dev[1];
+  o->nrm2_h[0] = h->nrm2_h[0];
+  o->nrm2_h[1] = h->nrm2_h[1];
+}
 
 // Fill pass of Q0 and, with Q1W >= 0, of Q1 (widths Q1W, 0, no dissipators; staging-free
 // rows only, i.e. Q1W = 0) in one persistent launch: units u = blockIdx.x + k gridDim.x over
@@ -1378,6 +1419,7 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     m0.fo.row_ptr[m0.pr.m] = *m0.fo.nnz;
     if (HAS1) m1.fo.row_ptr[m1.pr.m] = *m1.fo.nnz;
+    if (m0.hout) store_header(m0.hdr, m0.hout, HAS1);
   }
   // near units: NEAR_UNIT_ROWS side rows each (2 per near item)
   const long long nn0 = m0.near_sep ? 0 : (2 * (m0.pr.n * 2LL * m0.pr.W + m0.pr.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
@@ -1562,7 +1604,10 @@ template <int WK, int WL, int PT>
 __global__ void __launch_bounds__(256) k_fill2(const MatFill mf) {
   __shared__ NearRowP nrows[8][NEAR_WARP_ROWS];
   const Prob& p0 = mf.pr;
-  if (blockIdx.x == 0 && threadIdx.x == 0) mf.fo.row_ptr[p0.m] = *mf.fo.nnz;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    mf.fo.row_ptr[p0.m] = *mf.fo.nnz;
+    if (mf.hout) store_header(mf.hdr, mf.hout, 0);
+  }
   Prob pr = p0;
   pr.tau = *p0.tau_ptr;
   const long long nn = near_units(p0.n, p0.W);
@@ -2879,7 +2924,7 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
   return SUN_OK;
 }
 
-static int enqueue_count_general(sun_plan pl, cudaStream_t st) {
+static int enqueue_count_general(sun_plan pl, cudaStream_t st, bool scan_hdr) {
   const Layout& L = pl->lay;
   char* ws = pl->ws;
   DevHeader* hdr = (DevHeader*)(ws + L.hdr);
@@ -2919,15 +2964,17 @@ static int enqueue_count_general(sun_plan pl, cudaStream_t st) {
   CK(join_aux(pl, st, nmat));
   sa.ticket = hdr->ticket;
   sa.hdr = hdr;
-  sa.hout = pl->res.dpin;
+  sa.hout = scan_hdr ? pl->res.dpin : nullptr;
   k_scan_chain<<<dim3((unsigned)maxchunks, nmat), SCAN_THREADS, 0, st>>>(sa);
   CK(cudaGetLastError());
   return SUN_OK;
 }
 
-static int enqueue_count(sun_plan pl, cudaStream_t st) {
+// scan_hdr: the scan stores the header prefix into the mapped slot (else the fill does: see
+// header_in_fill)
+static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr) {
   NvtxRange r_("sunfold: expand (a1) + count (a3) + scan (a4)");
-  if (pl->general) return enqueue_count_general(pl, st);
+  if (pl->general) return enqueue_count_general(pl, st, scan_hdr);
   const Layout& L = pl->lay;
   const int n = pl->n;
   char* ws = pl->ws;
@@ -2987,7 +3034,7 @@ static int enqueue_count(sun_plan pl, cudaStream_t st) {
   if (nmat == 1) mc[1] = mc[0];
   sa.ticket = hdr->ticket;
   sa.hdr = hdr;
-  sa.hout = pl->res.dpin;
+  sa.hout = scan_hdr ? pl->res.dpin : nullptr;
   if (pl->combined) {
     CK(dispatch_count0(mc[0], mc[1], pl->has_h1 ? 0 : -1, st));
   } else {
@@ -3043,7 +3090,12 @@ int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
   return SUN_OK;
 }
 
-static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st) {
+// sun_run on a mode-0 / mode-2 plan with a mapped header slot: the fill kernel stores the header
+static bool header_in_fill(sun_plan pl) {
+  return pl->res.dpin && !pl->general && (pl->combined || (!pl->has_h1 && pl->pr[0].mode == 2));
+}
+
+static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st, bool fill_hdr) {
   NvtxRange r_("sunfold: fill (a5) + K + Q1 (a6)");
   const Layout& L = pl->lay;
   char* ws = pl->ws;
@@ -3056,6 +3108,10 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
                   (const long long*)(ws + (which ? L.toff1 : L.toff0)), &hdr->nnz[which]};
     mf[which] = MatFill{pl->pr[which], (const int*)(ws + (which ? L.cnt1 : L.cnt0)), fo, pl->side[which],
                         pl->n >= SUN_TILE_SYNC_MIN_N ? 1 : 0, 0};
+  }
+  if (fill_hdr) {
+    mf[0].hdr = hdr;
+    mf[0].hout = pl->res.dpin;
   }
   if (nmat == 1) mf[1] = mf[0];
   if (pl->general) {
@@ -3109,8 +3165,9 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
   const bool mapped = pl->res.dpin != nullptr;  // the scan stores the header into hpin itself
   auto direct = [&](cudaStream_t s) -> int {
     int rc = SUN_OK;
-    if (kind != 1) rc = enqueue_count(pl, s);
-    if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s);
+    const bool fill_hdr = kind == 2 && header_in_fill(pl);
+    if (kind != 1) rc = enqueue_count(pl, s, !fill_hdr);
+    if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s, fill_hdr);
     if (rc == SUN_OK && readback && !mapped) {
       const cudaError_t e =
           cudaMemcpyAsync(pl->hpin, pl->ws + pl->lay.hdr, sizeof(HeaderPrefix), cudaMemcpyDeviceToHost, s);
