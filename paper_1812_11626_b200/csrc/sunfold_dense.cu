@@ -187,7 +187,12 @@ __global__ void __launch_bounds__(DT, 2) k_dense_expand(const DenseArgs g) {
   const int nt = (n + TW - 1) / TW;
   const int hi = lane >> 4, lo = lane & 15;
   int cnt = 0;
-  for (int tb = 0; tb < nt; ++tb) {
+  // Only the half b <= a of Z is stored (Z[b][a][c][d] = conj(Z[a][b][d][c]) for Hermitian A,
+  // see k_dense_project; the plane b = a feeds G and the D rows): Z[b][x][.][.] for b <= x,
+  // Z[b][y][.][.] for b <= y.  A tile with b0 > y (so every b, d > y) has no output and is not
+  // read: its A entries reach Q through the conjugate entries of the rows (b, d) (A Hermitian).
+  const int tmax = y / TW + 1;  // tiles with b0 <= y
+  for (int tb = 0; tb < tmax; ++tb) {
     for (int td = tb; td < nt; ++td) {
       if (!WP && cnt++ % WPC != wid) continue;  // warp-uniform
       const int b0 = tb * TW, d0 = td * TW;
@@ -221,8 +226,8 @@ __global__ void __launch_bounds__(DT, 2) k_dense_expand(const DenseArgs g) {
               T.a[i][j] = jcomb(vS, vJ, true);   // Y[(x,y),(b,d)] -> Z[d][x][y][b]
               T.b[i][j] = jcomb(vS, vJ, false);  // Y[(y,x),(b,d)] -> Z[d][y][x][b]
             }
-            zxy[b * n3 + d] = jcomb(uS, uJ, true);
-            zyx[b * n3 + d] = jcomb(uS, uJ, false);
+            if (b <= x) zxy[b * n3 + d] = jcomb(uS, uJ, true);
+            if (b <= y) zyx[b * n3 + d] = jcomb(uS, uJ, false);
           }
         }
       }
@@ -232,8 +237,8 @@ __global__ void __launch_bounds__(DT, 2) k_dense_expand(const DenseArgs g) {
         const int i = 2 * k + hi, j = lo;  // row d = d0 + i, column b = b0 + j
         const int d = d0 + i, b = b0 + j;
         if (b < n && d < n && d > b) {
-          zxy[(long long)d * n3 + b] = T.a[j][i];
-          zyx[(long long)d * n3 + b] = T.b[j][i];
+          if (d <= x) zxy[(long long)d * n3 + b] = T.a[j][i];
+          if (d <= y) zyx[(long long)d * n3 + b] = T.b[j][i];
         }
       }
       __syncwarp();
@@ -323,8 +328,10 @@ __global__ void __launch_bounds__(DT, 2) k_dense_project(const DenseArgs g) {
   pair_of(n, p, x, y);
   const bool has_a = g.A != nullptr;
   const double2* Z = g.Z + (long long)r * n2 * n2;
+  // Row (b,a) = (x,y) of Z' only: L preserves Hermiticity (H and A Hermitian), so
+  // S[(ab),(cd)] = conj(S[(ba),(dc)]), i.e. Z'[y][x][c][d] = conj(Z'[x][y][d][c]); the row (y,x)
+  // is the conjugate transpose of the row (x,y) (and the expand stores only Z[b][a], b <= a).
   const double2* zxy = Z + ((long long)x * n + y) * n2;  // row (b,a) = (x,y)
-  const double2* zyx = Z + ((long long)y * n + x) * n2;  // row (b,a) = (y,x)
   const double2* kh = g.Kh + (long long)r * n2;
   double* qS = g.Q + (long long)(g.r0 + r) * m * m + p * m;
   double* qJ = qS + np * m;
@@ -335,42 +342,38 @@ __global__ void __launch_bounds__(DT, 2) k_dense_project(const DenseArgs g) {
     for (int tw = tu; tw < nt; ++tw) {
       if (!WP && cnt++ % WPC != wid) continue;  // warp-uniform
       const int u0 = tu * TW, w0 = tw * TW;
-      {  // stage the transposed blocks: all loads first
-        double2 za[8], zb[8];
+      {  // stage the transposed block Z'_xy[w][u]: all loads first
+        double2 za[8];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int i = 2 * k + hi, j = lo;  // row w = w0 + i, column u = u0 + j
           const bool ok = has_a && w0 + i < n && u0 + j < n;
           const long long o = ok ? (long long)(w0 + i) * n + (u0 + j) : 0;
           za[k] = ok ? __ldg(zxy + o) : make_double2(0.0, 0.0);
-          zb[k] = ok ? __ldg(zyx + o) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int i = 2 * k + hi, j = lo;
-          if (w0 + i < n && u0 + j < n) {
-            T.a[i][j] = zdelta(za[k], kh, n, x, y, w0 + i, u0 + j);
-            T.b[i][j] = zdelta(zb[k], kh, n, y, x, w0 + i, u0 + j);
-          }
+          if (w0 + i < n && u0 + j < n) T.a[i][j] = zdelta(za[k], kh, n, x, y, w0 + i, u0 + j);
         }
       }
       __syncwarp();
-      double2 za[8], zb[8];
+      double2 za[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {  // direct blocks: all loads first
+      for (int k = 0; k < 8; ++k) {  // direct block Z'_xy[u][w]: all loads first
         const int u = u0 + 2 * k + hi, w = w0 + lo;
         const bool ok = has_a && u < w && w < n;
         const long long o = ok ? (long long)u * n + w : 0;
         za[k] = ok ? __ldg(zxy + o) : make_double2(0.0, 0.0);
-        zb[k] = ok ? __ldg(zyx + o) : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int k = 0; k < TW / 2; ++k) {
         const int i = 2 * k + hi, j = lo;  // u = u0 + i, w = w0 + j
         const int u = u0 + i, w = w0 + j;
         if (u < w && w < n) {
-          const double2 a1 = zdelta(za[k], kh, n, x, y, u, w), b1 = zdelta(zb[k], kh, n, y, x, u, w);
-          const double2 a2 = T.a[j][i], b2 = T.b[j][i];
+          // a = Z'_xy, b = Z'_yx: b1 = Z'_yx[u][w] = conj(Z'_xy[w][u]), b2 = Z'_yx[w][u] = conj(Z'_xy[u][w])
+          const double2 a1 = zdelta(za[k], kh, n, x, y, u, w), a2 = T.a[j][i];
+          const double2 b1 = make_double2(a2.x, -a2.y), b2 = make_double2(a1.x, -a1.y);
           // V_S at (u,w), (w,u) and V_J at (u,w), (w,u)
           const double2 s1 = cscale(cadd(a1, b1), RS2), s2 = cscale(cadd(a2, b2), RS2);
           const double2 j1 = cscale(cadd(cmulmi(a1), cmuli(b1)), RS2), j2 = cscale(cadd(cmulmi(a2), cmuli(b2)), RS2);
@@ -386,9 +389,9 @@ __global__ void __launch_bounds__(DT, 2) k_dense_project(const DenseArgs g) {
     }
   }
   for (int c = WP ? lane : (int)threadIdx.x; c < n; c += WP ? 32 : DT) {
-    const double2 a = zprime(zxy, kh, n, has_a, x, y, c, c), b = zprime(zyx, kh, n, has_a, y, x, c, c);
-    sv[c] = (a.x + b.x) * RS2;            // Re V_S[c,c]
-    sv[n + c] = (a.y - b.y) * RS2;        // Re V_J[c,c] = Re((-i a + i b)/sqrt2)
+    const double2 a = zprime(zxy, kh, n, has_a, x, y, c, c);  // Z'_yx[c][c] = conj(a)
+    sv[c] = (a.x + a.x) * RS2;            // Re V_S[c,c] = Re(a + conj a)/sqrt2
+    sv[n + c] = (a.y + a.y) * RS2;        // Re V_J[c,c] = Re((-i a + i conj a)/sqrt2)
   }
   __shared__ double tot_all[WPC][2];
   double* tot = tot_all[WP ? wid : 0];
