@@ -596,7 +596,8 @@ def main():
               "roofline": {"bound": "hbm", "achieved": alg3 / t3 / 1e9, "peak": peak, "unit": "GB/s",
                            "frac": alg3 / t3 / 1e9 / peak, "algorithmic_bytes_per_realisation": alg3 // b3,
                            "note": "algorithmic = A, H read + Q, K written; the two-pass design also writes "
-                                   "and reads the realigned superoperator Z (16 N^4 B each way)"},
+                                   "and reads half of the realigned superoperator Z (8 N^4 B each way; "
+                                   "Hermiticity gives the other half)"},
               "gpu_launches": int(sun.lib().sun_dense_launches(n3, b3, 1, nb3)),
               "kernels": "k_dense_expand, k_dense_project (+ 5 O(N^3) D-row kernels)"}
         del H3, A3, Q3, K3, w3
