@@ -1153,7 +1153,7 @@ __device__ __forceinline__ TileIn load_tile_in(long long np, long long npt, long
 
 template <int WK, int WL, int PT>
 __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, long long t, const TileIn& ti,
-                                              const FillOut& fo, int* scol, double* sval, int& a_out, int& b_out) {
+                                              const FillOut& fo, int* scol, double* sval) {
   using MC = Mode0<WK, WL>;
   using FF = FillFar<WK, WL>;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1165,8 +1165,6 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
   const int exS = warp_excl_scan(cS, totS), exJ = warp_excl_scan(cJ, totJ);
   int a, b;
   warp_pairs(pr.n, t * TP0 + wid * 32, a, b);
-  a_out = a;
-  b_out = b;
   const bool far = valid && (b - a > 2 * MC::W);
   const bool nearp = valid && !far;
   const long long baseS = ti.baseS, baseJ = ti.baseJ;
@@ -1343,9 +1341,8 @@ __device__ __forceinline__ void fill_direct_tile(const FarCtx& pr, long long npt
 // Q1 rows of the warp's 32 pairs of Q0 far tile t (combined fill, Q1 = Q_H[diagonal H1], all
 // pairs "far" at width 0, rows of <= 2 entries): Q1's scan slot t covers the same 256 pairs,
 // so the warp's offset is the slot offset plus the counts of the tile's earlier warps.
-// (a, b): this lane's pair (the Q0 far tile's own decode).
 __device__ __forceinline__ void fill_q1_chunk(const FarCtx& f1, long long npt1, long long t, const int* __restrict__ cnt1,
-                                              const FillOut& fo, int a, int b) {
+                                              const FillOut& fo) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long np = f1.np;
   const long long p = t * TP0 + threadIdx.x;
@@ -1361,6 +1358,8 @@ __device__ __forceinline__ void fill_q1_chunk(const FarCtx& f1, long long npt1, 
   for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(FULL, before, o);
   int tot;
   const int ex = warp_excl_scan(c, tot);
+  int a, b;  // decoded again (cheaper than keeping the far tile's pair live across its staging)
+  warp_pairs(f1.n, t * TP0 + wid * 32, a, b);
   if (!valid) return;
   const long long rS = fo.toff[t] + before + ex, rJ = fo.toff[npt1 + t] + before + ex;
   fo.row_ptr[p] = rS;
@@ -1474,12 +1473,11 @@ __global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFil
       // writing one contiguous ~110 KB region together (DRAM write locality; measured at
       // N = 4000-8000: +14-24 %).  Outputs that stay in L2 are faster without it (N = 1000: -3 %).
       if (m0.tile_sync) __syncthreads();
-      int a = 0, b = 0;
       if constexpr (FF::DIRECT)
         fill_direct_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, m0.cnt, m0.fo);
       else
-        fill_far_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, cur, m0.fo, scol, sval, a, b);
-      if constexpr (Q1MERGED) fill_q1_chunk(prf1, m1.pr.npt, idx, m1.cnt, m1.fo, a, b);
+        fill_far_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, cur, m0.fo, scol, sval);
+      if constexpr (Q1MERGED) fill_q1_chunk(prf1, m1.pr.npt, idx, m1.cnt, m1.fo);
     } else if (kind == 1) {
 #ifndef SUN_EXP_NO_NEAR
       fill_near_unit_h<false>(m0.pr, idx, m0.cnt, m0.fo, m0.side, m0.pr.inv);

@@ -67,8 +67,8 @@ struct Prob {
 // kernel it is inlined into) performs the identical operations and the passes take identical
 // tau decisions.
 __device__ __forceinline__ void conj_mul_acc(double& x, double& y, const double2 la, const double2 lb) {
-  x = __dadd_rn(x, __fma_rn(la.x, lb.x, __dmul_rn(la.y, lb.y)));
-  y = __dadd_rn(y, __fma_rn(la.x, lb.y, -__dmul_rn(la.y, lb.x)));
+  x = __fma_rn(la.x, lb.x, __fma_rn(la.y, lb.y, x));   // two fused operations per component
+  y = __fma_rn(la.x, lb.y, __fma_rn(-la.y, lb.x, y));
 }
 
 __device__ __forceinline__ double2 bget(const Band B, int r, int c) {
