@@ -1544,8 +1544,8 @@ __global__ void __launch_bounds__(32) k_count2(const MatCount mc) {
   if (p < np && b - a > 2 * MC::W) {
     // the positions one by one with the fill's per-position expression (far_value_at)
     int nR = 0, nI = 0;
-#pragma unroll 4
-    for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
+#pragma unroll
+    for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {  // compile-time positions (decode folded away)
       double x, y;
       int c, d;
       if (far_value_at<WK, WL, PT>(pr, a, b, k, x, y, c, d)) {
