@@ -732,9 +732,9 @@ __device__ __forceinline__ void count_far_slot(const FarCtx& pr, long long npt, 
     if (far) {
       double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
       far_values<WK, WL, PT>(pr, a, b, ux, uy);
-      unsigned mr, mi;
+      typename FarT<WK, WL>::Mask mr, mi;
       far_masks<WK, WL>(pr.n, pr.tau, a, b, ux, uy, mr, mi);
-      const int cp = __popc(mr) + __popc(mi);
+      const int cp = mpopc(mr) + mpopc(mi);
       cnt[p] = cp;
       cnt[np + p] = cp;
       c += cp;
@@ -1132,6 +1132,9 @@ struct FillFar {
   static constexpr int VALW = DIRECT ? 0 : (CAPW + 2 + 1) & ~1;  // fp64 slots (+ pad)
   static constexpr int BYTES_PER_WARP = COLW * 4 + VALW * 8;
   static constexpr int SMEM = 8 * BYTES_PER_WARP;
+  // resident fill CTAs per SM: 2 (16 warps) while the staging fits twice; wide bands (e.g. 33
+  // positions: 203 KB of staging) run one CTA per SM with the whole register file per thread
+  static constexpr int MINB = SMEM <= 112 * 1024 ? 2 : 1;
 };
 
 // Far tile t (256 pairs, thread per pair): row_ptr of all the tile's rows, K of its pairs;
@@ -1185,8 +1188,8 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
   return;
 #endif
   double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
-  int q[FarT<WK, WL>::NPOS];
-  unsigned mr = 0u, mi = 0u;
+  int qb[2 * WK + 1];
+  typename FarT<WK, WL>::Mask mr = 0u, mi = 0u;
   if (far) {
 #ifdef SUN_EXP_NO_COMPUTE
 #pragma unroll
@@ -1198,7 +1201,7 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
     far_values<WK, WL, PT>(pr, a, b, ux, uy);
 #endif
     far_masks<WK, WL>(pr.n, pr.tau, a, b, ux, uy, mr, mi);
-    far_cols<WK, WL>(pr.n, a, b, q);
+    far_colbase<WK>(pr.n, a, b, qb);
   }
   const unsigned nearmask = __ballot_sync(FULL, nearp);
   if constexpr (FF::DIRECT) {
@@ -1209,13 +1212,13 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
 #pragma unroll
       for (int row = 0; row < 2; ++row) {
         const long long o = (row ? baseJ + exJ : baseS + exS);
-        const unsigned m1 = row ? mi : mr, m2 = row ? mr : mi;
-        int o1 = 0, o2 = __popc(m1);
-#pragma unroll
-        for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
-          if ((m1 >> k) & 1u) seg.emit(o + o1++, q[k], row ? uy[k] : ux[k]);
-          if ((m2 >> k) & 1u) seg.emit(o + o2++, (int)np + q[k], row ? ux[k] : -uy[k]);
-        }
+        const auto m1 = row ? mi : mr, m2 = row ? mr : mi;
+        int o1 = 0, o2 = mpopc(m1);
+        far_foreach<WK, WL>([&](int k, int dc, int dd) {
+          const int qk = qb[dc + WK] + dd;
+          if ((m1 >> k) & 1u) seg.emit(o + o1++, qk, row ? uy[k] : ux[k]);
+          if ((m2 >> k) & 1u) seg.emit(o + o2++, (int)np + qk, row ? ux[k] : -uy[k]);
+        });
       }
     }
   } else {
@@ -1239,7 +1242,7 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
         hb = warp_excl_scan(nearp ? c_me : 0, ht);
       }
 #ifndef SUN_EXP_NO_STAGE
-      if (far) far_stage_row<WK, WL, row>((int)np, q, ux, uy, mr, mi, scol + pc, sval + pv, ex_me - w0 - hb);
+      if (far) far_stage_row<WK, WL, row>((int)np, qb, ux, uy, mr, mi, scol + pc, sval + pv, ex_me - w0 - hb);
 #endif
 #ifndef SUN_EXP_NO_FENCE
       if (bulk) fence_async_smem();  // make the staged entries visible to the async (TMA) proxy
@@ -1414,7 +1417,7 @@ __device__ __forceinline__ void store_header(const DevHeader* h, HeaderPrefix* o
 //   [Q0 near units][Q0 far tiles, last first][Q1 near][Q1 tiles]
 // The next far tile's counts and offsets are loaded before the current unit runs.
 template <int WK, int WL, int PT, int Q1W>
-__global__ void __launch_bounds__(256, 2) k_fill0(const MatFill m0, const MatFill m1) {
+__global__ void __launch_bounds__(256, FillFar<WK, WL>::MINB) k_fill0(const MatFill m0, const MatFill m1) {
   using FF = FillFar<WK, WL>;
   static_assert(Q1W <= 0, "combined fill: Q1 rows must be staging-free");
   extern __shared__ __align__(128) unsigned char dyn[];
@@ -2414,12 +2417,17 @@ void build_far_positions(int W, int wL, int wK, std::vector<int>& dc, std::vecto
 #define SUN_MODE0_LIST(X)                                        \
   X(0, 0, 0) X(1, 0, 0) X(2, 0, 0) X(3, 0, 0)                    \
   X(0, 0, 1) X(1, 0, 1) X(2, 0, 1) X(3, 0, 1) X(2, 1, 1)         \
-  X(0, 0, -1) X(1, 0, -1) X(2, 0, -1) X(3, 0, -1) X(2, 1, -1)
+  X(0, 0, -1) X(1, 0, -1) X(2, 0, -1) X(3, 0, -1) X(2, 1, -1)    \
+  X(4, 2, 1) X(4, 2, -1)
 
 int mode0_pt(int P) { return P == 0 ? 0 : (P == 1 ? 1 : -1); }
 
 bool mode0_supported(int wK, int wL, int P) {
   const int pt = mode0_pt(P);
+  if (wK == 4 && wL == 2) {  // A/B against the warp-per-pair mode 2 (SUNFOLD_MODE2=1)
+    const char* m2 = getenv("SUNFOLD_MODE2");
+    if (m2 && m2[0] && m2[0] != '0') return false;
+  }
 #define SUN_X(WK, WL, PT) \
   if (wK == WK && wL == WL && pt == PT) return true;
   SUN_MODE0_LIST(SUN_X)
@@ -2870,9 +2878,12 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
     pl->combined = p0.mode == 0 && (!pl->has_h1 || (p1.mode == 0 && p1.wK == 0 && p1.wL == 0 && p1.P == 0));
   }
   pl->launches_count = 1 + (pl->combined ? 1 : nmat) + 1;  // expand, count, scan
-  {  // measured equal at c4 (k_near0 10.2 us + fill 53.2 us vs fill 61 us): off by default
+  {  // measured equal at c4 (k_near0 10.2 us + fill 53.2 us vs fill 61 us): off by default there;
+     // on for wide bands, whose fill runs one CTA (8 warps) per SM (c3: near units inside the
+     // fill 98 us, k_near0 12 us + fill 78 us)
     const char* nf = getenv("SUNFOLD_NEAR_SEP");
-    pl->near_sep = pl->combined && (nf && nf[0] && nf[0] != '0');
+    const bool dflt = pl->pr[0].W >= 4;
+    pl->near_sep = pl->combined && (nf && nf[0] ? nf[0] != '0' : dflt);
   }
   pl->launches_fill = pl->combined ? 1 + pl->near_sep : nmat;
   if (pl->general) {

@@ -36,6 +36,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace sunk {
 
 constexpr int WMAX = 15;               // max(wK, wL) supported by the banded kernels
@@ -576,6 +578,9 @@ __device__ __forceinline__ int warp_d_row(const Prob& pr, int lam, double* g, do
 }
 
 // ---------------------------------------------------------------------------------------
+#ifndef SUN_PB_WIDE
+#define SUN_PB_WIDE 1  // far_values, runtime P, wL >= 1: dissipators whose band rows are loaded together (2: spills, c3 fill 96 -> 102 us)
+#endif
 // Far pair (b - a > 2W) with compile-time half-bandwidths (WK >= WL), thread per pair: the
 // band values the pair needs are loaded up front (independent loads) and the NPOS values of
 // U = L^+(E_ab) stay in registers.  Far positions, in lexicographic (dc, dd) order, which is
@@ -586,7 +591,12 @@ template <int WK, int WL>
 struct FarT {
   static_assert(WK >= WL, "far-pair kernels need wK >= wL");
   static constexpr int NPOS = (2 * WK + 1) + 2 * WL * (2 * WL + 1) + 2 * (WK - WL);
+  static_assert(NPOS <= 64, "mask width");
+  // kept-position bit masks: 32 bits, or 64 for wide bands (e.g. (wK, wL) = (4, 2): 33 positions)
+  using Mask = typename std::conditional<(NPOS > 32), unsigned long long, unsigned>::type;
 };
+__device__ __forceinline__ int mpopc(unsigned m) { return __popc(m); }
+__device__ __forceinline__ int mpopc(unsigned long long m) { return __popcll(m); }
 
 template <int WK, int WL, class F>
 __device__ __forceinline__ void far_foreach(F&& f) {
@@ -637,9 +647,8 @@ __device__ __forceinline__ void far_values(const FarCtx& pr, int a, int b, doubl
   for (int i = 0; i < SL; ++i)
 #pragma unroll
     for (int j = 0; j < SL; ++j) ox[i][j] = oy[i][j] = 0.0;
-  if constexpr (PT != 0) {
-    const int np_ = PT < 0 ? pr.P : PT;
-    for (int p = 0; p < np_; ++p) {
+  if constexpr (PT > 0) {
+    for (int p = 0; p < PT; ++p) {
       const double2* La = pr.L + ((long long)p * n + a) * SL;
       const double2* Lb = pr.L + ((long long)p * n + b) * SL;
       double2 la[SL], lb[SL];
@@ -654,6 +663,34 @@ __device__ __forceinline__ void far_values(const FarCtx& pr, int a, int b, doubl
         for (int j = 0; j < SL; ++j) {
           conj_mul_acc(ox[i][j], oy[i][j], la[i], lb[j]);
         }
+    }
+  } else if constexpr (PT < 0) {
+    // runtime P: the band rows of PB dissipators are loaded together before their first use
+    // (one L2 round trip per PB dissipators instead of one per dissipator); the accumulation
+    // order p = 0, 1, ... is unchanged, so every value is bitwise the same
+    constexpr int PB = SL == 1 ? 8 : SUN_PB_WIDE;
+    const long long ps = (long long)n * SL;
+    const double2* La = pr.L + (long long)a * SL;
+    const double2* Lb = pr.L + (long long)b * SL;
+    for (int p0 = 0; p0 < pr.P; p0 += PB) {
+      double2 la[PB][SL], lb[PB][SL];
+#pragma unroll
+      for (int u = 0; u < PB; ++u)
+#pragma unroll
+        for (int i = 0; i < SL; ++i) {
+          const bool in = p0 + u < pr.P;
+          la[u][i] = in ? __ldg(La + (p0 + u) * ps + i) : make_double2(0.0, 0.0);
+          lb[u][i] = in ? __ldg(Lb + (p0 + u) * ps + i) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+      for (int u = 0; u < PB; ++u) {
+        if (p0 + u < pr.P) {
+#pragma unroll
+          for (int i = 0; i < SL; ++i)
+#pragma unroll
+            for (int j = 0; j < SL; ++j) conj_mul_acc(ox[i][j], oy[i][j], la[u][i], lb[u][j]);
+        }
+      }
     }
   }
   far_foreach<WK, WL>([&](int k, int dc, int dd) {
@@ -679,13 +716,14 @@ __device__ __forceinline__ void far_values(const FarCtx& pr, int a, int b, doubl
 // kept bits of the far positions: bit k of mr (Re U) / mi (Im U), |.| > tau and in range
 template <int WK, int WL>
 __device__ __forceinline__ void far_masks(int n, double tau, int a, int b, const double (&ux)[FarT<WK, WL>::NPOS],
-                                          const double (&uy)[FarT<WK, WL>::NPOS], unsigned& mr, unsigned& mi) {
-  static_assert(FarT<WK, WL>::NPOS <= 32, "mask width");
-  unsigned r = 0u, i = 0u;
+                                          const double (&uy)[FarT<WK, WL>::NPOS], typename FarT<WK, WL>::Mask& mr,
+                                          typename FarT<WK, WL>::Mask& mi) {
+  using M = typename FarT<WK, WL>::Mask;
+  M r = 0u, i = 0u;
   far_foreach<WK, WL>([&](int k, int dc, int dd) {
     const bool ok = (dc >= 0 || a + dc >= 0) && (dd <= 0 || b + dd < n);
-    r |= (unsigned)(ok && fabs(ux[k]) > tau) << k;
-    i |= (unsigned)(ok && fabs(uy[k]) > tau) << k;
+    r |= (M)(ok && fabs(ux[k]) > tau) << k;
+    i |= (M)(ok && fabs(uy[k]) > tau) << k;
   });
   mr = r;
   mi = i;
@@ -700,6 +738,17 @@ __device__ __forceinline__ void far_cols(int n, int a, int b, int (&q)[FarT<WK, 
     const int c = a + dc < 0 ? 0 : a + dc;
     q[k] = dc == 0 ? q0 + dd : pidx32(n, c, b + dd);
   });
+}
+
+// column bases of the far positions: q(a + dc, b + dd) = qb[dc + WK] + dd (p(c, d) is linear in d;
+// 2 WK + 1 registers instead of NPOS)
+template <int WK>
+__device__ __forceinline__ void far_colbase(int n, int a, int b, int (&qb)[2 * WK + 1]) {
+#pragma unroll
+  for (int dc = -WK; dc <= WK; ++dc) {
+    const int c = a + dc < 0 ? 0 : a + dc;  // rows c < 0 are masked out
+    qb[dc + WK] = pidx32(n, c, b);
+  }
 }
 
 // Predicated shared stores of one staged entry (col, val) at 32-bit shared addresses; the
@@ -718,23 +767,23 @@ __device__ __forceinline__ void sts_entry(unsigned keep, unsigned& pc, unsigned&
 // Two running pointers (first and second half of the row), one predicated store pair per
 // position and half; the masks are consumed bit by bit.
 template <int WK, int WL, int ROW>
-__device__ __forceinline__ void far_stage_row(int np, const int (&q)[FarT<WK, WL>::NPOS],
+__device__ __forceinline__ void far_stage_row(int np, const int (&qb)[2 * WK + 1],
                                               const double (&ux)[FarT<WK, WL>::NPOS],
-                                              const double (&uy)[FarT<WK, WL>::NPOS], unsigned mr, unsigned mi,
-                                              int* scol, double* sval, int off) {
-  unsigned m1 = ROW ? mi : mr, m2 = ROW ? mr : mi;
-  const int off2 = off + __popc(m1);
+                                              const double (&uy)[FarT<WK, WL>::NPOS], typename FarT<WK, WL>::Mask mr,
+                                              typename FarT<WK, WL>::Mask mi, int* scol, double* sval, int off) {
+  typename FarT<WK, WL>::Mask m1 = ROW ? mi : mr, m2 = ROW ? mr : mi;
+  const int off2 = off + mpopc(m1);
   unsigned pc1 = (unsigned)__cvta_generic_to_shared(scol + off), pv1 = (unsigned)__cvta_generic_to_shared(sval + off);
   unsigned pc2 = (unsigned)__cvta_generic_to_shared(scol + off2), pv2 = (unsigned)__cvta_generic_to_shared(sval + off2);
-#pragma unroll
-  for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
+  far_foreach<WK, WL>([&](int k, int dc, int dd) {
+    const int q = qb[dc + WK] + dd;
     const double v1 = ROW ? uy[k] : ux[k];
     const double v2 = ROW ? ux[k] : -uy[k];
-    sts_entry(m1 & 1u, pc1, pv1, q[k], v1);
-    sts_entry(m2 & 1u, pc2, pv2, np + q[k], v2);
+    sts_entry((unsigned)(m1 & 1u), pc1, pv1, q, v1);
+    sts_entry((unsigned)(m2 & 1u), pc2, pv2, np + q, v2);
     m1 >>= 1;
     m2 >>= 1;
-  }
+  });
 }
 
 // ---------------------------------------------------------------------------------------

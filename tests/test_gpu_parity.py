@@ -86,7 +86,7 @@ SMALL = [
     banded_random_problem(97, seed=7, wH=1, wL=3, P=2),
     banded_random_problem(150, seed=8, wH=5, wL=0, P=1, drive_w=2),
     banded_random_problem(70, seed=9, wH=15, wL=7, P=1),
-    banded_random_problem(50, seed=11, wH=4, wL=2, P=1),   # mode 2, one dissipator
+    banded_random_problem(50, seed=11, wH=4, wL=2, P=1),   # widths (4, 2), one dissipator
     banded_random_problem(45, seed=12, wH=3, wL=0, P=1),   # mode 0 widths (3, 0)
     banded_random_problem(77, seed=13, wH=1, wL=1, P=2),   # mode 0 widths (2, 1), runtime P
     dimer_problem(1300, True),                               # fill with a barrier per far tile (N >= 1200)
@@ -112,6 +112,32 @@ def test_parity_baseline_configs(idx):
         d = {(int(r), int(c)): v for r, c, v in zip(rows, col, val)}
         for (r, c), v in d.items():
             assert d[(c, r)] == -v
+
+
+WIDE = [banded_random_problem(50, seed=11, wH=4, wL=2, P=1), banded_random_problem(64, seed=6),
+        banded_random_problem(300, seed=21, wH=4, wL=2, P=3, drive_w=1)]
+
+
+@pytest.mark.parametrize("which", ["w50_P1", "w64_P4", "w300_P3_drive", "c3"])
+def test_wide_band_modes(which, monkeypatch):
+    """Widths (4, 2) (c3's): the thread-per-pair staged path (mode 0, the default) and the
+    warp-per-pair path (mode 2, SUNFOLD_MODE2=1) both match the oracle, and agree bit for bit."""
+    sun = _gpu()
+    prob = config(3) if which == "c3" else WIDE[["w50_P1", "w64_P4", "w300_P3_drive"].index(which)]
+    outs = []
+    for m2 in ("0", "1"):
+        monkeypatch.setenv("SUNFOLD_MODE2", m2)
+        if which != "c3" or m2 == "1":  # c3 in the default mode: test_parity_baseline_configs
+            Q0, Q1, K, info = _check_problem(sun, prob, determinism=False)
+        else:
+            plan, Q0, Q1, K, info = _run(sun, prob)
+            plan.close()
+        assert info["mode_q0"] == (2 if m2 == "1" else 0), info
+        outs.append((Q0, Q1, K))
+    (a0, a1, ak), (b0, b1, bk) = outs
+    for x, y in ((a0, b0),) + (((a1, b1),) if a1 is not None else ()):
+        assert torch.equal(x.row_ptr, y.row_ptr) and torch.equal(x.col, y.col) and torch.equal(x.val, y.val)
+    assert torch.equal(ak, bk)
 
 
 def test_apply_matches_lindbladian_c4():

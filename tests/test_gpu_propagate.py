@@ -200,16 +200,19 @@ def test_rk4_matrix_free_full_size_and_errors():
     pm.close()
 
 
+@pytest.mark.parametrize("mode", [0, 2])
 @pytest.mark.parametrize("which", ["small_P1", "small_P4", "c3"])
-def test_rk4_matrix_free_mode2(which):
-    """Mode-2 plans (widths (4, 2)): the matrix-free RK4 against the CSR RK4."""
+def test_rk4_matrix_free_wide(which, mode, monkeypatch):
+    """Plans of widths (4, 2), thread-per-pair (mode 0, default) or warp-per-pair (mode 2,
+    SUNFOLD_MODE2=1) count/fill: the matrix-free RK4 against the CSR RK4."""
+    monkeypatch.setenv("SUNFOLD_MODE2", "1" if mode == 2 else "0")
     sun = _sun()
     prob = {"small_P1": lambda: banded_random_problem(50, seed=11, wH=4, wL=2, P=1),
             "small_P4": lambda: banded_random_problem(64, seed=6),
             "c3": lambda: config(3)}[which]()
     plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
     Q0, Q1, K = plan.run()
-    assert plan.info()["mode_q0"] == 2
+    assert plan.info()["mode_q0"] == mode
     v0 = sun.expand_state(ZCSR.from_triplets(prob.n, [0], [0], [1.0]))
     va, vb = v0.clone(), v0.clone()
     h, steps = 1e-4, 5
