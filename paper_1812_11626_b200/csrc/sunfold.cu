@@ -247,6 +247,7 @@ struct sun_plan_s {
   NearSide side[2];
   int combined;         // mode 0 with Q1 absent or Q1 = Q_H[diagonal H1]: one launch per pass
   int near_sep = 0;     // combined: near rows by k_near0 before the fill (SUNFOLD_NEAR_SEP=1)
+  int pdl = 0;          // combined: programmatic dependent launch between the sequence's kernels
   long long fill_grid[2];
   // auxiliary streams: the Q1 passes and the near-item fill run concurrently with Q0's far
   // tiles (fork/join with events on the caller's stream; also valid under graph capture)
@@ -396,6 +397,7 @@ __device__ __forceinline__ double2 csr_get(const OpDesc& d, int r, int c) {
 }
 
 __global__ void __launch_bounds__(EXP_THREADS) k_expand(const ExpandArgs A) {
+  pdl_enter();
   const OpList& ops = A.ops;
   const int n = ops.n;
   const long long gtid = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -760,7 +762,15 @@ struct MatCount {
 // no dissipators) in one launch of single-warp CTAs:
 //   [Q0 near items][Q1 near items][Q0 far slots][Q1 far slots]   (long near items first)
 template <int WK, int WL, int PT, int Q1W>
+#ifndef SUN_PDL_COUNT
+#define SUN_PDL_COUNT 1  // 0: no PDL code in the count kernel, 1: wait only, 2: wait + early trigger
+#endif
 __global__ void __launch_bounds__(32) k_count0(const MatCount m0, const MatCount m1) {
+#if SUN_PDL_COUNT == 1
+  pdl_wait();
+#elif SUN_PDL_COUNT == 2
+  pdl_enter();
+#endif
   constexpr int Q1K = Q1W > 0 ? Q1W : 0;
   constexpr int PW0 = Mode0<WK, WL>::PER_WARP, PW1 = Mode0<Q1K, 0>::PER_WARP;
   __shared__ double scr[PW0 > PW1 ? PW0 : PW1];
@@ -1418,6 +1428,7 @@ __device__ __forceinline__ void store_header(const DevHeader* h, HeaderPrefix* o
 // The next far tile's counts and offsets are loaded before the current unit runs.
 template <int WK, int WL, int PT, int Q1W>
 __global__ void __launch_bounds__(256, FillFar<WK, WL>::MINB) k_fill0(const MatFill m0, const MatFill m1) {
+  pdl_enter();
   using FF = FillFar<WK, WL>;
   static_assert(Q1W <= 0, "combined fill: Q1 rows must be staging-free");
   extern __shared__ __align__(128) unsigned char dyn[];
@@ -1507,6 +1518,7 @@ __global__ void __launch_bounds__(256, FillFar<WK, WL>::MINB) k_fill0(const MatF
 // when it fits (NEAR_SMEM_INV doubles), not one dependent L2 load per entry.
 constexpr int NEAR_SMEM_INV = 8192;
 __global__ void __launch_bounds__(256) k_near0(const MatFill m0) {
+  pdl_enter();
   extern __shared__ double sinv[];
   const int n = m0.pr.n;
   if (n <= NEAR_SMEM_INV) {
@@ -1842,6 +1854,7 @@ struct ScanArgs {
 };
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_chain(ScanArgs A) {
+  pdl_enter();
   const int y = blockIdx.y;
   __shared__ unsigned int chunk_s;
   __shared__ long long wsum[32];
@@ -2392,6 +2405,24 @@ namespace {
     if (e_ != cudaSuccess) return cuda_fail(e_); \
   } while (0)
 
+// kernel launch, with the programmatic-dependent-launch attribute when `pdl` (the kernel
+// starts while its predecessor in the stream finishes; it waits in pdl_enter)
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 bool zcsr_ok(const sun_zcsr* A, int n) {
   return A && A->n == n && A->nnz >= 0 && A->row_ptr && (A->nnz == 0 || (A->col && A->val));
 }
@@ -2531,10 +2562,10 @@ void setup_prob(sun_plan_s* pl, int which) {
 
 // ---- mode-0 launchers.  Q1W = -1: one matrix per launch; Q1W = 0: Q0 + Q1 (Q1 = (0, 0, 0)).
 template <int WK, int WL, int PT, int Q1W>
-cudaError_t launch_count0(const MatCount& m0, const MatCount& m1, cudaStream_t st) {
+cudaError_t launch_count0(const MatCount& m0, const MatCount& m1, cudaStream_t st, bool pdl) {
   auto warps = [](const Prob& p) { return p.npt; };  // one count warp per scan slot
   const long long U = warps(m0.pr) + m0.pr.nb_near + (Q1W >= 0 ? warps(m1.pr) + m1.pr.nb_near : 0);
-  if (U > 0) k_count0<WK, WL, PT, Q1W><<<(unsigned)U, 32, 0, st>>>(m0, m1);
+  if (U > 0) return launch_k(pdl, k_count0<WK, WL, PT, Q1W>, dim3((unsigned)U), dim3(32), 0, st, m0, m1);
   return cudaGetLastError();
 }
 
@@ -2564,9 +2595,8 @@ cudaError_t attr_fill0(const Prob& p0, const Prob* p1, long long& grid) {
 }
 
 template <int WK, int WL, int PT, int Q1W>
-cudaError_t launch_fill0(const MatFill& m0, const MatFill& m1, long long grid, cudaStream_t st) {
-  k_fill0<WK, WL, PT, Q1W><<<(unsigned)grid, 256, FillFar<WK, WL>::SMEM, st>>>(m0, m1);
-  return cudaGetLastError();
+cudaError_t launch_fill0(const MatFill& m0, const MatFill& m1, long long grid, cudaStream_t st, bool pdl) {
+  return launch_k(pdl, k_fill0<WK, WL, PT, Q1W>, dim3((unsigned)grid), dim3(256), FillFar<WK, WL>::SMEM, st, m0, m1);
 }
 
 #define SUN_DISPATCH0(pr, q1w, CALL)                              \
@@ -2590,21 +2620,22 @@ cudaError_t dispatch_attr0(const Prob& p0, const Prob* p1, int q1w, long long& g
 #undef SUN_X1
 }
 
-cudaError_t dispatch_count0(const MatCount& m0, const MatCount& m1, int q1w, cudaStream_t st) {
+cudaError_t dispatch_count0(const MatCount& m0, const MatCount& m1, int q1w, cudaStream_t st, bool pdl) {
 #define SUN_X0(WK, WL, PT) \
-  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_count0<WK, WL, PT, 0>(m0, m1, st);
+  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_count0<WK, WL, PT, 0>(m0, m1, st, pdl);
 #define SUN_X1(WK, WL, PT) \
-  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_count0<WK, WL, PT, -1>(m0, m1, st);
+  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_count0<WK, WL, PT, -1>(m0, m1, st, pdl);
   SUN_DISPATCH0(m0.pr, q1w, 0);
 #undef SUN_X0
 #undef SUN_X1
 }
 
-cudaError_t dispatch_fill0(const MatFill& m0, const MatFill& m1, int q1w, long long grid, cudaStream_t st) {
+cudaError_t dispatch_fill0(const MatFill& m0, const MatFill& m1, int q1w, long long grid, cudaStream_t st,
+                           bool pdl) {
 #define SUN_X0(WK, WL, PT) \
-  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_fill0<WK, WL, PT, 0>(m0, m1, grid, st);
+  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_fill0<WK, WL, PT, 0>(m0, m1, grid, st, pdl);
 #define SUN_X1(WK, WL, PT) \
-  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_fill0<WK, WL, PT, -1>(m0, m1, grid, st);
+  if (m0.pr.wK == WK && m0.pr.wL == WL && pt_ == PT) return launch_fill0<WK, WL, PT, -1>(m0, m1, grid, st, pdl);
   SUN_DISPATCH0(m0.pr, q1w, 0);
 #undef SUN_X0
 #undef SUN_X1
@@ -2886,6 +2917,10 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
     pl->near_sep = pl->combined && (nf && nf[0] ? nf[0] != '0' : dflt);
   }
   pl->launches_fill = pl->combined ? 1 + pl->near_sep : nmat;
+  {
+    const char* np_ = getenv("SUNFOLD_NO_PDL");
+    pl->pdl = pl->combined && !(np_ && np_[0] && np_[0] != '0');
+  }
   if (pl->general) {
     pl->launches_count = (P > 0 ? sung::G_LAUNCHES_EXPAND : 1) + sung::G_LAUNCHES_COUNT * nmat + 1;
     pl->launches_fill = sung::G_LAUNCHES_FILL * nmat;
@@ -3053,14 +3088,14 @@ static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr) {
   sa.hdr = hdr;
   sa.hout = scan_hdr ? pl->res.dpin : nullptr;
   if (pl->combined) {
-    CK(dispatch_count0(mc[0], mc[1], pl->has_h1 ? 0 : -1, st));
+    CK(dispatch_count0(mc[0], mc[1], pl->has_h1 ? 0 : -1, st, pl->pdl && SUN_PDL_COUNT > 0));
   } else {
     if (pl->has_h1) CK(fork_aux(pl, st, 1));  // Q1's count pass runs concurrently on aux[0]
     for (int which = 0; which < nmat; ++which) {
       const Prob& pr = pl->pr[which];
       cudaStream_t s = which ? pl->aux[0] : st;
       if (pr.mode == 0) {
-        CK(dispatch_count0(mc[which], mc[which], -1, s));
+        CK(dispatch_count0(mc[which], mc[which], -1, s, false));
       } else if (pr.mode == 2) {
         CK(launch2(pr, &mc[which], nullptr, nullptr, 0, s));
       } else {
@@ -3071,8 +3106,7 @@ static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr) {
     if (pl->has_h1) CK(join_aux(pl, st, 1));
   }
   // (a4) chained scan of both matrices' slot sums
-  k_scan_chain<<<dim3((unsigned)maxchunks, nmat), SCAN_THREADS, 0, st>>>(sa);
-  CK(cudaGetLastError());
+  CK(launch_k(pl->combined && pl->pdl, k_scan_chain, dim3((unsigned)maxchunks, nmat), dim3(SCAN_THREADS), 0, st, sa));
   return SUN_OK;
 }
 
@@ -3112,7 +3146,9 @@ static bool header_in_fill(sun_plan pl) {
   return pl->res.dpin && !pl->general && (pl->combined || (!pl->has_h1 && pl->pr[0].mode == 2));
 }
 
-static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st, bool fill_hdr) {
+// pdl_first: the fill directly follows this plan's scan in the stream (sun_run)
+static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st, bool fill_hdr,
+                        bool pdl_first) {
   NvtxRange r_("sunfold: fill (a5) + K + Q1 (a6)");
   const Layout& L = pl->lay;
   char* ws = pl->ws;
@@ -3147,10 +3183,9 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
       const Prob& p0 = pl->pr[0];
       const long long nn0 = (2 * (p0.n * 2LL * p0.W + p0.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
       const size_t sm = p0.n <= NEAR_SMEM_INV ? (size_t)p0.n * sizeof(double) : 0;
-      if (nn0 > 0) k_near0<<<(unsigned)nn0, 256, sm, st>>>(mf[0]);
-      CK(cudaGetLastError());
+      if (nn0 > 0) CK(launch_k(pl->pdl && pdl_first, k_near0, dim3((unsigned)nn0), dim3(256), sm, st, mf[0]));
     }
-    CK(dispatch_fill0(mf[0], mf[1], pl->has_h1 ? 0 : -1, pl->fill_grid[0], st));
+    CK(dispatch_fill0(mf[0], mf[1], pl->has_h1 ? 0 : -1, pl->fill_grid[0], st, pl->pdl && pdl_first));
     return SUN_OK;
   }
   // Q0 on st; Q1 concurrently on aux[0]
@@ -3159,7 +3194,7 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
     const Prob& pr = pl->pr[which];
     cudaStream_t s = which ? pl->aux[0] : st;
     if (pr.mode == 0) {
-      CK(dispatch_fill0(mf[which], mf[which], -1, pl->fill_grid[which], s));
+      CK(dispatch_fill0(mf[which], mf[which], -1, pl->fill_grid[which], s, false));
     } else if (pr.mode == 2) {
       CK(launch2(pr, nullptr, &mf[which], nullptr, pl->fill_grid[which], s));
     } else {
@@ -3184,7 +3219,7 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
     int rc = SUN_OK;
     const bool fill_hdr = kind == 2 && header_in_fill(pl);
     if (kind != 1) rc = enqueue_count(pl, s, !fill_hdr);
-    if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s, fill_hdr);
+    if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s, fill_hdr, kind == 2);
     if (rc == SUN_OK && readback && !mapped) {
       const cudaError_t e =
           cudaMemcpyAsync(pl->hpin, pl->ws + pl->lay.hdr, sizeof(HeaderPrefix), cudaMemcpyDeviceToHost, s);

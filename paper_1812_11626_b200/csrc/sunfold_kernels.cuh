@@ -64,6 +64,18 @@ struct Prob {
   long long nb_near;   // mode 0: units of 8 near-pair / D-row items (one warp each)
 };
 
+// Programmatic dependent launch (sm_90+): a kernel launched with the PDL attribute may start
+// while its predecessor in the stream still runs; griddepcontrol.wait blocks until the
+// predecessor grid has completed and its writes are visible (a no-op without the attribute).
+// Every kernel of the unfold sequence waits before touching global memory, then lets its own
+// dependents launch, so the next kernel's CTAs are resident when this one ends.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+
 // (x, y) += conj(la) lb with every rounding explicit: the compiler has no contraction choice
 // left, so each evaluation of a value (count pass, fill pass, matrix-free stages; whatever
 // kernel it is inlined into) performs the identical operations and the passes take identical
