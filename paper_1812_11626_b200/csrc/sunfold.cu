@@ -657,9 +657,10 @@ __device__ __forceinline__ void pair_advance(int n, int& a, int& b, int k) {
 __device__ __forceinline__ int near_item(const Prob& pr, long long item, int& a, int& b, int& lam) {
   const int W2 = 2 * pr.W;
   const long long nnear = (long long)pr.n * W2;
-  if (item < nnear) {
-    a = (int)(item / W2);
-    b = a + 1 + (int)(item % W2);
+  if (item < nnear) {  // item < n 2W < 2^31: 32-bit division
+    const unsigned it = (unsigned)item, w2 = (unsigned)W2;
+    a = (int)(it / w2);
+    b = a + 1 + (int)(it - (unsigned)a * w2);
     return b < pr.n ? 1 : 0;
   }
   if (item < nnear + pr.n - 1) {
