@@ -479,6 +479,24 @@ __global__ void __launch_bounds__(EXP_THREADS) k_expand(const ExpandArgs A) {
     const int rf = (int)(tb / sw), rl = (int)min((long long)n - 1, (tb + blockDim.x - 1) / sw);
     const int x0 = max(0, rf - A.wL), nx = min(n - 1, rl + A.wL) - x0 + 1;
     const bool staged = A.P > 0 && (long long)A.P * nx * SLd <= EXP_LSTAGE;
+    // this thread's K entry (r, r + o) and its H0 / H1 lookups (independent of the staged rows:
+    // issued before the staging barrier, so both sets of loads are in flight together); offsets
+    // beyond an operator's planned width are zero (a value there raises F_PATTERN in the
+    // row blocks), so no CSR search runs for them
+    const bool kent = t < (long long)n * sw;
+    const int r = kent ? (int)(t / sw) : 0, o = kent ? (int)(t % sw) - A.wX : 0;
+    const int c = r + o;
+    const bool in = kent && c >= 0 && c < n;
+    const int wh = ops.wplan[0] >= 0 ? ops.wplan[0] : A.wK;
+    double2 h = make_double2(0.0, 0.0), ht = h, g = h, gt = h;
+    if (in && o >= -A.wK && o <= A.wK && o >= -wh && o <= wh) {
+      h = csr_get_band(ops.op[0], r, c, wh);
+      ht = csr_get_band(ops.op[0], c, r, wh);
+    }
+    if (in && ops.has_h1 && o >= -A.wH1 && o <= A.wH1) {
+      g = csr_get_band(ops.op[1], r, c, A.wH1);
+      gt = csr_get_band(ops.op[1], c, r, A.wH1);
+    }
     if (staged) {
       for (int e = threadIdx.x; e < A.P * nx * SLd; e += blockDim.x) {
         const int p = e / (nx * SLd), f = e % (nx * SLd), x = x0 + f / SLd, cc = x + f % SLd - A.wL;
@@ -486,10 +504,7 @@ __global__ void __launch_bounds__(EXP_THREADS) k_expand(const ExpandArgs A) {
       }
     }
     __syncthreads();
-    if (t < (long long)n * sw) {
-      const int r = (int)(t / sw), o = (int)(t % sw) - A.wX;
-      const int c = r + o;
-      const bool in = c >= 0 && c < n;
+    if (kent) {
       if (o >= -A.wK && o <= A.wK) {
         double2 kv = make_double2(0.0, 0.0);
         if (in) {
@@ -516,17 +531,13 @@ __global__ void __launch_bounds__(EXP_THREADS) k_expand(const ExpandArgs A) {
             mx += ops.gamma[2 + p] * px;
             my += ops.gamma[2 + p] * py;
           }
-          const int wh = ops.wplan[0] >= 0 ? ops.wplan[0] : A.wK;
-          const double2 h = csr_get_band(ops.op[0], r, c, wh), ht = csr_get_band(ops.op[0], c, r, wh);
           kv = make_double2(h.x - 0.5 * my, h.y + 0.5 * mx);
           d0 = (unsigned long long)__double_as_longlong(fmax(fabs(h.x - ht.x), fabs(h.y + ht.y)));
         }
         A.kb0[(long long)r * (2 * A.wK + 1) + (o + A.wK)] = kv;
       }
-      if (in && ops.has_h1 && o >= -A.wH1 && o <= A.wH1) {
-        const double2 g = csr_get_band(ops.op[1], r, c, A.wH1), gt = csr_get_band(ops.op[1], c, r, A.wH1);
+      if (in && ops.has_h1 && o >= -A.wH1 && o <= A.wH1)
         d1 = (unsigned long long)__double_as_longlong(fmax(fabs(g.x - gt.x), fabs(g.y + gt.y)));
-      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
