@@ -50,7 +50,10 @@ constexpr int EXP_LSTAGE = 2048;  // k_expand: staged dissipator band values per
 #ifndef SUN_SCAN_IPT
 #define SUN_SCAN_IPT 4
 #endif
-constexpr int SCAN_THREADS = 1024, SCAN_IPT = SUN_SCAN_IPT, SCAN_TILE = SCAN_THREADS * SCAN_IPT;  // 4k slots per chunk (16k measured slower at c4: 12 vs 8 us)
+#ifndef SUN_SCAN_THREADS
+#define SUN_SCAN_THREADS 256
+#endif
+constexpr int SCAN_THREADS = SUN_SCAN_THREADS, SCAN_IPT = SUN_SCAN_IPT, SCAN_TILE = SCAN_THREADS * SCAN_IPT;  // 1k slots per chunk (c4: 6.3 us; 4k: 8.2, 16k: 12, 512: 6.3-6.7)
 static_assert(SCAN_IPT % 4 == 0, "int4 loads");
 constexpr unsigned long long SCAN_A = 1ull << 62, SCAN_P = 2ull << 62, SCAN_V = (1ull << 62) - 1;
 
