@@ -943,26 +943,35 @@ __device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, co
     if (kind == 2 && half) kind = 0;
     if (kind == 1) p = (long long)pidx32(pr.n, a, b);
   }
+  // every lookup of the row issued together (metadata, slot offset, the slot's earlier counts:
+  // independent loads), reduced after: one round trip before the copy instead of three
+  NearMeta m{};
+  long long o = 0;
   int s1 = 0;
+  if (kind != 0) {
+    m = side.meta[srow];
+    o = kind == 1 ? __ldg(&fo.toff[(half ? pr.npt : 0) + p / pr.tp]) : __ldg(&fo.toff[2 * pr.npt + lam - 1]);
+  }
   if (kind == 1) {
     const long long ts = (p / pr.tp) * pr.tp;
     const int* c = cnt + (half ? np : 0);
-    for (long long q = ts + hl; q < p; q += NEAR_GL) s1 += __ldg(&c[q]) & CNT_MASK;  // mode 2 packs nR above
+    static_assert(SLOTS_PER_TILE * 32 == TP0, "slot = 32 pairs");
+#pragma unroll
+    for (int i = 0; i < 32 / NEAR_GL; ++i) {  // the slot's <= 31 earlier pairs (tp = 32)
+      const long long q = ts + hl + i * NEAR_GL;
+      s1 += q < p ? (__ldg(&c[q]) & CNT_MASK) : 0;  // mode 2 packs nR above
+    }
+    for (long long q = ts + hl + 32; q < p; q += NEAR_GL) s1 += __ldg(&c[q]) & CNT_MASK;  // (tp > 32)
   }
 #pragma unroll
   for (int sh = NEAR_GL / 2; sh > 0; sh >>= 1) s1 += __shfl_xor_sync(FULL, s1, sh);  // within each group
   if (kind == 0) return;  // no shuffles below
-  const NearMeta m = side.meta[srow];
-  long long o;
   if (kind == 1) {
-    o = fo.toff[(half ? pr.npt : 0) + p / pr.tp] + s1;
+    o += s1;
     if (hl == 0 && fo.K) fo.K[(half ? np : 0) + p] = m.k;
-  } else {
-    o = fo.toff[2 * pr.npt + lam - 1];
-    if (hl == 0) {
-      fo.row_ptr[2 * np + lam - 1] = o;
-      if (fo.K) fo.K[2 * np + lam - 1] = m.k;
-    }
+  } else if (hl == 0) {
+    fo.row_ptr[2 * np + lam - 1] = o;
+    if (fo.K) fo.K[2 * np + lam - 1] = m.k;
   }
   const long long lim = fo.cap - o;
   const int32_t* sc = side.col + srow * side.nc;
