@@ -1203,12 +1203,24 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
   const long long p = t * TP0 + threadIdx.x;
   const bool valid = p < np;
   const int cS = ti.cS, cJ = ti.cJ;
-  int totS, totJ;  // warp-local offsets: every warp has a scan slot of its own (no CTA barrier)
-  const int exS = warp_excl_scan(cS, totS), exJ = warp_excl_scan(cJ, totJ);
   int a, b;
   warp_pairs(pr.n, t * TP0 + wid * 32, a, b);
   const bool far = valid && (b - a > 2 * MC::W);
   const bool nearp = valid && !far;
+  // U values first, for every lane (any 0 <= a < b < n is a safe address set; non-far lanes
+  // are masked below): the band loads are in flight during the offset scans and row_ptr stores
+  double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
+#ifdef SUN_EXP_NO_COMPUTE
+#pragma unroll
+  for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
+    ux[k] = 1.0 + k;
+    uy[k] = k < 9 ? 1.0 : 0.0;
+  }
+#else
+  far_values<WK, WL, PT>(pr, a, b, ux, uy);
+#endif
+  int totS, totJ;  // warp-local offsets: every warp has a scan slot of its own (no CTA barrier)
+  const int exS = warp_excl_scan(cS, totS), exJ = warp_excl_scan(cJ, totJ);
   const long long baseS = ti.baseS, baseJ = ti.baseJ;
   if (valid) {
     fo.row_ptr[p] = baseS + exS;
@@ -1221,19 +1233,9 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
 #ifdef SUN_EXP_PROLOGUE_ONLY
   return;
 #endif
-  double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
   int qb[2 * WK + 1];
   typename FarT<WK, WL>::Mask mr = 0u, mi = 0u;
   if (far) {
-#ifdef SUN_EXP_NO_COMPUTE
-#pragma unroll
-    for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
-      ux[k] = 1.0 + k;
-      uy[k] = k < 9 ? 1.0 : 0.0;
-    }
-#else
-    far_values<WK, WL, PT>(pr, a, b, ux, uy);
-#endif
     far_masks<WK, WL>(pr.n, pr.tau, a, b, ux, uy, mr, mi);
     far_colbase<WK>(pr.n, a, b, qb);
   }
@@ -1389,25 +1391,31 @@ __device__ __forceinline__ void fill_q1_chunk(const FarCtx& f1, long long npt1, 
   const long long np = f1.np;
   const long long p = t * TP0 + threadIdx.x;
   const bool valid = p < np;
-  const int c = valid ? cnt1[p] : 0;  // S and J rows of a pair have the same length
+  // every load of the chunk issued before the first use (counts, slot offsets, the drive's
+  // diagonal values), one round trip
+  int a, b;  // decoded again (cheaper than keeping the far tile's pair live across its staging)
+  warp_pairs(f1.n, t * TP0 + wid * 32, a, b);
+  const int c = valid ? __ldg(&cnt1[p]) : 0;  // S and J rows of a pair have the same length
+  int bq[TP0 / 32 - 1];
+#pragma unroll
+  for (int i = 0; i < TP0 / 32 - 1; ++i) {  // the tile's earlier warps
+    const long long q = t * TP0 + i * 32 + lane;
+    bq[i] = (i < wid && q < np) ? __ldg(&cnt1[q]) : 0;
+  }
+  const long long b0S = __ldg(&fo.toff[t]), b0J = __ldg(&fo.toff[npt1 + t]);
+  double ux[1], uy[1];
+  far_values<0, 0, 0>(f1, a, b, ux, uy);
   int before = 0;
 #pragma unroll
-  for (int i = 0; i < TP0 / 32 - 1; ++i) {  // the tile's earlier warps: all loads in flight at once
-    const long long q = t * TP0 + i * 32 + lane;
-    before += (i < wid && q < np) ? __ldg(&cnt1[q]) : 0;
-  }
+  for (int i = 0; i < TP0 / 32 - 1; ++i) before += bq[i];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(FULL, before, o);
   int tot;
   const int ex = warp_excl_scan(c, tot);
-  int a, b;  // decoded again (cheaper than keeping the far tile's pair live across its staging)
-  warp_pairs(f1.n, t * TP0 + wid * 32, a, b);
   if (!valid) return;
-  const long long rS = fo.toff[t] + before + ex, rJ = fo.toff[npt1 + t] + before + ex;
+  const long long rS = b0S + before + ex, rJ = b0J + before + ex;
   fo.row_ptr[p] = rS;
   fo.row_ptr[np + p] = rJ;
-  double ux[1], uy[1];
-  far_values<0, 0, 0>(f1, a, b, ux, uy);
   unsigned mr, mi;
   far_masks<0, 0>(f1.n, f1.tau, a, b, ux, uy, mr, mi);
   const Seg seg = {fo.col, fo.val, fo.cap};
