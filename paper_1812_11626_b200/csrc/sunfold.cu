@@ -777,6 +777,12 @@ struct MatCount {
 // no dissipators) in one launch of single-warp CTAs:
 //   [Q0 near items][Q1 near items][Q0 far slots][Q1 far slots]   (long near items first)
 template <int WK, int WL, int PT, int Q1W>
+#ifndef SUN_PDL_DEFAULT
+#define SUN_PDL_DEFAULT 3  // launches with the PDL attribute (bits: 1 count, 2 scan, 4 near, 8 fill);
+// measured at c4 (B200, bench step, same box): sun_count's sequence 42.7 -> 39.6 us with count +
+// scan; inside the full sun_run sequence every PDL edge made the step slower (108.6 us without,
+// +0.8 scan, +1.6 fill, +3 count, +4 all), so sun_run launches without it
+#endif
 #ifndef SUN_PDL_COUNT
 #define SUN_PDL_COUNT 1  // 0: no PDL code in the count kernel, 1: wait only, 2: wait + early trigger
 #endif
@@ -2951,7 +2957,8 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
   pl->launches_fill = pl->combined ? 1 + pl->near_sep : nmat;
   {
     const char* np_ = getenv("SUNFOLD_NO_PDL");
-    pl->pdl = pl->combined && !(np_ && np_[0] && np_[0] != '0');
+    const char* pm = getenv("SUNFOLD_PDL_MASK");  // bits: 1 count, 2 scan, 4 near, 8 fill
+    pl->pdl = pl->combined && !(np_ && np_[0] && np_[0] != '0') ? (pm && pm[0] ? atoi(pm) : SUN_PDL_DEFAULT) : 0;
   }
   if (pl->general) {
     pl->launches_count = (P > 0 ? sung::G_LAUNCHES_EXPAND : 1) + sung::G_LAUNCHES_COUNT * nmat + 1;
@@ -3056,7 +3063,8 @@ static int enqueue_count_general(sun_plan pl, cudaStream_t st, bool scan_hdr) {
 
 // scan_hdr: the scan stores the header prefix into the mapped slot (else the fill does: see
 // header_in_fill)
-static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr) {
+// pdl_ok: programmatic dependent launch allowed (the count-only sequence; see SUN_PDL_DEFAULT)
+static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr, bool pdl_ok) {
   NvtxRange r_("sunfold: expand (a1) + count (a3) + scan (a4)");
   if (pl->general) return enqueue_count_general(pl, st, scan_hdr);
   const Layout& L = pl->lay;
@@ -3120,7 +3128,7 @@ static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr) {
   sa.hdr = hdr;
   sa.hout = scan_hdr ? pl->res.dpin : nullptr;
   if (pl->combined) {
-    CK(dispatch_count0(mc[0], mc[1], pl->has_h1 ? 0 : -1, st, pl->pdl && SUN_PDL_COUNT > 0));
+    CK(dispatch_count0(mc[0], mc[1], pl->has_h1 ? 0 : -1, st, pdl_ok && (pl->pdl & 1) && SUN_PDL_COUNT > 0));
   } else {
     if (pl->has_h1) CK(fork_aux(pl, st, 1));  // Q1's count pass runs concurrently on aux[0]
     for (int which = 0; which < nmat; ++which) {
@@ -3138,7 +3146,7 @@ static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr) {
     if (pl->has_h1) CK(join_aux(pl, st, 1));
   }
   // (a4) chained scan of both matrices' slot sums
-  CK(launch_k(pl->combined && pl->pdl, k_scan_chain, dim3((unsigned)maxchunks, nmat), dim3(SCAN_THREADS), 0, st, sa));
+  CK(launch_k(pdl_ok && pl->combined && (pl->pdl & 2), k_scan_chain, dim3((unsigned)maxchunks, nmat), dim3(SCAN_THREADS), 0, st, sa));
   return SUN_OK;
 }
 
@@ -3215,9 +3223,9 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
       const Prob& p0 = pl->pr[0];
       const long long nn0 = (2 * (p0.n * 2LL * p0.W + p0.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
       const size_t sm = p0.n <= NEAR_SMEM_INV ? (size_t)p0.n * sizeof(double) : 0;
-      if (nn0 > 0) CK(launch_k(pl->pdl && pdl_first, k_near0, dim3((unsigned)nn0), dim3(256), sm, st, mf[0]));
+      if (nn0 > 0) CK(launch_k((pl->pdl & 4) && pdl_first, k_near0, dim3((unsigned)nn0), dim3(256), sm, st, mf[0]));
     }
-    CK(dispatch_fill0(mf[0], mf[1], pl->has_h1 ? 0 : -1, pl->fill_grid[0], st, pl->pdl && pdl_first));
+    CK(dispatch_fill0(mf[0], mf[1], pl->has_h1 ? 0 : -1, pl->fill_grid[0], st, (pl->pdl & 8) && pdl_first));
     return SUN_OK;
   }
   // Q0 on st; Q1 concurrently on aux[0]
@@ -3250,7 +3258,7 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
   auto direct = [&](cudaStream_t s) -> int {
     int rc = SUN_OK;
     const bool fill_hdr = kind == 2 && header_in_fill(pl);
-    if (kind != 1) rc = enqueue_count(pl, s, !fill_hdr);
+    if (kind != 1) rc = enqueue_count(pl, s, !fill_hdr, kind == 0);
     if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s, fill_hdr, kind == 2);
     if (rc == SUN_OK && readback && !mapped) {
       const cudaError_t e =
