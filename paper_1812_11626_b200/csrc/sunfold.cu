@@ -22,6 +22,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
 #include <mutex>
 #include <type_traits>
 #include <vector>
@@ -65,6 +66,7 @@ struct DevHeader {
   double tau[2];                     // drop thresholds of Q0 / Q1 (R6), on the device
   unsigned long long herm_dev[2];    // max |H - H^+| (component-wise) of H0, H1 (bits of a double >= 0)
   double nrm2_h[2];                  // ||H0||_F^2, ||H1||_F^2 (this call's values)
+  unsigned int seq, pad2;            // banded count sequences run on this plan (k_expand counts)
   unsigned int ticket[2];            // chained-scan chunk tickets
   unsigned int done;                 // count-pass CTA completion counter (scan by the last CTA)
   int bw[MAXOPS];
@@ -77,6 +79,7 @@ struct HeaderPrefix {
   double tau[2];
   unsigned long long herm_dev[2];
   double nrm2_h[2];
+  unsigned int seq, pad2;  // written last by the fill (sun_run): the prefix of this sequence is complete
 };
 
 struct OpDesc {
@@ -274,6 +277,8 @@ struct sun_plan_s {
   bool use_graphs = true;
   HeaderPrefix* hpin = nullptr;  // pinned host copy of the header prefix (nnz readback)
   int hdr_enqueued = 0;          // the last count/run sequence already copies the header to hpin
+  int hdr_poll = 0;              // ... and its fill stores it with a sequence number (sun_run, modes 0/2)
+  unsigned seq_expect = 0;       // banded count sequences launched on this plan (DevHeader::seq)
   PlanRes res;                   // pooled streams / events / pinned slot (res_acquire)
   std::vector<std::vector<uintptr_t>> seen;  // enqueue keys run once directly (captured on reuse)
   ~sun_plan_s() {
@@ -614,6 +619,7 @@ __global__ void __launch_bounds__(EXP_THREADS) k_expand(const ExpandArgs A) {
     hdr->tau[0] = 1e-14 * s0;
     hdr->tau[1] = ops.has_h1 ? 1e-14 * sqrt(hdr->nrm2_h[1]) : 0.0;
     if (!ops.has_h1) hdr->nrm2_h[1] = 0.0;
+    hdr->seq = hdr->seq + 1u;  // one per banded count sequence (sun_plan_nnz waits for it, see store_header)
     *A.done = 0u;  // ready for the next launch
   }
 }
@@ -1458,6 +1464,11 @@ __device__ __forceinline__ void store_header(const DevHeader* h, HeaderPrefix* o
   o->herm_dev[1] = h->herm_dev[1];
   o->nrm2_h[0] = h->nrm2_h[0];
   o->nrm2_h[1] = h->nrm2_h[1];
+  o->pad2 = 0u;
+  // the sequence number last, after the fields are visible to the host: sun_plan_nnz returns as
+  // soon as it sees it (the fill keeps running; its outputs are ordered on the stream)
+  __threadfence_system();
+  *reinterpret_cast<volatile unsigned*>(&o->seq) = h->seq;
 }
 
 // Fill pass of Q0 and, with Q1W >= 0, of Q1 (widths Q1W, 0, no dissipators; staging-free
@@ -2977,6 +2988,8 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
     pl->ev_fork = pl->res.fork;
     pl->cap_stream = pl->res.cap;
     pl->hpin = pl->res.hpin;
+    // the pooled slot may hold another plan's sequence number: none of this plan's (1, 2, ...)
+    if (pl->hpin) *reinterpret_cast<volatile unsigned*>(&pl->hpin->seq) = 0xFFFFFFFFu;
     const char* ng = getenv("SUNFOLD_NO_GRAPHS");
     pl->use_graphs = !(ng && ng[0] && ng[0] != '0');
     if (pl->general) {
@@ -3156,10 +3169,27 @@ int sun_plan_nnz(sun_plan pl, int64_t* nnz_q0, int64_t* nnz_q1) {
   if (!pl->counted) return SUN_ERR_STATE;
   HeaderPrefix hloc;
   HeaderPrefix* hp = pl->hpin ? pl->hpin : &hloc;
-  if (!pl->hdr_enqueued)
-    CK(cudaMemcpyAsync(hp, pl->ws + pl->lay.hdr, sizeof(HeaderPrefix), cudaMemcpyDeviceToHost, pl->count_stream));
-  CK(cudaStreamSynchronize(pl->count_stream));
-  const HeaderPrefix h = *hp;
+  if (pl->hdr_poll && pl->hdr_enqueued && pl->hpin) {
+    // sun_run: the fill stores the header (final since the scan) into the mapped slot at its
+    // start, sequence number last; return as soon as this sequence's number is there instead of
+    // waiting for the whole stream (the fill's outputs stay ordered on the stream)
+    const volatile unsigned* vs = &pl->hpin->seq;
+    for (unsigned it = 0;; ++it) {
+      if (*vs == pl->seq_expect) break;
+      if ((it & 255u) == 255u) {
+        const cudaError_t q = cudaStreamQuery(pl->count_stream);
+        if (q == cudaSuccess) break;  // the sequence has completed: the slot is final
+        if (q != cudaErrorNotReady) return cuda_fail(q);
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+  } else {
+    if (!pl->hdr_enqueued)
+      CK(cudaMemcpyAsync(hp, pl->ws + pl->lay.hdr, sizeof(HeaderPrefix), cudaMemcpyDeviceToHost, pl->count_stream));
+    CK(cudaStreamSynchronize(pl->count_stream));
+  }
+  HeaderPrefix h;
+  memcpy(&h, (const void*)hp, sizeof(h));
   if (h.flags & F_MALFORMED) return SUN_ERR_ARG;
   for (int k = 0; k < 1 + pl->has_h1; ++k) {
     double dev;
@@ -3268,11 +3298,14 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
     return rc;
   };
   pl->hdr_enqueued = 0;
+  pl->hdr_poll = 0;
   auto mark = [&](int rc) {  // the pooled pinned slot is written by this sequence: track its end
     if (rc == SUN_OK && readback) {
       const cudaError_t e = cudaEventRecord(pl->res.done, st);
       if (e != cudaSuccess) return cuda_fail(e);
     }
+    if (rc == SUN_OK && kind != 1 && !pl->general) ++pl->seq_expect;  // k_expand ran once more
+    if (rc == SUN_OK && kind == 2 && mapped && header_in_fill(pl)) pl->hdr_poll = 1;
     return rc;
   };
   if (!pl->use_graphs) {

@@ -140,6 +140,26 @@ def test_wide_band_modes(which, monkeypatch):
     assert torch.equal(ak, bk)
 
 
+def test_nnz_readback_pooled_slots():
+    """sun_run returns nnz as soon as the fill has stored this sequence's header (mapped
+    slot, sequence number last).  Plans created one after another reuse pooled slots that hold
+    other plans' sequence numbers; every run must still report its own problem's nnz, equal to
+    the two-pass (count -> synchronous readback -> fill) result, with identical outputs."""
+    sun = _gpu()
+    probs = [config(1), config(2), dimer_problem(40, True), config(1), config(2), config(3)]
+    for prob in probs:
+        plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+        for _ in range(3):  # first call direct, then graph capture and replay
+            Q0, Q1, K = plan.run()
+        R0, R1, RK = plan.run_two_pass()
+        torch.cuda.synchronize()
+        assert Q0.nnz == R0.nnz and torch.equal(Q0.col, R0.col) and torch.equal(Q0.val, R0.val)
+        assert torch.equal(K, RK)
+        if Q1 is not None:
+            assert Q1.nnz == R1.nnz and torch.equal(Q1.val, R1.val)
+        plan.close()
+
+
 def test_apply_matches_lindbladian_c4():
     """Q(t) v + K from the GPU (sun_apply) equals proj L(t)(rho) for a random density matrix."""
     sun = _gpu()
