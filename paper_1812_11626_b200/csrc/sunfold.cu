@@ -254,6 +254,7 @@ struct sun_plan_s {
   int combined;         // mode 0 with Q1 absent or Q1 = Q_H[diagonal H1]: one launch per pass
   int near_sep = 0;     // combined: near rows by k_near0 before the fill (SUNFOLD_NEAR_SEP=1)
   int pdl = 0;          // combined: programmatic dependent launch between the sequence's kernels
+  int pdl_run = 0;      // PDL also inside sun_run's sequence (SUNFOLD_PDL_RUN=1; A/B only)
   long long fill_grid[2];
   // auxiliary streams: the Q1 passes and the near-item fill run concurrently with Q0's far
   // tiles (fork/join with events on the caller's stream; also valid under graph capture)
@@ -2969,6 +2970,8 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
   {
     const char* np_ = getenv("SUNFOLD_NO_PDL");
     const char* pm = getenv("SUNFOLD_PDL_MASK");  // bits: 1 count, 2 scan, 4 near, 8 fill
+    const char* pr_ = getenv("SUNFOLD_PDL_RUN");
+    pl->pdl_run = pr_ && pr_[0] && pr_[0] != '0';
     pl->pdl = pl->combined && !(np_ && np_[0] && np_[0] != '0') ? (pm && pm[0] ? atoi(pm) : SUN_PDL_DEFAULT) : 0;
   }
   if (pl->general) {
@@ -3288,7 +3291,7 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
   auto direct = [&](cudaStream_t s) -> int {
     int rc = SUN_OK;
     const bool fill_hdr = kind == 2 && header_in_fill(pl);
-    if (kind != 1) rc = enqueue_count(pl, s, !fill_hdr, kind == 0);
+    if (kind != 1) rc = enqueue_count(pl, s, !fill_hdr, kind == 0 || pl->pdl_run);
     if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s, fill_hdr, kind == 2);
     if (rc == SUN_OK && readback && !mapped) {
       const cudaError_t e =
