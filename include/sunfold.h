@@ -246,6 +246,17 @@ int sun_apply_plan(sun_plan plan, double eps, const double* v, double* dvdt, voi
  * sets the default to 0.  Errors: SUN_ERR_ARG. */
 int sun_plan_set_graphs(sun_plan plan, int32_t enable);
 
+/* Phase timing (SURVEY §5 tracing; bench.py's roofline): with enable = 1, every sun_run /
+ * sun_count / sun_unfold sequence of this plan records CUDA events (event-record nodes of its
+ * graph) before the count pass (expand + count + scan), between count and fill, and after the
+ * fill; sun_plan_phase_ms then returns the device time of the last sequence's phases in ms
+ * (count_ms: expand + count + scan, fill_ms: the fill pass incl. K and Q1; -1 for a phase the
+ * sequence did not run).  sun_plan_phase_ms waits for the last sequence to complete.  Toggling
+ * drops the plan's cached graphs.  Errors: SUN_ERR_ARG, SUN_ERR_STATE (no timed sequence yet),
+ * SUN_ERR_CUDA. */
+int sun_plan_set_timing(sun_plan plan, int32_t enable);
+int sun_plan_phase_ms(sun_plan plan, float* count_ms, float* fill_ms);
+
 /* ---- Dense unfold of a generator given by a rate matrix A -----------
  * PAPER.md Eq. 7 writes the dissipator with a positive semidefinite M x M rate
  * matrix A over the basis; P:568-570 samples "a 'dense', randomly generated, rate matrix A"

@@ -332,6 +332,18 @@ class Plan:
         """CUDA-graph replay of the enqueue sequences on (default) or off (sun_plan_set_graphs)."""
         _check(lib().sun_plan_set_graphs(self._plan, 1 if enable else 0), "sun_plan_set_graphs")
 
+    def set_timing(self, enable: bool):
+        """Phase timing on/off (sun_plan_set_timing): event records around the count and fill
+        passes inside each sequence (graph event-record nodes)."""
+        _check(lib().sun_plan_set_timing(self._plan, 1 if enable else 0), "sun_plan_set_timing")
+
+    def phase_ms(self):
+        """(count_ms, fill_ms) device time of the last timed sequence (sun_plan_phase_ms; -1 for
+        a phase it did not run).  Waits for that sequence."""
+        c, f = ctypes.c_float(), ctypes.c_float()
+        _check(lib().sun_plan_phase_ms(self._plan, ctypes.addressof(c), ctypes.addressof(f)), "sun_plan_phase_ms")
+        return float(c.value), float(f.value)
+
     def info(self) -> dict:
         inf = _lib.SunPlanInfo()
         _check(lib().sun_plan_info(self._plan, ctypes.addressof(inf)), "sun_plan_info")

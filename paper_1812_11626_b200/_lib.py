@@ -47,6 +47,8 @@ SIGNATURES = {
     "sun_nnz_bound": (ctypes.c_int64, [P, ctypes.c_int32]),
     "sun_plan_info": (ctypes.c_int, [P, P]),
     "sun_plan_set_graphs": (ctypes.c_int, [P, ctypes.c_int32]),
+    "sun_plan_set_timing": (ctypes.c_int, [P, ctypes.c_int32]),
+    "sun_plan_phase_ms": (ctypes.c_int, [P, P, P]),
     "sun_expand_state": (ctypes.c_int, [P, P, P]),
     "sun_state_diag": (ctypes.c_int, [P, ctypes.c_int32, P, P]),
     "sun_rk4": (ctypes.c_int, [P, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,

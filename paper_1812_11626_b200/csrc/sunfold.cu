@@ -124,7 +124,7 @@ struct FarPos {
 };
 
 struct Layout {
-  size_t hdr, fp0, fp1, inv, kb0, hb0, hb1, lb, blk, herm, ts0, ts1, st0, st1, toff0, toff1, cnt0, cnt1;
+  size_t hdr, fp0, fp1, inv, kb0, hb0, hb1, lb, blk, herm, ts0, ts1, st0, st1, toff0, toff1, cnt0, cnt1, sab;
   size_t side_col[2], side_val[2], side_meta[2], total;
   long long side_rows;
   long long maxslots, maxchunks, nrb;
@@ -157,6 +157,7 @@ Layout make_layout(int n, int P) {
   L.toff1 = off; off = align256(off + (size_t)maxslots * sizeof(long long));
   L.cnt0 = off; off = align256(off + (size_t)m * sizeof(int));
   L.cnt1 = off; off = align256(off + (size_t)m * sizeof(int));
+  L.sab = off;  off = align256(off + (size_t)maxslots * sizeof(int2));  // first pair of each Q0 scan slot
   // near-row side buffers of mode 0 (W <= 3): 2 rows per near item, (4W + 1)^2 entries per row
   // near-row side buffers of modes 0 and 2 (W <= 4): 2 rows per near item, (4W + 1)^2 entries
   const long long side_rows = 2 * ((long long)n * 2 * 4 + n);
@@ -255,6 +256,10 @@ struct sun_plan_s {
   int near_sep = 0;     // combined: near rows by k_near0 before the fill (SUNFOLD_NEAR_SEP=1)
   int pdl = 0;          // combined: programmatic dependent launch between the sequence's kernels
   int pdl_run = 0;      // PDL also inside sun_run's sequence (SUNFOLD_PDL_RUN=1; A/B only)
+  // phase timing (sun_plan_set_timing): events before the count, between count and fill, after
+  int timing = 0;
+  cudaEvent_t tev[3] = {nullptr, nullptr, nullptr};
+  int timed_kind = -1;  // kind of the last timed sequence (-1: none)
   long long fill_grid[2];
   // auxiliary streams: the Q1 passes and the near-item fill run concurrently with Q0's far
   // tiles (fork/join with events on the caller's stream; also valid under graph capture)
@@ -284,6 +289,8 @@ struct sun_plan_s {
   std::vector<std::vector<uintptr_t>> seen;  // enqueue keys run once directly (captured on reuse)
   ~sun_plan_s() {
     for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
+    for (auto& e : tev)
+      if (e) cudaEventDestroy(e);
     if (aux[0]) {  // nothing of this plan may still run on the pooled streams or write hpin
       cudaStreamSynchronize(aux[0]);
       cudaStreamSynchronize(aux[1]);
@@ -739,7 +746,7 @@ __device__ __forceinline__ void count_near_item(const Prob& pr, long long item, 
 
 template <int WK, int WL, int PT>
 __device__ __forceinline__ void count_far_slot(const FarCtx& pr, long long npt, long long s, int* __restrict__ cnt,
-                                               int* __restrict__ tsum) {
+                                               int* __restrict__ tsum, int2* __restrict__ sab) {
   using MC = Mode0<WK, WL>;
   using TL = Tiling<WK, WL>;
   const int lane = threadIdx.x & 31;
@@ -747,6 +754,7 @@ __device__ __forceinline__ void count_far_slot(const FarCtx& pr, long long npt, 
   const long long pw = s * (32 * TL::PPT);  // the slot's first pair
   int a, b;
   warp_pairs(pr.n, pw, a, b);
+  if (sab && lane == 0) sab[s] = make_int2(a, b);  // the fill warps of this slot start from it
   int c = 0;
 #pragma unroll 1
   for (int j = 0; j < TL::PPT; ++j) {
@@ -778,6 +786,7 @@ struct MatCount {
   int* cnt;
   int* tsum;
   NearSide side;
+  int2* sab;  // mode 0: first pair (a, b) of each scan slot, for the fill (nullptr: not stored)
 };
 
 // Count pass of Q0 (compile-time widths WK, WL, PT) and, with Q1W >= 0, of Q1 (widths Q1W, 0,
@@ -834,13 +843,13 @@ __global__ void __launch_bounds__(32) k_count0(const MatCount m0, const MatCount
   const long long nw0 = m0.pr.npt;  // one count warp per scan slot
   if (u < nw0) {
     const FarCtx prf{m0.pr.K.v, m0.pr.L, *m0.pr.tau_ptr, m0.pr.np, m0.pr.n, m0.pr.P};
-    count_far_slot<WK, WL, PT>(prf, m0.pr.npt, u, m0.cnt, m0.tsum);
+    count_far_slot<WK, WL, PT>(prf, m0.pr.npt, u, m0.cnt, m0.tsum, m0.sab);
     return;
   }
   u -= nw0;
   if constexpr (HAS1) {
     const FarCtx prf{m1.pr.K.v, m1.pr.L, *m1.pr.tau_ptr, m1.pr.np, m1.pr.n, m1.pr.P};
-    count_far_slot<Q1K, 0, 0>(prf, m1.pr.npt, u, m1.cnt, m1.tsum);
+    count_far_slot<Q1K, 0, 0>(prf, m1.pr.npt, u, m1.cnt, m1.tsum, nullptr);
   }
 }
 
@@ -1193,9 +1202,10 @@ struct FillFar {
 struct TileIn {
   int cS, cJ;
   long long baseS, baseJ;
+  int2 ab;  // first pair of the warp's slot (count pass table), x < 0: decode it
 };
 __device__ __forceinline__ TileIn load_tile_in(long long np, long long npt, long long t, const int* __restrict__ cnt,
-                                               const long long* __restrict__ toff) {
+                                               const long long* __restrict__ toff, const int2* __restrict__ sab) {
   const long long p = t * TP0 + threadIdx.x;
   const long long slot = t * SLOTS_PER_TILE + (threadIdx.x >> 5);  // the warp's 32 pairs
   TileIn ti;
@@ -1203,7 +1213,15 @@ __device__ __forceinline__ TileIn load_tile_in(long long np, long long npt, long
   ti.cJ = p < np ? cnt[np + p] : 0;
   ti.baseS = slot < npt ? toff[slot] : 0;
   ti.baseJ = slot < npt ? toff[npt + slot] : 0;
+  ti.ab = sab && slot < npt ? __ldg(&sab[slot]) : make_int2(-1, -1);
   return ti;
+}
+// the pairs of this warp's 32 lanes in far tile t: from the slot table, else decoded
+__device__ __forceinline__ void tile_pairs(int n, long long t, int2 ab, int& a, int& b) {
+  if (ab.x >= 0)
+    warp_pairs_from(n, ab.x, ab.y, a, b);
+  else
+    warp_pairs(n, t * TP0 + (threadIdx.x >> 5) * 32, a, b);
 }
 
 template <int WK, int WL, int PT>
@@ -1217,7 +1235,7 @@ __device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, l
   const bool valid = p < np;
   const int cS = ti.cS, cJ = ti.cJ;
   int a, b;
-  warp_pairs(pr.n, t * TP0 + wid * 32, a, b);
+  tile_pairs(pr.n, t, ti.ab, a, b);
   const bool far = valid && (b - a > 2 * MC::W);
   const bool nearp = valid && !far;
   // U values first, for every lane (any 0 <= a < b < n is a safe address set; non-far lanes
@@ -1399,15 +1417,15 @@ __device__ __forceinline__ void fill_direct_tile(const FarCtx& pr, long long npt
 // pairs "far" at width 0, rows of <= 2 entries): Q1's scan slot t covers the same 256 pairs,
 // so the warp's offset is the slot offset plus the counts of the tile's earlier warps.
 __device__ __forceinline__ void fill_q1_chunk(const FarCtx& f1, long long npt1, long long t, const int* __restrict__ cnt1,
-                                              const FillOut& fo) {
+                                              const FillOut& fo, int2 ab) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long np = f1.np;
   const long long p = t * TP0 + threadIdx.x;
   const bool valid = p < np;
   // every load of the chunk issued before the first use (counts, slot offsets, the drive's
   // diagonal values), one round trip
-  int a, b;  // decoded again (cheaper than keeping the far tile's pair live across its staging)
-  warp_pairs(f1.n, t * TP0 + wid * 32, a, b);
+  int a, b;  // walked again (cheaper than keeping the far tile's pair live across its staging)
+  tile_pairs(f1.n, t, ab, a, b);
   const int c = valid ? __ldg(&cnt1[p]) : 0;  // S and J rows of a pair have the same length
   int bq[TP0 / 32 - 1];
 #pragma unroll
@@ -1451,6 +1469,7 @@ struct MatFill {
   int near_sep;   // the near rows are written by k_near0 (launched before the fill), not by its units
   const DevHeader* hdr;  // with hout (sun_run of modes 0 / 2): CTA 0 stores the header prefix into
   HeaderPrefix* hout;    // mapped host memory at the start of the fill (final since the scan)
+  const int2* sab;       // mode 0, Q0: first pair of each scan slot (count pass), or nullptr
 };
 
 // header prefix -> mapped pinned host memory (sun_plan_nnz reads it after the stream)
@@ -1525,11 +1544,11 @@ __global__ void __launch_bounds__(256, FillFar<WK, WL>::MINB) k_fill0(const MatF
     idx = v - nn1;
     return 3;
   };
-  TileIn nxt{0, 0, 0, 0};
+  TileIn nxt{0, 0, 0, 0, make_int2(-1, -1)};
   auto prefetch = [&](long long v) {
     long long idx;
     if (v < U && decode(v, idx) == 0 && !FF::DIRECT)
-      nxt = load_tile_in(m0.pr.np, m0.pr.npt, idx, m0.cnt, m0.fo.toff);
+      nxt = load_tile_in(m0.pr.np, m0.pr.npt, idx, m0.cnt, m0.fo.toff, m0.sab);
   };
   prefetch(blockIdx.x);
   for (long long u = blockIdx.x; u < U; u += gridDim.x) {  // block-uniform
@@ -1546,7 +1565,7 @@ __global__ void __launch_bounds__(256, FillFar<WK, WL>::MINB) k_fill0(const MatF
         fill_direct_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, m0.cnt, m0.fo);
       else
         fill_far_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, cur, m0.fo, scol, sval);
-      if constexpr (Q1MERGED) fill_q1_chunk(prf1, m1.pr.npt, idx, m1.cnt, m1.fo);
+      if constexpr (Q1MERGED) fill_q1_chunk(prf1, m1.pr.npt, idx, m1.cnt, m1.fo, cur.ab);
     } else if (kind == 1) {
 #ifndef SUN_EXP_NO_NEAR
       fill_near_unit_h<false>(m0.pr, idx, m0.cnt, m0.fo, m0.side, m0.pr.inv);
@@ -3130,7 +3149,7 @@ static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr, bool pdl_o
     const Prob& pr = pl->pr[which];
     int* cnt = (int*)(ws + (which ? L.cnt1 : L.cnt0));
     int* ts = (int*)(ws + (which ? L.ts1 : L.ts0));
-    mc[which] = MatCount{pr, cnt, ts, pl->side[which]};
+    mc[which] = MatCount{pr, cnt, ts, pl->side[which], which == 0 && pr.mode == 0 ? (int2*)(ws + L.sab) : nullptr};
     sa.ts[which] = ts;
     sa.toff[which] = (long long*)(ws + (which ? L.toff1 : L.toff0));
     sa.status[which] = (unsigned long long*)(ws + (which ? L.st1 : L.st0));
@@ -3239,6 +3258,7 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
     mf[0].hdr = hdr;
     mf[0].hout = pl->res.dpin;
   }
+  if (pl->pr[0].mode == 0) mf[0].sab = (const int2*)(ws + L.sab);  // written by this plan's count pass
   if (nmat == 1) mf[1] = mf[0];
   if (pl->general) {
     CK(fork_aux(pl, st, nmat));  // heavy rows of matrix `which` on aux[which]
@@ -3288,11 +3308,22 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
   // graph into pinned host memory), so sun_plan_nnz only waits for the stream
   const bool readback = kind != 1 && pl->hpin;
   const bool mapped = pl->res.dpin != nullptr;  // the scan stores the header into hpin itself
+  // event records (external: event-record nodes under capture) around the phases when timing
+  auto tmark = [&](cudaStream_t s, int i) -> int {
+    if (!pl->timing) return SUN_OK;
+    const cudaError_t e = s == pl->cap_stream ? cudaEventRecordWithFlags(pl->tev[i], s, cudaEventRecordExternal)
+                                              : cudaEventRecord(pl->tev[i], s);
+    return e == cudaSuccess ? SUN_OK : cuda_fail(e);
+  };
   auto direct = [&](cudaStream_t s) -> int {
     int rc = SUN_OK;
     const bool fill_hdr = kind == 2 && header_in_fill(pl);
-    if (kind != 1) rc = enqueue_count(pl, s, !fill_hdr, kind == 0 || pl->pdl_run);
+    if (kind != 1) rc = tmark(s, 0);
+    if (rc == SUN_OK && kind != 1) rc = enqueue_count(pl, s, !fill_hdr, kind == 0 || pl->pdl_run);
+    if (rc == SUN_OK && kind != 0) rc = tmark(s, 1);
     if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s, fill_hdr, kind == 2);
+    if (rc == SUN_OK && kind == 0) rc = tmark(s, 1);
+    if (rc == SUN_OK && kind != 0) rc = tmark(s, 2);
     if (rc == SUN_OK && readback && !mapped) {
       const cudaError_t e =
           cudaMemcpyAsync(pl->hpin, pl->ws + pl->lay.hdr, sizeof(HeaderPrefix), cudaMemcpyDeviceToHost, s);
@@ -3308,6 +3339,7 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
       if (e != cudaSuccess) return cuda_fail(e);
     }
     if (rc == SUN_OK && kind != 1 && !pl->general) ++pl->seq_expect;  // k_expand ran once more
+    if (rc == SUN_OK && pl->timing) pl->timed_kind = kind;
     if (rc == SUN_OK && kind == 2 && mapped && header_in_fill(pl)) pl->hdr_poll = 1;
     return rc;
   };
@@ -3675,6 +3707,38 @@ int sun_rk4_plan(sun_plan pl, double eps0, double eps1, double omega, double t0,
 int sun_plan_set_graphs(sun_plan pl, int32_t enable) {
   if (!pl) return SUN_ERR_ARG;
   pl->use_graphs = enable != 0;
+  return SUN_OK;
+}
+
+int sun_plan_set_timing(sun_plan pl, int32_t enable) {
+  if (!pl) return SUN_ERR_ARG;
+  const int on = enable != 0;
+  if (on == pl->timing) return SUN_OK;
+  for (int i = 0; i < 3 && on; ++i)
+    if (!pl->tev[i]) CK(cudaEventCreate(&pl->tev[i]));
+  for (auto& g : pl->graphs) cudaGraphExecDestroy(g.exec);  // captured with / without the records
+  pl->graphs.clear();
+  pl->seen.clear();
+  pl->timing = on;
+  pl->timed_kind = -1;
+  return SUN_OK;
+}
+
+int sun_plan_phase_ms(sun_plan pl, float* count_ms, float* fill_ms) {
+  if (!pl) return SUN_ERR_ARG;
+  if (!pl->timing || pl->timed_kind < 0) return SUN_ERR_STATE;
+  const int k = pl->timed_kind;
+  float c = -1.0f, f = -1.0f;
+  if (k != 1) {
+    CK(cudaEventSynchronize(pl->tev[1]));
+    CK(cudaEventElapsedTime(&c, pl->tev[0], pl->tev[1]));
+  }
+  if (k != 0) {
+    CK(cudaEventSynchronize(pl->tev[2]));
+    CK(cudaEventElapsedTime(&f, pl->tev[1], pl->tev[2]));
+  }
+  if (count_ms) *count_ms = c;
+  if (fill_ms) *fill_ms = f;
   return SUN_OK;
 }
 

@@ -148,6 +148,26 @@ __device__ __forceinline__ void warp_pairs(int n, long long p_first, int& a, int
   b += k;
 }
 
+// Pairs of a warp whose first pair (a0, b0) is known (every lane holds it): the walk of
+// warp_pairs without the decode.
+__device__ __forceinline__ void warp_pairs_from(int n, int a0, int b0, int& a, int& b) {
+  int k = threadIdx.x & 31;
+  a = a0;
+  b = b0;
+  while (b + k >= n) {
+    if (a >= n - 2) {  // past the last pair (caller masks p >= NP)
+      a = n - 2;
+      b = n - 1;
+      k = 0;
+      break;
+    }
+    k -= n - b;
+    a += 1;
+    b = a + 1;
+  }
+  b += k;
+}
+
 // local upper-triangle index k in an nw x nw window -> (i, j), i < j
 __device__ __forceinline__ void win_decode(int nw, int k, int& i, int& j) {
   int r = 0;

@@ -160,6 +160,31 @@ def test_nnz_readback_pooled_slots():
         plan.close()
 
 
+def test_phase_timing():
+    """sun_plan_set_timing / sun_plan_phase_ms: event records around the count and fill passes
+    inside the (captured) sequence; outputs unchanged, phase times positive, state errors."""
+    sun = _gpu()
+    prob = config(2)
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    ref = plan.run()
+    with pytest.raises(sun.SunError):
+        plan.phase_ms()  # timing off
+    plan.set_timing(True)
+    with pytest.raises(sun.SunError):
+        plan.phase_ms()  # no timed sequence yet
+    for _ in range(3):  # direct, then captured with event-record nodes, then replayed
+        out = plan.run()
+        c, f = plan.phase_ms()
+        assert c > 0 and f > 0
+    torch.cuda.synchronize()
+    assert torch.equal(out[0].val, ref[0].val) and torch.equal(out[1].val, ref[1].val) and torch.equal(out[2], ref[2])
+    plan.count()
+    c, f = plan.phase_ms()
+    assert c > 0 and f == -1.0
+    plan.set_timing(False)
+    plan.close()
+
+
 def test_apply_matches_lindbladian_c4():
     """Q(t) v + K from the GPU (sun_apply) equals proj L(t)(rho) for a random density matrix."""
     sun = _gpu()
