@@ -69,6 +69,7 @@ struct DevHeader {
   unsigned int seq, pad2;            // banded count sequences run on this plan (k_expand counts)
   unsigned int ticket[2];            // chained-scan chunk tickets
   unsigned int done;                 // count-pass CTA completion counter (scan by the last CTA)
+  unsigned long long wctr[2];        // fill: dynamic warp-unit counter, finished warps (reset by the last)
   int bw[MAXOPS];
   double nrm2[MAXOPS];
 };
@@ -793,6 +794,9 @@ struct MatCount {
 // no dissipators) in one launch of single-warp CTAs:
 //   [Q0 near items][Q1 near items][Q0 far slots][Q1 far slots]   (long near items first)
 template <int WK, int WL, int PT, int Q1W>
+#ifndef SUN_FILL_DYN
+#define SUN_FILL_DYN 1  // k_fill0: warp-level units claimed from a global counter (combined plans)
+#endif
 #ifndef SUN_PDL_DEFAULT
 #define SUN_PDL_DEFAULT 3  // launches with the PDL attribute (bits: 1 count, 2 scan, 4 near, 8 fill);
 // measured at c4 (B200, bench step, same box): sun_count's sequence 42.7 -> 39.6 us with count +
@@ -949,14 +953,15 @@ constexpr int NEAR_RPW = SUN_NEAR_RPW;        // near rows per warp (lane groups
 constexpr int NEAR_GL = 32 / NEAR_RPW;        // lanes per row
 constexpr int NEAR_UROWS = 8 * NEAR_RPW;      // side rows per near unit
 // inv: the inv[l] table (SMEM_INV: a shared-memory copy, else global through the read-only path).
+// srow0: the warp's first side row (its NEAR_RPW rows are srow0, srow0 + 1, ...)
 template <bool SMEM_INV>
-__device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, const int* __restrict__ cnt,
+__device__ __forceinline__ void fill_near_rows_w(const Prob& pr, long long srow0, const int* __restrict__ cnt,
                                                  const FillOut& fo, const NearSide& side, const double* inv) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int hl = lane & (NEAR_GL - 1);
   const long long np = pr.np;
   const long long nside = 2 * ((long long)pr.n * 2 * pr.W + pr.n - 1);
-  const long long srow = j * NEAR_UROWS + wid * NEAR_RPW + lane / NEAR_GL;
+  const long long srow = srow0 + lane / NEAR_GL;
   int kind = 0, half = 0, a = 0, b = 0, lam = 0;
   long long p = 0;
   if (srow < nside) {
@@ -1020,6 +1025,13 @@ __device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, co
       fo.val[ot + k] = v;
     }
   }
+}
+
+// near unit j: side rows j NEAR_UROWS .. + NEAR_UROWS - 1 over the CTA's 8 warps
+template <bool SMEM_INV>
+__device__ __forceinline__ void fill_near_unit_h(const Prob& pr, long long j, const int* __restrict__ cnt,
+                                                 const FillOut& fo, const NearSide& side, const double* inv) {
+  fill_near_rows_w<SMEM_INV>(pr, j * NEAR_UROWS + (threadIdx.x >> 5) * NEAR_RPW, cnt, fo, side, inv);
 }
 
 __host__ __device__ inline long long near_units1(long long n, long long W) {  // units of 8 side rows
@@ -1204,10 +1216,12 @@ struct TileIn {
   long long baseS, baseJ;
   int2 ab;  // first pair of the warp's slot (count pass table), x < 0: decode it
 };
+// w: the warp's slot within the tile (its 32 pairs)
 __device__ __forceinline__ TileIn load_tile_in(long long np, long long npt, long long t, const int* __restrict__ cnt,
-                                               const long long* __restrict__ toff, const int2* __restrict__ sab) {
-  const long long p = t * TP0 + threadIdx.x;
-  const long long slot = t * SLOTS_PER_TILE + (threadIdx.x >> 5);  // the warp's 32 pairs
+                                               const long long* __restrict__ toff, const int2* __restrict__ sab,
+                                               int w) {
+  const long long p = t * TP0 + w * 32 + (threadIdx.x & 31);
+  const long long slot = t * SLOTS_PER_TILE + w;
   TileIn ti;
   ti.cS = p < np ? cnt[p] : 0;
   ti.cJ = p < np ? cnt[np + p] : 0;
@@ -1217,25 +1231,25 @@ __device__ __forceinline__ TileIn load_tile_in(long long np, long long npt, long
   return ti;
 }
 // the pairs of this warp's 32 lanes in far tile t: from the slot table, else decoded
-__device__ __forceinline__ void tile_pairs(int n, long long t, int2 ab, int& a, int& b) {
+__device__ __forceinline__ void tile_pairs(int n, long long t, int w, int2 ab, int& a, int& b) {
   if (ab.x >= 0)
     warp_pairs_from(n, ab.x, ab.y, a, b);
   else
-    warp_pairs(n, t * TP0 + (threadIdx.x >> 5) * 32, a, b);
+    warp_pairs(n, t * TP0 + w * 32, a, b);
 }
 
 template <int WK, int WL, int PT>
-__device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, long long t, const TileIn& ti,
+__device__ __forceinline__ void fill_far_tile(const FarCtx& pr, long long npt, long long t, int w, const TileIn& ti,
                                               const FillOut& fo, int* scol, double* sval) {
   using MC = Mode0<WK, WL>;
   using FF = FillFar<WK, WL>;
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const long long np = pr.np;
-  const long long p = t * TP0 + threadIdx.x;
+  const long long p = t * TP0 + w * 32 + lane;
   const bool valid = p < np;
   const int cS = ti.cS, cJ = ti.cJ;
   int a, b;
-  tile_pairs(pr.n, t, ti.ab, a, b);
+  tile_pairs(pr.n, t, w, ti.ab, a, b);
   const bool far = valid && (b - a > 2 * MC::W);
   const bool nearp = valid && !far;
   // U values first, for every lane (any 0 <= a < b < n is a safe address set; non-far lanes
@@ -1417,21 +1431,21 @@ __device__ __forceinline__ void fill_direct_tile(const FarCtx& pr, long long npt
 // pairs "far" at width 0, rows of <= 2 entries): Q1's scan slot t covers the same 256 pairs,
 // so the warp's offset is the slot offset plus the counts of the tile's earlier warps.
 __device__ __forceinline__ void fill_q1_chunk(const FarCtx& f1, long long npt1, long long t, const int* __restrict__ cnt1,
-                                              const FillOut& fo, int2 ab) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+                                              const FillOut& fo, int2 ab, int w) {
+  const int lane = threadIdx.x & 31;
   const long long np = f1.np;
-  const long long p = t * TP0 + threadIdx.x;
+  const long long p = t * TP0 + w * 32 + lane;
   const bool valid = p < np;
   // every load of the chunk issued before the first use (counts, slot offsets, the drive's
   // diagonal values), one round trip
   int a, b;  // walked again (cheaper than keeping the far tile's pair live across its staging)
-  tile_pairs(f1.n, t, ab, a, b);
+  tile_pairs(f1.n, t, w, ab, a, b);
   const int c = valid ? __ldg(&cnt1[p]) : 0;  // S and J rows of a pair have the same length
   int bq[TP0 / 32 - 1];
 #pragma unroll
   for (int i = 0; i < TP0 / 32 - 1; ++i) {  // the tile's earlier warps
     const long long q = t * TP0 + i * 32 + lane;
-    bq[i] = (i < wid && q < np) ? __ldg(&cnt1[q]) : 0;
+    bq[i] = (i < w && q < np) ? __ldg(&cnt1[q]) : 0;
   }
   const long long b0S = __ldg(&fo.toff[t]), b0J = __ldg(&fo.toff[npt1 + t]);
   double ux[1], uy[1];
@@ -1470,6 +1484,7 @@ struct MatFill {
   const DevHeader* hdr;  // with hout (sun_run of modes 0 / 2): CTA 0 stores the header prefix into
   HeaderPrefix* hout;    // mapped host memory at the start of the fill (final since the scan)
   const int2* sab;       // mode 0, Q0: first pair of each scan slot (count pass), or nullptr
+  unsigned long long* wctr;  // dynamic warp-level units (SUN_FILL_DYN; DevHeader::wctr), or nullptr
 };
 
 // header prefix -> mapped pinned host memory (sun_plan_nnz reads it after the stream)
@@ -1548,8 +1563,70 @@ __global__ void __launch_bounds__(256, FillFar<WK, WL>::MINB) k_fill0(const MatF
   auto prefetch = [&](long long v) {
     long long idx;
     if (v < U && decode(v, idx) == 0 && !FF::DIRECT)
-      nxt = load_tile_in(m0.pr.np, m0.pr.npt, idx, m0.cnt, m0.fo.toff, m0.sab);
+      nxt = load_tile_in(m0.pr.np, m0.pr.npt, idx, m0.cnt, m0.fo.toff, m0.sab, wid);
   };
+#if SUN_FILL_DYN
+  if constexpr (!FF::DIRECT && (Q1MERGED || !HAS1)) {
+    if (m0.wctr && !m0.tile_sync) {
+      // Warp-level units claimed dynamically (the SMs finished up to 9 % apart with CTA units
+      // assigned round robin): near units of NEAR_RPW side rows, then the far slots (32 pairs,
+      // last first); each warp's first unit is static, the next one is claimed from a global
+      // counter one unit ahead (its tile inputs prefetched).  The last warp to finish resets it.
+      const long long nside = 2 * (m0.pr.n * 2LL * m0.pr.W + m0.pr.n - 1);
+      const long long nw0 = m0.near_sep ? 0 : (nside + NEAR_RPW - 1) / NEAR_RPW;
+      const long long ns0 = nt0 * SLOTS_PER_TILE;
+      const long long UW = nw0 + ns0;
+      const long long nwarps = (long long)gridDim.x * (blockDim.x >> 5);
+      auto claim = [&]() -> long long {
+        unsigned long long v = 0;
+        if (lane == 0) v = atomicAdd(m0.wctr, 1ull);
+        return (long long)__shfl_sync(FULL, v, 0) + nwarps;
+      };
+      auto slot_of = [&](long long v, long long& t, int& w) {  // v >= nw0: far slot, last first
+        const long long sl = ns0 - 1 - (v - nw0);
+        t = sl / SLOTS_PER_TILE;
+        w = (int)(sl % SLOTS_PER_TILE);
+      };
+      TileIn nw{0, 0, 0, 0, make_int2(-1, -1)};
+      auto wprefetch = [&](long long v) {
+        if (v >= nw0 && v < UW) {
+          long long t;
+          int w;
+          slot_of(v, t, w);
+          nw = load_tile_in(m0.pr.np, m0.pr.npt, t, m0.cnt, m0.fo.toff, m0.sab, w);
+        }
+      };
+      long long u = (long long)blockIdx.x * (blockDim.x >> 5) + wid;
+      wprefetch(u);
+      while (u < UW) {  // warp-uniform
+        const TileIn cur = nw;
+        const long long un = claim();
+        wprefetch(un);
+        if (u < nw0) {
+#ifndef SUN_EXP_NO_NEAR
+          fill_near_rows_w<false>(m0.pr, u * NEAR_RPW, m0.cnt, m0.fo, m0.side, m0.pr.inv);
+#endif
+        } else {
+          long long t;
+          int w;
+          slot_of(u, t, w);
+          fill_far_tile<WK, WL, PT>(prf0, m0.pr.npt, t, w, cur, m0.fo, scol, sval);
+          if constexpr (Q1MERGED) fill_q1_chunk(prf1, m1.pr.npt, t, m1.cnt, m1.fo, cur.ab, w);
+        }
+        u = un;
+      }
+      if (lane == 0) {
+        bulk_wait0();  // staging must outlive the bulk reads
+        __threadfence();
+        if (atomicAdd(m0.wctr + 1, 1ull) == (unsigned long long)nwarps - 1) {  // every claim is done
+          m0.wctr[0] = 0ull;
+          m0.wctr[1] = 0ull;
+        }
+      }
+      return;
+    }
+  }
+#endif
   prefetch(blockIdx.x);
   for (long long u = blockIdx.x; u < U; u += gridDim.x) {  // block-uniform
     const TileIn cur = nxt;
@@ -1564,8 +1641,8 @@ __global__ void __launch_bounds__(256, FillFar<WK, WL>::MINB) k_fill0(const MatF
       if constexpr (FF::DIRECT)
         fill_direct_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, m0.cnt, m0.fo);
       else
-        fill_far_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, cur, m0.fo, scol, sval);
-      if constexpr (Q1MERGED) fill_q1_chunk(prf1, m1.pr.npt, idx, m1.cnt, m1.fo, cur.ab);
+        fill_far_tile<WK, WL, PT>(prf0, m0.pr.npt, idx, wid, cur, m0.fo, scol, sval);
+      if constexpr (Q1MERGED) fill_q1_chunk(prf1, m1.pr.npt, idx, m1.cnt, m1.fo, cur.ab, wid);
     } else if (kind == 1) {
 #ifndef SUN_EXP_NO_NEAR
       fill_near_unit_h<false>(m0.pr, idx, m0.cnt, m0.fo, m0.side, m0.pr.inv);
@@ -3259,6 +3336,7 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
     mf[0].hout = pl->res.dpin;
   }
   if (pl->pr[0].mode == 0) mf[0].sab = (const int2*)(ws + L.sab);  // written by this plan's count pass
+  if (pl->combined) mf[0].wctr = hdr->wctr;  // k_fill0's dynamic warp units (SUN_FILL_DYN)
   if (nmat == 1) mf[1] = mf[0];
   if (pl->general) {
     CK(fork_aux(pl, st, nmat));  // heavy rows of matrix `which` on aux[which]
