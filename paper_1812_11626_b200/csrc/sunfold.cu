@@ -763,11 +763,29 @@ __device__ __forceinline__ void count_far_slot(const FarCtx& pr, long long npt, 
     if (j) pair_advance(pr.n, a, b, 32);
     const bool far = p < np && (b - a > 2 * MC::W);
     if (far) {
-      double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
-      far_values<WK, WL, PT>(pr, a, b, ux, uy);
-      typename FarT<WK, WL>::Mask mr, mi;
-      far_masks<WK, WL>(pr.n, pr.tau, a, b, ux, uy, mr, mi);
-      const int cp = mpopc(mr) + mpopc(mi);
+      int cp = 0;
+      if constexpr (FarT<WK, WL>::NPOS > 32) {
+        // wide bands: the positions one by one with the per-position expression (far_value_at:
+        // the same operations as far_values, so the fill's decisions agree bit for bit) -- the
+        // 33 complex values of far_values would hold ~240 registers (8 count warps per SM)
+        Prob pp{};
+        pp.n = pr.n;
+        pp.P = pr.P;
+        pp.K.v = pr.K;
+        pp.L = pr.L;
+#pragma unroll
+        for (int k = 0; k < FarT<WK, WL>::NPOS; ++k) {
+          double x, y;
+          int cc, dd;
+          if (far_value_at<WK, WL, PT>(pp, a, b, k, x, y, cc, dd)) cp += (fabs(x) > pr.tau) + (fabs(y) > pr.tau);
+        }
+      } else {
+        double ux[FarT<WK, WL>::NPOS], uy[FarT<WK, WL>::NPOS];
+        far_values<WK, WL, PT>(pr, a, b, ux, uy);
+        typename FarT<WK, WL>::Mask mr, mi;
+        far_masks<WK, WL>(pr.n, pr.tau, a, b, ux, uy, mr, mi);
+        cp = mpopc(mr) + mpopc(mi);
+      }
       cnt[p] = cp;
       cnt[np + p] = cp;
       c += cp;
