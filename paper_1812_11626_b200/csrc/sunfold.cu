@@ -808,10 +808,6 @@ struct MatCount {
   int2* sab;  // mode 0: first pair (a, b) of each scan slot, for the fill (nullptr: not stored)
 };
 
-// Count pass of Q0 (compile-time widths WK, WL, PT) and, with Q1W >= 0, of Q1 (widths Q1W, 0,
-// no dissipators) in one launch of single-warp CTAs:
-//   [Q0 near items][Q1 near items][Q0 far slots][Q1 far slots]   (long near items first)
-template <int WK, int WL, int PT, int Q1W>
 #ifndef SUN_FILL_DYN
 #define SUN_FILL_DYN 1  // k_fill0: warp-level units claimed from a global counter (combined plans)
 #endif
@@ -824,18 +820,31 @@ template <int WK, int WL, int PT, int Q1W>
 #ifndef SUN_PDL_COUNT
 #define SUN_PDL_COUNT 1  // 0: no PDL code in the count kernel, 1: wait only, 2: wait + early trigger
 #endif
-__global__ void __launch_bounds__(32) k_count0(const MatCount m0, const MatCount m1) {
-#if SUN_PDL_COUNT == 1
-  pdl_wait();
-#elif SUN_PDL_COUNT == 2
-  pdl_enter();
-#endif
-  constexpr int Q1K = Q1W > 0 ? Q1W : 0;
-  constexpr int PW0 = Mode0<WK, WL>::PER_WARP, PW1 = Mode0<Q1K, 0>::PER_WARP;
-  __shared__ double scr[PW0 > PW1 ? PW0 : PW1];
-  constexpr bool HAS1 = Q1W >= 0;
+
+// One unit of the count pass of Q0 (compile-time widths WK, WL, PT) and, with Q1W >= 0, of Q1
+// (widths Q1W, 0, no dissipators), warp-cooperative; units in the order
+//   [Q0 near items][Q1 near items][Q0 far slots][Q1 far slots]   (long near items first)
+// scr: the warp's shared scratch (Mode0 PER_WARP doubles).
+template <int WK, int WL, int PT, int Q1W>
+struct Count0 {
+  static constexpr int Q1K = Q1W > 0 ? Q1W : 0;
+  static constexpr int PW0 = Mode0<WK, WL>::PER_WARP, PW1 = Mode0<Q1K, 0>::PER_WARP;
+  static constexpr int PW = PW0 > PW1 ? PW0 : PW1;
+  static constexpr bool HAS1 = Q1W >= 0;
+  static __host__ __device__ long long near_units(const MatCount& m0, const MatCount& m1) {
+    return m0.pr.nb_near + (HAS1 ? m1.pr.nb_near : 0);
+  }
+  static __host__ __device__ long long units(const MatCount& m0, const MatCount& m1) {
+    return near_units(m0, m1) + m0.pr.npt + (HAS1 ? m1.pr.npt : 0);
+  }
+};
+
+template <int WK, int WL, int PT, int Q1W>
+__device__ __forceinline__ void count0_unit(const MatCount& m0, const MatCount& m1, long long u, double* scr) {
+  using C = Count0<WK, WL, PT, Q1W>;
+  constexpr int Q1K = C::Q1K;
+  constexpr bool HAS1 = C::HAS1;
   const long long nn0 = m0.pr.nb_near, nn1 = HAS1 ? m1.pr.nb_near : 0;
-  long long u = blockIdx.x;
   if (u < nn0) {
     Prob prn = m0.pr;
     prn.tau = *m0.pr.tau_ptr;
@@ -873,6 +882,18 @@ __global__ void __launch_bounds__(32) k_count0(const MatCount m0, const MatCount
     const FarCtx prf{m1.pr.K.v, m1.pr.L, *m1.pr.tau_ptr, m1.pr.np, m1.pr.n, m1.pr.P};
     count_far_slot<Q1K, 0, 0>(prf, m1.pr.npt, u, m1.cnt, m1.tsum, nullptr);
   }
+}
+
+// one single-warp CTA per unit
+template <int WK, int WL, int PT, int Q1W>
+__global__ void __launch_bounds__(32) k_count0(const MatCount m0, const MatCount m1) {
+#if SUN_PDL_COUNT == 1
+  pdl_wait();
+#elif SUN_PDL_COUNT == 2
+  pdl_enter();
+#endif
+  __shared__ double scr[Count0<WK, WL, PT, Q1W>::PW];
+  count0_unit<WK, WL, PT, Q1W>(m0, m1, blockIdx.x, scr);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -2729,8 +2750,8 @@ template <int WK, int WL, int PT, int Q1W>
 cudaError_t launch_count0(const MatCount& m0, const MatCount& m1, cudaStream_t st, bool pdl) {
   auto warps = [](const Prob& p) { return p.npt; };  // one count warp per scan slot
   const long long U = warps(m0.pr) + m0.pr.nb_near + (Q1W >= 0 ? warps(m1.pr) + m1.pr.nb_near : 0);
-  if (U > 0) return launch_k(pdl, k_count0<WK, WL, PT, Q1W>, dim3((unsigned)U), dim3(32), 0, st, m0, m1);
-  return cudaGetLastError();
+  if (U <= 0) return cudaGetLastError();
+  return launch_k(pdl, k_count0<WK, WL, PT, Q1W>, dim3((unsigned)U), dim3(32), 0, st, m0, m1);
 }
 
 // called at plan creation (outside any graph capture): dynamic shared memory limit and the
