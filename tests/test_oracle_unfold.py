@@ -89,7 +89,7 @@ def test_o1_hamiltonian_part_skew_and_specials(n):
     Q1_, K1_ = dense.unfold_dense(H, [L1], [0.3])
     Q2_, K2_ = dense.unfold_dense(0 * H, [L2], [0.4])
     assert np.abs(Qa - (Q1_ + Q2_)).max() < 1e-12 * np.abs(Qa).max()
-    assert np.abs(Ka - (K1_ + K2_)).max() < 1e-12 * max(1, np.abs(Ka).max())
+    assert np.abs(Ka - (K1_ + K2_)).max() < 1e-12 * np.abs(Ka).max()
 
 
 @pytest.mark.parametrize("n", [2, 3, 5])
@@ -161,7 +161,8 @@ def test_o2_equals_o1(prob):
     r = sparse.unfold_csr(prob.H0, prob.Ls, prob.gammas, tau)
     assert np.array_equal(rp, r["row_ptr"]) and np.array_equal(ci, r["col"])
     assert np.abs(val - r["val"]).max() <= 1e-13 * np.abs(val).max()
-    assert np.abs(K - r["K"]).max() <= 1e-13 * max(1.0, np.abs(K).max())
+    sparse.assert_k_close(r["K"], K, prob.name + ":K", tau)
+    assert np.abs(K - r["K"]).max() <= 1e-13 * np.abs(K).max() or np.abs(K).max() <= tau
     sparse.assert_r6(r, tau, prob.name)
     if prob.H1 is not None:
         Q1, _ = dense.unfold_dense(prob.H1.to_dense())
@@ -181,7 +182,7 @@ def test_o2_c1_matches_o1():
     r = sparse.unfold_csr(prob.H0, prob.Ls, prob.gammas, tau)
     assert np.array_equal(rp, r["row_ptr"]) and np.array_equal(ci, r["col"])
     assert np.abs(val - r["val"]).max() <= 1e-12 * np.abs(val).max()
-    assert np.abs(K - r["K"]).max() <= 1e-12 * max(1.0, np.abs(K).max())
+    sparse.assert_k_close(r["K"], K, prob.name + ":K", tau)
 
 
 def _dense_lindblad_coeffs(prob, rho, eps):
