@@ -246,6 +246,21 @@ int sun_apply_plan(sun_plan plan, double eps, const double* v, double* dvdt, voi
  * sets the default to 0.  Errors: SUN_ERR_ARG. */
 int sun_plan_set_graphs(sun_plan plan, int32_t enable);
 
+/* Light-row stash of a general-pattern plan (mode 3).  The count pass assembles
+ * every row from its candidate terms (gather, sort by key, segmented reduction); with a stash,
+ * it also writes each light pair's two assembled rows (<= GW_CAP candidates, at most
+ * sun_plan_stash_bytes' per-row capacity of entries) into the stash, and the fill pass copies
+ * them to their CSR offsets instead of assembling them a second time (bit-identical output:
+ * the stash is written by the same operations in the same order as the fill's own writing
+ * pass).  sun_plan_stash_bytes: bytes the stash needs (0 for banded plans, whose fill does
+ * not assemble rows).  sun_plan_set_stash: `buf` = device memory of at least that many bytes,
+ * 256-byte aligned, caller-owned, kept until the plan is destroyed or the stash is changed;
+ * buf = NULL switches the stash off (the default).  Changing it drops the plan's cached
+ * graphs and requires a new count pass before the next fill (SUN_ERR_STATE otherwise).
+ * Errors: SUN_ERR_ARG (null plan; buffer too small or misaligned; a banded plan). */
+size_t sun_plan_stash_bytes(sun_plan plan);
+int sun_plan_set_stash(sun_plan plan, void* buf, size_t bytes);
+
 /* Phase timing (SURVEY §5 tracing; bench.py's roofline): with enable = 1, every sun_run /
  * sun_count / sun_unfold sequence of this plan records CUDA events (event-record nodes of its
  * graph) before the count pass (expand + count + scan), between count and fill, and after the

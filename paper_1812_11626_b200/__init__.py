@@ -190,6 +190,9 @@ class Plan:
         self._plan = plan
         self._caps = None  # output capacities for run(): previous nnz
         self._banded = self.info()["mode_q0"] != 3
+        self.stash = None
+        if not self._banded:
+            self.set_stash(True)
 
     def workspace_guard_intact(self) -> bool:
         if not self._guard:
@@ -327,6 +330,27 @@ class Plan:
         """Kernels of this library launched by one run() (sun_run: count + fill)."""
         inf = self.info()
         return int(inf["launches_count"] + inf["launches_fill"])
+
+    #: largest light-row stash set_stash(True) allocates (and at most a quarter of free memory)
+    STASH_MAX_BYTES = 8 << 30
+
+    def set_stash(self, enable: bool) -> bool:
+        """General-pattern plans: a device buffer in which the count pass keeps the assembled light
+        rows, so the fill copies them (sun_plan_set_stash; bit-identical output).  Enabled at plan
+        creation when it fits STASH_MAX_BYTES and a quarter of the free device memory.  Returns
+        whether a stash is set.  A new count pass is needed before the next fill."""
+        L = lib()
+        nb = int(L.sun_plan_stash_bytes(self._plan))
+        buf = None
+        if enable and nb > 0:
+            free = torch.cuda.mem_get_info()[0]
+            if nb <= min(self.STASH_MAX_BYTES, free // 4):
+                with _on(self.stream):
+                    buf = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        _check(L.sun_plan_set_stash(self._plan, ctypes.c_void_p(buf.data_ptr() if buf is not None else 0),
+                                    ctypes.c_size_t(nb if buf is not None else 0)), "sun_plan_set_stash")
+        self.stash = buf
+        return buf is not None
 
     def set_graphs(self, enable: bool):
         """CUDA-graph replay of the enqueue sequences on (default) or off (sun_plan_set_graphs)."""

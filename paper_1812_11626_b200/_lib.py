@@ -47,6 +47,8 @@ SIGNATURES = {
     "sun_nnz_bound": (ctypes.c_int64, [P, ctypes.c_int32]),
     "sun_plan_info": (ctypes.c_int, [P, P]),
     "sun_plan_set_graphs": (ctypes.c_int, [P, ctypes.c_int32]),
+    "sun_plan_stash_bytes": (ctypes.c_size_t, [P]),
+    "sun_plan_set_stash": (ctypes.c_int, [P, P, ctypes.c_size_t]),
     "sun_plan_set_timing": (ctypes.c_int, [P, ctypes.c_int32]),
     "sun_plan_phase_ms": (ctypes.c_int, [P, P, P]),
     "sun_expand_state": (ctypes.c_int, [P, P, P]),

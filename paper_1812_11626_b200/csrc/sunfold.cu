@@ -255,6 +255,7 @@ struct sun_plan_s {
   NearSide side[2];
   int combined;         // mode 0 with Q1 absent or Q1 = Q_H[diagonal H1]: one launch per pass
   int near_sep = 0;     // combined: near rows by k_near0 before the fill (SUNFOLD_NEAR_SEP=1)
+  int near_conc = 0;    // near_sep: k_near0 on aux[0] concurrently with the fill (SUNFOLD_NEAR_CONC)
   int pdl = 0;          // combined: programmatic dependent launch between the sequence's kernels
   int pdl_run = 0;      // PDL also inside sun_run's sequence (SUNFOLD_PDL_RUN=1; A/B only)
   // phase timing (sun_plan_set_timing): events before the count, between count and fill, after
@@ -278,6 +279,7 @@ struct sun_plan_s {
   // mode 3 (general-pattern operators, sunfold_general.cu)
   int general = 0;
   int small_cap = 0;  // SUN_PLAN_SMALLCAP (tests)
+  char* stash = nullptr;  // mode 3: light-row stash (sun_plan_set_stash; caller-owned)
   sung::GLayout glay;
   sung::GProb gp[2];
   unsigned long long graph_clock = 0;
@@ -1702,6 +1704,9 @@ __global__ void __launch_bounds__(256, FillFar<WK, WL>::MINB) k_fill0(const MatF
 // The chain tails (up to n entries per row, tr * inv[l]) read inv[] from a shared-memory copy
 // when it fits (NEAR_SMEM_INV doubles), not one dependent L2 load per entry.
 constexpr int NEAR_SMEM_INV = 8192;
+#ifndef SUN_NEAR_CONC_DEFAULT
+#define SUN_NEAR_CONC_DEFAULT 0
+#endif
 __global__ void __launch_bounds__(256) k_near0(const MatFill m0) {
   pdl_enter();
   extern __shared__ double sinv[];
@@ -3100,6 +3105,8 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
     const char* nf = getenv("SUNFOLD_NEAR_SEP");
     const bool dflt = pl->pr[0].W >= 4;
     pl->near_sep = pl->combined && (nf && nf[0] ? nf[0] != '0' : dflt);
+    const char* nc = getenv("SUNFOLD_NEAR_CONC");
+    pl->near_conc = pl->near_sep ? (nc && nc[0] ? atoi(nc) : SUN_NEAR_CONC_DEFAULT) : 0;
   }
   pl->launches_fill = pl->combined ? 1 + pl->near_sep : nmat;
   {
@@ -3393,6 +3400,17 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
       const Prob& p0 = pl->pr[0];
       const long long nn0 = (2 * (p0.n * 2LL * p0.W + p0.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
       const size_t sm = p0.n <= NEAR_SMEM_INV ? (size_t)p0.n * sizeof(double) : 0;
+      if (nn0 > 0 && pl->near_conc) {
+        // the near rows and the far tiles write disjoint outputs: k_near0 on aux[0] beside the
+        // fill (its CTAs hold SMs until the fill's persistent CTAs, which claim units
+        // dynamically, take them over)
+        CK(fork_aux(pl, st, 1));
+        const bool swap = pl->near_conc == 2;  // A/B: the fill on the aux stream instead
+        CK(launch_k(false, k_near0, dim3((unsigned)nn0), dim3(256), sm, swap ? st : pl->aux[0], mf[0]));
+        CK(dispatch_fill0(mf[0], mf[1], pl->has_h1 ? 0 : -1, pl->fill_grid[0], swap ? pl->aux[0] : st, false));
+        CK(join_aux(pl, st, 1));
+        return SUN_OK;
+      }
       if (nn0 > 0) CK(launch_k((pl->pdl & 4) && pdl_first, k_near0, dim3((unsigned)nn0), dim3(256), sm, st, mf[0]));
     }
     CK(dispatch_fill0(mf[0], mf[1], pl->has_h1 ? 0 : -1, pl->fill_grid[0], st, (pl->pdl & 8) && pdl_first));
@@ -3824,6 +3842,26 @@ int sun_rk4_plan(sun_plan pl, double eps0, double eps1, double omega, double t0,
 int sun_plan_set_graphs(sun_plan pl, int32_t enable) {
   if (!pl) return SUN_ERR_ARG;
   pl->use_graphs = enable != 0;
+  return SUN_OK;
+}
+
+size_t sun_plan_stash_bytes(sun_plan pl) {
+  if (!pl || !pl->general) return 0;
+  return sung::g_stash_bytes(pl->n) * (size_t)(1 + pl->has_h1);
+}
+
+int sun_plan_set_stash(sun_plan pl, void* buf, size_t bytes) {
+  if (!pl) return SUN_ERR_ARG;
+  if (buf && (!pl->general || bytes < sun_plan_stash_bytes(pl) || ((uintptr_t)buf & 255))) return SUN_ERR_ARG;
+  const size_t per = sung::g_stash_bytes(pl->n);
+  for (int which = 0; which < 1 + pl->has_h1 && pl->general; ++which)
+    sung::g_stash_set(pl->gp[which], buf ? (char*)buf + which * per : nullptr);
+  pl->stash = (char*)buf;
+  if (pl->general) pl->launches_fill = (sung::G_LAUNCHES_FILL + (buf ? 1 : 0)) * (1 + pl->has_h1);  // + k_g_copy
+  for (auto& g : pl->graphs) cudaGraphExecDestroy(g.exec);  // the kernels' arguments changed
+  pl->graphs.clear();
+  pl->seen.clear();
+  pl->counted = 0;  // the next fill needs a count pass that wrote the stash
   return SUN_OK;
 }
 

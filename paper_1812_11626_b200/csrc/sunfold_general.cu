@@ -20,7 +20,7 @@ constexpr unsigned FULLM = 0xffffffffu;
 constexpr int GF_MALFORMED = 1, GF_TOOBIG = 16;  // header flags (sunfold.cu F_*)
 constexpr int GE_THREADS = 256;                  // expand: rows per CTA
 #ifndef SUN_GW_CAP
-#define SUN_GW_CAP 128
+#define SUN_GW_CAP 256
 #endif
 #ifndef SUN_GW_WARPS
 #define SUN_GW_WARPS 8
@@ -845,16 +845,23 @@ __device__ __forceinline__ void warp_sort_regs(unsigned long long* key, int cnt)
     for (int j = k >> 1; j > 0; j >>= 1) {
       if (j >= 32) {  // partner in another register of this lane
         const int jq = j >> 5;
+        // register distance as a compile-time constant (a runtime q ^ jq index would put v[]
+        // in local memory)
 #pragma unroll
-        for (int q = 0; q < R; ++q) {
-          const int q2 = q ^ jq;
-          if (q2 > q && q2 < R) {
-            const int e = lane + 32 * q;
-            const bool asc = (e & k) == 0;
-            const unsigned long long a = v[q], b = v[q2];
-            if ((a > b) == asc) {
-              v[q] = b;
-              v[q2] = a;
+        for (int t = 1; t < R; t <<= 1) {
+          if (jq == t) {
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+              const int q2 = q ^ t;
+              if (q2 > q && q2 < R) {
+                const int e = lane + 32 * q;
+                const bool asc = (e & k) == 0;
+                const unsigned long long a = v[q], b = v[q2];
+                if ((a > b) == asc) {
+                  v[q] = b;
+                  v[q2] = a;
+                }
+              }
             }
           }
         }
@@ -879,10 +886,11 @@ __device__ __forceinline__ void warp_sort_regs(unsigned long long* key, int cnt)
 template <int NT, int CAP>
 __device__ __forceinline__ void sort_gathered(GBuf<CAP>& B) {
   if constexpr (NT == 32) {
-    static_assert(CAP <= 128, "register sort holds <= 4 keys per lane");
+    static_assert(CAP <= 256, "register sort holds <= 8 keys per lane");
     const int c = B.cnt;
     if (c <= 32) warp_sort_regs<1>(B.key, c);
     else if (c <= 64) warp_sort_regs<2>(B.key, c);
+    else if (c <= 128 || CAP <= 128) warp_sort_regs<(CAP < 128 ? CAP : 128) / 32>(B.key, c);
     else warp_sort_regs<CAP / 32>(B.key, c);
   } else {
     bitonic<NT>(B.key, B.slot, B.cnt);
@@ -1188,9 +1196,56 @@ __device__ void run_item(const GProb& G, const Item& it, long long idx, unsigned
     }
   }
   if (!FILL) {
-    if (path == 2) frame_sweep<NT, CAP>(G, it, nsrc, B, kmin, kmax, rs, PASS_COUNT, tau, O);
-    else sweep<NT, CAP>(G, it, nsrc, C, B, X, rs, PASS_COUNT, tau, O);
-    d_tail(G, it, rs, PASS_COUNT, tau, O);
+    // D row with a stash: the writing pass into the row's three stash segments (S, J, D parts at
+    // fixed offsets), which counts exactly as the counting pass does
+    const bool dst = it.kind == 1 && G.dseg > 0;
+    GOut CO = O;
+    int pc = PASS_COUNT;
+    if (dst) {
+      rs.O[0] = (long long)(it.lam - 1) * G.drow;
+      rs.TS[0] = rs.TJ[0] = G.dseg;
+      CO = GOut{nullptr, G.dcol, G.dval, (long long)it.lam * G.drow, nullptr, nullptr, nullptr};
+      pc = PASS_WRITE;
+    }
+    if (path == 2) frame_sweep<NT, CAP>(G, it, nsrc, B, kmin, kmax, rs, pc, tau, CO);
+    else sweep<NT, CAP>(G, it, nsrc, C, B, X, rs, pc, tau, CO);
+    d_tail(G, it, rs, (threadIdx.x < 32 || NT == 32) ? pc : PASS_COUNT, tau, CO);  // warp 0 owns the chain
+    if (dst && threadIdx.x == 0) {
+      const bool ok = rs.nS[0] <= G.dseg && rs.nJ[0] <= G.dseg;
+      G.dflag[it.lam - 1] = ok ? 1 : 0;
+      if (ok) G.dK[it.lam - 1] = rs.P[0] / (double)G.n;  // K_s = Tr(G_s)/N, as the fill writes it
+    }
+    if constexpr (NT == 32) {
+      // light pair (one sorted chunk, still in B): replay the fill's writing pass into the
+      // stash rows (same operations, same order as the fill's path 0: bit-identical entries)
+      if (G.scap > 0 && it.kind == 0) {
+        const bool ok = path == 0 && rs.nS[0] + rs.nJ[0] + rs.nD[0] <= G.scap &&
+                        rs.nS[1] + rs.nJ[1] + rs.nD[1] <= G.scap;
+        if (ok) {
+          RowState ws = rs;
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            ws.TS[r] = rs.nS[r];
+            ws.TJ[r] = rs.nJ[r];
+            ws.nS[r] = ws.nJ[r] = ws.nD[r] = 0;
+            ws.P[r] = 0.0;
+          }
+          ws.prev = 1;
+          ws.O[0] = idx * G.scap;
+          ws.O[1] = (np + idx) * G.scap;
+          const GOut SO{nullptr, G.scol, G.sval, 0x7fffffffffffffffLL, nullptr, nullptr, nullptr};
+          assemble_runs<NT, CAP>(G, it, B, ws, PASS_WRITE, tau, SO);
+          d_chain<NT, CAP>(G, it, B, ws, PASS_WRITE, tau, SO);
+          d_tail(G, it, ws, PASS_WRITE, tau, SO);
+          if (lane == 0) {  // K_s = Tr(G_s)/N, as the fill writes it
+            G.sK[idx] = ws.P[0] / (double)G.n;
+            G.sK[np + idx] = ws.P[1] / (double)G.n;
+          }
+        }
+        if (lane == 0) G.sflag[idx] = ok ? 1 : 0;
+        __syncwarp();
+      }
+    }
     if (grank<NT>() == 0) {
       if (it.kind == 0) {
         const int t0 = (int)(rs.nS[0] + rs.nJ[0] + rs.nD[0]), t1 = (int)(rs.nS[1] + rs.nJ[1] + rs.nD[1]);
@@ -1302,6 +1357,52 @@ __device__ void run_item(const GProb& G, const Item& it, long long idx, unsigned
   gsync<NT>();
 }
 
+// fill of a stashed light pair (warp): row offsets as run_item's fill, row_ptr, K, and the two
+// rows copied from the stash (lanes stride the concatenation of both rows)
+__device__ __forceinline__ void copy_stashed(const GProb& G, long long p, const int* __restrict__ cnt,
+                                             const GOut& O) {
+  const int lane = threadIdx.x & 31;
+  const long long np = G.np;
+  const long long s = p / GSLOT, q0 = s * GSLOT;
+  int a0 = 0, a1 = 0;
+  if (q0 + lane < p) {
+    a0 = __ldg(cnt + q0 + lane);
+    a1 = __ldg(cnt + np + q0 + lane);
+  }
+  const int t0 = __ldg(cnt + p), t1 = __ldg(cnt + np + p);
+  const long long b0 = __ldg(O.toff + s), b1 = __ldg(O.toff + G.npt + s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a0 += __shfl_xor_sync(FULLM, a0, o);
+    a1 += __shfl_xor_sync(FULLM, a1, o);
+  }
+  const long long o0 = b0 + a0, o1 = b1 + a1;
+  if (lane == 0) {
+    O.row_ptr[p] = o0;
+    O.row_ptr[np + p] = o1;
+    if (O.K) {
+      O.K[p] = __ldg(G.sK + p);
+      O.K[np + p] = __ldg(G.sK + np + p);
+    }
+  }
+  const long long s0 = p * G.scap, s1 = (np + p) * G.scap;
+  const int tt = t0 + t1;
+#pragma unroll 4
+  for (int k = lane; k < tt; k += 32) {
+    const bool r1 = k >= t0;
+    const long long src = r1 ? s1 + (k - t0) : s0 + k;
+    const long long dst = r1 ? o1 + (k - t0) : o0 + k;
+    put(O, dst, __ldg(G.scol + src), __ldg(G.sval + src));
+  }
+}
+
+// fill of the stashed light pairs: a warp per pair, no shared memory (full occupancy)
+__global__ void __launch_bounds__(256) k_g_copy(const GProb G, const int* __restrict__ cnt, const GOut O) {
+  const long long nw = (long long)gridDim.x * 8;
+  for (long long p = (long long)blockIdx.x * 8 + (threadIdx.x >> 5); p < G.np; p += nw)
+    if (__ldg(G.sflag + p)) copy_stashed(G, p, cnt, O);
+}
+
 // light engine: a warp per generator pair (rows S_ab, J_ab) with at most GW_CAP candidates;
 // heavier pairs are listed (count pass) for the heavy engine
 template <bool FILL>
@@ -1311,11 +1412,15 @@ __global__ void __launch_bounds__(32 * GW_WARPS) k_g_light(const GProb G, int* c
   const double tau = *G.tau_ptr;
   const long long nw = (long long)gridDim.x * GW_WARPS;
   for (long long p = (long long)blockIdx.x * GW_WARPS + (threadIdx.x >> 5); p < G.np; p += nw) {
+    if (FILL && G.scap > 0 && __ldg(G.sflag + p)) continue;  // written by k_g_copy
     const Item it = make_item(G, p, false, 0);
     const long long nsrc = num_sources(G, it);
     const unsigned long long C = total_candidates<32>(G, it, nsrc, B.sc);
     if (C > (unsigned long long)(G.cap < GW_CAP ? G.cap : GW_CAP)) {
-      if (!FILL && (threadIdx.x & 31) == 0) G.heavy[atomicAdd(G.nheavy, 1)] = (int)p;
+      if (!FILL && (threadIdx.x & 31) == 0) {
+        G.heavy[atomicAdd(G.nheavy, 1)] = (int)p;
+        if (G.scap > 0) G.sflag[p] = 0;
+      }
       continue;
     }
     run_item<32, GW_CAP, FILL>(G, it, p, C, B, nullptr, tau, cnt, ts, O);
@@ -1335,6 +1440,22 @@ __global__ void __launch_bounds__(GH_NT) k_g_heavy(const GProb G, int* cnt, int*
   if (FILL && part != 1 && blockIdx.x == 0 && threadIdx.x == 0) O.row_ptr[G.m] = *O.nnz;
   for (long long t = blockIdx.x; t < items; t += gridDim.x) {
     const bool isd = t < nd;
+    if (FILL && isd && G.dseg > 0 && __ldg(G.dflag + t)) {  // stashed D row lam = t + 1: copy its parts
+      const int lam = (int)t + 1;
+      const long long o = __ldg(O.toff + 2 * G.npt + lam - 1);
+      const int nS = __ldg(G.dtot + 2 * t), nJ = __ldg(G.dtot + 2 * t + 1);
+      const int tot = __ldg(cnt + 2 * G.np + t);
+      if (threadIdx.x == 0) {
+        O.row_ptr[2 * G.np + t] = o;
+        if (O.K) O.K[2 * G.np + t] = __ldg(G.dK + t);
+      }
+      const long long base = t * G.drow;
+      for (int k = threadIdx.x; k < tot; k += GH_NT) {
+        const long long src = base + (k < nS ? k : (k < nS + nJ ? G.dseg + (k - nS) : 2LL * G.dseg + (k - nS - nJ)));
+        put(O, o + k, __ldg(G.dcol + src), __ldg(G.dval + src));
+      }
+      continue;
+    }
     const long long p = isd ? 0 : (long long)__ldg(G.heavy + (t - nd));
     const Item it = make_item(G, p, isd, isd ? (int)t + 1 : 0);
     const long long nsrc = num_sources(G, it);
@@ -1361,6 +1482,7 @@ int sm_count() {
   return sms;
 }
 
+int light_occ = 1;  // resident light CTAs per SM (set_attrs)
 cudaError_t set_attrs() {
   static bool done = false;
   if (done) return cudaSuccess;
@@ -1371,6 +1493,14 @@ cudaError_t set_attrs() {
     e = cudaFuncSetAttribute(k_g_heavy<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HEAVY_SMEM);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_g_heavy<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)HEAVY_SMEM);
+  if (e == cudaSuccess) {  // the light engines' persistent grids: one wave of resident CTAs
+    int a = 0, b = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&a, k_g_light<false>, 32 * GW_WARPS, LIGHT_SMEM);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_g_light<true>, 32 * GW_WARPS, LIGHT_SMEM);
+    light_occ = a < b ? a : b;
+    if (light_occ < 1) light_occ = 1;
+  }
   done = e == cudaSuccess;
   return e;
 }
@@ -1378,6 +1508,63 @@ cudaError_t set_attrs() {
 size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 }  // namespace
+
+#ifndef SUN_G_SCAP_MAX
+#define SUN_G_SCAP_MAX 1024
+#endif
+// a light pair has <= GW_CAP candidates: <= 2 GW_CAP S/J entries per row, plus <= n - 1 D-part
+// entries; longer rows (n large) are assembled again by the fill
+int g_stash_scap(int n) {
+  const long long w = 2LL * GW_CAP + n - 1;
+  return (int)(((w < SUN_G_SCAP_MAX ? w : SUN_G_SCAP_MAX) + 3) & ~3LL);
+}
+#ifndef SUN_G_DSEG_MAX
+#define SUN_G_DSEG_MAX 16384
+#endif
+// D rows: S and J parts of at most dseg entries each (<= np distinct keys), D part <= n - 1
+static int g_dseg(int n) {
+  const long long np = (long long)n * (n - 1) / 2;
+  return (int)(((np < SUN_G_DSEG_MAX ? np : SUN_G_DSEG_MAX) + 3) & ~3LL);
+}
+static int g_drow(int n) { return (int)((2LL * g_dseg(n) + n - 1 + 3) & ~3LL); }
+size_t g_stash_bytes(int n) {
+  const long long np = (long long)n * (n - 1) / 2;
+  if (np <= 0) return 0;
+  const size_t sc = (size_t)g_stash_scap(n), nd = (size_t)(n - 1), dr = (size_t)g_drow(n);
+  return al256((size_t)np) + al256((size_t)2 * np * sizeof(double)) + al256((size_t)2 * np * sc * sizeof(int32_t)) +
+         al256((size_t)2 * np * sc * sizeof(double)) + al256(nd) + al256(nd * sizeof(double)) +
+         al256(nd * dr * sizeof(int32_t)) + al256(nd * dr * sizeof(double));
+}
+void g_stash_set(GProb& G, char* base) {
+  if (!base || G.np <= 0) {
+    G.scap = 0;
+    G.sflag = nullptr;
+    G.scol = nullptr;
+    G.sval = nullptr;
+    G.sK = nullptr;
+    G.dseg = G.drow = 0;
+    G.dflag = nullptr;
+    G.dcol = nullptr;
+    G.dval = nullptr;
+    G.dK = nullptr;
+    return;
+  }
+  const long long np = G.np;
+  const size_t sc = (size_t)g_stash_scap(G.n);
+  size_t off = 0;
+  G.sflag = reinterpret_cast<unsigned char*>(base + off); off += al256((size_t)np);
+  G.sK = reinterpret_cast<double*>(base + off);           off += al256((size_t)2 * np * sizeof(double));
+  G.scol = reinterpret_cast<int32_t*>(base + off);        off += al256((size_t)2 * np * sc * sizeof(int32_t));
+  G.sval = reinterpret_cast<double*>(base + off);          off += al256((size_t)2 * np * sc * sizeof(double));
+  G.scap = (int)sc;
+  const size_t nd = (size_t)(G.n - 1), dr = (size_t)g_drow(G.n);
+  G.dflag = reinterpret_cast<unsigned char*>(base + off); off += al256(nd);
+  G.dK = reinterpret_cast<double*>(base + off);           off += al256(nd * sizeof(double));
+  G.dcol = reinterpret_cast<int32_t*>(base + off);        off += al256(nd * dr * sizeof(int32_t));
+  G.dval = reinterpret_cast<double*>(base + off);
+  G.dseg = g_dseg(G.n);
+  G.drow = (int)dr;
+}
 
 GLayout g_layout(int n, int P, const long long* nnzL, size_t base) {
   GLayout g;
@@ -1455,7 +1642,8 @@ cudaError_t g_count(const GProb& pr, int* cnt, int* ts, cudaStream_t st, cudaStr
   GOut none{};
   const int sms = sm_count();
   const long long lw = (pr.np + GW_WARPS - 1) / GW_WARPS;
-  const unsigned lg = (unsigned)(lw < 4LL * sms ? (lw > 0 ? lw : 1) : 4LL * sms);
+  const long long lcap = (long long)light_occ * sms;
+  const unsigned lg = (unsigned)(lw < lcap ? (lw > 0 ? lw : 1) : lcap);
   const unsigned hd = (unsigned)(pr.n - 1 < 2LL * sms ? pr.n - 1 : 2LL * sms);
   k_g_heavy<false><<<hd > 0 ? hd : 1, GH_NT, HEAVY_SMEM, aux>>>(pr, cnt, ts, none, 0);
   k_g_light<false><<<lg, 32 * GW_WARPS, LIGHT_SMEM, st>>>(pr, cnt, ts, none);
@@ -1468,8 +1656,13 @@ cudaError_t g_fill(const GProb& pr, const int* cnt, const GOut& out, cudaStream_
   if (e != cudaSuccess) return e;
   const int sms = sm_count();
   const long long lw = (pr.np + GW_WARPS - 1) / GW_WARPS;
-  const unsigned lg = (unsigned)(lw < 4LL * sms ? (lw > 0 ? lw : 1) : 4LL * sms);
+  const long long lcap = (long long)light_occ * sms;
+  const unsigned lg = (unsigned)(lw < lcap ? (lw > 0 ? lw : 1) : lcap);
   k_g_heavy<true><<<(unsigned)(2 * sms), GH_NT, HEAVY_SMEM, aux>>>(pr, const_cast<int*>(cnt), nullptr, out, 2);
+  if (pr.scap > 0) {
+    const long long cw = (pr.np + 7) / 8, cc = 8LL * sms;
+    k_g_copy<<<(unsigned)(cw < cc ? (cw > 0 ? cw : 1) : cc), 256, 0, st>>>(pr, cnt, out);
+  }
   k_g_light<true><<<lg, 32 * GW_WARPS, LIGHT_SMEM, st>>>(pr, const_cast<int*>(cnt), nullptr, out);
   return cudaGetLastError();
 }

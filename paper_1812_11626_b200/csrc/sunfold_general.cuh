@@ -62,6 +62,22 @@ struct GProb {
   int* dtot;              // [2 (n-1)]: S / J part lengths of the D rows (count pass -> fill pass)
   int cap;                // candidate buffer limit (testing: a small value forces the chunked
                           // and single-key paths); the engines use min(their buffer, cap)
+  // light-row stash (sun_plan_set_stash; scap = 0: off): the count pass keeps the assembled
+  // entries of each light pair's two rows (when both have <= scap entries), the fill pass
+  // copies them to their offsets instead of assembling the rows again
+  int scap;               // entries per stashed row
+  unsigned char* sflag;   // [np]: 1 = pair p's rows S_p (stash row p) and J_p (row np + p) are stashed
+  int32_t* scol;          // [2 np][scap]
+  double* sval;           // [2 np][scap]
+  double* sK;             // [2 np]: K of the two rows
+  // D-row stash (same buffer): row lam's S part at dcol/dval[(lam - 1) drow], its J part at
+  // + dseg, its D part at + 2 dseg (the count pass writes the three parts while counting them;
+  // rows whose S or J part exceeds dseg entries are assembled again by the fill); dseg = 0: off
+  int dseg, drow;
+  unsigned char* dflag;   // [n - 1]
+  int32_t* dcol;          // [n - 1][drow]
+  double* dval;           // [n - 1][drow]
+  double* dK;             // [n - 1]
 };
 
 struct GOut {  // fill outputs (capacity-checked)
@@ -112,6 +128,11 @@ cudaError_t g_prepare();
 cudaError_t g_count(const GProb& pr, int* cnt, int* ts, cudaStream_t st, cudaStream_t aux);
 // fill pass (a5): row_ptr, col, val (and K); heavy rows on `aux`
 cudaError_t g_fill(const GProb& pr, const int* cnt, const GOut& out, cudaStream_t st, cudaStream_t aux);
+// light-row stash of one matrix: entries per row and bytes (0 when np = 0)
+int g_stash_scap(int n);
+size_t g_stash_bytes(int n);
+// points G's stash at `base` (g_stash_bytes(n) bytes), or switches it off (base = nullptr)
+void g_stash_set(GProb& G, char* base);
 // kernels per count / fill call
 constexpr int G_LAUNCHES_EXPAND = 4, G_LAUNCHES_COUNT = 3, G_LAUNCHES_FILL = 2;
 

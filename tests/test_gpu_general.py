@@ -186,3 +186,64 @@ def test_general_workspace_guard():
     torch.cuda.synchronize()
     assert plan.workspace_guard_intact()
     plan.close()
+
+
+STASH = [
+    random_sparse_problem(300, seed=21, P=2),
+    ring_dimer_problem(256, drive=True),
+    dense_dissipator_problem(24, seed=0),
+    random_sparse_problem(40, seed=5, P=2, drive=True),
+    column_jump_problem(20, seed=0),
+]
+
+
+@pytest.mark.parametrize("prob", STASH, ids=lambda p: p.name)
+def test_general_stash_bit_identical(prob):
+    """Light-row stash (sun_plan_set_stash): the count pass writes each light
+    pair's assembled rows, the fill copies them.  Output bit-identical to the plan without a
+    stash (the fill assembling every row itself); both equal the oracle (test_general_patterns
+    runs with the stash, the default)."""
+    sun = _gpu()
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    assert plan.stash is not None and plan.info()["mode_q0"] == 3
+    A = plan.run()
+    A2 = plan.run_two_pass()
+    assert not plan.set_stash(False) and plan.stash is None
+    B = plan.run()
+    torch.cuda.synchronize()
+    for X in (A2, B):
+        for i in (0, 1):
+            if A[i] is None:
+                assert X[i] is None
+                continue
+            assert torch.equal(A[i].row_ptr, X[i].row_ptr) and torch.equal(A[i].col, X[i].col)
+            assert torch.equal(A[i].val, X[i].val)
+        assert torch.equal(A[2], X[2])
+    ref = _ref(prob)
+    _compare_csr(A[0], ref["Q0"], prob.name + ":Q0")
+    plan.close()
+
+
+def test_general_stash_abi():
+    """sun_plan_stash_bytes is 0 for banded plans and set_stash rejects them; changing the stash
+    requires a new count pass before the next fill (SUN_ERR_STATE)."""
+    import ctypes
+
+    sun = _gpu()
+    L = sun.lib()
+    prob = config(2)
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    assert int(L.sun_plan_stash_bytes(plan._plan)) == 0 and plan.stash is None
+    buf = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    assert L.sun_plan_set_stash(plan._plan, ctypes.c_void_p(buf.data_ptr()), ctypes.c_size_t(1 << 20)) != 0
+    plan.close()
+    prob = random_sparse_problem(40, seed=5, P=2, drive=True)
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    nb = int(L.sun_plan_stash_bytes(plan._plan))
+    assert nb > 0 and plan.stash is not None and plan.stash.numel() == nb
+    assert L.sun_plan_set_stash(plan._plan, ctypes.c_void_p(plan.stash.data_ptr()), ctypes.c_size_t(nb - 1)) != 0
+    nnz = plan.count()
+    plan.set_stash(True)
+    with pytest.raises(Exception):
+        plan.fill(*nnz)
+    plan.close()

@@ -12,7 +12,7 @@ def main(path, title=""):
     for r in rows[1:]:
         d[r[ki].split("(")[0]].append(float(r[vi].replace(",", "")))
     def mine(k):  # this library's kernels (libsunfold.so): k_* names
-        base = k.replace("void ", "").split("<")[0].split("::")[-1]
+        base = k.replace("void ", "").replace("<unnamed>", "").split("<")[0].split("::")[-1]
         return base.startswith("k_")
 
     ours = {k: v for k, v in d.items() if mine(k)}
