@@ -763,8 +763,9 @@ __device__ void d_chain_f(const GProb& G, const Item& it, int nd, DG diag, RowSt
           const int offj = __shfl_sync(FULLM, offd, j), cj = __shfl_sync(FULLM, c, j);
           const double Pj = __shfl_sync(FULLM, Pb, j), vj = __shfl_sync(FULLM, vc, j);
           const bool aj = __shfl_sync(FULLM, atc ? 1 : 0, j) != 0;
-          for (int t = lane; t < k1j; t += 32) put(O, b0 + offj + t, dbase + s0j + t, Pj * __ldg(G.inv + s0j + t));
-          if (aj && lane == 0) put(O, b0 + offj + k1j, dbase + cj, vj);
+          const long long lim = O.dlim > 0 ? O.dlim - rs.nD[r] - offj : 0x7fffffffffffffffLL;
+          for (int t = lane; t < k1j && t < lim; t += 32) put(O, b0 + offj + t, dbase + s0j + t, Pj * __ldg(G.inv + s0j + t));
+          if (aj && lane == 0 && k1j < lim) put(O, b0 + offj + k1j, dbase + cj, vj);
         }
       }
       rs.nD[r] += totd;
@@ -795,7 +796,8 @@ __device__ __forceinline__ void d_tail(const GProb& G, const Item& it, RowState&
     const int k1 = seg_kept(rs.P[r], s0, G.n, G.inv, tau);
     if (pass == PASS_WRITE) {
       const long long b0 = rs.O[r] + rs.TS[r] + rs.TJ[r] + rs.nD[r];
-      for (int t = lane; t < k1; t += 32) put(O, b0 + t, dbase + s0 + t, rs.P[r] * __ldg(G.inv + s0 + t));
+      const long long lim = O.dlim > 0 ? O.dlim - rs.nD[r] : 0x7fffffffffffffffLL;
+      for (int t = lane; t < k1 && t < lim; t += 32) put(O, b0 + t, dbase + s0 + t, rs.P[r] * __ldg(G.inv + s0 + t));
     }
     rs.nD[r] += k1;
   }
@@ -1199,12 +1201,21 @@ __device__ void run_item(const GProb& G, const Item& it, long long idx, unsigned
     // D row with a stash: the writing pass into the row's three stash segments (S, J, D parts at
     // fixed offsets), which counts exactly as the counting pass does
     const bool dst = it.kind == 1 && G.dseg > 0;
+    // light pair with a stash (one sorted chunk): the same writing pass into its two stash rows
+    // (S part <= GW_CAP distinct keys, J part likewise; the D part bounded by dlim)
+    const bool pst = NT == 32 && it.kind == 0 && G.scap > 0 && path == 0;
     GOut CO = O;
     int pc = PASS_COUNT;
     if (dst) {
       rs.O[0] = (long long)(it.lam - 1) * G.drow;
       rs.TS[0] = rs.TJ[0] = G.dseg;
-      CO = GOut{nullptr, G.dcol, G.dval, (long long)it.lam * G.drow, nullptr, nullptr, nullptr};
+      CO = GOut{nullptr, G.dcol, G.dval, (long long)it.lam * G.drow, nullptr, nullptr, nullptr, 0};
+      pc = PASS_WRITE;
+    } else if (pst) {
+      rs.O[0] = idx * G.scap;
+      rs.O[1] = (np + idx) * G.scap;
+      rs.TS[0] = rs.TJ[0] = rs.TS[1] = rs.TJ[1] = GW_CAP;
+      CO = GOut{nullptr, G.scol, G.sval, 0x7fffffffffffffffLL, nullptr, nullptr, nullptr, (long long)G.scap - 2 * GW_CAP};
       pc = PASS_WRITE;
     }
     if (path == 2) frame_sweep<NT, CAP>(G, it, nsrc, B, kmin, kmax, rs, pc, tau, CO);
@@ -1215,37 +1226,17 @@ __device__ void run_item(const GProb& G, const Item& it, long long idx, unsigned
       G.dflag[it.lam - 1] = ok ? 1 : 0;
       if (ok) G.dK[it.lam - 1] = rs.P[0] / (double)G.n;  // K_s = Tr(G_s)/N, as the fill writes it
     }
-    if constexpr (NT == 32) {
-      // light pair (one sorted chunk, still in B): replay the fill's writing pass into the
-      // stash rows (same operations, same order as the fill's path 0: bit-identical entries)
-      if (G.scap > 0 && it.kind == 0) {
-        const bool ok = path == 0 && rs.nS[0] + rs.nJ[0] + rs.nD[0] <= G.scap &&
-                        rs.nS[1] + rs.nJ[1] + rs.nD[1] <= G.scap;
-        if (ok) {
-          RowState ws = rs;
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            ws.TS[r] = rs.nS[r];
-            ws.TJ[r] = rs.nJ[r];
-            ws.nS[r] = ws.nJ[r] = ws.nD[r] = 0;
-            ws.P[r] = 0.0;
-          }
-          ws.prev = 1;
-          ws.O[0] = idx * G.scap;
-          ws.O[1] = (np + idx) * G.scap;
-          const GOut SO{nullptr, G.scol, G.sval, 0x7fffffffffffffffLL, nullptr, nullptr, nullptr};
-          assemble_runs<NT, CAP>(G, it, B, ws, PASS_WRITE, tau, SO);
-          d_chain<NT, CAP>(G, it, B, ws, PASS_WRITE, tau, SO);
-          d_tail(G, it, ws, PASS_WRITE, tau, SO);
-          if (lane == 0) {  // K_s = Tr(G_s)/N, as the fill writes it
-            G.sK[idx] = ws.P[0] / (double)G.n;
-            G.sK[np + idx] = ws.P[1] / (double)G.n;
-          }
-        }
-        if (lane == 0) G.sflag[idx] = ok ? 1 : 0;
-        __syncwarp();
+    if (pst && lane == 0) {
+      const bool ok = rs.nD[0] <= G.scap - 2 * GW_CAP && rs.nD[1] <= G.scap - 2 * GW_CAP;
+      G.sflag[idx] = ok ? 1 : 0;
+      if (ok) {  // K_s = Tr(G_s)/N, as the fill writes it
+        G.sK[idx] = rs.P[0] / (double)G.n;
+        G.sK[np + idx] = rs.P[1] / (double)G.n;
+        G.snj[idx] = make_int2((int)rs.nS[0], (int)rs.nJ[0]);
+        G.snj[np + idx] = make_int2((int)rs.nS[1], (int)rs.nJ[1]);
       }
     }
+    if (NT == 32 && it.kind == 0 && G.scap > 0 && !pst && lane == 0) G.sflag[idx] = 0;
     if (grank<NT>() == 0) {
       if (it.kind == 0) {
         const int t0 = (int)(rs.nS[0] + rs.nJ[0] + rs.nD[0]), t1 = (int)(rs.nS[1] + rs.nJ[1] + rs.nD[1]);
@@ -1385,13 +1376,17 @@ __device__ __forceinline__ void copy_stashed(const GProb& G, long long p, const 
       O.K[np + p] = __ldg(G.sK + np + p);
     }
   }
+  const int2 nj0 = __ldg(G.snj + p), nj1 = __ldg(G.snj + np + p);
   const long long s0 = p * G.scap, s1 = (np + p) * G.scap;
   const int tt = t0 + t1;
 #pragma unroll 4
   for (int k = lane; k < tt; k += 32) {
     const bool r1 = k >= t0;
-    const long long src = r1 ? s1 + (k - t0) : s0 + k;
-    const long long dst = r1 ? o1 + (k - t0) : o0 + k;
+    const int e = r1 ? k - t0 : k;  // entry of the row: S part, J part, D part
+    const int2 nj = r1 ? nj1 : nj0;
+    const int seg = e < nj.x ? e : (e < nj.x + nj.y ? GW_CAP + (e - nj.x) : 2 * GW_CAP + (e - nj.x - nj.y));
+    const long long src = (r1 ? s1 : s0) + seg;
+    const long long dst = (r1 ? o1 : o0) + e;
     put(O, dst, __ldg(G.scol + src), __ldg(G.sval + src));
   }
 }
@@ -1512,8 +1507,9 @@ size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 #ifndef SUN_G_SCAP_MAX
 #define SUN_G_SCAP_MAX 1024
 #endif
-// a light pair has <= GW_CAP candidates: <= 2 GW_CAP S/J entries per row, plus <= n - 1 D-part
-// entries; longer rows (n large) are assembled again by the fill
+// a light pair has <= GW_CAP candidates: S and J parts of <= GW_CAP entries each per row, plus
+// <= n - 1 D-part entries (segment of at most SUN_G_SCAP_MAX - 2 GW_CAP: rows with a longer D
+// part are assembled again by the fill)
 int g_stash_scap(int n) {
   const long long w = 2LL * GW_CAP + n - 1;
   return (int)(((w < SUN_G_SCAP_MAX ? w : SUN_G_SCAP_MAX) + 3) & ~3LL);
@@ -1531,8 +1527,8 @@ size_t g_stash_bytes(int n) {
   const long long np = (long long)n * (n - 1) / 2;
   if (np <= 0) return 0;
   const size_t sc = (size_t)g_stash_scap(n), nd = (size_t)(n - 1), dr = (size_t)g_drow(n);
-  return al256((size_t)np) + al256((size_t)2 * np * sizeof(double)) + al256((size_t)2 * np * sc * sizeof(int32_t)) +
-         al256((size_t)2 * np * sc * sizeof(double)) + al256(nd) + al256(nd * sizeof(double)) +
+  return al256((size_t)np) + al256((size_t)2 * np * sizeof(double)) + al256((size_t)2 * np * sizeof(int2)) +
+         al256((size_t)2 * np * sc * sizeof(int32_t)) + al256((size_t)2 * np * sc * sizeof(double)) + al256(nd) + al256(nd * sizeof(double)) +
          al256(nd * dr * sizeof(int32_t)) + al256(nd * dr * sizeof(double));
 }
 void g_stash_set(GProb& G, char* base) {
@@ -1542,6 +1538,7 @@ void g_stash_set(GProb& G, char* base) {
     G.scol = nullptr;
     G.sval = nullptr;
     G.sK = nullptr;
+    G.snj = nullptr;
     G.dseg = G.drow = 0;
     G.dflag = nullptr;
     G.dcol = nullptr;
@@ -1554,6 +1551,7 @@ void g_stash_set(GProb& G, char* base) {
   size_t off = 0;
   G.sflag = reinterpret_cast<unsigned char*>(base + off); off += al256((size_t)np);
   G.sK = reinterpret_cast<double*>(base + off);           off += al256((size_t)2 * np * sizeof(double));
+  G.snj = reinterpret_cast<int2*>(base + off);            off += al256((size_t)2 * np * sizeof(int2));
   G.scol = reinterpret_cast<int32_t*>(base + off);        off += al256((size_t)2 * np * sc * sizeof(int32_t));
   G.sval = reinterpret_cast<double*>(base + off);          off += al256((size_t)2 * np * sc * sizeof(double));
   G.scap = (int)sc;

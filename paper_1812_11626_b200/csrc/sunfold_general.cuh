@@ -65,11 +65,13 @@ struct GProb {
   // light-row stash (sun_plan_set_stash; scap = 0: off): the count pass keeps the assembled
   // entries of each light pair's two rows (when both have <= scap entries), the fill pass
   // copies them to their offsets instead of assembling the rows again
+  // (stash row r: S part at r scap, J part at + GW_CAP, D part at + 2 GW_CAP, as the D rows)
   int scap;               // entries per stashed row
   unsigned char* sflag;   // [np]: 1 = pair p's rows S_p (stash row p) and J_p (row np + p) are stashed
   int32_t* scol;          // [2 np][scap]
   double* sval;           // [2 np][scap]
   double* sK;             // [2 np]: K of the two rows
+  int2* snj;              // [2 np]: S and J part lengths of the two rows
   // D-row stash (same buffer): row lam's S part at dcol/dval[(lam - 1) drow], its J part at
   // + dseg, its D part at + 2 dseg (the count pass writes the three parts while counting them;
   // rows whose S or J part exceeds dseg entries are assembled again by the fill); dseg = 0: off
@@ -88,6 +90,7 @@ struct GOut {  // fill outputs (capacity-checked)
   double* K;  // nullptr: not written (Q1)
   const long long* toff;
   const long long* nnz;
+  long long dlim;  // > 0: D-part entries of a row beyond dlim are not written (stash rows)
 };
 
 constexpr int GSLOT = 32;  // pairs per scan slot (as modes 0/2: S slots, J slots, one slot per D row)
