@@ -152,8 +152,9 @@ Layout make_layout(int n, int P) {
   L.herm = off; off = align256(off + (size_t)2 * ((long long)n * (2 * WMAX + 1) / EXP_THREADS + 2) * sizeof(unsigned long long));
   L.ts0 = off; off = align256(off + (size_t)maxslots * sizeof(int));   // [ts0, toff0) zeroed per count
   L.ts1 = off; off = align256(off + (size_t)maxslots * sizeof(int));
-  L.st0 = off; off = align256(off + (size_t)maxchunks * sizeof(unsigned long long));
-  L.st1 = off; off = align256(off + (size_t)maxchunks * sizeof(unsigned long long));
+  // status words of the chained scan, then one "offsets written" flag per chunk (k_scan_near0)
+  L.st0 = off; off = align256(off + (size_t)2 * maxchunks * sizeof(unsigned long long));
+  L.st1 = off; off = align256(off + (size_t)2 * maxchunks * sizeof(unsigned long long));
   L.toff0 = off; off = align256(off + (size_t)maxslots * sizeof(long long));
   L.toff1 = off; off = align256(off + (size_t)maxslots * sizeof(long long));
   L.cnt0 = off; off = align256(off + (size_t)m * sizeof(int));
@@ -256,6 +257,7 @@ struct sun_plan_s {
   int combined;         // mode 0 with Q1 absent or Q1 = Q_H[diagonal H1]: one launch per pass
   int near_sep = 0;     // combined: near rows by k_near0 before the fill (SUNFOLD_NEAR_SEP=1)
   int near_conc = 0;    // near_sep: k_near0 on aux[0] concurrently with the fill (SUNFOLD_NEAR_CONC)
+  int scan_near = 0;    // combined, sun_run: near rows written by the scan's launch (k_scan_near0)
   int pdl = 0;          // combined: programmatic dependent launch between the sequence's kernels
   int pdl_run = 0;      // PDL also inside sun_run's sequence (SUNFOLD_PDL_RUN=1; A/B only)
   // phase timing (sun_plan_set_timing): events before the count, between count and fill, after
@@ -995,9 +997,12 @@ constexpr int NEAR_GL = 32 / NEAR_RPW;        // lanes per row
 constexpr int NEAR_UROWS = 8 * NEAR_RPW;      // side rows per near unit
 // inv: the inv[l] table (SMEM_INV: a shared-memory copy, else global through the read-only path).
 // srow0: the warp's first side row (its NEAR_RPW rows are srow0, srow0 + 1, ...)
+// done: when not null, the scan of this launch is still running (k_scan_near0): the row's slot
+// offset is read once done[slot's chunk] is set, after every lookup that does not depend on it.
 template <bool SMEM_INV>
 __device__ __forceinline__ void fill_near_rows_w(const Prob& pr, long long srow0, const int* __restrict__ cnt,
-                                                 const FillOut& fo, const NearSide& side, const double* inv) {
+                                                 const FillOut& fo, const NearSide& side, const double* inv,
+                                                 const unsigned long long* done = nullptr) {
   const int lane = threadIdx.x & 31;
   const int hl = lane & (NEAR_GL - 1);
   const long long np = pr.np;
@@ -1016,9 +1021,10 @@ __device__ __forceinline__ void fill_near_rows_w(const Prob& pr, long long srow0
   NearMeta m{};
   long long o = 0;
   int s1 = 0;
+  const long long slot = kind == 1 ? (half ? pr.npt : 0) + p / pr.tp : 2 * pr.npt + lam - 1;
   if (kind != 0) {
     m = side.meta[srow];
-    o = kind == 1 ? __ldg(&fo.toff[(half ? pr.npt : 0) + p / pr.tp]) : __ldg(&fo.toff[2 * pr.npt + lam - 1]);
+    if (!done) o = __ldg(&fo.toff[slot]);
   }
   if (kind == 1) {
     const long long ts = (p / pr.tp) * pr.tp;
@@ -1033,6 +1039,16 @@ __device__ __forceinline__ void fill_near_rows_w(const Prob& pr, long long srow0
   }
 #pragma unroll
   for (int sh = NEAR_GL / 2; sh > 0; sh >>= 1) s1 += __shfl_xor_sync(FULL, s1, sh);  // within each group
+  if (done) {  // warp-uniform wait for the scan chunks of the warp's rows, then the offsets from L2
+    const volatile unsigned long long* vd = done + (kind != 0 ? slot / SCAN_TILE : 0);
+    bool ready = kind == 0 || *vd != 0ull;
+    while (!__all_sync(FULL, ready)) {
+      __nanosleep(64);
+      if (!ready) ready = *vd != 0ull;
+    }
+    __threadfence();
+    if (kind != 0) o = __ldcg(&fo.toff[slot]);
+  }
   if (kind == 0) return;  // no shuffles below
   if (kind == 1) {
     o += s1;
@@ -1704,6 +1720,9 @@ __global__ void __launch_bounds__(256, FillFar<WK, WL>::MINB) k_fill0(const MatF
 // The chain tails (up to n entries per row, tr * inv[l]) read inv[] from a shared-memory copy
 // when it fits (NEAR_SMEM_INV doubles), not one dependent L2 load per entry.
 constexpr int NEAR_SMEM_INV = 8192;
+#ifndef SUN_SCAN_NEAR_DEFAULT
+#define SUN_SCAN_NEAR_DEFAULT 0  // measured slower (c4 step 97 -> 106 us, c3 127 -> 131 us): A/B switch only
+#endif
 #ifndef SUN_NEAR_CONC_DEFAULT
 #define SUN_NEAR_CONC_DEFAULT 0
 #endif
@@ -2043,15 +2062,10 @@ struct ScanArgs {
   HeaderPrefix* hout;    // (sun_plan_nnz then reads it after the stream; no copy node)
 };
 
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_chain(ScanArgs A) {
-  pdl_enter();
-  const int y = blockIdx.y;
-  __shared__ unsigned int chunk_s;
-  __shared__ long long wsum[32];
-  __shared__ long long prefix_s;
-  if (threadIdx.x == 0) chunk_s = atomicAdd(&A.ticket[y], 1u);
-  __syncthreads();
-  const long long chunk = chunk_s;
+// One chunk (SCAN_TILE slots) of matrix y's chained scan by the whole CTA.  done: when not null,
+// done[chunk] is set once the chunk's offsets are in toff (k_scan_near0's near units wait on it).
+__device__ __forceinline__ void scan_chunk(const ScanArgs& A, int y, long long chunk, int ny, long long* wsum,
+                                           long long& prefix_s, unsigned long long* done) {
   const long long nslots = A.nslots[y];
   const long long nchunks = (nslots + SCAN_TILE - 1) / SCAN_TILE;
   if (chunk >= (nchunks > 0 ? nchunks : 1)) return;  // block-uniform
@@ -2124,7 +2138,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_chain(ScanArgs A) {
         A.hout->herm_dev[1] = h->herm_dev[1];
         A.hout->nrm2_h[0] = h->nrm2_h[0];
         A.hout->nrm2_h[1] = h->nrm2_h[1];
-        if (gridDim.y == 1) A.hout->nnz[1] = 0;
+        if (ny == 1) A.hout->nnz[1] = 0;
       }
     }
   }
@@ -2145,29 +2159,209 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_chain(ScanArgs A) {
     for (int i = 0; i < SCAN_IPT; ++i)
       if (c0 + i < nslots) out[c0 + i] = o[i];
   }
+  if (done) {  // publish: every thread's offsets before the flag
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicExch(&done[chunk], 1ull);
+  }
 }
 
-// (a7) dv/dt = Q0 v + eps Q1 v + K ; 8 lanes per row, fixed-order reduction.
-__global__ void k_apply(long long m, const int64_t* __restrict__ rp0, const int32_t* __restrict__ c0,
-                        const double* __restrict__ v0, const int64_t* __restrict__ rp1,
-                        const int32_t* __restrict__ c1, const double* __restrict__ v1, double eps,
-                        const double* __restrict__ Kv, const double* __restrict__ x, double* __restrict__ y) {
-  long long gt = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  long long row = gt >> 3;
-  int sub = threadIdx.x & 7;
-  bool ok = row < m;
-  double s0 = 0.0, s1 = 0.0;
-  if (ok) {
-    for (int64_t k = rp0[row] + sub; k < rp0[row + 1]; k += 8) s0 += v0[k] * __ldg(&x[c0[k]]);
-    if (rp1)
-      for (int64_t k = rp1[row] + sub; k < rp1[row + 1]; k += 8) s1 += v1[k] * __ldg(&x[c1[k]]);
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_chain(ScanArgs A) {
+  pdl_enter();
+  const int y = blockIdx.y;
+  __shared__ unsigned int chunk_s;
+  __shared__ long long wsum[32];
+  __shared__ long long prefix_s;
+  if (threadIdx.x == 0) chunk_s = atomicAdd(&A.ticket[y], 1u);
+  __syncthreads();
+  scan_chunk(A, y, chunk_s, (int)gridDim.y, wsum, prefix_s, nullptr);
+}
+
+// (a4) + the near rows of (a5) in one launch (sun_run on a combined mode-0 plan: the outputs are
+// known when the scan is enqueued).  CTAs take roles in ticket order: the first nch0 + nch1
+// tickets are the scan chunks of Q0 and Q1 (every scan CTA is resident before any near CTA takes
+// a ticket, and never waits on one), the rest are near units of NEAR_UROWS side rows.  A near
+// warp issues everything that does not depend on the scan (inv[] copy, metadata, the slot's
+// earlier counts) and then waits for its slot's chunk to be published, so the near rows' lookup
+// chains run under the scan's look-back chain instead of after it.
+struct ScanNearArgs {
+  ScanArgs sa;
+  long long nch[2];                  // scan chunks of Q0, Q1 (0: no Q1)
+  const unsigned long long* done0;   // Q0's per-chunk "offsets written" flags
+  unsigned long long* done[2];
+};
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_near0(const ScanNearArgs A, const MatFill m0) {
+  static_assert(SCAN_THREADS == 256, "near units: 8 warps");
+  extern __shared__ double sinv[];
+  __shared__ unsigned int ticket_s;
+  __shared__ long long wsum[32];
+  __shared__ long long prefix_s;
+  if (threadIdx.x == 0) ticket_s = atomicAdd(&A.sa.ticket[0], 1u);
+  __syncthreads();
+  const long long t = ticket_s;
+  const int ny = A.nch[1] > 0 ? 2 : 1;
+  if (t < A.nch[0]) {
+    scan_chunk(A.sa, 0, t, ny, wsum, prefix_s, A.done[0]);
+    return;
   }
+  if (t < A.nch[0] + A.nch[1]) {
+    scan_chunk(A.sa, 1, t - A.nch[0], ny, wsum, prefix_s, nullptr);
+    return;
+  }
+  const long long j = t - A.nch[0] - A.nch[1];
+  const int n = m0.pr.n;
+  if (n <= NEAR_SMEM_INV) {
+    for (int l = threadIdx.x; l < n; l += blockDim.x) sinv[l] = __ldg(&m0.pr.inv[l]);
+    __syncthreads();
+    fill_near_rows_w<true>(m0.pr, j * NEAR_UROWS + (threadIdx.x >> 5) * NEAR_RPW, m0.cnt, m0.fo, m0.side, sinv, A.done0);
+  } else {
+    fill_near_rows_w<false>(m0.pr, j * NEAR_UROWS + (threadIdx.x >> 5) * NEAR_RPW, m0.cnt, m0.fo, m0.side, m0.pr.inv,
+                            A.done0);
+  }
+}
+
+// (a7) dv/dt = Q0 v + eps Q1 v + K as a streamed CSR product.  A CTA owns R consecutive rows (R
+// chosen by the host from the mean row length so that a block holds about two tiles of entries;
+// the last row blocks, the long D rows, are scheduled first), reads their entries (col, val) as
+// one contiguous, fully coalesced stream in tiles of APPLY_TILE entries (the next tile's loads in
+// flight during the current tile's sums), gathers x (8 MB at N = 1000: L2 resident) and leaves
+// the products in shared memory.  The rows that intersect the tile (binary search in the staged
+// row pointers) are then summed by G = 256 / rows lanes each (a power of two <= 32), lane-strided
+// with a fixed shuffle tree; a row with more than APPLY_LONG G entries in the tile (a near row's
+// D-chain tail among short rows) is summed by its whole warp.  Blocks whose rows average <= 32
+// entries skip the search: thread t sums row t in entry order (long segments by the warp).  Every
+// order is fixed: the result is deterministic.  The 8-lanes-per-row kernel this replaces read col/val in 32- and 64-byte
+// pieces per row (120 us at c4, 0.33 of HBM).
+constexpr int APPLY_THREADS = 256, APPLY_TILE = 2048, APPLY_LONG = 64;
+// number of i in [0, n) with a[i] < key (strict = true) or a[i] <= key; a ascending (shared memory)
+__device__ __forceinline__ int apply_count_below(const long long* a, int n, long long key, bool strict) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    const long long x = a[mid];
+    if (strict ? x < key : x <= key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ double apply_stream_rows(const long long* rp_s, int nrows, const int32_t* __restrict__ col,
+                                                    const double* __restrict__ val, const double* __restrict__ x,
+                                                    double* prod, double* racc) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const long long eb = rp_s[0], ee = rp_s[nrows];
+  // a block whose rows average <= 32 entries: thread t owns row t (no search, no row accumulators)
+  const bool simple = ee - eb <= 32LL * nrows;
+  const long long rs = tid < nrows ? rp_s[tid] : ee, re = tid < nrows ? rp_s[tid + 1] : ee;
+  double acc1 = 0.0;
+  racc[tid] = 0.0;  // ordered before its first use by the tile loop's barrier
+  constexpr int IPT = APPLY_TILE / APPLY_THREADS;
+  int c[IPT];
+  double v[IPT];
+  auto load_tile = [&](long long e0) {  // the tile's entries, lane-contiguous (coalesced), streaming
 #pragma unroll
-  for (int o = 4; o > 0; o >>= 1) {
-    s0 += __shfl_xor_sync(FULL, s0, o);
-    s1 += __shfl_xor_sync(FULL, s1, o);
+    for (int i = 0; i < IPT; ++i) {
+      const long long k = e0 + i * APPLY_THREADS + tid;
+      const bool in = k >= eb && k < ee;
+      c[i] = in ? __ldcs(col + k) : 0;
+      v[i] = in ? __ldcs(val + k) : 0.0;
+    }
+  };
+  const long long e00 = eb - (eb & 31);
+  if (e00 < ee) load_tile(e00);
+  for (long long e0 = e00; e0 < ee; e0 += APPLY_TILE) {  // block-uniform
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) prod[i * APPLY_THREADS + tid] = v[i] * __ldg(&x[c[i]]);
+    __syncthreads();
+    const long long t1 = e0 + APPLY_TILE;
+    if (t1 < ee) load_tile(t1);  // in flight during this tile's sums
+    if (simple) {  // short rows: thread t sums row t in entry order, long segments by the warp
+      const int lo = (int)((rs > e0 ? rs : e0) - e0), hi = (int)((re < t1 ? re : t1) - e0);  // hi <= lo: none here
+      const bool lng = hi - lo > APPLY_LONG;
+      unsigned lm = __ballot_sync(FULL, lng);
+      double part = 0.0;
+      if (!lng)
+        for (int k = lo; k < hi; ++k) part += prod[k];
+      while (lm) {  // warp-uniform
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const int l = __shfl_sync(FULL, lo, src), h = __shfl_sync(FULL, hi, src);
+        double t = 0.0;
+        for (int k = l + lane; k < h; k += 32) t += prod[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+        if (lane == src) part = t;
+      }
+      acc1 += part;
+      __syncthreads();
+      continue;
+    }
+    // rows [rcur, rend) intersect the tile (empty rows among them are harmless)
+    int rcur = apply_count_below(rp_s, nrows + 1, e0, false) - 1;
+    if (rcur < 0) rcur = 0;
+    const int rend = apply_count_below(rp_s, nrows, t1, true);
+    const int nint = rend - rcur;
+    int G = 1;
+    while (G < 32 && 2 * G * nint <= APPLY_THREADS) G <<= 1;  // 256 / G >= nint: one row per group
+    const int g = tid / G, gl = tid & (G - 1), r = rcur + g;
+    const bool valid = g < nint;
+    int lo = 0, hi = 0;
+    if (valid) {
+      const long long a = rp_s[r], b = rp_s[r + 1];
+      lo = (int)((a > e0 ? a : e0) - e0);
+      hi = (int)((b < t1 ? b : t1) - e0);
+    }
+    const bool lng = hi - lo > APPLY_LONG * G;
+    double part = 0.0;
+    if (!lng) {
+#pragma unroll 4
+      for (int k = lo + gl; k < hi; k += G) part += prod[k];
+    }
+    unsigned lm = __ballot_sync(FULL, lng && gl == 0);
+    while (lm) {  // warp-uniform: the long rows of this warp's groups, one after the other
+      const int src = __ffs(lm) - 1;
+      lm &= lm - 1;
+      const int l = __shfl_sync(FULL, lo, src), h = __shfl_sync(FULL, hi, src);
+      double t = 0.0;
+#pragma unroll 4
+      for (int k = l + lane; k < h; k += 32) t += prod[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+      if (lane == src) part = t;  // the group's other lanes hold 0
+    }
+    for (int o = G >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+    if (valid && gl == 0) racc[r] += part;  // one group per row and tile; tiles in ascending order
+    __syncthreads();
   }
-  if (ok && sub == 0) y[row] = s0 + eps * s1 + (Kv ? Kv[row] : 0.0);
+  __syncthreads();
+  const double acc = simple ? acc1 : racc[tid];
+  __syncthreads();
+  return acc;
+}
+
+__global__ void __launch_bounds__(APPLY_THREADS) k_apply(long long m, int R, const int64_t* __restrict__ rp0,
+                                                         const int32_t* __restrict__ c0, const double* __restrict__ v0,
+                                                         const int64_t* __restrict__ rp1, const int32_t* __restrict__ c1,
+                                                         const double* __restrict__ v1, double eps,
+                                                         const double* __restrict__ Kv, const double* __restrict__ x,
+                                                         double* __restrict__ y) {
+  __shared__ double prod[APPLY_TILE];
+  __shared__ double racc[APPLY_THREADS];
+  __shared__ long long rp_s[2][APPLY_THREADS + 1];
+  const long long r0 = (long long)(gridDim.x - 1 - blockIdx.x) * R;  // last rows (the D rows: the longest) first
+  const int nrows = (int)(m - r0 < R ? m - r0 : R);
+  const int tid = threadIdx.x;
+  for (int i = tid; i <= nrows; i += APPLY_THREADS) {
+    rp_s[0][i] = rp0[r0 + i];
+    if (rp1) rp_s[1][i] = rp1[r0 + i];
+  }
+  const double kv = Kv && tid < nrows ? Kv[r0 + tid] : 0.0;
+  __syncthreads();
+  const double s0 = apply_stream_rows(rp_s[0], nrows, c0, v0, x, prod, racc);
+  double s1 = 0.0;
+  if (rp1) s1 = apply_stream_rows(rp_s[1], nrows, c1, v1, x, prod, racc);
+  if (tid < nrows) y[r0 + tid] = s0 + eps * s1 + kv;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -3109,6 +3303,10 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
     pl->near_conc = pl->near_sep ? (nc && nc[0] ? atoi(nc) : SUN_NEAR_CONC_DEFAULT) : 0;
   }
   pl->launches_fill = pl->combined ? 1 + pl->near_sep : nmat;
+  {  // sun_run: near rows inside the scan's launch (k_scan_near0); SUNFOLD_SCAN_NEAR=1 for A/B (off: slower)
+    const char* sn = getenv("SUNFOLD_SCAN_NEAR");
+    pl->scan_near = pl->combined && (sn && sn[0] ? sn[0] != '0' : SUN_SCAN_NEAR_DEFAULT);
+  }
   {
     const char* np_ = getenv("SUNFOLD_NO_PDL");
     const char* pm = getenv("SUNFOLD_PDL_MASK");  // bits: 1 count, 2 scan, 4 near, 8 fill
@@ -3144,6 +3342,9 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
       static bool near_attr = false;  // k_near0's shared inv[] table: up to 64 KB
       if (e1 == cudaSuccess && !near_attr) {
         e1 = cudaFuncSetAttribute(k_near0, cudaFuncAttributeMaxDynamicSharedMemorySize, NEAR_SMEM_INV * (int)sizeof(double));
+        if (e1 == cudaSuccess)
+          e1 = cudaFuncSetAttribute(k_scan_near0, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    NEAR_SMEM_INV * (int)sizeof(double));
         near_attr = e1 == cudaSuccess;
       }
     } else {
@@ -3222,7 +3423,9 @@ static int enqueue_count_general(sun_plan pl, cudaStream_t st, bool scan_hdr) {
 // scan_hdr: the scan stores the header prefix into the mapped slot (else the fill does: see
 // header_in_fill)
 // pdl_ok: programmatic dependent launch allowed (the count-only sequence; see SUN_PDL_DEFAULT)
-static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr, bool pdl_ok) {
+// near_mf: sun_run on a combined plan (scan_near_fused): the fill arguments of Q0; the scan's
+// launch then also writes the near rows (k_scan_near0)
+static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr, bool pdl_ok, const MatFill* near_mf = nullptr) {
   NvtxRange r_("sunfold: expand (a1) + count (a3) + scan (a4)");
   if (pl->general) return enqueue_count_general(pl, st, scan_hdr);
   const Layout& L = pl->lay;
@@ -3304,6 +3507,23 @@ static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr, bool pdl_o
     if (pl->has_h1) CK(join_aux(pl, st, 1));
   }
   // (a4) chained scan of both matrices' slot sums
+  if (near_mf) {
+    const Prob& p0 = pl->pr[0];
+    ScanNearArgs na;
+    na.sa = sa;
+    for (int which = 0; which < 2; ++which) {
+      na.nch[which] = which < nmat ? (sa.nslots[which] + SCAN_TILE - 1) / SCAN_TILE : 0;
+      if (which < nmat && na.nch[which] < 1) na.nch[which] = 1;  // the empty matrix's chunk writes nnz = 0
+      na.done[which] = which < nmat ? sa.status[which] + L.maxchunks : nullptr;
+    }
+    na.done0 = na.done[0];
+    MatFill m0 = *near_mf;
+    m0.near_sep = 1;
+    const long long nn0 = (2 * (p0.n * 2LL * p0.W + p0.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
+    const size_t sm = p0.n <= NEAR_SMEM_INV ? (size_t)p0.n * sizeof(double) : 0;
+    CK(launch_k(false, k_scan_near0, dim3((unsigned)(na.nch[0] + na.nch[1] + nn0)), dim3(SCAN_THREADS), sm, st, na, m0));
+    return SUN_OK;
+  }
   CK(launch_k(pdl_ok && pl->combined && (pl->pdl & 2), k_scan_chain, dim3((unsigned)maxchunks, nmat), dim3(SCAN_THREADS), 0, st, sa));
   return SUN_OK;
 }
@@ -3361,15 +3581,12 @@ static bool header_in_fill(sun_plan pl) {
   return pl->res.dpin && !pl->general && (pl->combined || (!pl->has_h1 && pl->pr[0].mode == 2));
 }
 
-// pdl_first: the fill directly follows this plan's scan in the stream (sun_run)
-static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st, bool fill_hdr,
-                        bool pdl_first) {
-  NvtxRange r_("sunfold: fill (a5) + K + Q1 (a6)");
+// the fill pass's per-matrix arguments for these outputs
+static void build_matfill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, bool fill_hdr, MatFill mf[2]) {
   const Layout& L = pl->lay;
   char* ws = pl->ws;
   DevHeader* hdr = (DevHeader*)(ws + L.hdr);
   const int nmat = 1 + pl->has_h1;
-  MatFill mf[2];
   for (int which = 0; which < nmat; ++which) {
     sun_dcsr* Q = which ? Q1 : Q0;
     FillOut fo = {Q->row_ptr, Q->col, Q->val, (long long)Q->nnz, which ? nullptr : K,
@@ -3384,6 +3601,21 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
   if (pl->pr[0].mode == 0) mf[0].sab = (const int2*)(ws + L.sab);  // written by this plan's count pass
   if (pl->combined) mf[0].wctr = hdr->wctr;  // k_fill0's dynamic warp units (SUN_FILL_DYN)
   if (nmat == 1) mf[1] = mf[0];
+}
+
+// sun_run on a combined plan: the near rows are written by the scan's launch (k_scan_near0)
+static bool scan_near_fused(sun_plan pl, int kind) { return kind == 2 && pl->combined && pl->scan_near; }
+
+// pdl_first: the fill directly follows this plan's scan in the stream (sun_run)
+// near_done: the near rows have been written by k_scan_near0 (the count sequence of this sun_run)
+static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cudaStream_t st, bool fill_hdr,
+                        bool pdl_first, bool near_done) {
+  NvtxRange r_("sunfold: fill (a5) + K + Q1 (a6)");
+  const Layout& L = pl->lay;
+  char* ws = pl->ws;
+  const int nmat = 1 + pl->has_h1;
+  MatFill mf[2];
+  build_matfill(pl, Q0, Q1, K, fill_hdr, mf);
   if (pl->general) {
     CK(fork_aux(pl, st, nmat));  // heavy rows of matrix `which` on aux[which]
     for (int which = 0; which < nmat; ++which) {
@@ -3395,7 +3627,9 @@ static int enqueue_fill(sun_plan pl, sun_dcsr* Q0, sun_dcsr* Q1, double* K, cuda
     return SUN_OK;
   }
   if (pl->combined) {
-    if (pl->near_sep) {
+    if (near_done) {
+      mf[0].near_sep = 1;
+    } else if (pl->near_sep) {
       mf[0].near_sep = 1;
       const Prob& p0 = pl->pr[0];
       const long long nn0 = (2 * (p0.n * 2LL * p0.W + p0.n - 1) + NEAR_UROWS - 1) / NEAR_UROWS;
@@ -3453,10 +3687,13 @@ static int enqueue_kind(sun_plan pl, int kind, sun_dcsr* Q0, sun_dcsr* Q1, doubl
   auto direct = [&](cudaStream_t s) -> int {
     int rc = SUN_OK;
     const bool fill_hdr = kind == 2 && header_in_fill(pl);
+    const bool fused = scan_near_fused(pl, kind);
+    MatFill nmf[2];
+    if (fused) build_matfill(pl, Q0, Q1, K, false, nmf);
     if (kind != 1) rc = tmark(s, 0);
-    if (rc == SUN_OK && kind != 1) rc = enqueue_count(pl, s, !fill_hdr, kind == 0 || pl->pdl_run);
+    if (rc == SUN_OK && kind != 1) rc = enqueue_count(pl, s, !fill_hdr, kind == 0 || pl->pdl_run, fused ? &nmf[0] : nullptr);
     if (rc == SUN_OK && kind != 0) rc = tmark(s, 1);
-    if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s, fill_hdr, kind == 2);
+    if (rc == SUN_OK && kind != 0) rc = enqueue_fill(pl, Q0, Q1, K, s, fill_hdr, kind == 2, fused);
     if (rc == SUN_OK && kind == 0) rc = tmark(s, 1);
     if (rc == SUN_OK && kind != 0) rc = tmark(s, 2);
     if (rc == SUN_OK && readback && !mapped) {
@@ -3616,9 +3853,12 @@ int sun_apply(const sun_dcsr* Q0, const sun_dcsr* Q1, double eps, const double* 
   if (Q1 && (Q1->m != Q0->m || !Q1->row_ptr)) return SUN_ERR_ARG;
   long long m = Q0->m;
   if (m <= 0) return SUN_ERR_DIM;
-  long long threads = m * 8;
-  k_apply<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      m, Q0->row_ptr, Q0->col, Q0->val, Q1 ? Q1->row_ptr : nullptr, Q1 ? Q1->col : nullptr,
+  // rows per CTA: about two tiles of entries per block (8 .. 256 rows, a power of two)
+  const long long nz = Q0->nnz + (Q1 ? Q1->nnz : 0);
+  int R = APPLY_THREADS;
+  while (R > 8 && nz > 0 && (long long)(R / 2) * nz >= 2LL * APPLY_TILE * m) R >>= 1;
+  k_apply<<<(unsigned)((m + R - 1) / R), APPLY_THREADS, 0, (cudaStream_t)stream>>>(
+      m, R, Q0->row_ptr, Q0->col, Q0->val, Q1 ? Q1->row_ptr : nullptr, Q1 ? Q1->col : nullptr,
       Q1 ? Q1->val : nullptr, eps, K, v, dvdt);
   CK(cudaGetLastError());
   return SUN_OK;

@@ -140,6 +140,26 @@ def test_wide_band_modes(which, monkeypatch):
     assert torch.equal(ak, bk)
 
 
+@pytest.mark.parametrize("idx", [2, 3])
+def test_scan_near_fused_switch(idx, monkeypatch):
+    """SUNFOLD_SCAN_NEAR=1 (A/B switch, off by default: measured slower): sun_run writes the near
+    rows from the scan's launch (k_scan_near0, near warps wait on per-chunk flags of the chained
+    scan).  Its outputs equal the two-pass path's bit for bit, direct and graph-replayed."""
+    sun = _gpu()
+    monkeypatch.setenv("SUNFOLD_SCAN_NEAR", "1")
+    prob = config(idx)
+    plan = sun.Plan(prob.H0, prob.H1, prob.Ls, prob.gammas)
+    for _ in range(3):
+        Q0, Q1, K = plan.run()
+    R0, R1, RK = plan.run_two_pass()
+    torch.cuda.synchronize()
+    assert Q0.nnz == R0.nnz and torch.equal(Q0.row_ptr, R0.row_ptr)
+    assert torch.equal(Q0.col, R0.col) and torch.equal(Q0.val, R0.val) and torch.equal(K, RK)
+    if Q1 is not None:
+        assert Q1.nnz == R1.nnz and torch.equal(Q1.col, R1.col) and torch.equal(Q1.val, R1.val)
+    plan.close()
+
+
 def test_nnz_readback_pooled_slots():
     """sun_run returns nnz as soon as the fill has stored this sequence's header (mapped
     slot, sequence number last).  Plans created one after another reuse pooled slots that hold
