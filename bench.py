@@ -521,6 +521,29 @@ def main():
     # F1: RK4 propagation of the unfolded system from rho(0) = |0><0|,
     # timed on the device (L2 flushed before).  h = 1e-5 keeps RK4 stable: BASELINE's
     # dissipator has no gamma/(N-1) prefactor (reading R9), |lambda|max ~ gamma N^2.
+    # (a7) sun_apply: dv/dt = Q0 v + eps Q1 v + K on the unfold's outputs (L2 flushed before each
+    # call); algorithmic bytes = 12 B per nonzero + the row pointers + x, K read and dv/dt written
+    apply_line = None
+    if not args.no_rk4:
+        xa = torch.randn(m, dtype=torch.float64, device="cuda")
+        ya = torch.empty_like(xa)
+        sun.apply(Q0, Q1, 1.3, K, xa, out=ya)
+        ap_ev = []
+        for _ in range(max(5, min(args.steps, 30))):
+            flush.fill_(1.0)
+            torch.cuda._sleep(200_000)
+            a, b = ev(), ev()
+            a.record(stream)
+            sun.apply(Q0, Q1, 1.3, K, xa, out=ya)
+            b.record(stream)
+            ap_ev.append((a, b))
+        torch.cuda.synchronize()
+        ap_ms = statistics.mean([a.elapsed_time(b) for a, b in ap_ev])
+        ap_bytes = 12 * nnz_total + 8 * (m + 1) * (2 if Q1 is not None else 1) + 8 * m * 3
+        apply_line = {"ms": ap_ms, "algorithmic_bytes": ap_bytes, "kernel": "k_apply (streamed CSR product, one launch)",
+                      "roofline": {"bound": "hbm", "achieved": ap_bytes / (ap_ms * 1e-3) / 1e9, "peak": peak,
+                                   "unit": "GB/s", "frac": ap_bytes / (ap_ms * 1e-3) / 1e9 / peak}}
+        del xa, ya
     rk4 = None
     if not args.no_rk4:
         from workloads import ZCSR as _Z
@@ -706,6 +729,7 @@ def main():
         "gpu_launches": args.steps * launches_per_step,
         "roofline": roofline,
         "cpu_baseline": cpu,
+        "apply": apply_line,
         "rk4": rk4,
         "f3_dense": f3,
         "configs": extra,

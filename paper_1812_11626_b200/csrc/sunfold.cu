@@ -888,7 +888,8 @@ __device__ __forceinline__ void count0_unit(const MatCount& m0, const MatCount& 
   }
 }
 
-// one single-warp CTA per unit
+// one single-warp CTA per unit (2 or 4 independent warps per CTA measured slower at c3 and c4: the
+// step 127 -> 134 us and 97 -> 99 / 103 us)
 template <int WK, int WL, int PT, int Q1W>
 __global__ void __launch_bounds__(32) k_count0(const MatCount m0, const MatCount m1) {
 #if SUN_PDL_COUNT == 1
@@ -2232,7 +2233,10 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_near0(const ScanNearArgs 
 // entries skip the search: thread t sums row t in entry order (long segments by the warp).  Every
 // order is fixed: the result is deterministic.  The 8-lanes-per-row kernel this replaces read col/val in 32- and 64-byte
 // pieces per row (120 us at c4, 0.33 of HBM).
-constexpr int APPLY_THREADS = 256, APPLY_TILE = 2048, APPLY_LONG = 64;
+#ifndef SUN_APPLY_TILE
+#define SUN_APPLY_TILE 2048
+#endif
+constexpr int APPLY_THREADS = 256, APPLY_TILE = SUN_APPLY_TILE, APPLY_LONG = 64;
 // number of i in [0, n) with a[i] < key (strict = true) or a[i] <= key; a ascending (shared memory)
 __device__ __forceinline__ int apply_count_below(const long long* a, int n, long long key, bool strict) {
   int lo = 0, hi = n;
@@ -2246,10 +2250,73 @@ __device__ __forceinline__ int apply_count_below(const long long* a, int n, long
   }
   return lo;
 }
+// The sums of one tile: prod holds the products of entries [e0, e0 + APPLY_TILE) (0 outside the
+// block).  simple: thread t adds row t's part to acc1; else the intersecting rows' parts go to racc.
+__device__ __forceinline__ void apply_tile_sums(const long long* rp_s, int nrows, long long e0, const double* prod,
+                                                bool simple, long long rs, long long re, double& acc1, double* racc) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const long long t1 = e0 + APPLY_TILE;
+  if (simple) {  // short rows: thread t sums row t in entry order, long segments by the warp
+    const int lo = (int)((rs > e0 ? rs : e0) - e0), hi = (int)((re < t1 ? re : t1) - e0);  // hi <= lo: none here
+    const bool lng = hi - lo > APPLY_LONG;
+    unsigned lm = __ballot_sync(FULL, lng);
+    double part = 0.0;
+    if (!lng)
+      for (int k = lo; k < hi; ++k) part += prod[k];
+    while (lm) {  // warp-uniform
+      const int src = __ffs(lm) - 1;
+      lm &= lm - 1;
+      const int l = __shfl_sync(FULL, lo, src), h = __shfl_sync(FULL, hi, src);
+      double t = 0.0;
+      for (int k = l + lane; k < h; k += 32) t += prod[k];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+      if (lane == src) part = t;
+    }
+    acc1 += part;
+    return;
+  }
+  // rows [rcur, rend) intersect the tile (empty rows among them are harmless)
+  int rcur = apply_count_below(rp_s, nrows + 1, e0, false) - 1;
+  if (rcur < 0) rcur = 0;
+  const int rend = apply_count_below(rp_s, nrows, t1, true);
+  const int nint = rend - rcur;
+  int G = 1;
+  while (G < 32 && 2 * G * nint <= APPLY_THREADS) G <<= 1;  // 256 / G >= nint: one row per group
+  const int g = tid / G, gl = tid & (G - 1), r = rcur + g;
+  const bool valid = g < nint;
+  int lo = 0, hi = 0;
+  if (valid) {
+    const long long a = rp_s[r], b = rp_s[r + 1];
+    lo = (int)((a > e0 ? a : e0) - e0);
+    hi = (int)((b < t1 ? b : t1) - e0);
+  }
+  const bool lng = hi - lo > APPLY_LONG * G;
+  double part = 0.0;
+  if (!lng) {
+#pragma unroll 4
+    for (int k = lo + gl; k < hi; k += G) part += prod[k];
+  }
+  unsigned lm = __ballot_sync(FULL, lng && gl == 0);
+  while (lm) {  // warp-uniform: the long rows of this warp's groups, one after the other
+    const int src = __ffs(lm) - 1;
+    lm &= lm - 1;
+    const int l = __shfl_sync(FULL, lo, src), h = __shfl_sync(FULL, hi, src);
+    double t = 0.0;
+#pragma unroll 4
+    for (int k = l + lane; k < h; k += 32) t += prod[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
+    if (lane == src) part = t;  // the group's other lanes hold 0
+  }
+  for (int o = G >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
+  if (valid && gl == 0) racc[r] += part;  // one group per row and tile; tiles in ascending order
+}
+
 __device__ __forceinline__ double apply_stream_rows(const long long* rp_s, int nrows, const int32_t* __restrict__ col,
                                                     const double* __restrict__ val, const double* __restrict__ x,
                                                     double* prod, double* racc) {
-  const int tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x;
   const long long eb = rp_s[0], ee = rp_s[nrows];
   // a block whose rows average <= 32 entries: thread t owns row t (no search, no row accumulators)
   const bool simple = ee - eb <= 32LL * nrows;
@@ -2276,62 +2343,7 @@ __device__ __forceinline__ double apply_stream_rows(const long long* rp_s, int n
     __syncthreads();
     const long long t1 = e0 + APPLY_TILE;
     if (t1 < ee) load_tile(t1);  // in flight during this tile's sums
-    if (simple) {  // short rows: thread t sums row t in entry order, long segments by the warp
-      const int lo = (int)((rs > e0 ? rs : e0) - e0), hi = (int)((re < t1 ? re : t1) - e0);  // hi <= lo: none here
-      const bool lng = hi - lo > APPLY_LONG;
-      unsigned lm = __ballot_sync(FULL, lng);
-      double part = 0.0;
-      if (!lng)
-        for (int k = lo; k < hi; ++k) part += prod[k];
-      while (lm) {  // warp-uniform
-        const int src = __ffs(lm) - 1;
-        lm &= lm - 1;
-        const int l = __shfl_sync(FULL, lo, src), h = __shfl_sync(FULL, hi, src);
-        double t = 0.0;
-        for (int k = l + lane; k < h; k += 32) t += prod[k];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
-        if (lane == src) part = t;
-      }
-      acc1 += part;
-      __syncthreads();
-      continue;
-    }
-    // rows [rcur, rend) intersect the tile (empty rows among them are harmless)
-    int rcur = apply_count_below(rp_s, nrows + 1, e0, false) - 1;
-    if (rcur < 0) rcur = 0;
-    const int rend = apply_count_below(rp_s, nrows, t1, true);
-    const int nint = rend - rcur;
-    int G = 1;
-    while (G < 32 && 2 * G * nint <= APPLY_THREADS) G <<= 1;  // 256 / G >= nint: one row per group
-    const int g = tid / G, gl = tid & (G - 1), r = rcur + g;
-    const bool valid = g < nint;
-    int lo = 0, hi = 0;
-    if (valid) {
-      const long long a = rp_s[r], b = rp_s[r + 1];
-      lo = (int)((a > e0 ? a : e0) - e0);
-      hi = (int)((b < t1 ? b : t1) - e0);
-    }
-    const bool lng = hi - lo > APPLY_LONG * G;
-    double part = 0.0;
-    if (!lng) {
-#pragma unroll 4
-      for (int k = lo + gl; k < hi; k += G) part += prod[k];
-    }
-    unsigned lm = __ballot_sync(FULL, lng && gl == 0);
-    while (lm) {  // warp-uniform: the long rows of this warp's groups, one after the other
-      const int src = __ffs(lm) - 1;
-      lm &= lm - 1;
-      const int l = __shfl_sync(FULL, lo, src), h = __shfl_sync(FULL, hi, src);
-      double t = 0.0;
-#pragma unroll 4
-      for (int k = l + lane; k < h; k += 32) t += prod[k];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULL, t, o);
-      if (lane == src) part = t;  // the group's other lanes hold 0
-    }
-    for (int o = G >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(FULL, part, o);
-    if (valid && gl == 0) racc[r] += part;  // one group per row and tile; tiles in ascending order
+    apply_tile_sums(rp_s, nrows, e0, prod, simple, rs, re, acc1, racc);
     __syncthreads();
   }
   __syncthreads();
@@ -2340,7 +2352,15 @@ __device__ __forceinline__ double apply_stream_rows(const long long* rp_s, int n
   return acc;
 }
 
-__global__ void __launch_bounds__(APPLY_THREADS) k_apply(long long m, int R, const int64_t* __restrict__ rp0,
+// Tried and removed (measured on B200, same box): the entry tiles brought in by TMA 1D bulk loads
+// (cp.async.bulk.shared.global on an mbarrier, a two-stage shared-memory ring, products in place):
+// c4 82.0 us with either kernel, c3 121 us against 86 us.  ncu shows why the loads are not the
+// limiter: the L1 data pipe (shared-memory product stores and reads plus the gathers' wavefronts)
+// is the busiest unit at 65 % of peak, L2 at 30 %, DRAM below that.
+#ifndef SUN_APPLY_MINB
+#define SUN_APPLY_MINB 4
+#endif
+__global__ void __launch_bounds__(APPLY_THREADS, SUN_APPLY_MINB) k_apply(long long m, int R, const int64_t* __restrict__ rp0,
                                                          const int32_t* __restrict__ c0, const double* __restrict__ v0,
                                                          const int64_t* __restrict__ rp1, const int32_t* __restrict__ c1,
                                                          const double* __restrict__ v1, double eps,
@@ -3853,10 +3873,10 @@ int sun_apply(const sun_dcsr* Q0, const sun_dcsr* Q1, double eps, const double* 
   if (Q1 && (Q1->m != Q0->m || !Q1->row_ptr)) return SUN_ERR_ARG;
   long long m = Q0->m;
   if (m <= 0) return SUN_ERR_DIM;
-  // rows per CTA: about two tiles of entries per block (8 .. 256 rows, a power of two)
+  // rows per CTA: at least 4096 entries per block on average (8 .. 256 rows, a power of two)
   const long long nz = Q0->nnz + (Q1 ? Q1->nnz : 0);
   int R = APPLY_THREADS;
-  while (R > 8 && nz > 0 && (long long)(R / 2) * nz >= 2LL * APPLY_TILE * m) R >>= 1;
+  while (R > 8 && nz > 0 && (long long)(R / 2) * nz >= 4096LL * m) R >>= 1;
   k_apply<<<(unsigned)((m + R - 1) / R), APPLY_THREADS, 0, (cudaStream_t)stream>>>(
       m, R, Q0->row_ptr, Q0->col, Q0->val, Q1 ? Q1->row_ptr : nullptr, Q1 ? Q1->col : nullptr,
       Q1 ? Q1->val : nullptr, eps, K, v, dvdt);
