@@ -258,6 +258,7 @@ struct sun_plan_s {
   int near_sep = 0;     // combined: near rows by k_near0 before the fill (SUNFOLD_NEAR_SEP=1)
   int near_conc = 0;    // near_sep: k_near0 on aux[0] concurrently with the fill (SUNFOLD_NEAR_CONC)
   int scan_near = 0;    // combined, sun_run: near rows written by the scan's launch (k_scan_near0)
+  int scan_direct = 1;  // chain-free scan while the chunks are few (SUNFOLD_SCAN_DIRECT=0 for A/B)
   int pdl = 0;          // combined: programmatic dependent launch between the sequence's kernels
   int pdl_run = 0;      // PDL also inside sun_run's sequence (SUNFOLD_PDL_RUN=1; A/B only)
   // phase timing (sun_plan_set_timing): events before the count, between count and fill, after
@@ -2061,7 +2062,15 @@ struct ScanArgs {
   unsigned int* ticket;
   const DevHeader* hdr;  // with hout: the header prefix is also stored in mapped host memory
   HeaderPrefix* hout;    // (sun_plan_nnz then reads it after the stream; no copy node)
+  int direct;            // few chunks: every CTA sums the slots before its chunk itself (no chain)
 };
+// Up to this many chunks per matrix a chunk's CTA computes its own prefix: it re-reads the slot sums
+// before its chunk (at most SCAN_DIRECT_MAX x 4 KB, from L2, all loads independent) instead of
+// waiting on its predecessors' status words (one dependent L2 round trip per link of the chain).
+// Integer sums: bit-identical.
+#ifndef SUN_SCAN_DIRECT_MAX
+#define SUN_SCAN_DIRECT_MAX 16  // measured: 3 chunks (c2) step 41.9 -> 40.2 us, 9 chunks (c3) equal, 32 chunks (c4) scan 6.7 -> 8.0 us
+#endif
 
 // One chunk (SCAN_TILE slots) of matrix y's chained scan by the whole CTA.  done: when not null,
 // done[chunk] is set once the chunk's offsets are in toff (k_scan_near0's near units wait on it).
@@ -2083,16 +2092,30 @@ __device__ __forceinline__ void scan_chunk(const ScanArgs& A, int y, long long c
 #pragma unroll
     for (int i = 0; i < SCAN_IPT; ++i) v[i] = c0 + i < nslots ? ts[c0 + i] : 0;
   }
+  long long pre = 0;
+  if (A.direct) {  // the slots before this chunk (chunk * SCAN_TILE of them: whole int4s)
+    const int4* p4 = reinterpret_cast<const int4*>(ts);
+    const long long n4 = chunk * (SCAN_TILE / 4);
+#pragma unroll 4
+    for (long long i = threadIdx.x; i < n4; i += SCAN_THREADS) {
+      const int4 q = __ldcg(p4 + i);
+      pre += (long long)q.x + q.y + q.z + q.w;
+    }
+  }
   long long local = 0;
 #pragma unroll
   for (int i = 0; i < SCAN_IPT; ++i) local += v[i];
   long long total;
   const long long ex = block_scan_ll(local, wsum, total);
+  long long pre_total = 0;
+  if (A.direct) block_scan_ll(pre, wsum, pre_total);
   unsigned long long* st = A.status[y];
   if (threadIdx.x < 32) {  // warp 0: publish the aggregate, then a warp-parallel look-back
     const int lane = threadIdx.x;
     long long prefix = 0;
-    if (chunk == 0) {
+    if (A.direct) {
+      prefix = pre_total;
+    } else if (chunk == 0) {
       if (lane == 0) {
         __threadfence();
         atomicExch(&st[0], SCAN_P | (unsigned long long)total);
@@ -2173,7 +2196,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_chain(ScanArgs A) {
   __shared__ unsigned int chunk_s;
   __shared__ long long wsum[32];
   __shared__ long long prefix_s;
-  if (threadIdx.x == 0) chunk_s = atomicAdd(&A.ticket[y], 1u);
+  if (threadIdx.x == 0) chunk_s = A.direct ? blockIdx.x : atomicAdd(&A.ticket[y], 1u);
   __syncthreads();
   scan_chunk(A, y, chunk_s, (int)gridDim.y, wsum, prefix_s, nullptr);
 }
@@ -3323,6 +3346,10 @@ int sun_plan_create_ex(sun_plan* out, const sun_zcsr* H0, const sun_zcsr* H1, co
     pl->near_conc = pl->near_sep ? (nc && nc[0] ? atoi(nc) : SUN_NEAR_CONC_DEFAULT) : 0;
   }
   pl->launches_fill = pl->combined ? 1 + pl->near_sep : nmat;
+  {
+    const char* sd = getenv("SUNFOLD_SCAN_DIRECT");
+    pl->scan_direct = !(sd && sd[0] == '0');
+  }
   {  // sun_run: near rows inside the scan's launch (k_scan_near0); SUNFOLD_SCAN_NEAR=1 for A/B (off: slower)
     const char* sn = getenv("SUNFOLD_SCAN_NEAR");
     pl->scan_near = pl->combined && (sn && sn[0] ? sn[0] != '0' : SUN_SCAN_NEAR_DEFAULT);
@@ -3527,6 +3554,7 @@ static int enqueue_count(sun_plan pl, cudaStream_t st, bool scan_hdr, bool pdl_o
     if (pl->has_h1) CK(join_aux(pl, st, 1));
   }
   // (a4) chained scan of both matrices' slot sums
+  sa.direct = pl->scan_direct && maxchunks <= SUN_SCAN_DIRECT_MAX ? 1 : 0;
   if (near_mf) {
     const Prob& p0 = pl->pr[0];
     ScanNearArgs na;
