@@ -241,6 +241,70 @@ def test_apply_against_oracle_spmv_c3():
     assert np.abs(y - yr).max() <= 1e-12 * np.abs(yr).max()
 
 
+def _csr_from_lengths(lens, m, seed):
+    """A random square CSR (m rows) with the given row lengths: ascending distinct columns per row."""
+    rng = np.random.default_rng(seed)
+    rp = np.zeros(m + 1, dtype=np.int64)
+    rp[1:] = np.cumsum(lens)
+    col = np.empty(rp[-1], dtype=np.int32)
+    for r in range(m):
+        col[rp[r]:rp[r + 1]] = np.sort(rng.choice(m, size=int(lens[r]), replace=False))
+    return rp, col, rng.standard_normal(rp[-1])
+
+
+@pytest.mark.parametrize("shape", ["short", "one_long_among_short", "all_long", "wide_multi_tile", "empty_rows",
+                                   "single_row", "no_entries"])
+def test_apply_row_shapes(shape):
+    """sun_apply (a7, Eq. 9) on synthetic CSR matrices that reach every summation path of
+    the streamed kernel (thread per row, a long segment summed by its warp, G lanes per intersecting
+    row, rows spanning several tiles, rows per CTA below 256, ragged last block), against the plain
+    definition y_r = sum_k Q0[r,k] x_k + eps sum_k Q1[r,k] x_k + K_r in fp64."""
+    sun = _gpu()
+    rng = np.random.default_rng(5)
+    m = {"single_row": 1, "all_long": 300, "wide_multi_tile": 2600}.get(shape, 1301)
+    if shape == "short":
+        l0 = rng.integers(0, 30, m)
+    elif shape == "one_long_among_short":
+        l0 = rng.integers(5, 25, m)
+        l0[[3, 700, 1300]] = [1200, 900, 1301]
+    elif shape == "all_long":
+        l0 = rng.integers(150, 300, m)
+    elif shape == "wide_multi_tile":
+        l0 = rng.integers(2200, 2600, m)  # every row longer than a 2048-entry tile, 8 rows per CTA
+    elif shape == "empty_rows":
+        l0 = np.where(rng.random(m) < 0.7, 0, rng.integers(1, 400, m))
+    elif shape == "single_row":
+        l0 = np.array([1])
+    else:
+        l0 = np.zeros(m, dtype=np.int64)
+    l1 = np.minimum(rng.integers(0, 4, m), m)
+    A0, A1 = _csr_from_lengths(l0, m, 1), _csr_from_lengths(l1, m, 2)
+    x, Kv, eps = rng.standard_normal(m), rng.standard_normal(m), 0.7
+
+    def dev(A):
+        # entries at an offset inside a larger buffer when empty (a null data pointer is an error)
+        rp, col, val = (torch.tensor(a, device="cuda") for a in A)
+        if col.numel() == 0:
+            col, val = torch.zeros(4, dtype=torch.int32, device="cuda")[:0], torch.zeros(4, dtype=torch.float64, device="cuda")[:0]
+        return sun.CSR(rp, col, val)
+
+    def ref(A):
+        rp, col, val = A
+        y = np.zeros(m)
+        for r in range(m):
+            y[r] = np.dot(val[rp[r]:rp[r + 1]], x[col[rp[r]:rp[r + 1]]])
+        return y
+
+    want = ref(A0) + eps * ref(A1) + Kv
+    scale = np.abs(want).max() + 1.0
+    xd = torch.tensor(x, device="cuda")
+    for Q1, K, w in ((dev(A1), torch.tensor(Kv, device="cuda"), want), (None, None, ref(A0))):
+        got = _np(sun.apply(dev(A0), Q1, eps, K, xd))
+        assert np.abs(got - w).max() <= 1e-12 * scale, (shape, np.abs(got - w).max())
+        again = _np(sun.apply(dev(A0), Q1, eps, K, xd))
+        assert np.array_equal(got, again), "sun_apply is deterministic"
+
+
 def test_edge_cases():
     sun = _gpu()
     n = 6
